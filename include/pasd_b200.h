@@ -1,0 +1,191 @@
+/*
+ * pasd_b200.h — C-ABI of the B200-native PASD ADMM solver (tensor robust PCA,
+ * arXiv 1712.09999).  Plain pointers and sizes only: no torch, no C++ types.
+ *
+ * This is the drop-in boundary for the reference solver entry point
+ *   tenrec::pasd_recover(const DenseTensor&, const PasdConfig&,
+ *                        const IterationObserver&)        (proj/include/tenrec/pasd.hpp:65-66)
+ * with
+ *   PasdConfig      -> pasd_options         (proj/include/tenrec/pasd.hpp:8-27)
+ *   RecoveryResult  -> pasd_outputs         (proj/include/tenrec/recovery.hpp:20-34)
+ *   Certificate     -> pasd_outputs.cert_*  (proj/include/tenrec/recovery.hpp:14-18)
+ *   IterationView   -> pasd_iteration_view  (proj/include/tenrec/recovery.hpp:38-48)
+ *   exceptions      -> PASD_ERR_* + errbuf  (proj/include/tenrec/errors.hpp:9-30)
+ *
+ * Tensors are dense float64 with the FIRST index varying fastest
+ * (proj/include/tenrec/tensor.hpp:23-24).  Matrices are column-major.
+ *
+ * No global mutable state: every call owns its stream(s), device buffers and
+ * (multi-GPU) NCCL communicator, so concurrent calls from several host threads
+ * are safe (the reference harness calls the solver from a thread pool,
+ * proj/src/bench.cpp:226-248).
+ */
+#ifndef PASD_B200_H
+#define PASD_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PASD_B200_ABI_VERSION 1
+
+/* Status codes.  The numeric values follow the reference CLI's exit-code
+ * taxonomy (proj/tools/cli.hpp:9-14): argument 1, I/O 2, numerical 3.  State
+ * errors (certificate misuse) are 4 and CUDA/NCCL failures 5. */
+enum {
+  PASD_OK = 0,
+  PASD_ERR_ARGUMENT = 1,  /* tenrec::ArgumentError  */
+  PASD_ERR_IO = 2,        /* tenrec::IoError        */
+  PASD_ERR_NUMERICAL = 3, /* tenrec::NumericalError */
+  PASD_ERR_STATE = 4,     /* tenrec::StateError     */
+  PASD_ERR_CUDA = 5       /* device / NCCL failure (no reference analogue) */
+};
+
+/* pasd_options.flags */
+enum {
+  PASD_FLAG_NONE = 0,
+  /* Skip the certificate even when converged (reference always computes it,
+   * pasd.cpp:272-273; this only saves the final ||T||_1 pass). */
+  PASD_FLAG_NO_CERTIFICATE = 1u << 0,
+  /* Deterministic fixed-iteration mode: ignore eps, run exactly maxiter
+   * iterations (BASELINE "fixed N iters" runs).  converged is reported 0. */
+  PASD_FLAG_FIXED_ITERS = 1u << 1
+};
+
+/* Mirror of tenrec::PasdConfig (pasd.hpp:8-27) plus placement. */
+typedef struct pasd_options {
+  int32_t order;                 /* N = number of modes                           */
+  const int64_t* dims;           /* [N] I_1..I_N                                   */
+  const int64_t* ranks;          /* [N] R_n  (PasdConfig::ranks)                   */
+  const double* lambdas;         /* [N] lambda_n (PasdConfig::lambdas)             */
+  const double* output_weights;  /* [N] alpha_n, NULL = lambdas (pasd.hpp:16,26)   */
+  double mu0;                    /* default 1e-4  (pasd.hpp:11)                    */
+  double mu_max;                 /* default 1e10  (pasd.hpp:12)                    */
+  double rho;                    /* default 1.1   (pasd.hpp:13)                    */
+  double eps;                    /* default 1e-5  (pasd.hpp:14)                    */
+  int32_t maxiter;               /* default 1000  (pasd.hpp:15)                    */
+  int32_t device;                /* CUDA ordinal                                   */
+  uint32_t flags;                /* PASD_FLAG_*                                    */
+  int32_t poll_every;            /* host polls the on-device stop flag every k
+                                    iterations (0 = auto). Results never depend on
+                                    it: iterations after the stop are no-ops.      */
+} pasd_options;
+
+/* Multi-GPU slab sharding along the LAST mode (one process per GPU).  A NULL
+ * shard means the whole tensor on one device. */
+typedef struct pasd_shard {
+  int32_t rank;                  /* this process's rank                            */
+  int32_t nranks;                /* world size                                     */
+  const void* nccl_unique_id;    /* 128-byte ncclUniqueId from rank 0 (NULL if nranks==1) */
+  int64_t slab_begin;            /* first last-mode index owned by this rank       */
+  int64_t slab_end;              /* one past the last                              */
+} pasd_shard;
+
+/* Snapshot handed to the observer after each completed iteration
+ * (tenrec::IterationView, recovery.hpp:38-48).  Pointers are host copies valid
+ * only during the callback (pasd.cpp:241-242). */
+typedef struct pasd_iteration_view {
+  int32_t iter;                  /* 1-based count of completed iterations          */
+  double mu_used;
+  double mu_next;
+  const double* residual_inf;    /* [N]                                            */
+  const double* e;               /* S                                              */
+  const double* const* z;        /* [N] x S                                        */
+  const double* const* y;        /* [N] x S                                        */
+  const double* const* u;        /* [N] x (I_n x R_n) column-major                 */
+  const double* const* v;        /* [N] x (R_n x J_n) column-major, J_n = S / I_n  */
+} pasd_iteration_view;
+
+typedef void (*pasd_observer_fn)(const pasd_iteration_view* view, void* user);
+
+/* Mirror of tenrec::RecoveryResult (recovery.hpp:20-34).  Every tensor pointer
+ * is a caller-allocated HOST buffer of S doubles or NULL (= not wanted). */
+typedef struct pasd_outputs {
+  double* x;                     /* combined low-rank estimate                     */
+  double* e;                     /* sparse estimate                                */
+  double* const* z;              /* [N] per-mode Z_n, or NULL                      */
+  double* const* y;              /* [N] final multipliers, or NULL                 */
+  double* const* y_hat;          /* [N] auxiliary multipliers, or NULL             */
+  double* residual_history;      /* capacity maxiter, or NULL                      */
+  double* final_residuals;       /* [N], or NULL                                   */
+  int32_t iters;
+  int32_t converged;
+  double objective;
+  int32_t has_certificate;
+  double cert_epsilon_hat;
+  double cert_c;
+  double cert_bound;
+} pasd_outputs;
+
+/* ---- one-call drop-in --------------------------------------------------- */
+
+/* Full solve from a HOST tensor: H2D of t, the device-resident ADMM loop, the
+ * finalisation and D2H of the requested outputs.  Returns PASD_OK or an error
+ * code; errbuf receives the reference's exception message text. */
+int pasd_b200_recover(const double* t, const pasd_options* opt, pasd_outputs* out,
+                      pasd_observer_fn observer, void* user, char* errbuf, size_t errlen);
+
+/* ---- device-resident solver handle (benchmarks, multi-GPU) -------------- */
+
+typedef struct pasd_solver pasd_solver;
+
+int pasd_b200_solver_create(const pasd_options* opt, const pasd_shard* shard, pasd_solver** out,
+                            char* errbuf, size_t errlen);
+/* Upload the (local slab of the) observed tensor.  `t_is_device` != 0 means t
+ * is a device pointer on the solver's device (device-to-device copy). */
+int pasd_b200_solver_load(pasd_solver* s, const double* t, int t_is_device, char* errbuf,
+                          size_t errlen);
+/* Reset the iterate to the initial state (E=0, Y=0, U=eye, V=0, mu=mu0). */
+int pasd_b200_solver_reset(pasd_solver* s, char* errbuf, size_t errlen);
+/* Run up to `iters` further iterations (stops early on convergence). */
+int pasd_b200_solver_run(pasd_solver* s, int32_t iters, int32_t* iters_done, int32_t* converged,
+                         char* errbuf, size_t errlen);
+/* Finalise (Y-hat, objective, X, certificate) and copy requested outputs to
+ * host buffers (local slab only for a sharded solver). */
+int pasd_b200_solver_finalize(pasd_solver* s, pasd_outputs* out, char* errbuf, size_t errlen);
+/* Device pointers of the local slab of E and of Y_n (diagnostics / zero-copy). */
+const double* pasd_b200_solver_device_e(const pasd_solver* s);
+/* The CUDA stream (cudaStream_t) the solver launches on. */
+void* pasd_b200_solver_stream(const pasd_solver* s);
+/* Number of kernel launches issued by the last pasd_b200_solver_run call. */
+int64_t pasd_b200_solver_launches(const pasd_solver* s);
+void pasd_b200_solver_destroy(pasd_solver* s);
+
+/* ---- reference-shaped helpers (pasd.hpp:51-58, tensor.hpp:86-91) -------- */
+
+/* lambda_n = sqrt(max(I_n, prod_{j!=n} I_j)) / N  (pasd.cpp:51-60). */
+int pasd_b200_default_lambdas(int32_t order, const int64_t* dims, double* lambdas_out,
+                              char* errbuf, size_t errlen);
+/* R = floor(1.2 r) in integer arithmetic (pasd.cpp:62-66). */
+int pasd_b200_default_rank_bound(int64_t target_rank, int64_t* out, char* errbuf, size_t errlen);
+/* PasdConfig::validate (pasd.cpp:12-49): same checks, same messages. */
+int pasd_b200_validate(const pasd_options* opt, char* errbuf, size_t errlen);
+
+/* Device implementations of the reference linops (linops.hpp:15-46), built
+ * from the same kernels the solver uses (k_gram + k_svt, k_contract_W +
+ * k_polar).  Host buffers in, host buffers out; column-major.
+ *   svt:        rows <= 64 (the R side of the Gram eigenproblem).  tau == 0
+ *               returns m unchanged (linops.cpp:80-81).  *kept = #sigma > tau.
+ *   procrustes: U = polar(g v^T) for g (I x P), v (R x P), R <= 64.  Returns
+ *               *degenerate = 1 and leaves u_out untouched when
+ *               ||g v^T||_F <= 1e-14 max(1, ||g||_F ||v||_F) (linops.cpp:99-101).
+ *               u_prev (I x R, may be NULL = identity) seeds the deterministic
+ *               completion of numerically null directions. */
+int pasd_b200_svt(const double* m, int64_t rows, int64_t cols, double tau, double* out, int32_t* kept,
+                  int32_t device, char* errbuf, size_t errlen);
+int pasd_b200_procrustes(const double* g, int64_t i_rows, int64_t p_cols, const double* v, int64_t r_rows,
+                         const double* u_prev, double* u_out, int32_t* degenerate, int32_t* rank, int32_t device,
+                         char* errbuf, size_t errlen);
+
+/* Library / build identification. */
+int pasd_b200_abi_version(void);
+const char* pasd_b200_build_info(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* PASD_B200_H */

@@ -1,0 +1,853 @@
+// =============================================================================
+// pasd_oracle.cpp — CPU RESTATEMENT OF THE REFERENCE PASD SOLVER.
+//
+// TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and the
+// cpu_baseline / --impl reference legs of bench.py may load this library, and
+// only as the checker or the timed CPU baseline — never as the product path.
+//
+// What it restates (file:line under /root/reference):
+//   * PasdConfig::validate / default_lambdas / default_rank_bound  pasd.cpp:12-66
+//   * the ADMM loop pasd_recover, exact elementwise op order        pasd.cpp:132-275
+//   * update_u_from / update_v_from                                  pasd.cpp:70-78
+//   * suboptimality_certificate                                      pasd.cpp:277-309
+//   * thin_svd (LAPACKE dgesdd 'S') + sign convention, svt,
+//     procrustes (1e-14 degenerate rule), soft_threshold, shrink     linops.cpp:25-113, linops.hpp:37-43
+//   * unfold_into / fold_into index maps                             tensor.cpp:98-127
+//   * weighted_mean                                                  recovery.cpp:7-25
+//   * splitmix64 / derive_seed / RngStream                           rng.hpp:17-79
+//   * gen_lowrank_tucker (Haar factors), corrupt_sparse              synth.cpp:40-121
+//
+// Third-party arithmetic: the reference uses Eigen3 (>=3.3, unpinned;
+// proj/CMakeLists.txt:12) for GEMM/transposes/norms and LAPACKE dgesdd
+// (unpinned; linops.cpp:62).  Neither Eigen nor lapacke.h exists in this image,
+// so the reference is UNBUILDABLE here.  This restatement uses the OpenBLAS
+// 0.3.31.dev bundled with scipy (scipy_dgemm_, scipy_LAPACKE_dgesdd) pinned to
+// one thread exactly like linops.cpp:17-23.  Parity is PINNED against the
+// reference's own known-answer examples and
+// UNPINNED at the Eigen/LAPACK summation-order boundary: GEMM results differ
+// from Eigen's at ULP level.  Elementwise ops follow the reference's operation
+// order exactly and are compiled with -ffp-contract=off (the reference is built
+// without -march, so GCC emits no FMA: proj/src/CMakeLists.txt:14).
+// =============================================================================
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+#include <cstdio>
+#include <cstring>
+#include <limits>
+#include <numeric>
+#include <random>
+#include <stdexcept>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "../include/pasd_b200.h"
+
+// ---------------------------------------------------------------- BLAS/LAPACK
+extern "C" {
+void scipy_dgemm_(const char* ta, const char* tb, const int* m, const int* n, const int* k,
+                  const double* alpha, const double* a, const int* lda, const double* b,
+                  const int* ldb, const double* beta, double* c, const int* ldc, size_t, size_t);
+int scipy_LAPACKE_dgesdd(int layout, char jobz, int m, int n, double* a, int lda, double* s,
+                         double* u, int ldu, double* vt, int ldvt);
+int scipy_LAPACKE_dgesvd(int layout, char jobu, char jobvt, int m, int n, double* a, int lda,
+                         double* s, double* u, int ldu, double* vt, int ldvt, double* superb);
+int scipy_LAPACKE_dgeqrf(int layout, int m, int n, double* a, int lda, double* tau);
+int scipy_LAPACKE_dorgqr(int layout, int m, int n, int k, double* a, int lda, const double* tau);
+void scipy_openblas_set_num_threads(int);
+}
+static constexpr int kColMajor = 102;
+
+namespace oracle {
+
+using Index = std::int64_t;
+
+struct ArgumentError : std::invalid_argument { using std::invalid_argument::invalid_argument; };
+struct NumericalError : std::runtime_error { using std::runtime_error::runtime_error; };
+struct StateError : std::logic_error { using std::logic_error::logic_error; };
+
+// Column-major dense matrix (the reference's Eigen::MatrixXd, tensor.hpp:14-15).
+struct Matrix {
+  Index rows = 0, cols = 0;
+  std::vector<double> d;
+  Matrix() = default;
+  Matrix(Index r, Index c, double fill = 0.0) : rows(r), cols(c), d(size_t(r * c), fill) {}
+  double& operator()(Index i, Index j) { return d[size_t(i + rows * j)]; }
+  double operator()(Index i, Index j) const { return d[size_t(i + rows * j)]; }
+  double* data() { return d.data(); }
+  const double* data() const { return d.data(); }
+  static Matrix eye(Index r, Index c) {
+    Matrix m(r, c);
+    for (Index j = 0; j < std::min(r, c); ++j) m(j, j) = 1.0;
+    return m;
+  }
+  double norm() const {  // Frobenius
+    double s = 0.0;
+    for (double x : d) s += x * x;
+    return std::sqrt(s);
+  }
+  bool all_finite() const {
+    for (double x : d)
+      if (!std::isfinite(x)) return false;
+    return true;
+  }
+};
+
+static int g_threads = 1;
+
+// Static-partition parallel loop over [0, n) on g_threads std::threads (no
+// OpenMP runtime in this image).  Elementwise results do not depend on it.
+template <class F>
+static void par_for(Index n, F&& f) {
+  const int T = g_threads;
+  if (T <= 1 || n < 65536) {
+    f(Index(0), n, 0);
+    return;
+  }
+  std::vector<std::thread> th;
+  for (int k = 0; k < T; ++k) {
+    const Index b = n * k / T, e = n * (k + 1) / T;
+    th.emplace_back([&f, b, e, k] { f(b, e, k); });
+  }
+  for (auto& t : th) t.join();
+}
+
+// C = op(A) op(B), using one-thread OpenBLAS (stand-in for Eigen's GEMM).
+static Matrix gemm(const Matrix& a, bool ta, const Matrix& b, bool tb) {
+  const int m = int(ta ? a.cols : a.rows), k = int(ta ? a.rows : a.cols);
+  const int n = int(tb ? b.rows : b.cols);
+  Matrix c(m, n);
+  if (m == 0 || n == 0) return c;
+  if (k == 0) return c;
+  const double one = 1.0, zero = 0.0;
+  const int lda = std::max<int>(1, int(a.rows)), ldb = std::max<int>(1, int(b.rows)), ldc = std::max(1, m);
+  scipy_dgemm_(ta ? "T" : "N", tb ? "T" : "N", &m, &n, &k, &one, a.data(), &lda, b.data(), &ldb,
+               &zero, c.data(), &ldc, 1, 1);
+  return c;
+}
+
+// ------------------------------------------------------------------ tensor.cpp
+static Index dims_product(const std::vector<Index>& dims) {  // tensor.cpp:9-23
+  if (dims.empty()) throw ArgumentError("tensor order must be at least 1");
+  Index prod = 1;
+  for (size_t n = 0; n < dims.size(); ++n) {
+    const Index d = dims[n];
+    if (d < 1)
+      throw ArgumentError("dimension " + std::to_string(n + 1) + " must be positive, got " +
+                          std::to_string(d));
+    if (prod > std::numeric_limits<Index>::max() / d) throw ArgumentError("dimension product overflows");
+    prod *= d;
+  }
+  return prod;
+}
+
+struct ModeSplit { Index inner, mode_dim, outer; };
+static ModeSplit split_dims(const std::vector<Index>& dims, Index mode) {  // tensor.cpp:87-94
+  ModeSplit s{1, dims[size_t(mode - 1)], 1};
+  for (Index l = 0; l < mode - 1; ++l) s.inner *= dims[size_t(l)];
+  for (Index l = mode; l < Index(dims.size()); ++l) s.outer *= dims[size_t(l)];
+  return s;
+}
+
+// tensor.cpp:98-113: entry (p, r, q) at p + inner*r + slab*q -> row r, col p + inner*q.
+static void unfold_into(const double* src, const std::vector<Index>& dims, Index mode, double* dst) {
+  const ModeSplit s = split_dims(dims, mode);
+  const Index slab = s.inner * s.mode_dim;
+  if (s.inner == 1) {
+    std::memcpy(dst, src, size_t(slab * s.outer) * sizeof(double));
+    return;
+  }
+  par_for(s.outer, [&](Index qb, Index qe, int) {
+    for (Index q = qb; q < qe; ++q)
+      for (Index p = 0; p < s.inner; ++p)
+        for (Index r = 0; r < s.mode_dim; ++r)
+          dst[q * slab + r + s.mode_dim * p] = src[q * slab + p + s.inner * r];
+  });
+}
+
+// tensor.cpp:115-127 (inverse map).
+static void fold_into(const double* src, const std::vector<Index>& dims, Index mode, double* dst) {
+  const ModeSplit s = split_dims(dims, mode);
+  const Index slab = s.inner * s.mode_dim;
+  if (s.inner == 1) {
+    std::memcpy(dst, src, size_t(slab * s.outer) * sizeof(double));
+    return;
+  }
+  par_for(s.outer, [&](Index qb, Index qe, int) {
+    for (Index q = qb; q < qe; ++q)
+      for (Index r = 0; r < s.mode_dim; ++r)
+        for (Index p = 0; p < s.inner; ++p)
+          dst[q * slab + p + s.inner * r] = src[q * slab + r + s.mode_dim * p];
+  });
+}
+
+// ------------------------------------------------------------------ linops.cpp
+struct ThinSvd { Matrix u; std::vector<double> s; Matrix v; };
+
+static int g_svd_variant = 0;  // 0 = dgesdd (reference), 1 = dgesvd (parity-floor probe)
+
+static void pin_blas_threads() { scipy_openblas_set_num_threads(g_threads); }  // linops.cpp:17-23
+
+static void apply_sign_convention(Matrix& u, Matrix& v) {  // linops.cpp:25-41
+  for (Index j = 0; j < u.cols; ++j) {
+    Index pivot = 0;
+    double best = std::abs(u(0, j));
+    for (Index i = 1; i < u.rows; ++i) {
+      const double a = std::abs(u(i, j));
+      if (a > best) {
+        best = a;
+        pivot = i;
+      }
+    }
+    if (u(pivot, j) < 0.0) {
+      for (Index i = 0; i < u.rows; ++i) u(i, j) = -u(i, j);
+      for (Index i = 0; i < v.rows; ++i) v(i, j) = -v(i, j);
+    }
+  }
+}
+
+static ThinSvd thin_svd(const Matrix& m) {  // linops.cpp:45-72
+  if (m.rows < 1 || m.cols < 1) throw ArgumentError("thin_svd: matrix must be nonempty");
+  if (!m.all_finite()) throw ArgumentError("thin_svd: input contains non-finite entries");
+  pin_blas_threads();
+  const int rows = int(m.rows), cols = int(m.cols), k = std::min(rows, cols);
+  Matrix work = m;
+  ThinSvd out;
+  out.u = Matrix(rows, k);
+  out.s.assign(static_cast<size_t>(k), 0.0);
+  Matrix vt(k, cols);
+  int info;
+  if (g_svd_variant == 1) {
+    std::vector<double> superb(size_t(std::max(1, k - 1)));
+    info = scipy_LAPACKE_dgesvd(kColMajor, 'S', 'S', rows, cols, work.data(), rows, out.s.data(),
+                                out.u.data(), rows, vt.data(), k, superb.data());
+  } else {
+    info = scipy_LAPACKE_dgesdd(kColMajor, 'S', rows, cols, work.data(), rows, out.s.data(),
+                                out.u.data(), rows, vt.data(), k);
+  }
+  if (info > 0)
+    throw NumericalError("thin_svd: dgesdd did not converge (info=" + std::to_string(info) + ")");
+  if (info < 0) throw ArgumentError("thin_svd: bad argument " + std::to_string(-info) + " to dgesdd");
+  out.v = Matrix(cols, k);
+  for (Index i = 0; i < k; ++i)
+    for (Index j = 0; j < cols; ++j) out.v(j, i) = vt(i, j);
+  apply_sign_convention(out.u, out.v);
+  return out;
+}
+
+static double nuclear_norm(const Matrix& m) {  // linops.cpp:74-76
+  const ThinSvd s = thin_svd(m);
+  double acc = 0.0;
+  for (double x : s.s) acc += x;
+  return acc;
+}
+
+static Matrix svt(const Matrix& m, double tau, Index* kept = nullptr) {  // linops.cpp:78-91
+  if (tau < 0.0 || !std::isfinite(tau)) throw ArgumentError("svt: threshold must be a nonnegative finite number");
+  if (tau == 0.0) return m;
+  const ThinSvd svd = thin_svd(m);
+  Index keep = 0;
+  while (keep < Index(svd.s.size()) && svd.s[size_t(keep)] > tau) ++keep;
+  if (kept) *kept = keep;
+  if (keep == 0) return Matrix(m.rows, m.cols);
+  // u_k * diag(s_k - tau) * v_k^T
+  Matrix us(m.rows, keep);
+  for (Index j = 0; j < keep; ++j) {
+    const double sh = svd.s[size_t(j)] - tau;
+    for (Index i = 0; i < m.rows; ++i) us(i, j) = svd.u(i, j) * sh;
+  }
+  Matrix vk(m.cols, keep);
+  for (Index j = 0; j < keep; ++j)
+    for (Index i = 0; i < m.cols; ++i) vk(i, j) = svd.v(i, j);
+  return gemm(us, false, vk, true);
+}
+
+// linops.cpp:93-104; returns false for the degenerate case.
+static bool procrustes(const Matrix& g, const Matrix& v, Matrix& u_out) {
+  if (g.cols != v.cols) throw ArgumentError("procrustes: g and v must have the same number of columns");
+  if (v.rows > g.rows) throw ArgumentError("procrustes: v has more rows than g (R must not exceed I)");
+  const Matrix w = gemm(g, false, v, true);
+  const double scale = std::max(1.0, g.norm() * v.norm());
+  if (w.norm() <= 1e-14 * scale) return false;
+  const ThinSvd svd = thin_svd(w);
+  u_out = gemm(svd.u, false, svd.v, true);
+  return true;
+}
+
+static inline double soft_threshold(double x, double tau) {  // linops.hpp:37-43
+  if (x > tau) return x - tau;
+  if (x < -tau) return x + tau;
+  return 0.0;
+}
+
+// -------------------------------------------------------------------- pasd.cpp
+struct Config {
+  std::vector<double> lambdas;
+  std::vector<Index> ranks;
+  double mu0 = 1e-4, mu_max = 1e10, rho = 1.1, eps = 1e-5;
+  int maxiter = 1000;
+  std::vector<double> output_weights;
+  bool fixed_iters = false;
+  const std::vector<double>& alphas() const { return output_weights.empty() ? lambdas : output_weights; }
+};
+
+static void validate(const Config& c, const std::vector<Index>& dims) {  // pasd.cpp:12-49
+  const size_t n_modes = dims.size();
+  dims_product(dims);
+  if (c.lambdas.size() != n_modes)
+    throw ArgumentError("config: expected " + std::to_string(n_modes) + " lambdas, got " +
+                        std::to_string(c.lambdas.size()));
+  for (size_t n = 0; n < n_modes; ++n)
+    if (!(c.lambdas[n] > 0.0) || !std::isfinite(c.lambdas[n]))
+      throw ArgumentError("config: lambda of mode " + std::to_string(n + 1) + " must be positive");
+  if (c.ranks.size() != n_modes)
+    throw ArgumentError("config: expected " + std::to_string(n_modes) + " ranks, got " +
+                        std::to_string(c.ranks.size()));
+  for (size_t n = 0; n < n_modes; ++n) {
+    if (c.ranks[n] < 1) throw ArgumentError("config: rank of mode " + std::to_string(n + 1) + " must be positive");
+    if (c.ranks[n] > dims[n])
+      throw ArgumentError("config: rank " + std::to_string(c.ranks[n]) + " exceeds dimension " +
+                          std::to_string(dims[n]) + " in mode " + std::to_string(n + 1));
+  }
+  if (!(c.mu0 > 0.0) || !std::isfinite(c.mu0)) throw ArgumentError("config: mu0 must be positive");
+  if (!(c.mu_max >= c.mu0)) throw ArgumentError("config: mu_max must be at least mu0");
+  if (!(c.rho > 1.0) || !std::isfinite(c.rho)) throw ArgumentError("config: rho must exceed 1");
+  if (!(c.eps > 0.0)) throw ArgumentError("config: eps must be positive");
+  if (c.maxiter < 1) throw ArgumentError("config: maxiter must be positive");
+  if (!c.output_weights.empty()) {
+    if (c.output_weights.size() != n_modes)
+      throw ArgumentError("config: expected " + std::to_string(n_modes) + " output weights");
+    for (size_t n = 0; n < n_modes; ++n)
+      if (!(c.output_weights[n] > 0.0) || !std::isfinite(c.output_weights[n]))
+        throw ArgumentError("config: output weight of mode " + std::to_string(n + 1) + " must be positive");
+  }
+}
+
+struct Result {
+  std::vector<double> x, e;
+  std::vector<std::vector<double>> z, y, y_hat;
+  int iters = 0;
+  bool converged = false;
+  std::vector<double> residual_history, final_residuals;
+  double objective = 0.0;
+  bool has_cert = false;
+  double eps_hat = 0, c = 0, bound = 0;
+};
+
+struct Observer {
+  pasd_observer_fn fn = nullptr;
+  void* user = nullptr;
+};
+
+static void certificate(Result& res, const double* t, Index total, size_t n_modes, const Config& cfg) {
+  // pasd.cpp:277-309
+  if (!res.converged) throw StateError("certificate requires a converged result");
+  std::vector<double> acc(static_cast<size_t>(total), 0.0);
+  for (size_t n = 0; n < n_modes; ++n) {
+    const double* yd = res.y[n].data();
+    const double* hd = res.y_hat[n].data();
+    for (Index i = 0; i < total; ++i) acc[size_t(i)] += yd[i] - hd[i];
+  }
+  double eps_hat = 0.0;
+  for (double a : acc) eps_hat = std::max(eps_hat, std::fabs(a));
+  const int k_star = res.iters - 1;
+  const double geom = cfg.rho * (1.0 + cfg.rho) / (cfg.rho - 1.0) + 0.5 / std::pow(cfg.rho, k_star);
+  double dim_sum = 0.0, lam_term = 0.0;
+  for (size_t n = 0; n < n_modes; ++n) {
+    dim_sum += double(total);
+    lam_term += cfg.lambdas[n] * double(total) * cfg.eps;
+  }
+  const double nn = double(n_modes);
+  double l1 = 0.0;
+  for (Index i = 0; i < total; ++i) l1 += std::fabs(t[i]);
+  const double c = dim_sum * geom / (cfg.mu0 * nn * nn) + l1;
+  res.has_cert = true;
+  res.eps_hat = eps_hat;
+  res.c = c;
+  res.bound = c * eps_hat + lam_term;
+}
+
+static Result pasd_recover(const double* td, const std::vector<Index>& dims, const Config& cfg,
+                           const Observer& observer) {
+  validate(cfg, dims);  // pasd.cpp:134
+  const Index total = dims_product(dims);
+  for (Index i = 0; i < total; ++i)
+    if (!std::isfinite(td[i])) throw ArgumentError("pasd: input tensor contains non-finite entries");
+  const Index n_modes = Index(dims.size());
+
+  // pasd.cpp:143-166
+  double mu = cfg.mu0;
+  std::vector<double> e(static_cast<size_t>(total), 0.0);
+  std::vector<std::vector<double>> y(static_cast<size_t>(n_modes), std::vector<double>(static_cast<size_t>(total), 0.0));
+  std::vector<Matrix> u(static_cast<size_t>(n_modes)), v(static_cast<size_t>(n_modes));
+  for (Index n = 0; n < n_modes; ++n) {
+    const Index rows = dims[size_t(n)], rank = cfg.ranks[size_t(n)];
+    u[size_t(n)] = Matrix::eye(rows, rank);
+    v[size_t(n)] = Matrix(rank, total / rows);
+  }
+  std::vector<std::vector<double>> z(static_cast<size_t>(n_modes), std::vector<double>(static_cast<size_t>(total), 0.0));
+  std::vector<double> scratch(static_cast<size_t>(total), 0.0), e_prev(static_cast<size_t>(total), 0.0);
+  std::vector<double> resid(static_cast<size_t>(n_modes), std::numeric_limits<double>::infinity());
+  Result res;
+  res.residual_history.reserve(size_t(cfg.maxiter));
+  bool converged = false;
+  double mu_used = mu;
+  int iter = 0;
+  const int T = g_threads;
+
+  while (iter < cfg.maxiter && !converged) {  // pasd.cpp:168
+    mu_used = mu;
+    const double inv_mu = 1.0 / mu;
+    for (Index n = 0; n < n_modes; ++n) {  // pasd.cpp:175-191
+      const size_t ni = size_t(n);
+      const Index rows = dims[ni];
+      {
+        const double* ed = e.data();
+        const double* yd = y[ni].data();
+        double* sd = scratch.data();
+        par_for(total, [&](Index b, Index e_, int) {
+          for (Index i = b; i < e_; ++i) sd[i] = td[i] - ed[i] + yd[i] * inv_mu;
+        });
+      }
+      Matrix g(rows, total / rows);
+      unfold_into(scratch.data(), dims, n + 1, g.data());
+      Matrix un;
+      if (procrustes(g, v[ni], un)) u[ni] = std::move(un);              // update_u_from, pasd.cpp:70-74
+      v[ni] = svt(gemm(u[ni], true, g, false), cfg.lambdas[ni] / mu);   // update_v_from, pasd.cpp:76-78
+      const Matrix zmat = gemm(u[ni], false, v[ni], false);              // pasd.cpp:189
+      fold_into(zmat.data(), dims, n + 1, z[ni].data());
+    }
+    e_prev = e;  // pasd.cpp:194
+    {
+      double* sd = scratch.data();
+      std::fill(sd, sd + total, 0.0);
+      for (Index n = 0; n < n_modes; ++n) {
+        const double* zd = z[size_t(n)].data();
+        const double* yd = y[size_t(n)].data();
+        par_for(total, [&](Index b, Index e_, int) {
+          for (Index i = b; i < e_; ++i) sd[i] += td[i] - zd[i] + yd[i] * inv_mu;
+        });
+      }
+      const double inv_n = 1.0 / double(n_modes);
+      const double tau = 1.0 / (mu * double(n_modes));
+      double* ed = e.data();
+      par_for(total, [&](Index b, Index e_, int) {
+        for (Index i = b; i < e_; ++i) ed[i] = soft_threshold(sd[i] * inv_n, tau);
+      });
+    }
+    bool bad = false;  // pasd.cpp:211-228
+    for (Index n = 0; n < n_modes; ++n) {
+      const size_t ni = size_t(n);
+      const double* zd = z[ni].data();
+      const double* ed = e.data();
+      double* yd = y[ni].data();
+      std::vector<double> worst_t(size_t(std::max(1, T)), 0.0);
+      std::vector<int> bad_t(size_t(std::max(1, T)), 0);
+      par_for(total, [&](Index b, Index e_, int k) {
+        double worst = 0.0;
+        int nbad = 0;
+        for (Index i = b; i < e_; ++i) {
+          const double r = td[i] - zd[i] - ed[i];
+          yd[i] += mu * r;
+          const double a = std::fabs(r);
+          if (a > worst) worst = a;
+          nbad |= !std::isfinite(r);
+        }
+        worst_t[size_t(k)] = worst;
+        bad_t[size_t(k)] = nbad;
+      });
+      double worst = 0.0;
+      for (size_t k = 0; k < worst_t.size(); ++k) {
+        if (worst_t[k] > worst) worst = worst_t[k];
+        bad = bad || bad_t[k];
+      }
+      resid[ni] = worst;
+    }
+    const double mu_next = std::min(cfg.rho * mu, cfg.mu_max);
+    ++iter;
+    if (bad) throw NumericalError("pasd: non-finite iterate at iteration " + std::to_string(iter));
+    res.residual_history.push_back(*std::max_element(resid.begin(), resid.end()));
+    converged = true;
+    for (double r : resid) converged = converged && (r < cfg.eps);
+    if (cfg.fixed_iters) converged = false;
+    mu = mu_next;
+    if (observer.fn) {
+      std::vector<const double*> zp, yp, up, vp;
+      for (Index n = 0; n < n_modes; ++n) {
+        zp.push_back(z[size_t(n)].data());
+        yp.push_back(y[size_t(n)].data());
+        up.push_back(u[size_t(n)].data());
+        vp.push_back(v[size_t(n)].data());
+      }
+      pasd_iteration_view view{iter, mu_used, mu_next, resid.data(), e.data(), zp.data(), yp.data(),
+                               up.data(), vp.data()};
+      observer.fn(&view, observer.user);
+    }
+  }
+
+  // pasd.cpp:246-258
+  std::vector<std::vector<double>> y_hat(static_cast<size_t>(n_modes), std::vector<double>(static_cast<size_t>(total), 0.0));
+  for (Index n = 0; n < n_modes; ++n) {
+    const double* yd = y[size_t(n)].data();
+    double* hd = y_hat[size_t(n)].data();
+    for (Index i = 0; i < total; ++i) hd[i] = yd[i] + mu_used * (e[size_t(i)] - e_prev[size_t(i)]);
+  }
+  res.converged = converged;
+  res.iters = iter;
+  res.final_residuals = resid;
+  double l1 = 0.0;
+  for (double x : e) l1 += std::fabs(x);
+  res.objective = l1;
+  for (Index n = 0; n < n_modes; ++n) res.objective += cfg.lambdas[size_t(n)] * nuclear_norm(v[size_t(n)]);
+  // recovery.cpp:7-25
+  const std::vector<double>& w = cfg.alphas();
+  double wsum = 0.0;
+  for (double x : w) wsum += x;
+  res.x.assign(static_cast<size_t>(total), 0.0);
+  for (Index n = 0; n < n_modes; ++n) {
+    const double c = w[size_t(n)] / wsum;
+    const double* zd = z[size_t(n)].data();
+    for (Index i = 0; i < total; ++i) res.x[size_t(i)] = res.x[size_t(i)] + c * zd[i];
+  }
+  res.e = std::move(e);
+  res.z = std::move(z);
+  res.y = std::move(y);
+  res.y_hat = std::move(y_hat);
+  if (converged) certificate(res, td, total, static_cast<size_t>(n_modes), cfg);
+  return res;
+}
+
+// -------------------------------------------------------------- rng.hpp/synth
+static constexpr std::uint64_t splitmix64(std::uint64_t x) {  // rng.hpp:17-22
+  x += 0x9e3779b97f4a7c15ULL;
+  x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  x = (x ^ (x >> 27)) * 0x94d049bb133111ebULL;
+  return x ^ (x >> 31);
+}
+static constexpr std::uint64_t derive_seed(std::uint64_t seed, std::uint64_t stream, std::uint64_t purpose) {
+  return splitmix64(splitmix64(splitmix64(seed) ^ stream) ^ (purpose * 0x2545f4914f6cdd1dULL));
+}
+struct RngStream {  // rng.hpp:37-79
+  std::mt19937_64 engine;
+  bool have_spare = false;
+  double spare = 0.0;
+  RngStream(std::uint64_t seed, std::uint64_t stream, std::uint64_t purpose)
+      : engine(derive_seed(seed, stream, purpose)) {}
+  std::uint64_t next_u64() { return engine(); }
+  double uniform01() { return double(next_u64() >> 11) * 0x1.0p-53; }
+  double uniform(double lo, double hi) { return lo + (hi - lo) * uniform01(); }
+  std::uint64_t below(std::uint64_t n) {
+    const std::uint64_t limit = UINT64_MAX - UINT64_MAX % n;
+    std::uint64_t x;
+    do x = next_u64();
+    while (x >= limit);
+    return x % n;
+  }
+  double gaussian() {
+    if (have_spare) {
+      have_spare = false;
+      return spare;
+    }
+    const double u1 = double((next_u64() >> 11) + 1) * 0x1.0p-53;
+    const double u2 = uniform01();
+    const double r = std::sqrt(-2.0 * std::log(u1));
+    const double a = 6.283185307179586476925286766559 * u2;
+    spare = r * std::sin(a);
+    have_spare = true;
+    return r * std::cos(a);
+  }
+};
+namespace purpose {  // rng.hpp:28-35, plus tags for the BASELINE C3/C4 recipes
+constexpr std::uint64_t core = 1, support = 2, noise = 3, factor = 16;
+constexpr std::uint64_t block_support = 64, block_noise = 65;  // C4 foreground (new)
+}
+
+// Haar factor: Q of a Gaussian matrix's QR, sign-fixed by diag(R) (synth.cpp:40-53).
+// kind 1 (C4 recipe): |N(0,1)| entries, columns l2-normalised (not orthonormal).
+static Matrix factor_matrix(Index rows, Index cols, RngStream& rng, int kind) {
+  Matrix a(rows, cols);
+  for (Index j = 0; j < cols; ++j)
+    for (Index i = 0; i < rows; ++i) a(i, j) = rng.gaussian();
+  if (kind == 1) {
+    for (Index j = 0; j < cols; ++j) {
+      double s = 0.0;
+      for (Index i = 0; i < rows; ++i) {
+        a(i, j) = std::fabs(a(i, j));
+        s += a(i, j) * a(i, j);
+      }
+      s = std::sqrt(s);
+      for (Index i = 0; i < rows; ++i) a(i, j) /= s;
+    }
+    return a;
+  }
+  std::vector<double> tau(static_cast<size_t>(cols));
+  if (scipy_LAPACKE_dgeqrf(kColMajor, int(rows), int(cols), a.data(), int(rows), tau.data()) != 0)
+    throw NumericalError("dgeqrf failed");
+  std::vector<double> rdiag(static_cast<size_t>(cols));
+  for (Index j = 0; j < cols; ++j) rdiag[size_t(j)] = a(j, j);
+  if (scipy_LAPACKE_dorgqr(kColMajor, int(rows), int(cols), int(cols), a.data(), int(rows), tau.data()) != 0)
+    throw NumericalError("dorgqr failed");
+  for (Index j = 0; j < cols; ++j)
+    if (rdiag[size_t(j)] < 0.0)
+      for (Index i = 0; i < rows; ++i) a(i, j) = -a(i, j);
+  return a;
+}
+
+// tensor.cpp:162-172: fold(m * unfold(t, mode), mode, new_dims).
+static std::vector<double> mode_product(const std::vector<double>& t, std::vector<Index>& dims,
+                                        const Matrix& m, Index mode) {
+  const Index rows = dims[size_t(mode - 1)];
+  const Index total = dims_product(dims);
+  Matrix unf(rows, total / rows);
+  unfold_into(t.data(), dims, mode, unf.data());
+  const Matrix prod = gemm(m, false, unf, false);
+  dims[size_t(mode - 1)] = m.rows;
+  std::vector<double> out(size_t(dims_product(dims)));
+  fold_into(prod.data(), dims, mode, out.data());
+  return out;
+}
+
+}  // namespace oracle
+
+// ======================================================================= C ABI
+using namespace oracle;
+
+static int set_err(char* buf, size_t len, const char* msg) {
+  if (buf && len) {
+    std::snprintf(buf, len, "%s", msg);
+  }
+  return 0;
+}
+
+template <class F>
+static int guarded(char* err, size_t errlen, F&& f) {
+  try {
+    f();
+    return PASD_OK;
+  } catch (const ArgumentError& e) {
+    set_err(err, errlen, e.what());
+    return PASD_ERR_ARGUMENT;
+  } catch (const NumericalError& e) {
+    set_err(err, errlen, e.what());
+    return PASD_ERR_NUMERICAL;
+  } catch (const StateError& e) {
+    set_err(err, errlen, e.what());
+    return PASD_ERR_STATE;
+  } catch (const std::exception& e) {
+    set_err(err, errlen, e.what());
+    return PASD_ERR_NUMERICAL;
+  }
+}
+
+static std::vector<Index> to_dims(int order, const int64_t* dims) {
+  std::vector<Index> d;
+  for (int i = 0; i < order; ++i) d.push_back(dims[i]);
+  return d;
+}
+
+extern "C" {
+
+// Full reference-restated solve.  svd_variant: 0 = dgesdd (reference), 1 = dgesvd.
+// threads: OpenBLAS + elementwise-loop threads (1 = the reference's setting).
+int oracle_pasd_recover(const double* t, const pasd_options* opt, pasd_outputs* out,
+                        pasd_observer_fn obs, void* user, int svd_variant, int threads, char* err,
+                        size_t errlen) {
+  return guarded(err, errlen, [&] {
+    if (!opt || opt->order < 1) throw ArgumentError("tensor order must be at least 1");
+    g_svd_variant = svd_variant;
+    g_threads = std::max(1, threads);
+    scipy_openblas_set_num_threads(g_threads);
+    const std::vector<Index> dims = to_dims(opt->order, opt->dims);
+    Config cfg;
+    for (int n = 0; n < opt->order; ++n) {
+      cfg.lambdas.push_back(opt->lambdas[n]);
+      cfg.ranks.push_back(opt->ranks[n]);
+      if (opt->output_weights) cfg.output_weights.push_back(opt->output_weights[n]);
+    }
+    cfg.mu0 = opt->mu0;
+    cfg.mu_max = opt->mu_max;
+    cfg.rho = opt->rho;
+    cfg.eps = opt->eps;
+    cfg.maxiter = opt->maxiter;
+    cfg.fixed_iters = (opt->flags & PASD_FLAG_FIXED_ITERS) != 0;
+    Observer o{obs, user};
+    Result r = pasd_recover(t, dims, cfg, o);
+    const size_t total = r.e.size();
+    auto put = [&](double* dst, const std::vector<double>& src) {
+      if (dst) std::memcpy(dst, src.data(), total * sizeof(double));
+    };
+    put(out->x, r.x);
+    put(out->e, r.e);
+    for (int n = 0; n < opt->order; ++n) {
+      if (out->z) put(out->z[n], r.z[size_t(n)]);
+      if (out->y) put(out->y[n], r.y[size_t(n)]);
+      if (out->y_hat) put(out->y_hat[n], r.y_hat[size_t(n)]);
+      if (out->final_residuals) out->final_residuals[n] = r.final_residuals[size_t(n)];
+    }
+    if (out->residual_history)
+      std::memcpy(out->residual_history, r.residual_history.data(), r.residual_history.size() * sizeof(double));
+    out->iters = r.iters;
+    out->converged = r.converged;
+    out->objective = r.objective;
+    out->has_certificate = r.has_cert;
+    out->cert_epsilon_hat = r.eps_hat;
+    out->cert_c = r.c;
+    out->cert_bound = r.bound;
+  });
+}
+
+// Reference generator gen_lowrank_tucker (synth.cpp:71-89) without the rank
+// verification SVD; kind 0 = Haar factors + N(0,1) core (reference), kind 1 =
+// non-negative C4 recipe (|N(0,1)| core and column-normalised |N(0,1)| factors,
+// rescaled by 1/max into [0,1]).
+int oracle_gen_tucker(int order, const int64_t* dims, const int64_t* ranks, uint64_t seed, int kind,
+                      double* out, char* err, size_t errlen) {
+  return guarded(err, errlen, [&] {
+    g_threads = 1;
+    scipy_openblas_set_num_threads(1);
+    std::vector<Index> cur = to_dims(order, ranks);
+    const Index core_size = dims_product(cur);
+    RngStream core_rng(seed, 0, purpose::core);
+    std::vector<double> t(static_cast<size_t>(core_size));
+    for (double& x : t) x = core_rng.gaussian();
+    if (kind == 1)
+      for (double& x : t) x = std::fabs(x);
+    for (int n = 0; n < order; ++n) {
+      RngStream frng(seed, 0, purpose::factor + uint64_t(n) + 1);
+      const Matrix q = factor_matrix(dims[n], ranks[n], frng, kind);
+      t = mode_product(t, cur, q, n + 1);
+    }
+    if (kind == 1) {
+      double mx = 0.0;
+      for (double x : t) mx = std::max(mx, x);
+      if (mx > 0.0)
+        for (double& x : t) x = x / mx;
+    }
+    std::memcpy(out, t.data(), t.size() * sizeof(double));
+  });
+}
+
+// corrupt_sparse (synth.cpp:91-121) generalised: mode 0 adds U[lo,hi]
+// (reference: lo=-1, hi=1), mode 1 replaces with U[lo,hi] (reference: 0..255).
+int oracle_corrupt_sparse(const double* t, int64_t total, double rho, uint64_t seed, int mode, double lo,
+                          double hi, double* out, int64_t* count_out, char* err, size_t errlen) {
+  return guarded(err, errlen, [&] {
+    if (!(rho >= 0.0 && rho <= 1.0)) throw ArgumentError("corrupt_sparse: rho must lie in [0, 1]");
+    const Index count = Index(std::llround(rho * double(total)));
+    std::memcpy(out, t, static_cast<size_t>(total) * sizeof(double));
+    if (count_out) *count_out = count;
+    if (count == 0) return;
+    RngStream support_rng(seed, 0, purpose::support);
+    std::vector<Index> pool(static_cast<size_t>(total));
+    std::iota(pool.begin(), pool.end(), Index{0});
+    for (Index i = 0; i < count; ++i) {
+      const Index j = i + Index(support_rng.below(uint64_t(total - i)));
+      std::swap(pool[size_t(i)], pool[size_t(j)]);
+    }
+    pool.resize(size_t(count));
+    std::sort(pool.begin(), pool.end());
+    RngStream noise_rng(seed, 0, purpose::noise);
+    for (Index idx : pool) {
+      if (mode == 0)
+        out[idx] += noise_rng.uniform(lo, hi);
+      else
+        out[idx] = noise_rng.uniform(lo, hi);
+    }
+  });
+}
+
+// C4 foreground: per frame (last mode), `cells` of the aligned block x block
+// cells of the (mode-1 x mode-2) plane, drawn without replacement, replaced by
+// U[lo,hi].  New recipe (BASELINE configs[3]); purposes 64/65.
+int oracle_corrupt_blocks(const double* t, int order, const int64_t* dims, int64_t block, int64_t cells,
+                          uint64_t seed, double lo, double hi, double* out, char* err, size_t errlen) {
+  return guarded(err, errlen, [&] {
+    if (order != 3) throw ArgumentError("corrupt_blocks: order-3 tensors only");
+    const Index i1 = dims[0], i2 = dims[1], i3 = dims[2];
+    const Index c1 = i1 / block, c2 = i2 / block, ncell = c1 * c2;
+    if (cells > ncell) throw ArgumentError("corrupt_blocks: too many cells");
+    const Index total = i1 * i2 * i3;
+    std::memcpy(out, t, static_cast<size_t>(total) * sizeof(double));
+    RngStream srng(seed, 0, purpose::block_support);
+    RngStream nrng(seed, 0, purpose::block_noise);
+    std::vector<Index> pool(static_cast<size_t>(ncell));
+    for (Index k = 0; k < i3; ++k) {
+      std::iota(pool.begin(), pool.end(), Index{0});
+      for (Index i = 0; i < cells; ++i) {
+        const Index j = i + Index(srng.below(uint64_t(ncell - i)));
+        std::swap(pool[size_t(i)], pool[size_t(j)]);
+      }
+      std::vector<Index> chosen(pool.begin(), pool.begin() + cells);
+      std::sort(chosen.begin(), chosen.end());
+      for (Index cidx : chosen) {
+        const Index b1 = cidx % c1, b2 = cidx / c1;
+        for (Index jj = 0; jj < block; ++jj)
+          for (Index ii = 0; ii < block; ++ii) {
+            const Index off = (b1 * block + ii) + i1 * ((b2 * block + jj) + i2 * k);
+            out[off] = nrng.uniform(lo, hi);
+          }
+      }
+    }
+  });
+}
+
+// ---- single-op entry points for the known-answer tests (SPEC.md examples) ---
+int oracle_unfold(const double* t, int order, const int64_t* dims, int mode, double* out, char* err,
+                  size_t errlen) {
+  return guarded(err, errlen, [&] {
+    const std::vector<Index> d = to_dims(order, dims);
+    dims_product(d);
+    if (mode < 1 || mode > order)
+      throw ArgumentError("mode " + std::to_string(mode) + " out of range 1.." + std::to_string(order));
+    unfold_into(t, d, mode, out);
+  });
+}
+int oracle_fold(const double* m, int order, const int64_t* dims, int mode, double* out, char* err,
+                size_t errlen) {
+  return guarded(err, errlen, [&] {
+    const std::vector<Index> d = to_dims(order, dims);
+    dims_product(d);
+    if (mode < 1 || mode > order)
+      throw ArgumentError("mode " + std::to_string(mode) + " out of range 1.." + std::to_string(order));
+    fold_into(m, d, mode, out);
+  });
+}
+int oracle_thin_svd(const double* m, int64_t rows, int64_t cols, double* u, double* s, double* v, char* err,
+                    size_t errlen) {
+  return guarded(err, errlen, [&] {
+    Matrix a(rows, cols);
+    std::memcpy(a.data(), m, size_t(rows * cols) * sizeof(double));
+    g_threads = 1;
+    ThinSvd r = thin_svd(a);
+    std::memcpy(u, r.u.data(), r.u.d.size() * sizeof(double));
+    std::memcpy(s, r.s.data(), r.s.size() * sizeof(double));
+    std::memcpy(v, r.v.data(), r.v.d.size() * sizeof(double));
+  });
+}
+int oracle_svt(const double* m, int64_t rows, int64_t cols, double tau, double* out, char* err, size_t errlen) {
+  return guarded(err, errlen, [&] {
+    Matrix a(rows, cols);
+    std::memcpy(a.data(), m, size_t(rows * cols) * sizeof(double));
+    g_threads = 1;
+    Matrix r = svt(a, tau);
+    std::memcpy(out, r.data(), r.d.size() * sizeof(double));
+  });
+}
+// Returns 1 in *degenerate when procrustes signals the degenerate case.
+int oracle_procrustes(const double* g, int64_t i_rows, int64_t p_cols, const double* v, int64_t r_rows,
+                      double* out, int* degenerate, char* err, size_t errlen) {
+  return guarded(err, errlen, [&] {
+    Matrix gm(i_rows, p_cols), vm(r_rows, p_cols);
+    std::memcpy(gm.data(), g, size_t(i_rows * p_cols) * sizeof(double));
+    std::memcpy(vm.data(), v, size_t(r_rows * p_cols) * sizeof(double));
+    g_threads = 1;
+    Matrix u;
+    const bool ok = procrustes(gm, vm, u);
+    *degenerate = ok ? 0 : 1;
+    if (ok) std::memcpy(out, u.data(), u.d.size() * sizeof(double));
+  });
+}
+double oracle_soft_threshold(double x, double tau) { return soft_threshold(x, tau); }
+
+}  // extern "C"

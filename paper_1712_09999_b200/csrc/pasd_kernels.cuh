@@ -1,0 +1,436 @@
+// pasd_kernels.cuh — sm_100a kernels of one PASD ADMM iteration
+// (Algorithm 1; reference loop proj/src/pasd.cpp:168-244).
+//
+// Per iteration, in stream order (all scalars live in device memory, so the
+// sequence can be captured once as a CUDA graph and replayed):
+//   k_polar        Procrustes U_n <- polar(G_n V_n^T)          pasd.cpp:70-74,187; linops.cpp:93-104
+//   k_contract_A   A_n = U_n^T G_(n), G = (T-E)+Y_n/mu          pasd.cpp:77,178-186
+//   k_gram         Gram_n = A_n A_n^T (partials)                 (replaces dgesdd of A_n, linops.cpp:83)
+//   k_svt          eig(Gram_n) -> M_n with V_n = SVT(A_n)=M_n A_n linops.cpp:78-91
+//   k_update       Z_n refold + E shrink + Y ascent + residuals  pasd.cpp:189-228
+//   k_finish       mu schedule, history, stop rule               pasd.cpp:229-239
+//   k_contract_W   Wt_n = G_(n)^{next} A_n^T, ||G^{next}||^2     (next iteration's procrustes product)
+// Elementwise arithmetic that the reference performs on tensors uses explicit
+// round-to-nearest intrinsics (no FMA contraction), in the reference's
+// operation order, so E/Y are bit-identical whenever Z is.
+#pragma once
+#include <cuda_runtime.h>
+#include <math_constants.h>
+
+#include "pasd_common.cuh"
+
+namespace pasd {
+
+constexpr int kThreads = 256;
+
+__host__ __device__ __forceinline__ int64_t imin64(int64_t a, int64_t b) { return a < b ? a : b; }
+
+// G_n element: (T - E) + Y_n * inv_mu                          (pasd.cpp:183)
+__device__ __forceinline__ double g_elem(double t, double e, double y, double inv_mu) {
+  return __dadd_rn(__dsub_rn(t, e), __dmul_rn(y, inv_mu));
+}
+
+// soft_threshold (linops.hpp:37-43)
+__device__ __forceinline__ double soft(double x, double tau) {
+  if (x > tau) return __dsub_rn(x, tau);
+  if (x < -tau) return __dadd_rn(x, tau);
+  return 0.0;
+}
+
+__device__ __forceinline__ int64_t elem_offset(const ModeDev& m, int64_t kap, int64_t i) {
+  const int64_t q = kap / m.inner;
+  const int64_t p = kap - q * m.inner;
+  return p + m.inner * (i + m.I * q);
+}
+
+__device__ __forceinline__ int64_t a_offset(const ModeDev& m, int64_t kap, int r) {
+  const int64_t q = kap / m.inner;
+  const int64_t p = kap - q * m.inner;
+  return p + m.inner * ((int64_t)r + (int64_t)m.R * q);
+}
+
+// ---------------------------------------------------------------------------
+// Block reductions.
+// Fixed reduction tree (shuffle within warps, then warp 0 over warp sums), so
+// results are deterministic; `Op::identity()` pads the unused lanes.
+template <class T, class Op>
+__device__ T block_reduce(T v, Op op, T* sh) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+  for (int o = 16; o > 0; o >>= 1) v = op(v, __shfl_down_sync(0xffffffffu, v, o));
+  __syncthreads();
+  if (lane == 0) sh[wid] = v;
+  __syncthreads();
+  if (wid == 0) {
+    v = lane < nw ? sh[lane] : Op::identity();
+    for (int o = 16; o > 0; o >>= 1) v = op(v, __shfl_down_sync(0xffffffffu, v, o));
+    if (lane == 0) sh[0] = v;
+  }
+  __syncthreads();
+  T r = sh[0];
+  __syncthreads();
+  return r;
+}
+struct AddOp {
+  __device__ double operator()(double a, double b) const { return a + b; }
+  __device__ static double identity() { return 0.0; }
+};
+struct MaxOp {  // inputs are |x| >= 0
+  __device__ double operator()(double a, double b) const { return a > b ? a : b; }
+  __device__ static double identity() { return 0.0; }
+};
+struct OrOp {
+  __device__ int operator()(int a, int b) const { return a | b; }
+  __device__ static int identity() { return 0; }
+};
+
+// ---------------------------------------------------------------------------
+// Pass 1: A_n[kappa, r] = sum_i U_n[i, r] * G_n[kappa, i]  for 64 columns x all R.
+constexpr int CA_KT = 64;  // columns per CTA
+constexpr int CA_IC = 32;  // i chunk
+template <int RPT>
+__global__ void __launch_bounds__(kThreads) k_contract_A(ModeDev m, const double* __restrict__ T,
+                                                        const double* __restrict__ E0,
+                                                        const double* __restrict__ E1,
+                                                        const double* __restrict__ Y, const Ctl* ctl) {
+  if (ctl->done) return;
+  const double* __restrict__ E = ctl->ecur ? E1 : E0;
+  const double inv_mu = __ddiv_rn(1.0, ctl->mu);  // pasd.cpp:170
+  __shared__ double Gs[CA_IC][CA_KT + 1];
+  __shared__ double Us[CA_IC][PASD_MAX_RANK + 1];
+  const int tid = threadIdx.x, kl = tid % CA_KT, rg = tid / CA_KT;
+  const int64_t k0 = (int64_t)blockIdx.x * CA_KT;
+  double acc[RPT];
+#pragma unroll
+  for (int j = 0; j < RPT; ++j) acc[j] = 0.0;
+  for (int64_t i0 = 0; i0 < m.I; i0 += CA_IC) {
+    const int ic = (int)imin64(CA_IC, m.I - i0);
+    for (int idx = tid; idx < CA_IC * CA_KT; idx += kThreads) {
+      int il, kk;
+      if (m.inner > 1) { kk = idx % CA_KT; il = idx / CA_KT; }
+      else { il = idx % CA_IC; kk = idx / CA_IC; }
+      const int64_t kap = k0 + kk;
+      double v = 0.0;
+      if (kap < m.J && il < ic) {
+        const int64_t off = elem_offset(m, kap, i0 + il);
+        v = g_elem(T[off], E[off], Y[off], inv_mu);
+      }
+      Gs[il][kk] = v;
+    }
+    for (int idx = tid; idx < CA_IC * m.R; idx += kThreads) {
+      const int il = idx % CA_IC, r = idx / CA_IC;
+      Us[il][r] = il < ic ? m.U[i0 + il + m.I * r] : 0.0;
+    }
+    __syncthreads();
+    for (int il = 0; il < ic; ++il) {
+      const double g = Gs[il][kl];
+#pragma unroll
+      for (int j = 0; j < RPT; ++j) acc[j] = fma(g, Us[il][rg + 4 * j], acc[j]);
+    }
+    __syncthreads();
+  }
+  const int64_t kap = k0 + kl;
+  if (kap < m.J) {
+#pragma unroll
+    for (int j = 0; j < RPT; ++j) {
+      const int r = rg + 4 * j;
+      if (r < m.R) m.A[a_offset(m, kap, r)] = acc[j];
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Gram partials: Gpart[kc][r][s] = sum_{kappa in chunk kc} A[kappa,r] A[kappa,s].
+constexpr int GR_KC = 32;
+__global__ void __launch_bounds__(kThreads) k_gram(ModeDev m, const Ctl* ctl) {
+  if (ctl->done) return;
+  __shared__ double As[GR_KC][PASD_MAX_RANK + 1];
+  const int tid = threadIdx.x, R = m.R, RR = R * R;
+  const int64_t kr = (m.J + m.nkc_g - 1) / m.nkc_g;
+  const int64_t ks = (int64_t)blockIdx.x * kr, ke = imin64(m.J, ks + kr);
+  double acc[16];
+#pragma unroll
+  for (int j = 0; j < 16; ++j) acc[j] = 0.0;
+  for (int64_t c0 = ks; c0 < ke; c0 += GR_KC) {
+    for (int idx = tid; idx < GR_KC * R; idx += kThreads) {
+      int kk, r;
+      if (m.inner > 1) { kk = idx % GR_KC; r = idx / GR_KC; }
+      else { r = idx % R; kk = idx / R; }
+      const int64_t kap = c0 + kk;
+      As[kk][r] = kap < ke ? m.A[a_offset(m, kap, r)] : 0.0;
+    }
+    __syncthreads();
+    const int kn = (int)imin64(GR_KC, ke - c0);
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const int e = tid + kThreads * j;
+      if (e < RR) {
+        const int r = e / R, s = e - r * R;
+        double a = acc[j];
+        for (int kk = 0; kk < kn; ++kk) a = fma(As[kk][r], As[kk][s], a);
+        acc[j] = a;
+      }
+    }
+    __syncthreads();
+  }
+  double* out = m.Gpart + (int64_t)blockIdx.x * RR;
+#pragma unroll
+  for (int j = 0; j < 16; ++j) {
+    const int e = tid + kThreads * j;
+    if (e < RR) out[e] = acc[j];
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Pass 2 (generic order N): refold, E shrink, multiplier ascent, residuals.
+struct ModePack {
+  ModeDev m[PASD_MAX_ORDER];
+  double* Y[PASD_MAX_ORDER];
+  int order;
+};
+
+__global__ void __launch_bounds__(kThreads) k_update(const ModePack* __restrict__ mp, const double* __restrict__ T,
+                                                    double* E0, double* E1, double* resid_part,
+                                                    int* bad_part, int64_t S, const Ctl* ctl) {
+  if (ctl->done) return;
+  __shared__ double red[32];
+  __shared__ int redi[32];
+  const int N = mp->order;
+  double* __restrict__ Enew = ctl->ecur ? E0 : E1;
+  const double mu = ctl->mu;
+  const double inv_mu = __ddiv_rn(1.0, mu);                 // pasd.cpp:170
+  const double dn = (double)N;
+  const double inv_n = __ddiv_rn(1.0, dn);                  // pasd.cpp:204
+  const double tau = __ddiv_rn(1.0, __dmul_rn(mu, dn));     // pasd.cpp:205
+  double worst[PASD_MAX_ORDER];
+  for (int n = 0; n < PASD_MAX_ORDER; ++n) worst[n] = 0.0;
+  int bad = 0;
+  for (int64_t idx = (int64_t)blockIdx.x * kThreads + threadIdx.x; idx < S;
+       idx += (int64_t)gridDim.x * kThreads) {
+    const double t = T[idx];
+    double zt[PASD_MAX_ORDER], yv[PASD_MAX_ORDER];
+    double h = 0.0;
+    for (int n = 0; n < N; ++n) {
+      const ModeDev& m = mp->m[n];
+      const int64_t rest = idx / m.inner;
+      const int64_t p = idx - rest * m.inner;
+      const int64_t q = rest / m.I;
+      const int64_t i = rest - q * m.I;
+      const double* __restrict__ a = m.A + p + m.inner * (int64_t)m.R * q;
+      const double* __restrict__ um = m.UM + i;
+      double z = 0.0;
+      for (int r = 0; r < m.R; ++r) z = fma(um[m.I * r], a[m.inner * r], z);
+      zt[n] = __dsub_rn(t, z);                                       // T - Z_n
+      yv[n] = mp->Y[n][idx];
+      h = __dadd_rn(h, __dadd_rn(zt[n], __dmul_rn(yv[n], inv_mu)));  // pasd.cpp:202
+    }
+    const double e = soft(__dmul_rn(h, inv_n), tau);                 // pasd.cpp:208
+    Enew[idx] = e;
+    for (int n = 0; n < N; ++n) {
+      const double r = __dsub_rn(zt[n], e);                          // pasd.cpp:220
+      mp->Y[n][idx] = __dadd_rn(yv[n], __dmul_rn(mu, r));            // pasd.cpp:221
+      const double a = fabs(r);
+      if (a > worst[n]) worst[n] = a;
+      bad |= !isfinite(r);
+    }
+  }
+  for (int n = 0; n < N; ++n) {
+    const double w = block_reduce(worst[n], MaxOp(), red);
+    if (threadIdx.x == 0) resid_part[(int64_t)blockIdx.x * PASD_MAX_ORDER + n] = w;
+  }
+  const int b = block_reduce(bad, OrOp(), redi);
+  if (threadIdx.x == 0) bad_part[blockIdx.x] = b;
+}
+
+// mu schedule, residual history and stop rule (pasd.cpp:229-239).
+__global__ void k_finish(Ctl* ctl, const double* __restrict__ resid_part, const int* __restrict__ bad_part,
+                         int nblocks, double* history) {
+  if (ctl->done) return;
+  __shared__ double red[32];
+  __shared__ int redi[32];
+  const int N = ctl->order;
+  double resid[PASD_MAX_ORDER];
+  for (int n = 0; n < N; ++n) {
+    double w = 0.0;
+    for (int b = threadIdx.x; b < nblocks; b += blockDim.x) {
+      const double v = resid_part[(int64_t)b * PASD_MAX_ORDER + n];
+      if (v > w) w = v;
+    }
+    resid[n] = block_reduce(w, MaxOp(), red);
+  }
+  int bad = 0;
+  for (int b = threadIdx.x; b < nblocks; b += blockDim.x) bad |= bad_part[b];
+  bad = block_reduce(bad, OrOp(), redi);
+  if (threadIdx.x == 0) {
+    const double mu = ctl->mu;
+    const double cand = __dmul_rn(ctl->rho, mu);
+    const double mu_next = (ctl->mu_max < cand) ? ctl->mu_max : cand;  // std::min(rho*mu, mu_max)
+    const int iter = ctl->iter + 1;
+    double hmax = resid[0];
+    bool conv = true;
+    for (int n = 0; n < N; ++n) {
+      ctl->resid[n] = resid[n];
+      if (resid[n] > hmax) hmax = resid[n];
+      conv = conv && (resid[n] < ctl->eps);
+    }
+    if (ctl->fixed_iters) conv = false;
+    history[iter - 1] = hmax;
+    ctl->iter = iter;
+    ctl->mu_used_last = mu;
+    ctl->mu = mu_next;
+    ctl->ecur ^= 1;
+    ctl->converged = conv ? 1 : 0;
+    if (bad) ctl->nan_flag = 1;
+    if (bad || conv || iter >= ctl->maxiter) ctl->done = 1;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Wt_n partials: Wpart[kc][i][r] = sum_{kappa in chunk} G^{next}[kappa,i] A[kappa,r]
+// with G^{next} = (T - E_new) + Y_n_new / mu_next, plus ||G^{next}||^2 partials.
+constexpr int CW_IT = 64;  // i rows per CTA
+constexpr int CW_KC = 32;  // kappa sub-chunk
+template <int RPT>
+__global__ void __launch_bounds__(kThreads) k_contract_W(ModeDev m, const double* __restrict__ T,
+                                                        const double* __restrict__ E0,
+                                                        const double* __restrict__ E1,
+                                                        const double* __restrict__ Y, const Ctl* ctl) {
+  if (ctl->done) return;
+  __shared__ double Gs[CW_KC][CW_IT + 1];
+  __shared__ double As[CW_KC][PASD_MAX_RANK + 1];
+  __shared__ double red[32];
+  const double* __restrict__ E = ctl->ecur ? E1 : E0;
+  const double inv_mu = __ddiv_rn(1.0, ctl->mu);
+  const int tid = threadIdx.x, il = tid % CW_IT, rg = tid / CW_IT;
+  const int64_t i0 = (int64_t)blockIdx.y * CW_IT;
+  const int64_t kr = (m.J + m.nkc_w - 1) / m.nkc_w;
+  const int64_t ks = (int64_t)blockIdx.x * kr, ke = imin64(m.J, ks + kr);
+  double acc[RPT];
+#pragma unroll
+  for (int j = 0; j < RPT; ++j) acc[j] = 0.0;
+  double gsq = 0.0;
+  for (int64_t c0 = ks; c0 < ke; c0 += CW_KC) {
+    for (int idx = tid; idx < CW_KC * CW_IT; idx += kThreads) {
+      int kk, ii;
+      if (m.inner > 1) { kk = idx % CW_KC; ii = idx / CW_KC; }
+      else { ii = idx % CW_IT; kk = idx / CW_IT; }
+      const int64_t kap = c0 + kk, i = i0 + ii;
+      double v = 0.0;
+      if (kap < ke && i < m.I) {
+        const int64_t off = elem_offset(m, kap, i);
+        v = g_elem(T[off], E[off], Y[off], inv_mu);
+      }
+      Gs[kk][ii] = v;
+    }
+    for (int idx = tid; idx < CW_KC * m.R; idx += kThreads) {
+      int kk, r;
+      if (m.inner > 1) { kk = idx % CW_KC; r = idx / CW_KC; }
+      else { r = idx % m.R; kk = idx / m.R; }
+      const int64_t kap = c0 + kk;
+      As[kk][r] = kap < ke ? m.A[a_offset(m, kap, r)] : 0.0;
+    }
+    __syncthreads();
+    const int kn = (int)imin64(CW_KC, ke - c0);
+    for (int kk = 0; kk < kn; ++kk) {
+      const double g = Gs[kk][il];
+      if (rg == 0) gsq = fma(g, g, gsq);
+#pragma unroll
+      for (int j = 0; j < RPT; ++j) acc[j] = fma(g, As[kk][rg + 4 * j], acc[j]);
+    }
+    __syncthreads();
+  }
+  const int64_t i = i0 + il;
+  if (i < m.I) {
+    double* out = m.Wpart + ((int64_t)blockIdx.x * m.I + i) * m.R;
+#pragma unroll
+    for (int j = 0; j < RPT; ++j) {
+      const int r = rg + 4 * j;
+      if (r < m.R) out[r] = acc[j];
+    }
+  }
+  const double g2 = block_reduce(gsq, AddOp(), red);
+  if (tid == 0) m.gpart[(int64_t)blockIdx.x * m.nib_w + blockIdx.y] = g2;
+}
+
+// ---------------------------------------------------------------------------
+// Finalisation / observer kernels.
+__global__ void k_materialize_z(ModeDev m, double* __restrict__ out, int64_t S) {
+  for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < S; idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t rest = idx / m.inner;
+    const int64_t p = idx - rest * m.inner;
+    const int64_t q = rest / m.I;
+    const int64_t i = rest - q * m.I;
+    const double* a = m.A + p + m.inner * (int64_t)m.R * q;
+    const double* um = m.UM + i;
+    double z = 0.0;
+    for (int r = 0; r < m.R; ++r) z = fma(um[m.I * r], a[m.inner * r], z);
+    out[idx] = z;
+  }
+}
+
+// x = x + (w_n / wsum) * z_n, accumulated from zero in mode order (recovery.cpp:12-23).
+__global__ void k_accum_x(double* __restrict__ x, const double* __restrict__ z, double c, int first, int64_t S) {
+  for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < S; idx += (int64_t)gridDim.x * blockDim.x) {
+    const double prev = first ? 0.0 : x[idx];
+    x[idx] = __dadd_rn(prev, __dmul_rn(c, z[idx]));
+  }
+}
+
+// Yhat_n = Y_n + mu_used * (E - E_prev)  (pasd.cpp:257); also accumulates
+// acc += Y_n - Yhat_n for the certificate (pasd.cpp:287-292).
+__global__ void k_yhat(const double* __restrict__ y, const double* __restrict__ e, const double* __restrict__ ep,
+                       double mu_used, double* __restrict__ yhat, double* __restrict__ acc, int first, int64_t S) {
+  for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < S; idx += (int64_t)gridDim.x * blockDim.x) {
+    const double yv = y[idx];
+    const double h = __dadd_rn(yv, __dmul_rn(mu_used, __dsub_rn(e[idx], ep[idx])));
+    if (yhat) yhat[idx] = h;
+    if (acc) {
+      const double prev = first ? 0.0 : acc[idx];
+      acc[idx] = __dadd_rn(prev, __dsub_rn(yv, h));
+    }
+  }
+}
+
+// Per-block partial sums of |x| and maxima of |x| over a buffer.
+__global__ void k_abs_stats(const double* __restrict__ x, int64_t S, double* sum_part, double* max_part) {
+  __shared__ double red[32];
+  double s = 0.0, mx = 0.0;
+  for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < S; idx += (int64_t)gridDim.x * blockDim.x) {
+    const double a = fabs(x[idx]);
+    s += a;
+    if (a > mx) mx = a;
+  }
+  s = block_reduce(s, AddOp(), red);
+  mx = block_reduce(mx, MaxOp(), red);
+  if (threadIdx.x == 0) {
+    sum_part[blockIdx.x] = s;
+    max_part[blockIdx.x] = mx;
+  }
+}
+
+__global__ void k_sumsq(const double* __restrict__ x, int64_t S, double* out) {
+  __shared__ double red[32];
+  double s = 0.0;
+  for (int64_t idx = threadIdx.x; idx < S; idx += blockDim.x) s = fma(x[idx], x[idx], s);
+  s = block_reduce(s, AddOp(), red);
+  if (threadIdx.x == 0) *out = s;
+}
+
+// Non-finite scan of the input (pasd.cpp:135-136).
+__global__ void k_nonfinite(const double* __restrict__ x, int64_t S, int* flag) {
+  for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < S; idx += (int64_t)gridDim.x * blockDim.x)
+    if (!isfinite(x[idx])) *flag = 1;
+}
+
+// V_n = M_n A_n in the reference's unfolding layout (R x J column-major).
+__global__ void k_materialize_v(ModeDev m, double* __restrict__ out) {
+  const int64_t total = m.J * m.R;
+  for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total; idx += (int64_t)gridDim.x * blockDim.x) {
+    const int r = (int)(idx % m.R);
+    const int64_t kap = idx / m.R;
+    double v = 0.0;
+    for (int s = 0; s < m.R; ++s) v = fma(m.M[r + m.R * s], m.A[a_offset(m, kap, s)], v);
+    out[idx] = v;
+  }
+}
+
+}  // namespace pasd

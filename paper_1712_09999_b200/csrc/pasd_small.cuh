@@ -1,0 +1,429 @@
+// pasd_small.cuh — the r x r solves of one PASD iteration, one CTA per mode.
+//
+// The reference runs LAPACK dgesdd twice per mode and iteration
+// (linops.cpp:62 via svt, linops.cpp:83, and procrustes, linops.cpp:98-103).
+// Both reduce to R_n x R_n symmetric eigenproblems:
+//   * SVT:  A_n = U_n^T G_(n) (R x J).  eig(A A^T) = P diag(sigma^2) P^T, so
+//           SVT_tau(A) = P diag((sigma-tau)_+/sigma) P^T A = M_n A_n  (the
+//           kept set is sigma_i > tau strictly, linops.cpp:85).
+//   * Procrustes: W = G V^T (I x R).  polar(W) = u v^T of its thin SVD.  We
+//           take two Gram/Jacobi passes (eig(W^T W) -> rotate -> re-Gram) so
+//           small singular directions are resolved to working accuracy, and
+//           complete numerically-null directions deterministically from the
+//           previous basis (the reference inherits dgesdd's rounding-noise
+//           completion there; any orthonormal completion is a valid polar
+//           factor — see DESIGN.md "parity floor").
+// Eigenproblems use a CTA-parallel cyclic Jacobi (round-robin ordering, R/2
+// disjoint rotations per step) in shared memory.
+#pragma once
+#include "pasd_kernels.cuh"
+
+namespace pasd {
+
+constexpr int kSmallThreads = 256;
+
+// Shared-memory workspace of one small-solve CTA (dynamic smem).
+struct SmallWs {
+  int Rp, ld;
+  double* S;    // Rp x ld   working matrix (row-major)
+  double* V;    // Rp x ld   eigenvectors / rotations
+  double* Q;    // Rp x ld   accumulated rotation / misc
+  double* Z;    // Rp x ld   misc
+  double* T64;  // 64 x ld   row staging of the tall-skinny products
+  double* cs;   // Rp/2
+  double* sn;   // Rp/2
+  double* lam;  // Rp
+  double* red;  // 32
+  int* pq;      // Rp
+  int* perm;    // Rp
+};
+
+__host__ __device__ inline size_t small_ws_bytes(int R) {
+  const int Rp = R + (R & 1);
+  const int ld = Rp + 1;
+  return sizeof(double) * (4 * (size_t)Rp * ld + 64 * (size_t)ld + Rp + Rp + 32) + sizeof(int) * (2 * (size_t)Rp) +
+         64;
+}
+
+__device__ inline SmallWs make_ws(int R, void* base) {
+  SmallWs w;
+  w.Rp = R + (R & 1);
+  w.ld = w.Rp + 1;
+  double* d = reinterpret_cast<double*>(base);
+  const size_t mat = (size_t)w.Rp * w.ld;
+  w.S = d;
+  w.V = d + mat;
+  w.Q = d + 2 * mat;
+  w.Z = d + 3 * mat;
+  w.T64 = d + 4 * mat;
+  w.cs = w.T64 + 64 * (size_t)w.ld;
+  w.sn = w.cs + w.Rp / 2;
+  w.lam = w.sn + w.Rp / 2;
+  w.red = w.lam + w.Rp;
+  w.pq = reinterpret_cast<int*>(w.red + 32);
+  w.perm = w.pq + w.Rp;
+  return w;
+}
+
+__device__ __forceinline__ int rr_pos(int m, int round, int Rp) {
+  return m == 0 ? 0 : 1 + (m - 1 + round) % (Rp - 1);
+}
+
+// Cyclic parallel Jacobi on the symmetric n x n matrix in ws.S (row-major, ld).
+// On exit diag(S) holds eigenvalues, ws.V (row-major) the eigenvectors as
+// columns: S_in = V diag V^T.  Then sorts eigenpairs descending into
+// lam[0..n) and the columns of V.
+__device__ void cta_jacobi_eig(SmallWs& ws, int n) {
+  const int Rp = ws.Rp, ld = ws.ld, tid = threadIdx.x, nt = blockDim.x;
+  double* S = ws.S;
+  double* V = ws.V;
+  // pad odd n with an isolated zero row/column
+  for (int idx = tid; idx < Rp * Rp; idx += nt) {
+    const int r = idx / Rp, c = idx % Rp;
+    if (r >= n || c >= n) S[r * ld + c] = 0.0;
+    V[r * ld + c] = (r == c) ? 1.0 : 0.0;
+  }
+  __syncthreads();
+  const int npairs = Rp / 2;
+  __shared__ int rotated;
+  for (int sweep = 0; sweep < 30 && Rp > 1; ++sweep) {
+    if (tid == 0) rotated = 0;
+    __syncthreads();
+    for (int round = 0; round < Rp - 1; ++round) {
+      for (int j = tid; j < npairs; j += nt) {
+        const int a = rr_pos(j, round, Rp), b = rr_pos(Rp - 1 - j, round, Rp);
+        const int p = a < b ? a : b, q = a < b ? b : a;
+        const double apq = S[p * ld + q];
+        const double app = S[p * ld + p], aqq = S[q * ld + q];
+        double c = 1.0, s = 0.0;
+        // Skip rotations below rounding level (relative-accuracy criterion for
+        // symmetric PSD Jacobi); a sweep without rotations terminates.
+        if (fabs(apq) > 2.2e-16 * sqrt(fabs(app) * fabs(aqq)) && fabs(apq) > 1e-300) {
+          const double zeta = (aqq - app) / (2.0 * apq);
+          const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+          c = 1.0 / sqrt(1.0 + t * t);
+          s = t * c;
+          rotated = 1;
+        }
+        ws.cs[j] = c;
+        ws.sn[j] = s;
+        ws.pq[2 * j] = p;
+        ws.pq[2 * j + 1] = q;
+      }
+      __syncthreads();
+      for (int idx = tid; idx < npairs * Rp; idx += nt) {  // rows p, q
+        const int j = idx / Rp, k = idx % Rp;
+        const double s = ws.sn[j];
+        if (s == 0.0) continue;
+        const int p = ws.pq[2 * j], q = ws.pq[2 * j + 1];
+        const double c = ws.cs[j];
+        const double a = S[p * ld + k], b = S[q * ld + k];
+        S[p * ld + k] = c * a - s * b;
+        S[q * ld + k] = s * a + c * b;
+      }
+      __syncthreads();
+      for (int idx = tid; idx < npairs * Rp; idx += nt) {  // columns p, q of S and V
+        const int j = idx / Rp, k = idx % Rp;
+        const double s = ws.sn[j];
+        if (s == 0.0) continue;
+        const int p = ws.pq[2 * j], q = ws.pq[2 * j + 1];
+        const double c = ws.cs[j];
+        const double a = S[k * ld + p], b = S[k * ld + q];
+        S[k * ld + p] = c * a - s * b;
+        S[k * ld + q] = s * a + c * b;
+        const double va = V[k * ld + p], vb = V[k * ld + q];
+        V[k * ld + p] = c * va - s * vb;
+        V[k * ld + q] = s * va + c * vb;
+      }
+      __syncthreads();
+    }
+    if (rotated == 0) break;
+    __syncthreads();
+  }
+  // sort descending (stable on index): perm[rank] = j
+  for (int j = tid; j < n; j += nt) {
+    const double lj = S[j * ld + j];
+    int rank = 0;
+    for (int i = 0; i < n; ++i) {
+      const double li = S[i * ld + i];
+      rank += (li > lj) || (li == lj && i < j);
+    }
+    ws.perm[rank] = j;
+  }
+  __syncthreads();
+  for (int j = tid; j < n; j += nt) ws.lam[j] = S[ws.perm[j] * ld + ws.perm[j]];
+  // sorted eigenvectors into Z (row-major, column j = eigenvector j), then back to V
+  for (int idx = tid; idx < n * n; idx += nt) {
+    const int r = idx / n, j = idx % n;
+    ws.Z[r * ld + j] = V[r * ld + ws.perm[j]];
+  }
+  __syncthreads();
+  for (int idx = tid; idx < n * n; idx += nt) {
+    const int r = idx / n, j = idx % n;
+    V[r * ld + j] = ws.Z[r * ld + j];
+  }
+  __syncthreads();
+}
+
+// out(R x R2, smem row-major ld) = X^T Y with X (I x R), Y (I x R2) global column-major.
+__device__ void cta_gram_tn(const double* X, const double* Y, int64_t I, int R, int R2, double* out, int ld,
+                            double* stage /* 2 x 32 x ld */) {
+  const int tid = threadIdx.x, nt = blockDim.x;
+  double* Xs = stage;
+  double* Ys = stage + 32 * ld;
+  for (int idx = tid; idx < R * R2; idx += nt) out[(idx / R2) * ld + idx % R2] = 0.0;
+  __syncthreads();
+  for (int64_t i0 = 0; i0 < I; i0 += 32) {
+    const int ic = (int)imin64(32, I - i0);
+    for (int idx = tid; idx < 32 * R; idx += nt) {
+      const int il = idx % 32, r = idx / 32;
+      Xs[il * ld + r] = il < ic ? X[i0 + il + I * r] : 0.0;
+    }
+    for (int idx = tid; idx < 32 * R2; idx += nt) {
+      const int il = idx % 32, r = idx / 32;
+      Ys[il * ld + r] = il < ic ? Y[i0 + il + I * r] : 0.0;
+    }
+    __syncthreads();
+    for (int idx = tid; idx < R * R2; idx += nt) {
+      const int r = idx / R2, s = idx % R2;
+      double a = out[r * ld + s];
+      for (int il = 0; il < ic; ++il) a = fma(Xs[il * ld + r], Ys[il * ld + s], a);
+      out[r * ld + s] = a;
+    }
+    __syncthreads();
+  }
+}
+
+// out(I x R2, global col-major) = X (I x R, global col-major) * B (R x R2, smem row-major ld)
+__device__ void cta_mul_nn(const double* X, int64_t I, int R, const double* B, int ld, int R2, double* out) {
+  const int64_t total = I * R2;
+  for (int64_t idx = threadIdx.x; idx < total; idx += blockDim.x) {
+    const int64_t i = idx % I;
+    const int s = (int)(idx / I);
+    double a = 0.0;
+    for (int r = 0; r < R; ++r) a = fma(X[i + I * r], B[r * ld + s], a);
+    out[i + I * s] = a;
+  }
+  __syncthreads();
+}
+
+// ---------------------------------------------------------------------------
+// SVT factor: M_n = P diag(f) P^T, f_i = (sigma_i - tau)/sigma_i for sigma_i > tau.
+__global__ void __launch_bounds__(kSmallThreads) k_svt(const ModePack* __restrict__ mp, Ctl* ctl) {
+  if (ctl->done) return;
+  extern __shared__ double smem[];
+  const int n = blockIdx.x;
+  const ModeDev& m = mp->m[n];
+  const int R = m.R, tid = threadIdx.x, nt = blockDim.x;
+  SmallWs ws = make_ws(R, smem);
+  const int ld = ws.ld;
+  // Gram = sum of partials in fixed chunk order (deterministic)
+  for (int idx = tid; idx < R * R; idx += nt) {
+    double a = 0.0;
+    for (int kc = 0; kc < m.nkc_g; ++kc) a += m.Gpart[(int64_t)kc * R * R + idx];
+    ws.S[(idx / R) * ld + idx % R] = a;
+    m.Gram[idx] = a;
+  }
+  __syncthreads();
+  cta_jacobi_eig(ws, R);
+  const double tau = __ddiv_rn(m.lambda, ctl->mu);  // lambda / mu (pasd.cpp:77)
+  if (tid == 0) {
+    int keep = 0;
+    double vn2 = 0.0, nuc = 0.0;
+    for (int j = 0; j < R; ++j) {
+      const double sg = sqrt(fmax(ws.lam[j], 0.0));
+      ws.lam[j] = sg;
+      m.sig[j] = sg;
+    }
+    while (keep < R && ws.lam[keep] > tau) ++keep;  // linops.cpp:84-86
+    for (int j = 0; j < R; ++j) {
+      double f = 0.0;
+      if (j < keep) {
+        const double sh = ws.lam[j] - tau;
+        f = sh / ws.lam[j];
+        vn2 += sh * sh;
+        nuc += sh;
+      }
+      ws.Q[j] = f;  // row 0 of Q holds f_j
+    }
+    ctl->keep[n] = keep;
+    ctl->vnorm2[n] = vn2;
+    ctl->nuclear[n] = nuc;
+  }
+  __syncthreads();
+  // M = P diag(f) P^T  -> S (row-major) and global m.M (column-major == same, symmetric)
+  for (int idx = tid; idx < R * R; idx += nt) {
+    const int r = idx / R, s = idx % R;
+    double a = 0.0;
+    for (int j = 0; j < R; ++j) a = fma(ws.V[r * ld + j] * ws.Q[j], ws.V[s * ld + j], a);
+    ws.Z[r * ld + s] = a;
+  }
+  __syncthreads();
+  for (int idx = tid; idx < R * R; idx += nt) {
+    const int r = idx / R, s = idx % R;
+    // symmetrise exactly
+    const double a = 0.5 * (ws.Z[r * ld + s] + ws.Z[s * ld + r]);
+    ws.S[r * ld + s] = a;
+    m.M[r + R * s] = a;
+    m.P[r + R * s] = ws.V[r * ld + s];
+  }
+  __syncthreads();
+  // UM = U * M
+  cta_mul_nn(m.U, m.I, R, ws.S, ld, R, m.UM);
+}
+
+// ---------------------------------------------------------------------------
+// Procrustes: U_n <- polar(Wt_n M_n) unless degenerate (linops.cpp:93-104).
+__global__ void __launch_bounds__(kSmallThreads) k_polar(const ModePack* __restrict__ mp, Ctl* ctl) {
+  if (ctl->done) return;
+  extern __shared__ double smem[];
+  const int n = blockIdx.x;
+  const ModeDev& m = mp->m[n];
+  const int R = m.R, tid = threadIdx.x, nt = blockDim.x;
+  const int64_t I = m.I, IR = I * R;
+  SmallWs ws = make_ws(R, smem);
+  const int ld = ws.ld;
+  double* Wt = m.scratch;           // I x R
+  double* X = m.scratch + IR;       // I x R
+  double* X2 = m.scratch + 2 * IR;  // I x R
+  // 1. Wt = sum_kc Wpart[kc] (fixed order); ||G||^2 = sum gpart
+  const int nkc = m.nkc_w;
+  for (int64_t idx = tid; idx < IR; idx += nt) {
+    const int64_t i = idx % I;
+    const int r = (int)(idx / I);
+    double a = 0.0;
+    for (int kc = 0; kc < nkc; ++kc) a += m.Wpart[((int64_t)kc * I + i) * R + r];
+    Wt[idx] = a;
+  }
+  double g2 = 0.0;
+  for (int j = tid; j < nkc * m.nib_w; j += nt) g2 += m.gpart[j];
+  g2 = block_reduce(g2, AddOp(), ws.red);
+  // 2. W = Wt M  (M in S)
+  for (int idx = tid; idx < R * R; idx += nt) ws.S[(idx / R) * ld + idx % R] = m.M[(idx / R) + R * (idx % R)];
+  __syncthreads();
+  cta_mul_nn(Wt, I, R, ws.S, ld, R, X);
+  double w2 = 0.0;
+  for (int64_t idx = tid; idx < IR; idx += nt) w2 += X[idx] * X[idx];
+  w2 = block_reduce(w2, AddOp(), ws.red);
+  const double gnorm = sqrt(g2), vnorm = sqrt(ctl->vnorm2[n]);
+  const double scale = fmax(1.0, gnorm * vnorm);  // linops.cpp:99
+  if (tid == 0) ctl->gnorm2[n] = g2;
+  if (sqrt(w2) <= 1e-14 * scale) {                // linops.cpp:100-101 -> keep U (pasd.cpp:70-74)
+    if (tid == 0) { ctl->degenerate[n] = 1; ctl->polar_rank[n] = 0; }
+    return;
+  }
+  // 3. first Gram/Jacobi pass: C = W^T W = Q1 L Q1^T ; X2 = W Q1
+  cta_gram_tn(X, X, I, R, R, ws.S, ld, ws.T64);
+  cta_jacobi_eig(ws, R);
+  for (int idx = tid; idx < R * R; idx += nt) ws.Q[(idx / R) * ld + idx % R] = ws.V[(idx / R) * ld + idx % R];
+  __syncthreads();
+  cta_mul_nn(X, I, R, ws.Q, ld, R, X2);
+#ifdef PASD_DEBUG_POLAR
+  if (tid == 0) {
+    printf("lam1:"); for (int j = 0; j < R; ++j) printf(" %g", ws.lam[j]); printf("\n");
+    printf("Q1:"); for (int r = 0; r < R; ++r) { for (int j = 0; j < R; ++j) printf(" %g", ws.Q[r * ld + j]); printf(" |"); } printf("\n");
+    printf("X row0:"); for (int j = 0; j < R; ++j) printf(" %g", X[I * j]); printf("\n");
+    printf("X2 row0:"); for (int j = 0; j < R; ++j) printf(" %g", X2[I * j]); printf("\n");
+  }
+  __syncthreads();
+#endif
+  // 4. second pass on the rotated columns: C2 = X2^T X2 = Q2 L2 Q2^T ; X = X2 Q2 ; Q = Q1 Q2
+  cta_gram_tn(X2, X2, I, R, R, ws.S, ld, ws.T64);
+  cta_jacobi_eig(ws, R);
+  cta_mul_nn(X2, I, R, ws.V, ld, R, X);
+  for (int idx = tid; idx < R * R; idx += nt) {
+    const int r = idx / R, s = idx % R;
+    double a = 0.0;
+    for (int j = 0; j < R; ++j) a = fma(ws.Q[r * ld + j], ws.V[j * ld + s], a);
+    ws.Z[r * ld + s] = a;
+  }
+  __syncthreads();
+  for (int idx = tid; idx < R * R; idx += nt) ws.Q[(idx / R) * ld + idx % R] = ws.Z[(idx / R) * ld + idx % R];
+  __syncthreads();
+  // 5. column norms sigma_j of X (sorted descending by the Jacobi pass)
+  for (int j = 0; j < R; ++j) {
+    double a = 0.0;
+    for (int64_t i = tid; i < I; i += nt) a += X[i + I * j] * X[i + I * j];
+    a = block_reduce(a, AddOp(), ws.red);
+    if (tid == 0) ws.lam[j] = sqrt(a);
+  }
+  __syncthreads();
+#ifdef PASD_DEBUG_POLAR
+  if (tid == 0) {
+    printf("sig:"); for (int j = 0; j < R; ++j) printf(" %g", ws.lam[j]); printf("\n");
+    printf("Q:"); for (int r = 0; r < R; ++r) { for (int j = 0; j < R; ++j) printf(" %g", ws.Q[r * ld + j]); printf(" |"); } printf("\n");
+    double d01 = 0; for (int64_t i = 0; i < I; ++i) d01 += X[i] * X[i + I]; printf("X col0.col1 = %g\n", d01);
+  }
+  __syncthreads();
+#endif
+  const double smax = ws.lam[0] > 0.0 ? ws.lam[0] : 1.0;
+  int k = 0;
+  while (k < R && ws.lam[k] > 1e-12 * smax) ++k;
+  if (tid == 0) { ctl->degenerate[n] = 0; ctl->polar_rank[n] = k; }
+  // U_tilde columns j < k: X[:, j] / sigma_j   (written into X in place)
+  for (int64_t idx = tid; idx < I * k; idx += nt) {
+    const int j = (int)(idx / I);
+    X[idx] = X[idx] / ws.lam[j];
+  }
+  __syncthreads();
+  if (k < R) {
+    // 6. completion: B = (I - Ut Ut^T) U_prev Q[:, k:], then polar(B).
+    const int mcols = R - k;
+    double* B = X2;  // I x mcols (columns k.. of X2 are free to use)
+    // B = U_prev * Q[:, k:]
+    for (int64_t idx = tid; idx < I * mcols; idx += nt) {
+      const int64_t i = idx % I;
+      const int c = (int)(idx / I);
+      double a = 0.0;
+      for (int r = 0; r < R; ++r) a = fma(m.U[i + I * r], ws.Q[r * ld + k + c], a);
+      B[idx] = a;
+    }
+    __syncthreads();
+    for (int pass = 0; pass < 2; ++pass) {
+      if (k > 0) {
+        cta_gram_tn(X, B, I, k, mcols, ws.S, ld, ws.T64);  // S (k x mcols) = Ut^T B
+        for (int64_t idx = tid; idx < I * mcols; idx += nt) {
+          const int64_t i = idx % I;
+          const int c = (int)(idx / I);
+          double a = B[idx];
+          for (int j = 0; j < k; ++j) a = fma(-X[i + I * j], ws.S[j * ld + c], a);
+          B[idx] = a;
+        }
+        __syncthreads();
+      }
+    }
+    // polar(B) = B Qb Lb^{-1/2} Qb^T via eig(B^T B)
+    cta_gram_tn(B, B, I, mcols, mcols, ws.S, ld, ws.T64);
+    cta_jacobi_eig(ws, mcols);
+    // Z = Qb diag(lb^{-1/2}) Qb^T  (mcols x mcols)
+    for (int idx = tid; idx < mcols * mcols; idx += nt) {
+      const int r = idx / mcols, s = idx % mcols;
+      double a = 0.0;
+      for (int j = 0; j < mcols; ++j) {
+        const double l = ws.lam[j];
+        const double inv = l > 1e-24 ? 1.0 / sqrt(l) : 0.0;
+        a = fma(ws.V[r * ld + j] * inv, ws.V[s * ld + j], a);
+      }
+      ws.Z[r * ld + s] = a;
+    }
+    __syncthreads();
+    // X[:, k + c] = B * Z[:, c]
+    for (int64_t idx = tid; idx < I * mcols; idx += nt) {
+      const int64_t i = idx % I;
+      const int c = (int)(idx / I);
+      double a = 0.0;
+      for (int j = 0; j < mcols; ++j) a = fma(B[i + I * j], ws.Z[j * ld + c], a);
+      X[i + I * (k + c)] = a;
+    }
+    __syncthreads();
+  }
+  // 7. U = Ut Q^T
+  for (int idx = tid; idx < R * R; idx += nt) {
+    const int r = idx / R, s = idx % R;
+    ws.S[r * ld + s] = ws.Q[s * ld + r];
+  }
+  __syncthreads();
+  cta_mul_nn(X, I, R, ws.S, ld, R, m.U);
+}
+
+}  // namespace pasd

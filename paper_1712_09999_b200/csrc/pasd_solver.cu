@@ -1,0 +1,846 @@
+// pasd_solver.cu — host driver and C-ABI of the B200-native PASD solver.
+//
+// Drop-in for tenrec::pasd_recover (proj/include/tenrec/pasd.hpp:65-66,
+// proj/src/pasd.cpp:132-275): same options (PasdConfig, pasd.hpp:8-27), same
+// validation messages (pasd.cpp:12-49), same outputs (RecoveryResult,
+// recovery.hpp:20-34) and the same error taxonomy (errors.hpp:9-30), mapped to
+// status codes + message text at the C boundary (include/pasd_b200.h).
+//
+// The ADMM loop is device resident: one iteration is a fixed sequence of
+// kernels that read mu / iteration / stop flag from device memory, captured
+// once into a CUDA graph and replayed; the host only polls the stop flag every
+// `poll_every` iterations.  Iterations launched after the stop are no-ops, so
+// results never depend on the polling period.  No CPU fallback exists: every
+// per-iteration step is a kernel in pasd_kernels.cuh / pasd_small.cuh.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <functional>
+#include <limits>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/pasd_b200.h"
+#include "pasd_common.cuh"
+#include "pasd_kernels.cuh"
+#include "pasd_small.cuh"
+
+using namespace pasd;
+
+namespace {
+
+struct PasdError : std::runtime_error {
+  int code;
+  PasdError(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+[[noreturn]] void fail(int code, const std::string& msg) { throw PasdError(code, msg); }
+
+void ck(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) fail(PASD_ERR_CUDA, std::string("cuda: ") + what + ": " + cudaGetErrorString(e));
+}
+#define CK(x) ck((x), #x)
+
+int guarded_call(char* err, size_t errlen, const std::function<void()>& f);
+
+void set_err(char* err, size_t len, const std::string& m) {
+  if (err && len) std::snprintf(err, len, "%s", m.c_str());
+}
+
+struct Dims {
+  std::vector<int64_t> d;
+  int64_t total = 0;
+};
+
+// dims_product (tensor.cpp:9-23)
+int64_t dims_product(const std::vector<int64_t>& dims) {
+  if (dims.empty()) fail(PASD_ERR_ARGUMENT, "tensor order must be at least 1");
+  int64_t prod = 1;
+  for (size_t n = 0; n < dims.size(); ++n) {
+    const int64_t d = dims[n];
+    if (d < 1)
+      fail(PASD_ERR_ARGUMENT, "dimension " + std::to_string(n + 1) + " must be positive, got " + std::to_string(d));
+    if (prod > std::numeric_limits<int64_t>::max() / d) fail(PASD_ERR_ARGUMENT, "dimension product overflows");
+    prod *= d;
+  }
+  return prod;
+}
+
+// PasdConfig::validate (pasd.cpp:12-49), same checks and messages, plus the
+// kernel limits of this build (rank <= 64, order <= 8).
+void validate_options(const pasd_options* o) {
+  if (!o) fail(PASD_ERR_ARGUMENT, "config: null options");
+  if (o->order < 1 || !o->dims) fail(PASD_ERR_ARGUMENT, "tensor order must be at least 1");
+  const size_t n_modes = (size_t)o->order;
+  std::vector<int64_t> dims(o->dims, o->dims + n_modes);
+  dims_product(dims);
+  if (!o->lambdas) fail(PASD_ERR_ARGUMENT, "config: expected " + std::to_string(n_modes) + " lambdas, got 0");
+  for (size_t n = 0; n < n_modes; ++n)
+    if (!(o->lambdas[n] > 0.0) || !std::isfinite(o->lambdas[n]))
+      fail(PASD_ERR_ARGUMENT, "config: lambda of mode " + std::to_string(n + 1) + " must be positive");
+  if (!o->ranks) fail(PASD_ERR_ARGUMENT, "config: expected " + std::to_string(n_modes) + " ranks, got 0");
+  for (size_t n = 0; n < n_modes; ++n) {
+    if (o->ranks[n] < 1) fail(PASD_ERR_ARGUMENT, "config: rank of mode " + std::to_string(n + 1) + " must be positive");
+    if (o->ranks[n] > dims[n])
+      fail(PASD_ERR_ARGUMENT, "config: rank " + std::to_string(o->ranks[n]) + " exceeds dimension " +
+                                  std::to_string(dims[n]) + " in mode " + std::to_string(n + 1));
+  }
+  if (!(o->mu0 > 0.0) || !std::isfinite(o->mu0)) fail(PASD_ERR_ARGUMENT, "config: mu0 must be positive");
+  if (!(o->mu_max >= o->mu0)) fail(PASD_ERR_ARGUMENT, "config: mu_max must be at least mu0");
+  if (!(o->rho > 1.0) || !std::isfinite(o->rho)) fail(PASD_ERR_ARGUMENT, "config: rho must exceed 1");
+  if (!(o->eps > 0.0)) fail(PASD_ERR_ARGUMENT, "config: eps must be positive");
+  if (o->maxiter < 1) fail(PASD_ERR_ARGUMENT, "config: maxiter must be positive");
+  if (o->output_weights) {
+    for (size_t n = 0; n < n_modes; ++n)
+      if (!(o->output_weights[n] > 0.0) || !std::isfinite(o->output_weights[n]))
+        fail(PASD_ERR_ARGUMENT, "config: output weight of mode " + std::to_string(n + 1) + " must be positive");
+  }
+  // Limits of this build (no reference analogue).
+  if (o->order > PASD_MAX_ORDER)
+    fail(PASD_ERR_ARGUMENT, "pasd_b200: order " + std::to_string(o->order) + " exceeds the supported maximum " +
+                                std::to_string(PASD_MAX_ORDER));
+  for (size_t n = 0; n < n_modes; ++n)
+    if (o->ranks[n] > PASD_MAX_RANK)
+      fail(PASD_ERR_ARGUMENT, "pasd_b200: rank " + std::to_string(o->ranks[n]) + " of mode " + std::to_string(n + 1) +
+                                  " exceeds the supported maximum " + std::to_string(PASD_MAX_RANK));
+}
+
+template <class T>
+T* dalloc(size_t count) {
+  void* p = nullptr;
+  if (count == 0) count = 1;
+  CK(cudaMalloc(&p, count * sizeof(T)));
+  return static_cast<T*>(p);
+}
+
+int rpt_for(int R) { return R <= 8 ? 2 : R <= 16 ? 4 : R <= 32 ? 8 : 16; }
+
+}  // namespace
+
+// ============================================================================
+struct pasd_solver {
+  // configuration
+  int N = 0;
+  std::vector<int64_t> dims;
+  int64_t S = 0;
+  std::vector<int64_t> ranks;
+  std::vector<double> lambdas, alphas;
+  double mu0 = 1e-4, mu_max = 1e10, rho = 1.1, eps = 1e-5;
+  int maxiter = 1000;
+  uint32_t flags = 0;
+  int poll_every = 8;
+  int device = 0;
+  // device state
+  cudaStream_t stream = nullptr;
+  double* T = nullptr;
+  double* E[2] = {nullptr, nullptr};
+  std::vector<double*> Y;
+  std::vector<ModeDev> modes;
+  std::vector<void*> owned;
+  ModePack* d_pack = nullptr;
+  ModePack h_pack{};
+  Ctl* d_ctl = nullptr;
+  Ctl* h_ctl = nullptr;  // pinned mirror
+  double* d_hist = nullptr;
+  double* d_resid_part = nullptr;
+  int* d_bad_part = nullptr;
+  int nblk_update = 0;
+  size_t small_smem = 0;
+  double* zbuf = nullptr;  // S scratch (finalisation / observer)
+  double* xbuf = nullptr;  // S scratch
+  double* d_stats = nullptr;
+  int* d_flag = nullptr;
+  cudaGraphExec_t graph_exec = nullptr;
+  cudaGraph_t graph = nullptr;
+  int64_t launches_last_run = 0;
+  int launches_per_iter = 0;
+  bool loaded = false;
+
+  ~pasd_solver() {
+    if (graph_exec) cudaGraphExecDestroy(graph_exec);
+    if (graph) cudaGraphDestroy(graph);
+    for (void* p : owned) cudaFree(p);
+    if (h_ctl) cudaFreeHost(h_ctl);
+    if (stream) cudaStreamDestroy(stream);
+  }
+
+  template <class T>
+  T* alloc(size_t count) {
+    T* p = dalloc<T>(count);
+    owned.push_back(p);
+    return p;
+  }
+};
+
+namespace {
+
+void launch_iteration(pasd_solver* s, cudaStream_t st) {
+  const int N = s->N;
+  int launches = 0;
+  k_polar<<<N, kSmallThreads, s->small_smem, st>>>(s->d_pack, s->d_ctl);
+  ++launches;
+  for (int n = 0; n < N; ++n) {
+    const ModeDev& m = s->modes[n];
+    const unsigned grid = (unsigned)((m.J + CA_KT - 1) / CA_KT);
+    switch (rpt_for(m.R)) {
+      case 2: k_contract_A<2><<<grid, kThreads, 0, st>>>(m, s->T, s->E[0], s->E[1], s->Y[n], s->d_ctl); break;
+      case 4: k_contract_A<4><<<grid, kThreads, 0, st>>>(m, s->T, s->E[0], s->E[1], s->Y[n], s->d_ctl); break;
+      case 8: k_contract_A<8><<<grid, kThreads, 0, st>>>(m, s->T, s->E[0], s->E[1], s->Y[n], s->d_ctl); break;
+      default: k_contract_A<16><<<grid, kThreads, 0, st>>>(m, s->T, s->E[0], s->E[1], s->Y[n], s->d_ctl); break;
+    }
+    ++launches;
+    k_gram<<<m.nkc_g, kThreads, 0, st>>>(m, s->d_ctl);
+    ++launches;
+  }
+  k_svt<<<N, kSmallThreads, s->small_smem, st>>>(s->d_pack, s->d_ctl);
+  ++launches;
+  k_update<<<s->nblk_update, kThreads, 0, st>>>(s->d_pack, s->T, s->E[0], s->E[1], s->d_resid_part, s->d_bad_part,
+                                                s->S, s->d_ctl);
+  ++launches;
+  k_finish<<<1, kThreads, 0, st>>>(s->d_ctl, s->d_resid_part, s->d_bad_part, s->nblk_update, s->d_hist);
+  ++launches;
+  for (int n = 0; n < N; ++n) {
+    const ModeDev& m = s->modes[n];
+    const dim3 grid(m.nkc_w, m.nib_w);
+    switch (rpt_for(m.R)) {
+      case 2: k_contract_W<2><<<grid, kThreads, 0, st>>>(m, s->T, s->E[0], s->E[1], s->Y[n], s->d_ctl); break;
+      case 4: k_contract_W<4><<<grid, kThreads, 0, st>>>(m, s->T, s->E[0], s->E[1], s->Y[n], s->d_ctl); break;
+      case 8: k_contract_W<8><<<grid, kThreads, 0, st>>>(m, s->T, s->E[0], s->E[1], s->Y[n], s->d_ctl); break;
+      default: k_contract_W<16><<<grid, kThreads, 0, st>>>(m, s->T, s->E[0], s->E[1], s->Y[n], s->d_ctl); break;
+    }
+    ++launches;
+  }
+  s->launches_per_iter = launches;
+  CK(cudaGetLastError());
+}
+
+__global__ void k_init_state(ModePack* mp, Ctl* ctl, double mu0, double rho, double mu_max, double eps, int maxiter,
+                             int fixed) {
+  const int N = mp->order;
+  for (int n = 0; n < N; ++n) {
+    ModeDev& m = mp->m[n];
+    const int64_t IR = m.I * m.R;
+    for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < IR; idx += (int64_t)gridDim.x * blockDim.x) {
+      const int64_t i = idx % m.I, r = idx / m.I;
+      m.U[idx] = (i == r) ? 1.0 : 0.0;  // Matrix::Identity(rows, rank) (pasd.cpp:152)
+      m.UM[idx] = 0.0;
+    }
+    for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < (int64_t)m.R * m.R;
+         idx += (int64_t)gridDim.x * blockDim.x)
+      m.M[idx] = 0.0;  // V = 0 (pasd.cpp:153) <=> M = 0
+    const int64_t wp = (int64_t)m.nkc_w * m.I * m.R;
+    for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < wp; idx += (int64_t)gridDim.x * blockDim.x)
+      m.Wpart[idx] = 0.0;
+    for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < (int64_t)m.nkc_w * m.nib_w;
+         idx += (int64_t)gridDim.x * blockDim.x)
+      m.gpart[idx] = 0.0;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    ctl->mu = mu0;
+    ctl->mu_used_last = mu0;
+    ctl->rho = rho;
+    ctl->mu_max = mu_max;
+    ctl->eps = eps;
+    ctl->iter = 0;
+    ctl->maxiter = maxiter;
+    ctl->done = 0;
+    ctl->converged = 0;
+    ctl->nan_flag = 0;
+    ctl->ecur = 0;
+    ctl->fixed_iters = fixed;
+    ctl->order = N;
+    for (int n = 0; n < PASD_MAX_ORDER; ++n) {
+      ctl->resid[n] = CUDART_INF;
+      ctl->gnorm2[n] = 0.0;
+      ctl->vnorm2[n] = 0.0;
+      ctl->nuclear[n] = 0.0;
+      ctl->keep[n] = 0;
+      ctl->degenerate[n] = 0;
+      ctl->polar_rank[n] = 0;
+    }
+  }
+}
+
+void reset_state(pasd_solver* s) {
+  CK(cudaMemsetAsync(s->E[0], 0, s->S * sizeof(double), s->stream));
+  CK(cudaMemsetAsync(s->E[1], 0, s->S * sizeof(double), s->stream));
+  for (int n = 0; n < s->N; ++n) CK(cudaMemsetAsync(s->Y[n], 0, s->S * sizeof(double), s->stream));
+  k_init_state<<<64, 256, 0, s->stream>>>(s->d_pack, s->d_ctl, s->mu0, s->rho, s->mu_max, s->eps, s->maxiter,
+                                          (s->flags & PASD_FLAG_FIXED_ITERS) ? 1 : 0);
+  CK(cudaGetLastError());
+}
+
+pasd_solver* create_solver(const pasd_options* o, const pasd_shard* shard) {
+  validate_options(o);
+  if (shard && shard->nranks > 1)
+    fail(PASD_ERR_ARGUMENT, "pasd_b200: multi-rank sharding is not available in this build");
+  auto s = std::make_unique<pasd_solver>();
+  s->N = o->order;
+  s->dims.assign(o->dims, o->dims + o->order);
+  s->S = dims_product(s->dims);
+  s->ranks.assign(o->ranks, o->ranks + o->order);
+  s->lambdas.assign(o->lambdas, o->lambdas + o->order);
+  if (o->output_weights)
+    s->alphas.assign(o->output_weights, o->output_weights + o->order);
+  else
+    s->alphas = s->lambdas;  // PasdConfig::alphas (pasd.hpp:26)
+  s->mu0 = o->mu0;
+  s->mu_max = o->mu_max;
+  s->rho = o->rho;
+  s->eps = o->eps;
+  s->maxiter = o->maxiter;
+  s->flags = o->flags;
+  s->poll_every = o->poll_every > 0 ? o->poll_every : 8;
+  s->device = o->device;
+  CK(cudaSetDevice(s->device));
+  CK(cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking));
+  const int64_t S = s->S;
+  s->T = s->alloc<double>(S);
+  s->E[0] = s->alloc<double>(S);
+  s->E[1] = s->alloc<double>(S);
+  for (int n = 0; n < s->N; ++n) s->Y.push_back(s->alloc<double>(S));
+  int maxR = 1;
+  for (int n = 0; n < s->N; ++n) {
+    ModeDev m{};
+    m.mode = n;
+    m.I = s->dims[n];
+    m.inner = 1;
+    for (int l = 0; l < n; ++l) m.inner *= s->dims[l];
+    m.outer = 1;
+    for (int l = n + 1; l < s->N; ++l) m.outer *= s->dims[l];
+    m.J = m.inner * m.outer;
+    m.R = (int)s->ranks[n];
+    maxR = std::max(maxR, m.R);
+    m.lambda = s->lambdas[n];
+    const int64_t IR = m.I * m.R, RR = (int64_t)m.R * m.R;
+    m.U = s->alloc<double>(IR);
+    m.UM = s->alloc<double>(IR);
+    m.M = s->alloc<double>(RR);
+    m.A = s->alloc<double>((size_t)m.J * m.R);
+    m.Wt = s->alloc<double>(IR);
+    m.nib_w = (int)((m.I + CW_IT - 1) / CW_IT);
+    const int64_t kchunks = (m.J + CW_KC - 1) / CW_KC;
+    m.nkc_w = (int)std::max<int64_t>(1, std::min<int64_t>(kchunks, std::max(1, 592 / m.nib_w)));
+    m.Wpart = s->alloc<double>((size_t)m.nkc_w * IR);
+    m.gpart = s->alloc<double>((size_t)m.nkc_w * m.nib_w);
+    m.nkc_g = (int)std::max<int64_t>(1, std::min<int64_t>((m.J + GR_KC - 1) / GR_KC, 296));
+    m.Gpart = s->alloc<double>((size_t)m.nkc_g * RR);
+    m.Gram = s->alloc<double>(RR);
+    m.sig = s->alloc<double>(m.R);
+    m.P = s->alloc<double>(RR);
+    m.scratch = s->alloc<double>(3 * IR);
+    s->modes.push_back(m);
+  }
+  std::memset(&s->h_pack, 0, sizeof(ModePack));
+  s->h_pack.order = s->N;
+  for (int n = 0; n < s->N; ++n) {
+    s->h_pack.m[n] = s->modes[n];
+    s->h_pack.Y[n] = s->Y[n];
+  }
+  s->d_pack = s->alloc<ModePack>(1);
+  CK(cudaMemcpy(s->d_pack, &s->h_pack, sizeof(ModePack), cudaMemcpyHostToDevice));
+  s->d_ctl = s->alloc<Ctl>(1);
+  CK(cudaMallocHost(&s->h_ctl, sizeof(Ctl)));
+  s->d_hist = s->alloc<double>(std::max(1, s->maxiter));
+  int sms = 148;
+  CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, s->device));
+  s->nblk_update = (int)std::max<int64_t>(1, std::min<int64_t>((S + kThreads - 1) / kThreads, (int64_t)sms * 8));
+  s->d_resid_part = s->alloc<double>((size_t)s->nblk_update * PASD_MAX_ORDER);
+  s->d_bad_part = s->alloc<int>(s->nblk_update);
+  s->small_smem = small_ws_bytes(maxR);
+  CK(cudaFuncSetAttribute(k_svt, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->small_smem));
+  CK(cudaFuncSetAttribute(k_polar, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->small_smem));
+  s->d_stats = s->alloc<double>(2 * 2048);
+  s->d_flag = s->alloc<int>(1);
+  reset_state(s.get());
+  CK(cudaStreamSynchronize(s->stream));
+  return s.release();
+}
+
+void build_graph(pasd_solver* s) {
+  if (s->graph_exec) return;
+  CK(cudaStreamBeginCapture(s->stream, cudaStreamCaptureModeThreadLocal));
+  launch_iteration(s, s->stream);
+  CK(cudaStreamEndCapture(s->stream, &s->graph));
+  CK(cudaGraphInstantiate(&s->graph_exec, s->graph, 0));
+}
+
+void sync_ctl(pasd_solver* s) {
+  CK(cudaMemcpyAsync(s->h_ctl, s->d_ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, s->stream));
+  CK(cudaStreamSynchronize(s->stream));
+}
+
+void load_tensor(pasd_solver* s, const double* t, int is_device) {
+  CK(cudaMemcpyAsync(s->T, t, s->S * sizeof(double), is_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
+                     s->stream));
+  CK(cudaMemsetAsync(s->d_flag, 0, sizeof(int), s->stream));
+  k_nonfinite<<<1184, 256, 0, s->stream>>>(s->T, s->S, s->d_flag);
+  int flag = 0;
+  CK(cudaMemcpyAsync(&flag, s->d_flag, sizeof(int), cudaMemcpyDeviceToHost, s->stream));
+  CK(cudaStreamSynchronize(s->stream));
+  if (flag) fail(PASD_ERR_ARGUMENT, "pasd: input tensor contains non-finite entries");  // pasd.cpp:135-136
+  s->loaded = true;
+}
+
+// Observer snapshot (recovery.hpp:38-48): host copies of e, z, y, u, v.
+struct HostView {
+  std::vector<double> e;
+  std::vector<std::vector<double>> z, y, u, v;
+};
+
+void deliver_observer(pasd_solver* s, pasd_observer_fn fn, void* user, HostView& hv) {
+  const int N = s->N;
+  const int64_t S = s->S;
+  const Ctl& c = *s->h_ctl;
+  hv.e.resize(S);
+  hv.z.resize(N);
+  hv.y.resize(N);
+  hv.u.resize(N);
+  hv.v.resize(N);
+  CK(cudaMemcpyAsync(hv.e.data(), s->E[c.ecur], S * sizeof(double), cudaMemcpyDeviceToHost, s->stream));
+  for (int n = 0; n < N; ++n) {
+    const ModeDev& m = s->modes[n];
+    hv.z[n].resize(S);
+    hv.y[n].resize(S);
+    hv.u[n].resize(m.I * m.R);
+    hv.v[n].resize(m.J * m.R);
+    k_materialize_z<<<1184, 256, 0, s->stream>>>(m, s->zbuf, S);
+    CK(cudaMemcpyAsync(hv.z[n].data(), s->zbuf, S * sizeof(double), cudaMemcpyDeviceToHost, s->stream));
+    CK(cudaMemcpyAsync(hv.y[n].data(), s->Y[n], S * sizeof(double), cudaMemcpyDeviceToHost, s->stream));
+    CK(cudaMemcpyAsync(hv.u[n].data(), m.U, m.I * m.R * sizeof(double), cudaMemcpyDeviceToHost, s->stream));
+    k_materialize_v<<<1184, 256, 0, s->stream>>>(m, s->xbuf);
+    CK(cudaMemcpyAsync(hv.v[n].data(), s->xbuf, m.J * m.R * sizeof(double), cudaMemcpyDeviceToHost, s->stream));
+  }
+  CK(cudaStreamSynchronize(s->stream));
+  std::vector<const double*> zp, yp, up, vp;
+  for (int n = 0; n < N; ++n) {
+    zp.push_back(hv.z[n].data());
+    yp.push_back(hv.y[n].data());
+    up.push_back(hv.u[n].data());
+    vp.push_back(hv.v[n].data());
+  }
+  pasd_iteration_view view{c.iter, c.mu_used_last, c.mu, c.resid, hv.e.data(), zp.data(), yp.data(), up.data(),
+                           vp.data()};
+  fn(&view, user);
+}
+
+void ensure_scratch(pasd_solver* s) {
+  if (!s->zbuf) s->zbuf = s->alloc<double>(s->S);
+  if (!s->xbuf) {
+    int64_t need = s->S;
+    for (const auto& m : s->modes) need = std::max<int64_t>(need, m.J * m.R);
+    s->xbuf = s->alloc<double>(need);
+  }
+}
+
+// Runs until stop or `iters` more iterations.
+void run_solver(pasd_solver* s, int iters, pasd_observer_fn obs, void* user) {
+  if (!s->loaded) fail(PASD_ERR_STATE, "pasd_b200: no tensor loaded");
+  sync_ctl(s);
+  if (s->h_ctl->done) return;
+  build_graph(s);
+  HostView hv;
+  if (obs) ensure_scratch(s);
+  int launched = 0;
+  s->launches_last_run = 0;
+  while (launched < iters) {
+    const int chunk = obs ? 1 : std::min(s->poll_every, iters - launched);
+    for (int k = 0; k < chunk; ++k) CK(cudaGraphLaunch(s->graph_exec, s->stream));
+    launched += chunk;
+    s->launches_last_run += (int64_t)chunk * s->launches_per_iter;
+    sync_ctl(s);
+    const Ctl& c = *s->h_ctl;
+    if (c.nan_flag)  // pasd.cpp:230-232
+      fail(PASD_ERR_NUMERICAL, "pasd: non-finite iterate at iteration " + std::to_string(c.iter));
+    if (obs) deliver_observer(s, obs, user, hv);
+    if (c.done) break;
+  }
+}
+
+void finalize_solver(pasd_solver* s, pasd_outputs* out) {
+  sync_ctl(s);
+  const Ctl c = *s->h_ctl;
+  const int N = s->N;
+  const int64_t S = s->S;
+  ensure_scratch(s);
+  cudaStream_t st = s->stream;
+  const double* e = s->E[c.ecur];
+  const double* ep = s->E[c.ecur ^ 1];
+  const double mu_used = c.mu_used_last;
+  // iteration bookkeeping
+  out->iters = c.iter;
+  out->converged = c.converged;
+  if (out->residual_history && c.iter > 0)
+    CK(cudaMemcpyAsync(out->residual_history, s->d_hist, c.iter * sizeof(double), cudaMemcpyDeviceToHost, st));
+  if (out->final_residuals)
+    for (int n = 0; n < N; ++n) out->final_residuals[n] = c.resid[n];
+  // X = weighted mean of Z_n (recovery.cpp:7-25) and optional Z_n
+  double wsum = 0.0;
+  for (double w : s->alphas) wsum += w;
+  const int blocks = 1184;
+  const bool want_x = out->x != nullptr;
+  for (int n = 0; n < N; ++n) {
+    const bool want_z = out->z && out->z[n];
+    if (!want_x && !want_z) continue;
+    k_materialize_z<<<blocks, 256, 0, st>>>(s->modes[n], s->zbuf, S);
+    if (want_x) k_accum_x<<<blocks, 256, 0, st>>>(s->xbuf, s->zbuf, s->alphas[n] / wsum, n == 0, S);
+    if (want_z) CK(cudaMemcpyAsync(out->z[n], s->zbuf, S * sizeof(double), cudaMemcpyDeviceToHost, st));
+  }
+  if (want_x) CK(cudaMemcpyAsync(out->x, s->xbuf, S * sizeof(double), cudaMemcpyDeviceToHost, st));
+  if (out->e) CK(cudaMemcpyAsync(out->e, e, S * sizeof(double), cudaMemcpyDeviceToHost, st));
+  // objective = ||E||_1 + sum_n lambda_n ||V_n||_*  (pasd.cpp:263-266)
+  std::vector<double> sums(blocks), maxs(blocks);
+  auto abs_stats = [&](const double* x, double* sum, double* mx) {
+    k_abs_stats<<<blocks, 256, 0, st>>>(x, S, s->d_stats, s->d_stats + 2048);
+    CK(cudaMemcpyAsync(sums.data(), s->d_stats, blocks * sizeof(double), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(maxs.data(), s->d_stats + 2048, blocks * sizeof(double), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    double a = 0.0, m = 0.0;
+    for (int b = 0; b < blocks; ++b) {
+      a += sums[b];
+      m = std::max(m, maxs[b]);
+    }
+    if (sum) *sum = a;
+    if (mx) *mx = m;
+  };
+  CK(cudaStreamSynchronize(st));
+  double l1 = 0.0;
+  abs_stats(e, &l1, nullptr);
+  double obj = l1;
+  for (int n = 0; n < N; ++n) obj += s->lambdas[n] * c.nuclear[n];
+  out->objective = obj;
+  // Yhat and certificate (pasd.cpp:246-258, 277-309)
+  const bool want_cert = c.converged && !(s->flags & PASD_FLAG_NO_CERTIFICATE);
+  for (int n = 0; n < N; ++n) {
+    const bool want_yh = out->y_hat && out->y_hat[n];
+    if (out->y && out->y[n])
+      CK(cudaMemcpyAsync(out->y[n], s->Y[n], S * sizeof(double), cudaMemcpyDeviceToHost, st));
+    if (!want_yh && !want_cert) continue;
+    k_yhat<<<blocks, 256, 0, st>>>(s->Y[n], e, ep, mu_used, s->zbuf, want_cert ? s->xbuf : nullptr, n == 0, S);
+    if (want_yh) CK(cudaMemcpyAsync(out->y_hat[n], s->zbuf, S * sizeof(double), cudaMemcpyDeviceToHost, st));
+  }
+  out->has_certificate = 0;
+  out->cert_epsilon_hat = out->cert_c = out->cert_bound = 0.0;
+  if (want_cert) {
+    double eps_hat = 0.0, tl1 = 0.0;
+    abs_stats(s->xbuf, nullptr, &eps_hat);
+    abs_stats(s->T, &tl1, nullptr);
+    const int k_star = c.iter - 1;
+    const double geom = s->rho * (1.0 + s->rho) / (s->rho - 1.0) + 0.5 / std::pow(s->rho, k_star);
+    double dim_sum = 0.0, lam_term = 0.0;
+    for (int n = 0; n < N; ++n) {
+      dim_sum += (double)S;
+      lam_term += s->lambdas[n] * (double)S * s->eps;
+    }
+    const double nn = (double)N;
+    const double cc = dim_sum * geom / (s->mu0 * nn * nn) + tl1;
+    out->has_certificate = 1;
+    out->cert_epsilon_hat = eps_hat;
+    out->cert_c = cc;
+    out->cert_bound = cc * eps_hat + lam_term;
+  }
+  CK(cudaStreamSynchronize(st));
+}
+
+int guarded_call(char* err, size_t errlen, const std::function<void()>& f) {
+  try {
+    f();
+    return PASD_OK;
+  } catch (const PasdError& e) {
+    set_err(err, errlen, e.what());
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    set_err(err, errlen, "pasd_b200: host allocation failed");
+    return PASD_ERR_CUDA;
+  } catch (const std::exception& e) {
+    set_err(err, errlen, e.what());
+    return PASD_ERR_CUDA;
+  }
+}
+
+}  // namespace
+
+// ============================================================================ C ABI
+extern "C" {
+
+int pasd_b200_abi_version(void) { return PASD_B200_ABI_VERSION; }
+
+const char* pasd_b200_build_info(void) {
+  return "pasd_b200 sm_100a fp64; kernels: polar,contract_A,gram,svt,update,finish,contract_W";
+}
+
+int pasd_b200_validate(const pasd_options* opt, char* errbuf, size_t errlen) {
+  return guarded_call(errbuf, errlen, [&] { validate_options(opt); });
+}
+
+int pasd_b200_default_lambdas(int32_t order, const int64_t* dims, double* out, char* errbuf, size_t errlen) {
+  return guarded_call(errbuf, errlen, [&] {
+    if (order < 1 || !dims) fail(PASD_ERR_ARGUMENT, "tensor order must be at least 1");
+    std::vector<int64_t> d(dims, dims + order);
+    const int64_t total = dims_product(d);  // pasd.cpp:51-60
+    const double n_modes = (double)order;
+    for (int n = 0; n < order; ++n) {
+      const double big = (double)std::max(d[n], total / d[n]);
+      out[n] = std::sqrt(big) / n_modes;
+    }
+  });
+}
+
+int pasd_b200_default_rank_bound(int64_t target_rank, int64_t* out, char* errbuf, size_t errlen) {
+  return guarded_call(errbuf, errlen, [&] {
+    if (target_rank < 1) fail(PASD_ERR_ARGUMENT, "target rank must be positive");  // pasd.cpp:62-66
+    *out = (12 * target_rank) / 10;
+  });
+}
+
+int pasd_b200_solver_create(const pasd_options* opt, const pasd_shard* shard, pasd_solver** out, char* errbuf,
+                            size_t errlen) {
+  return guarded_call(errbuf, errlen, [&] {
+    if (!out) fail(PASD_ERR_ARGUMENT, "pasd_b200: null output handle");
+    *out = create_solver(opt, shard);
+  });
+}
+
+int pasd_b200_solver_load(pasd_solver* s, const double* t, int t_is_device, char* errbuf, size_t errlen) {
+  return guarded_call(errbuf, errlen, [&] {
+    if (!s || !t) fail(PASD_ERR_ARGUMENT, "pasd_b200: null argument");
+    CK(cudaSetDevice(s->device));
+    load_tensor(s, t, t_is_device);
+  });
+}
+
+int pasd_b200_solver_reset(pasd_solver* s, char* errbuf, size_t errlen) {
+  return guarded_call(errbuf, errlen, [&] {
+    if (!s) fail(PASD_ERR_ARGUMENT, "pasd_b200: null solver");
+    CK(cudaSetDevice(s->device));
+    reset_state(s);
+    CK(cudaStreamSynchronize(s->stream));
+  });
+}
+
+int pasd_b200_solver_run(pasd_solver* s, int32_t iters, int32_t* iters_done, int32_t* converged, char* errbuf,
+                         size_t errlen) {
+  return guarded_call(errbuf, errlen, [&] {
+    if (!s) fail(PASD_ERR_ARGUMENT, "pasd_b200: null solver");
+    CK(cudaSetDevice(s->device));
+    run_solver(s, iters, nullptr, nullptr);
+    if (iters_done) *iters_done = s->h_ctl->iter;
+    if (converged) *converged = s->h_ctl->converged;
+  });
+}
+
+int pasd_b200_solver_finalize(pasd_solver* s, pasd_outputs* out, char* errbuf, size_t errlen) {
+  return guarded_call(errbuf, errlen, [&] {
+    if (!s || !out) fail(PASD_ERR_ARGUMENT, "pasd_b200: null argument");
+    CK(cudaSetDevice(s->device));
+    finalize_solver(s, out);
+  });
+}
+
+const double* pasd_b200_solver_device_e(const pasd_solver* s) {
+  if (!s) return nullptr;
+  return s->E[s->h_ctl ? s->h_ctl->ecur : 0];
+}
+
+void* pasd_b200_solver_stream(const pasd_solver* s) { return s ? (void*)s->stream : nullptr; }
+
+int64_t pasd_b200_solver_launches(const pasd_solver* s) { return s ? s->launches_last_run : 0; }
+
+void pasd_b200_solver_destroy(pasd_solver* s) {
+  if (s) {
+    cudaSetDevice(s->device);
+    delete s;
+  }
+}
+
+int pasd_b200_recover(const double* t, const pasd_options* opt, pasd_outputs* out, pasd_observer_fn observer,
+                      void* user, char* errbuf, size_t errlen) {
+  pasd_solver* s = nullptr;
+  const int rc = guarded_call(errbuf, errlen, [&] {
+    if (!t || !out) fail(PASD_ERR_ARGUMENT, "pasd_b200: null argument");
+    s = create_solver(opt, nullptr);
+    load_tensor(s, t, 0);
+    run_solver(s, s->maxiter, observer, user);
+    finalize_solver(s, out);
+  });
+  pasd_b200_solver_destroy(s);
+  return rc;
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------- linops ABI
+namespace {
+
+struct TmpDev {
+  std::vector<void*> ptrs;
+  ~TmpDev() {
+    for (void* p : ptrs) cudaFree(p);
+  }
+  template <class T>
+  T* alloc(size_t n) {
+    T* p = dalloc<T>(n);
+    ptrs.push_back(p);
+    return p;
+  }
+};
+
+__global__ void k_set_ctl(Ctl* ctl, double mu, double vnorm2) {
+  ctl->mu = mu;
+  ctl->mu_used_last = mu;
+  ctl->done = 0;
+  ctl->ecur = 0;
+  ctl->order = 1;
+  ctl->vnorm2[0] = vnorm2;
+}
+
+void device_svt(const double* m_h, int64_t rows, int64_t cols, double tau, double* out_h, int32_t* kept, int device) {
+  if (tau < 0.0 || !std::isfinite(tau)) fail(PASD_ERR_ARGUMENT, "svt: threshold must be a nonnegative finite number");
+  if (rows < 1 || cols < 1) fail(PASD_ERR_ARGUMENT, "thin_svd: matrix must be nonempty");
+  for (int64_t i = 0; i < rows * cols; ++i)
+    if (!std::isfinite(m_h[i])) fail(PASD_ERR_ARGUMENT, "thin_svd: input contains non-finite entries");
+  if (tau == 0.0) {  // linops.cpp:80-81
+    std::memcpy(out_h, m_h, sizeof(double) * rows * cols);
+    if (kept) *kept = (int32_t)std::min(rows, cols);
+    return;
+  }
+  if (rows > PASD_MAX_RANK)
+    fail(PASD_ERR_ARGUMENT, "pasd_b200: svt supports at most " + std::to_string(PASD_MAX_RANK) + " rows");
+  CK(cudaSetDevice(device));
+  TmpDev t;
+  ModeDev m{};
+  m.inner = 1;
+  m.I = rows;
+  m.outer = cols;
+  m.J = cols;
+  m.R = (int)rows;
+  m.lambda = tau;
+  const int R = m.R;
+  m.A = t.alloc<double>(rows * cols);
+  m.U = t.alloc<double>(R * R);
+  m.UM = t.alloc<double>(R * R);
+  m.M = t.alloc<double>(R * R);
+  m.Gram = t.alloc<double>(R * R);
+  m.P = t.alloc<double>(R * R);
+  m.sig = t.alloc<double>(R);
+  m.nkc_g = (int)std::max<int64_t>(1, std::min<int64_t>((m.J + GR_KC - 1) / GR_KC, 296));
+  m.Gpart = t.alloc<double>((size_t)m.nkc_g * R * R);
+  std::vector<double> eye(R * R, 0.0);
+  for (int i = 0; i < R; ++i) eye[i + R * i] = 1.0;
+  CK(cudaMemcpy(m.U, eye.data(), sizeof(double) * R * R, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(m.A, m_h, sizeof(double) * rows * cols, cudaMemcpyHostToDevice));
+  ModePack pack{};
+  pack.order = 1;
+  pack.m[0] = m;
+  ModePack* d_pack = t.alloc<ModePack>(1);
+  CK(cudaMemcpy(d_pack, &pack, sizeof(pack), cudaMemcpyHostToDevice));
+  Ctl* ctl = t.alloc<Ctl>(1);
+  k_set_ctl<<<1, 1>>>(ctl, 1.0, 0.0);
+  k_gram<<<m.nkc_g, kThreads>>>(m, ctl);
+  const size_t smem = small_ws_bytes(R);
+  CK(cudaFuncSetAttribute(k_svt, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  k_svt<<<1, kSmallThreads, smem>>>(d_pack, ctl);
+  double* V = t.alloc<double>(rows * cols);
+  k_materialize_v<<<256, 256>>>(m, V);
+  CK(cudaGetLastError());
+  CK(cudaMemcpy(out_h, V, sizeof(double) * rows * cols, cudaMemcpyDeviceToHost));
+  Ctl hc;
+  CK(cudaMemcpy(&hc, ctl, sizeof(Ctl), cudaMemcpyDeviceToHost));
+  if (kept) *kept = hc.keep[0];
+}
+
+void device_procrustes(const double* g_h, int64_t I, int64_t P, const double* v_h, int64_t R64, const double* u_prev,
+                       double* u_out, int32_t* degenerate, int32_t* rank, int device) {
+  if (R64 > I) fail(PASD_ERR_ARGUMENT, "procrustes: v has more rows than g (R must not exceed I)");
+  if (I < 1 || P < 1 || R64 < 1) fail(PASD_ERR_ARGUMENT, "thin_svd: matrix must be nonempty");
+  if (R64 > PASD_MAX_RANK)
+    fail(PASD_ERR_ARGUMENT, "pasd_b200: procrustes supports at most " + std::to_string(PASD_MAX_RANK) + " rows of v");
+  CK(cudaSetDevice(device));
+  const int R = (int)R64;
+  TmpDev t;
+  ModeDev m{};
+  m.inner = 1;
+  m.I = I;
+  m.outer = P;
+  m.J = P;
+  m.R = R;
+  const int64_t IR = I * R;
+  double* G = t.alloc<double>(I * P);
+  double* Z0 = t.alloc<double>(I * P);
+  CK(cudaMemset(Z0, 0, sizeof(double) * I * P));
+  CK(cudaMemcpy(G, g_h, sizeof(double) * I * P, cudaMemcpyHostToDevice));
+  m.A = t.alloc<double>(R * P);
+  CK(cudaMemcpy(m.A, v_h, sizeof(double) * R * P, cudaMemcpyHostToDevice));
+  m.U = t.alloc<double>(IR);
+  std::vector<double> up(IR, 0.0);
+  if (u_prev)
+    std::memcpy(up.data(), u_prev, sizeof(double) * IR);
+  else
+    for (int i = 0; i < R; ++i) up[i + I * i] = 1.0;
+  CK(cudaMemcpy(m.U, up.data(), sizeof(double) * IR, cudaMemcpyHostToDevice));
+  m.M = t.alloc<double>(R * R);
+  std::vector<double> eye(R * R, 0.0);
+  for (int i = 0; i < R; ++i) eye[i + R * i] = 1.0;
+  CK(cudaMemcpy(m.M, eye.data(), sizeof(double) * R * R, cudaMemcpyHostToDevice));
+  m.nib_w = (int)((I + CW_IT - 1) / CW_IT);
+  m.nkc_w = (int)std::max<int64_t>(1, std::min<int64_t>((P + CW_KC - 1) / CW_KC, std::max(1, 592 / m.nib_w)));
+  m.Wpart = t.alloc<double>((size_t)m.nkc_w * IR);
+  m.gpart = t.alloc<double>((size_t)m.nkc_w * m.nib_w);
+  m.scratch = t.alloc<double>(3 * IR);
+  Ctl* ctl = t.alloc<Ctl>(1);
+  double* vn = t.alloc<double>(1);
+  k_sumsq<<<1, 1024>>>(m.A, R * P, vn);
+  double vnorm2 = 0.0;
+  CK(cudaMemcpy(&vnorm2, vn, sizeof(double), cudaMemcpyDeviceToHost));
+  k_set_ctl<<<1, 1>>>(ctl, 1.0, vnorm2);
+  const dim3 grid(m.nkc_w, m.nib_w);
+  switch (rpt_for(R)) {
+    case 2: k_contract_W<2><<<grid, kThreads>>>(m, G, Z0, Z0, Z0, ctl); break;
+    case 4: k_contract_W<4><<<grid, kThreads>>>(m, G, Z0, Z0, Z0, ctl); break;
+    case 8: k_contract_W<8><<<grid, kThreads>>>(m, G, Z0, Z0, Z0, ctl); break;
+    default: k_contract_W<16><<<grid, kThreads>>>(m, G, Z0, Z0, Z0, ctl); break;
+  }
+  ModePack pack{};
+  pack.order = 1;
+  pack.m[0] = m;
+  ModePack* d_pack = t.alloc<ModePack>(1);
+  CK(cudaMemcpy(d_pack, &pack, sizeof(pack), cudaMemcpyHostToDevice));
+  const size_t smem = small_ws_bytes(R);
+  CK(cudaFuncSetAttribute(k_polar, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  k_polar<<<1, kSmallThreads, smem>>>(d_pack, ctl);
+  CK(cudaGetLastError());
+  Ctl hc;
+  CK(cudaMemcpy(&hc, ctl, sizeof(Ctl), cudaMemcpyDeviceToHost));
+  if (degenerate) *degenerate = hc.degenerate[0];
+  if (rank) *rank = hc.polar_rank[0];
+  if (!hc.degenerate[0]) CK(cudaMemcpy(u_out, m.U, sizeof(double) * IR, cudaMemcpyDeviceToHost));
+}
+
+}  // namespace
+
+extern "C" {
+
+int pasd_b200_svt(const double* m, int64_t rows, int64_t cols, double tau, double* out, int32_t* kept, int32_t device,
+                  char* errbuf, size_t errlen) {
+  return guarded_call(errbuf, errlen, [&] {
+    if (!m || !out) fail(PASD_ERR_ARGUMENT, "pasd_b200: null argument");
+    device_svt(m, rows, cols, tau, out, kept, device);
+  });
+}
+
+int pasd_b200_procrustes(const double* g, int64_t i_rows, int64_t p_cols, const double* v, int64_t r_rows,
+                         const double* u_prev, double* u_out, int32_t* degenerate, int32_t* rank, int32_t device,
+                         char* errbuf, size_t errlen) {
+  return guarded_call(errbuf, errlen, [&] {
+    if (!g || !v || !u_out) fail(PASD_ERR_ARGUMENT, "pasd_b200: null argument");
+    device_procrustes(g, i_rows, p_cols, v, r_rows, u_prev, u_out, degenerate, rank, device);
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,238 @@
+"""Host-side mirror of the reference entry point over the C-ABI library.
+
+``pasd_recover`` is the drop-in for ``tenrec::pasd_recover``
+(proj/include/tenrec/pasd.hpp:65-66): it hands the host tensor to
+``pasd_b200_recover`` (include/pasd_b200.h), which runs every per-iteration
+step as sm_100a kernels.  There is no CPU fallback: if ``libpasd_b200.so`` is
+missing or no CUDA device is present the call raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from typing import Optional, Sequence
+
+import numpy as np
+
+from . import _abi
+from .api import (ArgumentError, DeviceError, PasdConfig, RecoveryResult, as_tensor, build_options,
+                  count_checks, raise_for_status, run_recover)
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libpasd_b200.so")
+_LIB = None
+
+
+def lib():
+    """Load libpasd_b200.so (raises if it was not built)."""
+    global _LIB
+    if _LIB is None:
+        if not os.path.exists(LIB_PATH):
+            raise DeviceError(f"{LIB_PATH} not built: run __graft_entry__.build() (make -C csrc)")
+        L = C.CDLL(LIB_PATH)
+        L.pasd_b200_recover.restype = C.c_int
+        L.pasd_b200_recover.argtypes = [_abi.c_double_p, C.POINTER(_abi.PasdOptions), C.POINTER(_abi.PasdOutputs),
+                                        _abi.PasdObserverFn, C.c_void_p, C.c_char_p, C.c_size_t]
+        L.pasd_b200_validate.restype = C.c_int
+        L.pasd_b200_validate.argtypes = [C.POINTER(_abi.PasdOptions), C.c_char_p, C.c_size_t]
+        L.pasd_b200_default_lambdas.restype = C.c_int
+        L.pasd_b200_default_lambdas.argtypes = [C.c_int32, _abi.c_int64_p, _abi.c_double_p, C.c_char_p, C.c_size_t]
+        L.pasd_b200_default_rank_bound.restype = C.c_int
+        L.pasd_b200_default_rank_bound.argtypes = [C.c_int64, _abi.c_int64_p, C.c_char_p, C.c_size_t]
+        L.pasd_b200_solver_create.restype = C.c_int
+        L.pasd_b200_solver_create.argtypes = [C.POINTER(_abi.PasdOptions), C.POINTER(_abi.PasdShard),
+                                              C.POINTER(C.c_void_p), C.c_char_p, C.c_size_t]
+        L.pasd_b200_solver_load.restype = C.c_int
+        L.pasd_b200_solver_load.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_char_p, C.c_size_t]
+        L.pasd_b200_solver_reset.restype = C.c_int
+        L.pasd_b200_solver_reset.argtypes = [C.c_void_p, C.c_char_p, C.c_size_t]
+        L.pasd_b200_solver_run.restype = C.c_int
+        L.pasd_b200_solver_run.argtypes = [C.c_void_p, C.c_int32, C.POINTER(C.c_int32), C.POINTER(C.c_int32),
+                                           C.c_char_p, C.c_size_t]
+        L.pasd_b200_solver_finalize.restype = C.c_int
+        L.pasd_b200_solver_finalize.argtypes = [C.c_void_p, C.POINTER(_abi.PasdOutputs), C.c_char_p, C.c_size_t]
+        L.pasd_b200_solver_device_e.restype = C.c_void_p
+        L.pasd_b200_solver_device_e.argtypes = [C.c_void_p]
+        L.pasd_b200_solver_stream.restype = C.c_void_p
+        L.pasd_b200_solver_stream.argtypes = [C.c_void_p]
+        L.pasd_b200_solver_launches.restype = C.c_int64
+        L.pasd_b200_solver_launches.argtypes = [C.c_void_p]
+        L.pasd_b200_solver_destroy.restype = None
+        L.pasd_b200_solver_destroy.argtypes = [C.c_void_p]
+        L.pasd_b200_abi_version.restype = C.c_int
+        L.pasd_b200_build_info.restype = C.c_char_p
+        _LIB = L
+    return _LIB
+
+
+def _err():
+    return C.create_string_buffer(1024)
+
+
+def validate_config(config: PasdConfig, dims: Sequence[int]) -> None:
+    """PasdConfig::validate (pasd.cpp:12-49) through the C-ABI."""
+    dims = [int(d) for d in dims]
+    count_checks(dims, config)
+    opt, keep = build_options(dims, config)
+    err = _err()
+    raise_for_status(lib().pasd_b200_validate(C.byref(opt), err, len(err)), err)
+
+
+def default_lambdas(dims: Sequence[int]):
+    d = np.asarray([int(x) for x in dims], dtype=np.int64)
+    out = np.zeros(len(d))
+    err = _err()
+    rc = lib().pasd_b200_default_lambdas(len(d), d.ctypes.data_as(_abi.c_int64_p), _abi.dptr(out), err, len(err))
+    raise_for_status(rc, err)
+    return [float(x) for x in out]
+
+
+def default_rank_bound(target_rank: int) -> int:
+    out = C.c_int64(0)
+    err = _err()
+    rc = lib().pasd_b200_default_rank_bound(int(target_rank), C.byref(out), err, len(err))
+    raise_for_status(rc, err)
+    return int(out.value)
+
+
+def pasd_recover(t, config: PasdConfig, observer=None, *, device: int = 0, fixed_iters: bool = False,
+                 want_z: bool = True, want_y: bool = True, poll_every: int = 0) -> RecoveryResult:
+    """Drop-in for tenrec::pasd_recover (pasd.hpp:65-66) on a B200."""
+    flags = _abi.PASD_FLAG_FIXED_ITERS if fixed_iters else 0
+    return run_recover(lib().pasd_b200_recover, t, config, observer, flags=flags, want_z=want_z, want_y=want_y,
+                       device=device, poll_every=poll_every)
+
+
+class Solver:
+    """Device-resident solver handle (``pasd_b200_solver_*``) for benchmarks
+    and sharded runs.  ``t`` may be a host numpy array or, with
+    ``t_is_device``, an integer device pointer (e.g. ``torch_tensor.data_ptr()``)."""
+
+    def __init__(self, dims: Sequence[int], config: PasdConfig, *, device: int = 0, fixed_iters: bool = False,
+                 poll_every: int = 0, shard: Optional[_abi.PasdShard] = None):
+        self.dims = [int(d) for d in dims]
+        self.config = config
+        count_checks(self.dims, config)
+        flags = _abi.PASD_FLAG_FIXED_ITERS if fixed_iters else 0
+        self._opt, self._keep = build_options(self.dims, config, device=device, flags=flags, poll_every=poll_every)
+        self._h = C.c_void_p()
+        err = _err()
+        rc = lib().pasd_b200_solver_create(C.byref(self._opt), C.byref(shard) if shard is not None else None,
+                                           C.byref(self._h), err, len(err))
+        raise_for_status(rc, err)
+
+    def load(self, t, t_is_device: bool = False) -> None:
+        err = _err()
+        if t_is_device:
+            ptr = C.c_void_p(int(t))
+            self._t_keep = None
+        else:
+            flat = np.ravel(as_tensor(t), order="F")
+            self._t_keep = flat
+            ptr = C.c_void_p(flat.ctypes.data)
+        rc = lib().pasd_b200_solver_load(self._h, ptr, 1 if t_is_device else 0, err, len(err))
+        raise_for_status(rc, err)
+
+    def reset(self) -> None:
+        err = _err()
+        raise_for_status(lib().pasd_b200_solver_reset(self._h, err, len(err)), err)
+
+    def run(self, iters: int):
+        done = C.c_int32(0)
+        conv = C.c_int32(0)
+        err = _err()
+        rc = lib().pasd_b200_solver_run(self._h, int(iters), C.byref(done), C.byref(conv), err, len(err))
+        raise_for_status(rc, err)
+        return int(done.value), bool(conv.value)
+
+    @property
+    def stream(self) -> int:
+        return int(lib().pasd_b200_solver_stream(self._h) or 0)
+
+    @property
+    def launches(self) -> int:
+        return int(lib().pasd_b200_solver_launches(self._h))
+
+    def finalize(self, want_x=True, want_e=True, want_z=False, want_y=False):
+        n = len(self.dims)
+        total = int(np.prod(self.dims))
+        x = np.empty(total) if want_x else None
+        e = np.empty(total) if want_e else None
+        z = [np.empty(total) for _ in range(n)] if want_z else None
+        y = [np.empty(total) for _ in range(n)] if want_y else None
+        yh = [np.empty(total) for _ in range(n)] if want_y else None
+        hist = np.zeros(max(1, int(self.config.maxiter)))
+        fres = np.zeros(n)
+        out = _abi.PasdOutputs()
+        out.x, out.e = _abi.dptr(x), _abi.dptr(e)
+        zp, yp, yhp = _abi.ptr_array(z), _abi.ptr_array(y), _abi.ptr_array(yh)
+        out.z, out.y, out.y_hat = zp, yp, yhp
+        out.residual_history = _abi.dptr(hist)
+        out.final_residuals = _abi.dptr(fres)
+        err = _err()
+        raise_for_status(lib().pasd_b200_solver_finalize(self._h, C.byref(out), err, len(err)), err)
+        shape = tuple(self.dims)
+
+        def rs(a):
+            return None if a is None else a.reshape(shape, order="F")
+
+        from .api import Certificate
+        return RecoveryResult(
+            x=rs(x), e=rs(e), z=[rs(a) for a in z] if z else None, iters=int(out.iters),
+            converged=bool(out.converged), residual_history=[float(h) for h in hist[: out.iters]],
+            final_residuals=[float(r) for r in fres], objective=float(out.objective),
+            certificate=Certificate(out.cert_epsilon_hat, out.cert_c, out.cert_bound) if out.has_certificate else None,
+            y=[rs(a) for a in y] if y else None, y_hat=[rs(a) for a in yh] if yh else None)
+
+    def close(self) -> None:
+        if getattr(self, "_h", None) and self._h.value:
+            lib().pasd_b200_solver_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def svt(m, tau: float, *, device: int = 0):
+    """SVT_tau(m) on the device (linops.cpp:78-91); returns (V, kept)."""
+    m = np.asfortranarray(np.asarray(m, dtype=np.float64))
+    if m.ndim != 2:
+        raise ArgumentError("svt: expected a matrix")
+    out = np.empty(m.shape, order="F")
+    kept = C.c_int32(0)
+    err = _err()
+    L = lib()
+    L.pasd_b200_svt.restype = C.c_int
+    rc = L.pasd_b200_svt(_abi.dptr(np.ravel(m, order="F")), C.c_int64(m.shape[0]), C.c_int64(m.shape[1]),
+                         C.c_double(tau), out.ctypes.data_as(_abi.c_double_p), C.byref(kept), C.c_int32(device),
+                         err, C.c_size_t(len(err)))
+    raise_for_status(rc, err)
+    return out, int(kept.value)
+
+
+def procrustes(g, v, u_prev=None, *, device: int = 0):
+    """polar(g v^T) on the device (linops.cpp:93-104).
+
+    Returns (U or None for the degenerate case, numerical rank of g v^T)."""
+    g = np.asfortranarray(np.asarray(g, dtype=np.float64))
+    v = np.asfortranarray(np.asarray(v, dtype=np.float64))
+    if g.ndim != 2 or v.ndim != 2:
+        raise ArgumentError("procrustes: expected matrices")
+    if g.shape[1] != v.shape[1]:
+        raise ArgumentError("procrustes: g and v must have the same number of columns")
+    out = np.empty((g.shape[0], v.shape[0]), order="F")
+    up = None if u_prev is None else np.ravel(np.asfortranarray(np.asarray(u_prev, dtype=np.float64)), order="F")
+    deg = C.c_int32(0)
+    rank = C.c_int32(0)
+    err = _err()
+    L = lib()
+    L.pasd_b200_procrustes.restype = C.c_int
+    rc = L.pasd_b200_procrustes(_abi.dptr(np.ravel(g, order="F")), C.c_int64(g.shape[0]), C.c_int64(g.shape[1]),
+                                _abi.dptr(np.ravel(v, order="F")), C.c_int64(v.shape[0]), _abi.dptr(up),
+                                out.ctypes.data_as(_abi.c_double_p), C.byref(deg), C.byref(rank), C.c_int32(device),
+                                err, C.c_size_t(len(err)))
+    raise_for_status(rc, err)
+    return (None if deg.value else out), int(rank.value)
