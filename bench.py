@@ -1,0 +1,339 @@
+#!/usr/bin/env python
+"""PASD ADMM iteration throughput on B200 (BASELINE.json metric).
+
+One "step" = one PASD ADMM iteration (Algorithm 1, proj/src/pasd.cpp:168-244)
+over the resident state of the configured workload.  Default workload: C5,
+1000^3 fp64, Tucker/solver rank 50, 10% corruption (BASELINE configs[4], the
+largest config of the 1/2/4/8-GPU sweep).
+
+  python bench.py [--gpus N --steps K --warmup W --config c5 --impl ours|reference]
+
+Prints ONE JSON line (rank 0).  `value` = iterations/s with the state resident
+in HBM (CUDA events on the solver's stream, max over ranks); `e2e` = the same
+metric through the C-ABI drop-in pasd_b200_recover with host buffers (H2D of
+T, the loop, finalisation, D2H of X and E inside the timed region);
+`roofline` = the dominant kernel's achieved throughput from CUDA events around
+each kernel; `cpu_baseline` = the reference restatement (oracle/) on the host.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+
+def parse_args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default=os.environ.get("PASD_BENCH_CONFIG", "c5"))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--profile-iters", type=int, default=3)
+    return ap.parse_args()
+
+
+def load_peaks():
+    peaks = {"hbm_gbs": 6538.9, "source_hbm": "fallback"}
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        peaks["hbm_gbs"] = float(d["hbm_gbs"])
+        peaks["source_hbm"] = "measured (MEASURED_PEAKS.json)"
+    except Exception:
+        pass
+    # FP64 pipe: measured on this pool with tools/fp64_peak.cu (profiles/r01_fp64_peak.txt):
+    # DMMA m16n8k4 37.0 TF/s, DFMA 34.1 TF/s (burst).
+    peaks["fp64_tflops"] = 37.0
+    peaks["source_fp64"] = "measured DMMA burst, profiles/r01_fp64_peak.txt"
+    return peaks
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.path = None
+
+    def start(self):
+        try:
+            fd, self.path = tempfile.mkstemp(suffix=".csv")
+            os.close(fd)
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+            time.sleep(0.25)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        out = {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        if self.proc is None:
+            return out
+        time.sleep(0.15)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        with open(self.path) as f:
+            for line in f:
+                parts = [p.strip() for p in line.split(",")]
+                if len(parts) < 7:
+                    continue
+                try:
+                    sm.append(float(parts[0]))
+                    mx.append(float(parts[1]))
+                except ValueError:
+                    continue
+                for nm, v in zip(names, parts[3:7]):
+                    if v.lower().startswith("active"):
+                        reasons.add(nm)
+        os.unlink(self.path)
+        if sm:
+            out = {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                   "samples": len(sm)}
+        return out
+
+
+def cpu_sample_dims(w):
+    """Bounded CPU sample of workload w: the full config when small, else the
+    leading slab (I_1 x I_2 x 50) with the same solver ranks."""
+    if w.size <= 8_000_000:
+        return tuple(w.dims), tuple(w.tucker), tuple(w.ranks)
+    d3 = max(w.ranks[2], 50)
+    return (w.dims[0], w.dims[1], d3), (w.tucker[0], w.tucker[1], min(w.tucker[2], d3)), \
+        (w.ranks[0], w.ranks[1], min(w.ranks[2], d3))
+
+
+def cpu_baseline(w, threads: int, iters: int = 3):
+    """Time the oracle (reference restatement) per iteration on a bounded sample.
+
+    Per-iteration time = median gap between observer callbacks after the first
+    iteration (reference timing pattern: warm-up excluded, bench.cpp:274-286)."""
+    import oracle
+    from paper_1712_09999_b200 import _abi
+    from paper_1712_09999_b200.api import PasdConfig
+
+    dims, tucker, ranks = cpu_sample_dims(w)
+    L0 = oracle.gen_tucker(dims, tucker, seed=0, kind=1 if w.kind == "nonneg" else 0)
+    T = oracle.corrupt_sparse(L0, w.rho, seed=0, mode=0 if w.mode == "add" else 1, lo=w.noise[0], hi=w.noise[1])
+    total = int(np.prod(dims))
+    n = float(len(dims))
+    lam = [math.sqrt(float(max(d, total // d))) / n for d in dims]
+    stamps = []
+    cb = _abi.PasdObserverFn(lambda v, u: stamps.append(time.perf_counter()))
+    cfg = PasdConfig(lambdas=lam, ranks=list(ranks), maxiter=iters, eps=w.eps)
+    oracle.pasd_recover(T, cfg, observer=cb, fixed_iters=True, threads=threads, want_z=False, want_y=False)
+    gaps = [b - a for a, b in zip(stamps[:-1], stamps[1:])]
+    per_iter = statistics.median(gaps)
+    elem_rate = total / per_iter
+    return {
+        "value": elem_rate / w.size,
+        "unit": "iter/s",
+        "cores": threads,
+        "kind": "port",
+        "elem_iters_per_s": elem_rate,
+        "sample": f"oracle/ (C++ restatement of proj/src/pasd.cpp, OpenBLAS dgesdd/dgemm) on dims {list(dims)} "
+                  f"ranks {list(ranks)}, {iters} fixed iterations, per-iteration time = median gap between "
+                  f"iterations 2..{iters}; value = sample elem*iters/s / S({w.name}) = {per_iter:.3f} s/iter "
+                  f"on {total} elements",
+    }
+
+
+def e2e_recover(w, T_dev, steps: int):
+    """Whole-solve throughput through the C-ABI drop-in with host buffers."""
+    import torch
+    from paper_1712_09999_b200 import _abi, solver as S
+    from paper_1712_09999_b200.api import PasdConfig, build_options, raise_for_status
+
+    total = w.size
+    Th = torch.empty(total, dtype=torch.float64, pin_memory=True)
+    Th.copy_(T_dev.view(-1))
+    xh = torch.empty(total, dtype=torch.float64, pin_memory=True)
+    eh = torch.empty(total, dtype=torch.float64, pin_memory=True)
+    cfg = PasdConfig(lambdas=w.lambdas(), ranks=list(w.ranks), eps=w.eps, maxiter=steps)
+    opt, keep = build_options(list(w.dims), cfg, flags=_abi.PASD_FLAG_FIXED_ITERS, poll_every=steps)
+    out = _abi.PasdOutputs()
+    out.x = C.cast(C.c_void_p(xh.data_ptr()), _abi.c_double_p)
+    out.e = C.cast(C.c_void_p(eh.data_ptr()), _abi.c_double_p)
+    hist = np.zeros(steps)
+    fres = np.zeros(len(w.dims))
+    out.residual_history = _abi.dptr(hist)
+    out.final_residuals = _abi.dptr(fres)
+    err = C.create_string_buffer(1024)
+    tptr = C.cast(C.c_void_p(Th.data_ptr()), _abi.c_double_p)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    rc = S.lib().pasd_b200_recover(tptr, C.byref(opt), C.byref(out), _abi.PasdObserverFn(), None, err, len(err))
+    t1 = time.perf_counter()
+    raise_for_status(rc, err)
+    sec = t1 - t0
+    return {
+        "value": steps / sec,
+        "unit": "iter/s",
+        "h2d_bytes_per_step": 8 * total / steps,
+        "d2h_bytes_per_step": (16 * total + 8 * steps) / steps,
+        "seconds": sec,
+        "iters": int(out.iters),
+        "note": "one pasd_b200_recover call (C-ABI) on pinned host buffers: H2D of T, "
+                f"{steps} fixed iterations, finalisation, D2H of X and E; bytes amortised per iteration",
+    }
+
+
+def roofline_from_profile(prof, peaks, iters):
+    # Dominant kernel = largest share of device time.
+    name = max(prof, key=lambda k: prof[k]["ms"])
+    p = prof[name]
+    per_launch_ms = p["ms"] / max(1, p["launches"])
+    launches_per_iter = p["launches"] / max(1, iters)
+    bytes_per_launch = p["bytes"] / max(1.0, launches_per_iter)
+    flops_per_launch = p["flops"] / max(1.0, launches_per_iter)
+    gbs = bytes_per_launch / (per_launch_ms * 1e-3) / 1e9
+    tfs = flops_per_launch / (per_launch_ms * 1e-3) / 1e12
+    hbm_frac = gbs / peaks["hbm_gbs"]
+    fp_frac = tfs / peaks["fp64_tflops"]
+    intensity = flops_per_launch / max(1.0, bytes_per_launch)
+    ridge = peaks["fp64_tflops"] * 1e12 / (peaks["hbm_gbs"] * 1e9)
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tpath):
+        try:
+            with open(tpath) as f:
+                traffic = json.load(f).get(name)
+        except Exception:
+            traffic = None
+    total_ms = sum(v["ms"] for v in prof.values())
+    shares = {k: round(v["ms"] / total_ms, 4) for k, v in prof.items()}
+    if intensity > ridge:
+        r = {"bound": "fp64", "achieved": round(tfs, 3), "peak": peaks["fp64_tflops"], "unit": "TFLOP/s",
+             "frac": round(fp_frac, 4), "peak_source": peaks["source_fp64"]}
+    else:
+        r = {"bound": "hbm", "achieved": round(gbs, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
+             "frac": round(hbm_frac, 4), "peak_source": peaks["source_hbm"]}
+    r.update({"kernel": name, "traffic": traffic, "algorithmic_bytes_per_launch": bytes_per_launch,
+              "algorithmic_flops_per_launch": flops_per_launch, "ms_per_launch": round(per_launch_ms, 4),
+              "hbm_gbs": round(gbs, 1), "fp64_tflops": round(tfs, 3), "kernel_time_shares": shares})
+    return r
+
+
+def main():
+    args = parse_args()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    from paper_1712_09999_b200.workloads import WORKLOADS
+
+    w = WORKLOADS[args.config]
+
+    if args.impl == "reference":
+        if rank != 0:
+            return 0
+        threads = os.cpu_count() or 1
+        cb = cpu_baseline(w, threads, iters=max(3, min(args.steps, 6)))
+        line = {
+            "impl": "reference", "metric": "PASD ADMM iters/s", "value": cb["value"], "unit": "iter/s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": w.name, "dims": list(w.dims), "ranks": list(w.ranks)},
+            "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
+            "e2e": {"value": cb["value"], "unit": "iter/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "elem_iters_per_s": cb["elem_iters_per_s"],
+        }
+        print(json.dumps(line), flush=True)
+        return 0
+
+    import torch
+    import paper_1712_09999_b200 as pb
+    from paper_1712_09999_b200.api import PasdConfig
+    from paper_1712_09999_b200.workloads import generate_gpu
+
+    if world > 1:
+        raise SystemExit("bench.py: multi-GPU sharding is not wired into this bench yet")
+    torch.cuda.set_device(0)
+    peaks = load_peaks()
+    K, W = args.steps, max(3, args.warmup)
+    T = generate_gpu(w, seed=0)
+    cfg = PasdConfig(lambdas=w.lambdas(), ranks=list(w.ranks), eps=w.eps, maxiter=W + K + args.profile_iters + 1)
+    sol = pb.Solver(w.dims, cfg, fixed_iters=True, poll_every=K)
+    sol.load(T.data_ptr(), t_is_device=True)
+    sol.run(W)
+    stream = torch.cuda.ExternalStream(sol.stream)
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    clk = ClockSampler(torch.cuda.current_device())
+    clk.start()
+    torch.cuda.synchronize()
+    ev0.record(stream)
+    done, _ = sol.run(K)
+    ev1.record(stream)
+    ev1.synchronize()
+    clocks = clk.stop()
+    ms = ev0.elapsed_time(ev1)
+    launches = sol.launches
+    prof = sol.profile(args.profile_iters)
+    sol.close()
+    del sol
+    value = K / (ms * 1e-3)
+    roof = roofline_from_profile(prof, peaks, args.profile_iters)
+    # Whole-iteration roofline against the canonical fused-schedule work.
+    S = w.size
+    N = len(w.dims)
+    RJ = sum(r * (S // d) for r, d in zip(w.ranks, w.dims))
+    B_iter = 8.0 * ((3 * N + 4) * S + 2 * RJ)
+    F_iter = 6.0 * S * sum(w.ranks)
+    t_roof = max(B_iter / (peaks["hbm_gbs"] * 1e9), F_iter / (peaks["fp64_tflops"] * 1e12))
+    iteration_roofline = {"B_iter": B_iter, "F_iter": F_iter, "t_roof_ms": t_roof * 1e3,
+                          "t_measured_ms": ms / K, "frac": round(t_roof / (ms / K * 1e-3), 4)}
+    line = {
+        "metric": "PASD ADMM iters/s", "value": round(value, 4), "unit": "iter/s", "n_gpus": world,
+        "steps": K, "warmup": W, "ms_per_step": round(ms / K, 4), "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": w.name, "dims": list(w.dims), "ranks": list(w.ranks), "rho": w.rho,
+                   "noise": list(w.noise), "iters_fixed": True, "l2": "inputs larger than L2 (5 x 8 GB resident)"
+                   if S * 8 > 126e6 else "inputs L2-resident"},
+        "elem_iters_per_s": value * S,
+        "gpu_launches": int(launches),
+        "clocks": clocks,
+        "roofline": roof,
+        "iteration_roofline": iteration_roofline,
+    }
+    del T
+    torch.cuda.empty_cache()
+    if not args.no_e2e:
+        Tg = generate_gpu(w, seed=0)
+        line["e2e"] = e2e_recover(w, Tg, K)
+        del Tg
+        torch.cuda.empty_cache()
+    if not args.no_cpu_baseline:
+        try:
+            line["cpu_baseline"] = cpu_baseline(w, threads=1)
+        except Exception as exc:  # reported, never fatal
+            line["cpu_baseline"] = {"error": str(exc)}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -146,10 +146,35 @@ int pasd_b200_solver_run(pasd_solver* s, int32_t iters, int32_t* iters_done, int
 /* Finalise (Y-hat, objective, X, certificate) and copy requested outputs to
  * host buffers (local slab only for a sharded solver). */
 int pasd_b200_solver_finalize(pasd_solver* s, pasd_outputs* out, char* errbuf, size_t errlen);
+/* Replace the iterate (tenrec::PasdState, pasd.hpp:33-41) from HOST buffers:
+ * e (S), y[N] (S each), u[N] (I_n x R_n), v[N] (R_n x J_n, unfolding layout),
+ * the penalty mu of the next iteration and the completed-iteration count.
+ * Used for single-step parity: the next pasd_b200_solver_run(s, 1, ...) then
+ * performs exactly the reference iteration from that state (pasd.cpp:168-244). */
+int pasd_b200_solver_set_state(pasd_solver* s, const double* e, const double* const* y, const double* const* u,
+                               const double* const* v, double mu, int32_t iter, char* errbuf, size_t errlen);
 /* Device pointers of the local slab of E and of Y_n (diagnostics / zero-copy). */
 const double* pasd_b200_solver_device_e(const pasd_solver* s);
 /* The CUDA stream (cudaStream_t) the solver launches on. */
 void* pasd_b200_solver_stream(const pasd_solver* s);
+/* Kernel classes of one iteration, in launch order. */
+enum {
+  PASD_K_POLAR = 0,      /* Procrustes small solve (one CTA per mode)        */
+  PASD_K_CONTRACT_A = 1, /* A_n = U_n^T G_(n)                                */
+  PASD_K_GRAM = 2,       /* Gram_n partials                                  */
+  PASD_K_SVT = 3,        /* SVT small solve (one CTA per mode)               */
+  PASD_K_UPDATE = 4,     /* refold + E shrink + Y ascent + residuals         */
+  PASD_K_FINISH = 5,     /* mu schedule / stop rule                          */
+  PASD_K_CONTRACT_W = 6, /* Wt_n = G_(n)^{next} A_n^T                        */
+  PASD_NUM_KERNEL_CLASSES = 7
+};
+/* Profiling run: `iters` further iterations launched eagerly (no graph) with
+ * CUDA events around every kernel on the solver's stream.  Fills, per kernel
+ * class, the summed device time in ms, the launch count, and the algorithmic
+ * bytes / flops of one launch of that class summed over modes.
+ * The iterate advances exactly as pasd_b200_solver_run would advance it. */
+int pasd_b200_solver_profile(pasd_solver* s, int32_t iters, double* kernel_ms, int64_t* kernel_launches,
+                             double* kernel_bytes, double* kernel_flops, char* errbuf, size_t errlen);
 /* Number of kernel launches issued by the last pasd_b200_solver_run call. */
 int64_t pasd_b200_solver_launches(const pasd_solver* s);
 void pasd_b200_solver_destroy(pasd_solver* s);

@@ -151,7 +151,7 @@ def procrustes(g, v):
     err = _err()
     rc = lib().oracle_procrustes(_abi.dptr(np.ravel(g, order="F")), C.c_int64(g.shape[0]), C.c_int64(g.shape[1]),
                                  _abi.dptr(np.ravel(v, order="F")), C.c_int64(v.shape[0]),
-                                 out.ctypes.data_as(_abi.c_double_p), C.byref(deg), err, C.c_size_t(len(err)))
+                                 C.c_int64(v.shape[1]), out.ctypes.data_as(_abi.c_double_p), C.byref(deg), err, C.c_size_t(len(err)))
     raise_for_status(rc, err)
     return None if deg.value else out
 

@@ -836,11 +836,11 @@ int oracle_svt(const double* m, int64_t rows, int64_t cols, double tau, double* 
 }
 // Returns 1 in *degenerate when procrustes signals the degenerate case.
 int oracle_procrustes(const double* g, int64_t i_rows, int64_t p_cols, const double* v, int64_t r_rows,
-                      double* out, int* degenerate, char* err, size_t errlen) {
+                      int64_t v_cols, double* out, int* degenerate, char* err, size_t errlen) {
   return guarded(err, errlen, [&] {
-    Matrix gm(i_rows, p_cols), vm(r_rows, p_cols);
+    Matrix gm(i_rows, p_cols), vm(r_rows, v_cols);
     std::memcpy(gm.data(), g, size_t(i_rows * p_cols) * sizeof(double));
-    std::memcpy(vm.data(), v, size_t(r_rows * p_cols) * sizeof(double));
+    std::memcpy(vm.data(), v, size_t(r_rows * v_cols) * sizeof(double));
     g_threads = 1;
     Matrix u;
     const bool ok = procrustes(gm, vm, u);

@@ -19,6 +19,8 @@ PASD_FLAG_NONE = 0
 PASD_FLAG_NO_CERTIFICATE = 1 << 0
 PASD_FLAG_FIXED_ITERS = 1 << 1
 
+PASD_KERNEL_CLASSES = ("polar", "contract_A", "gram", "svt", "update", "finish", "contract_W")
+
 c_double_p = C.POINTER(C.c_double)
 c_int64_p = C.POINTER(C.c_int64)
 
@@ -93,11 +95,13 @@ HEADER_SYMBOLS = (
     "pasd_b200_solver_create",
     "pasd_b200_solver_load",
     "pasd_b200_solver_reset",
+    "pasd_b200_solver_set_state",
     "pasd_b200_solver_run",
     "pasd_b200_solver_finalize",
     "pasd_b200_solver_device_e",
     "pasd_b200_solver_stream",
     "pasd_b200_solver_launches",
+    "pasd_b200_solver_profile",
     "pasd_b200_solver_destroy",
     "pasd_b200_default_lambdas",
     "pasd_b200_default_rank_bound",

@@ -194,6 +194,8 @@ def make_observer(dims: Sequence[int], ranks: Sequence[int], user_fn: Optional[I
     """Wrap a Python observer as a pasd_observer_fn (copies the host view)."""
     if user_fn is None:
         return _abi.PasdObserverFn()
+    if isinstance(user_fn, _abi.PasdObserverFn):  # raw C callback, passed through
+        return user_fn
     dims = [int(x) for x in dims]
     total = int(np.prod(dims))
     n = len(dims)

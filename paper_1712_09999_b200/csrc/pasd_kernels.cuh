@@ -421,6 +421,16 @@ __global__ void k_nonfinite(const double* __restrict__ x, int64_t S, int* flag) 
     if (!isfinite(x[idx])) *flag = 1;
 }
 
+// A_n (kappa-major per r) <- V_n given in the reference's unfolding layout.
+__global__ void k_load_v_as_a(ModeDev m, const double* __restrict__ v) {
+  const int64_t total = m.J * m.R;
+  for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total; idx += (int64_t)gridDim.x * blockDim.x) {
+    const int r = (int)(idx % m.R);
+    const int64_t kap = idx / m.R;
+    m.A[a_offset(m, kap, r)] = v[idx];
+  }
+}
+
 // V_n = M_n A_n in the reference's unfolding layout (R x J column-major).
 __global__ void k_materialize_v(ModeDev m, double* __restrict__ out) {
   const int64_t total = m.J * m.R;

@@ -367,20 +367,27 @@ __global__ void __launch_bounds__(kSmallThreads) k_polar(const ModePack* __restr
   }
   __syncthreads();
   if (k < R) {
-    // 6. completion: B = (I - Ut Ut^T) U_prev Q[:, k:], then polar(B).
+    // 6. completion of the numerically null directions Q[:, k:].
+    //    Candidates: Wt Q[:, k:] = G^{next} A_prev^T Q_null (one subspace-
+    //    iteration step of G G^T on the sub-threshold directions), projected
+    //    off range(Ut) and symmetrically orthonormalised (polar).  If those are
+    //    ill-conditioned (e.g. at the first non-degenerate step), fall back to
+    //    the previous basis U_prev Q[:, k:] (for k = 0 that reproduces the
+    //    reference's keep-U rule, pasd.cpp:70-74).
     const int mcols = R - k;
-    double* B = X2;  // I x mcols (columns k.. of X2 are free to use)
-    // B = U_prev * Q[:, k:]
-    for (int64_t idx = tid; idx < I * mcols; idx += nt) {
-      const int64_t i = idx % I;
-      const int c = (int)(idx / I);
-      double a = 0.0;
-      for (int r = 0; r < R; ++r) a = fma(m.U[i + I * r], ws.Q[r * ld + k + c], a);
-      B[idx] = a;
-    }
-    __syncthreads();
-    for (int pass = 0; pass < 2; ++pass) {
-      if (k > 0) {
+    double* B = X2;  // I x mcols
+    double* Tm = Wt;  // I x mcols temp (Wt is consumed by attempt 0)
+    for (int attempt = 0; attempt < 2; ++attempt) {
+      const double* src = attempt == 0 ? Wt : m.U;
+      for (int64_t idx = tid; idx < I * mcols; idx += nt) {
+        const int64_t i = idx % I;
+        const int c = (int)(idx / I);
+        double a = 0.0;
+        for (int r = 0; r < R; ++r) a = fma(src[i + I * r], ws.Q[r * ld + k + c], a);
+        B[idx] = a;
+      }
+      __syncthreads();
+      for (int pass = 0; pass < 2 && k > 0; ++pass) {
         cta_gram_tn(X, B, I, k, mcols, ws.S, ld, ws.T64);  // S (k x mcols) = Ut^T B
         for (int64_t idx = tid; idx < I * mcols; idx += nt) {
           const int64_t i = idx % I;
@@ -391,31 +398,40 @@ __global__ void __launch_bounds__(kSmallThreads) k_polar(const ModePack* __restr
         }
         __syncthreads();
       }
-    }
-    // polar(B) = B Qb Lb^{-1/2} Qb^T via eig(B^T B)
-    cta_gram_tn(B, B, I, mcols, mcols, ws.S, ld, ws.T64);
-    cta_jacobi_eig(ws, mcols);
-    // Z = Qb diag(lb^{-1/2}) Qb^T  (mcols x mcols)
-    for (int idx = tid; idx < mcols * mcols; idx += nt) {
-      const int r = idx / mcols, s = idx % mcols;
-      double a = 0.0;
-      for (int j = 0; j < mcols; ++j) {
-        const double l = ws.lam[j];
-        const double inv = l > 1e-24 ? 1.0 / sqrt(l) : 0.0;
-        a = fma(ws.V[r * ld + j] * inv, ws.V[s * ld + j], a);
+      cta_gram_tn(B, B, I, mcols, mcols, ws.S, ld, ws.T64);
+      cta_jacobi_eig(ws, mcols);
+      const bool ok = ws.lam[0] > 0.0 && ws.lam[mcols - 1] >= 1e-8 * ws.lam[0];
+      if (!ok && attempt == 0) continue;
+      // two symmetric-orthonormalisation passes: Y <- Y (Y^T Y)^{-1/2}
+      for (int pass = 0; pass < 2; ++pass) {
+        const double* in = pass == 0 ? B : Tm;
+        double* outp = pass == 0 ? Tm : X + I * k;
+        if (pass == 1) {
+          cta_gram_tn(Tm, Tm, I, mcols, mcols, ws.S, ld, ws.T64);
+          cta_jacobi_eig(ws, mcols);
+        }
+        for (int idx = tid; idx < mcols * mcols; idx += nt) {
+          const int r = idx / mcols, c = idx % mcols;
+          double a = 0.0;
+          for (int j = 0; j < mcols; ++j) {
+            const double l = ws.lam[j];
+            const double inv = l > 1e-280 ? 1.0 / sqrt(l) : 0.0;
+            a = fma(ws.V[r * ld + j] * inv, ws.V[c * ld + j], a);
+          }
+          ws.Z[r * ld + c] = a;
+        }
+        __syncthreads();
+        for (int64_t idx = tid; idx < I * mcols; idx += nt) {
+          const int64_t i = idx % I;
+          const int c = (int)(idx / I);
+          double a = 0.0;
+          for (int j = 0; j < mcols; ++j) a = fma(in[i + I * j], ws.Z[j * ld + c], a);
+          outp[i + I * c] = a;
+        }
+        __syncthreads();
       }
-      ws.Z[r * ld + s] = a;
+      break;
     }
-    __syncthreads();
-    // X[:, k + c] = B * Z[:, c]
-    for (int64_t idx = tid; idx < I * mcols; idx += nt) {
-      const int64_t i = idx % I;
-      const int c = (int)(idx / I);
-      double a = 0.0;
-      for (int j = 0; j < mcols; ++j) a = fma(B[i + I * j], ws.Z[j * ld + c], a);
-      X[i + I * (k + c)] = a;
-    }
-    __syncthreads();
   }
   // 7. U = Ut Q^T
   for (int idx = tid; idx < R * R; idx += nt) {

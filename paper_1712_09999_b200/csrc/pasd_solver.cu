@@ -180,44 +180,86 @@ struct pasd_solver {
 
 namespace {
 
-void launch_iteration(pasd_solver* s, cudaStream_t st) {
+// Launches one iteration.  `mark(cls, begin)` (optional) is called around
+// every kernel; the profiler records CUDA events there.
+template <class Mark>
+void launch_iteration_marked(pasd_solver* s, cudaStream_t st, Mark&& mark) {
   const int N = s->N;
   int launches = 0;
+  mark(PASD_K_POLAR, true);
   k_polar<<<N, kSmallThreads, s->small_smem, st>>>(s->d_pack, s->d_ctl);
+  mark(PASD_K_POLAR, false);
   ++launches;
   for (int n = 0; n < N; ++n) {
     const ModeDev& m = s->modes[n];
     const unsigned grid = (unsigned)((m.J + CA_KT - 1) / CA_KT);
+    mark(PASD_K_CONTRACT_A, true);
     switch (rpt_for(m.R)) {
       case 2: k_contract_A<2><<<grid, kThreads, 0, st>>>(m, s->T, s->E[0], s->E[1], s->Y[n], s->d_ctl); break;
       case 4: k_contract_A<4><<<grid, kThreads, 0, st>>>(m, s->T, s->E[0], s->E[1], s->Y[n], s->d_ctl); break;
       case 8: k_contract_A<8><<<grid, kThreads, 0, st>>>(m, s->T, s->E[0], s->E[1], s->Y[n], s->d_ctl); break;
       default: k_contract_A<16><<<grid, kThreads, 0, st>>>(m, s->T, s->E[0], s->E[1], s->Y[n], s->d_ctl); break;
     }
+    mark(PASD_K_CONTRACT_A, false);
     ++launches;
+    mark(PASD_K_GRAM, true);
     k_gram<<<m.nkc_g, kThreads, 0, st>>>(m, s->d_ctl);
+    mark(PASD_K_GRAM, false);
     ++launches;
   }
+  mark(PASD_K_SVT, true);
   k_svt<<<N, kSmallThreads, s->small_smem, st>>>(s->d_pack, s->d_ctl);
+  mark(PASD_K_SVT, false);
   ++launches;
+  mark(PASD_K_UPDATE, true);
   k_update<<<s->nblk_update, kThreads, 0, st>>>(s->d_pack, s->T, s->E[0], s->E[1], s->d_resid_part, s->d_bad_part,
                                                 s->S, s->d_ctl);
+  mark(PASD_K_UPDATE, false);
   ++launches;
+  mark(PASD_K_FINISH, true);
   k_finish<<<1, kThreads, 0, st>>>(s->d_ctl, s->d_resid_part, s->d_bad_part, s->nblk_update, s->d_hist);
+  mark(PASD_K_FINISH, false);
   ++launches;
   for (int n = 0; n < N; ++n) {
     const ModeDev& m = s->modes[n];
     const dim3 grid(m.nkc_w, m.nib_w);
+    mark(PASD_K_CONTRACT_W, true);
     switch (rpt_for(m.R)) {
       case 2: k_contract_W<2><<<grid, kThreads, 0, st>>>(m, s->T, s->E[0], s->E[1], s->Y[n], s->d_ctl); break;
       case 4: k_contract_W<4><<<grid, kThreads, 0, st>>>(m, s->T, s->E[0], s->E[1], s->Y[n], s->d_ctl); break;
       case 8: k_contract_W<8><<<grid, kThreads, 0, st>>>(m, s->T, s->E[0], s->E[1], s->Y[n], s->d_ctl); break;
       default: k_contract_W<16><<<grid, kThreads, 0, st>>>(m, s->T, s->E[0], s->E[1], s->Y[n], s->d_ctl); break;
     }
+    mark(PASD_K_CONTRACT_W, false);
     ++launches;
   }
   s->launches_per_iter = launches;
   CK(cudaGetLastError());
+}
+
+void launch_iteration(pasd_solver* s, cudaStream_t st) {
+  launch_iteration_marked(s, st, [](int, bool) {});
+}
+
+// Algorithmic bytes / flops of one launch of each kernel class summed over
+// modes: the data the kernel's function must touch once.
+void kernel_work(const pasd_solver* s, double* bytes, double* flops) {
+  const double S = (double)s->S, N = (double)s->N;
+  for (int k = 0; k < PASD_NUM_KERNEL_CLASSES; ++k) bytes[k] = flops[k] = 0.0;
+  for (const ModeDev& m : s->modes) {
+    const double RJ = (double)m.R * (double)m.J, R = m.R;
+    bytes[PASD_K_CONTRACT_A] += 8.0 * (3.0 * S + RJ);        // T, E, Y_n in; A_n out
+    flops[PASD_K_CONTRACT_A] += 2.0 * R * S;
+    bytes[PASD_K_GRAM] += 8.0 * RJ;                         // A_n in
+    flops[PASD_K_GRAM] += 2.0 * R * RJ;
+    bytes[PASD_K_UPDATE] += 8.0 * RJ;                       // A_n in
+    flops[PASD_K_UPDATE] += 2.0 * R * S;
+    bytes[PASD_K_CONTRACT_W] += 8.0 * (3.0 * S + RJ);       // T, E, Y_n, A_n in
+    flops[PASD_K_CONTRACT_W] += 2.0 * R * S;
+    bytes[PASD_K_POLAR] += 8.0 * 4.0 * (double)m.I * R;
+    bytes[PASD_K_SVT] += 8.0 * 2.0 * (double)m.I * R;
+  }
+  bytes[PASD_K_UPDATE] += 8.0 * (2.0 * N + 2.0) * S;         // T, Y_1..N in; E, Y_1..N out
 }
 
 __global__ void k_init_state(ModePack* mp, Ctl* ctl, double mu0, double rho, double mu_max, double eps, int maxiter,
@@ -363,6 +405,8 @@ pasd_solver* create_solver(const pasd_options* o, const pasd_shard* shard) {
   return s.release();
 }
 
+void ensure_scratch(pasd_solver* s);
+
 void build_graph(pasd_solver* s) {
   if (s->graph_exec) return;
   CK(cudaStreamBeginCapture(s->stream, cudaStreamCaptureModeThreadLocal));
@@ -386,6 +430,57 @@ void load_tensor(pasd_solver* s, const double* t, int is_device) {
   CK(cudaStreamSynchronize(s->stream));
   if (flag) fail(PASD_ERR_ARGUMENT, "pasd: input tensor contains non-finite entries");  // pasd.cpp:135-136
   s->loaded = true;
+}
+
+__global__ void k_state_ctl(Ctl* ctl, ModePack* mp, double mu, int iter, const double* vn2) {
+  ctl->mu = mu;
+  ctl->mu_used_last = mu;
+  ctl->iter = iter;
+  ctl->done = 0;
+  ctl->converged = 0;
+  ctl->nan_flag = 0;
+  ctl->ecur = 0;
+  for (int n = 0; n < mp->order; ++n) {
+    ctl->vnorm2[n] = vn2[n];
+    const int R = mp->m[n].R;
+    for (int i = 0; i < R * R; ++i) mp->m[n].M[i] = (i % (R + 1) == 0) ? 1.0 : 0.0;  // M = I: V = A
+  }
+}
+
+void set_state(pasd_solver* s, const double* e, const double* const* y, const double* const* u,
+               const double* const* v, double mu, int iter) {
+  if (!s->loaded) fail(PASD_ERR_STATE, "pasd_b200: no tensor loaded");
+  if (!e || !y || !u || !v) fail(PASD_ERR_ARGUMENT, "pasd_b200: null state buffer");
+  if (iter >= s->maxiter) fail(PASD_ERR_ARGUMENT, "pasd_b200: state iteration must be below maxiter");
+  cudaStream_t st = s->stream;
+  const int64_t S = s->S;
+  CK(cudaMemcpyAsync(s->E[0], e, S * sizeof(double), cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(s->E[1], e, S * sizeof(double), cudaMemcpyHostToDevice, st));
+  std::vector<double> vn2(s->N, 0.0);
+  double* d_vn2 = s->d_stats;  // scratch (finalisation reuses it later)
+  ensure_scratch(s);
+  for (int n = 0; n < s->N; ++n) {
+    const ModeDev& m = s->modes[n];
+    CK(cudaMemcpyAsync(s->Y[n], y[n], S * sizeof(double), cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(m.U, u[n], m.I * m.R * sizeof(double), cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(s->xbuf, v[n], m.J * m.R * sizeof(double), cudaMemcpyHostToDevice, st));
+    k_load_v_as_a<<<1184, 256, 0, st>>>(m, s->xbuf);
+    k_sumsq<<<1, 1024, 0, st>>>(s->xbuf, m.J * m.R, d_vn2 + n);
+  }
+  k_state_ctl<<<1, 1, 0, st>>>(s->d_ctl, s->d_pack, mu, iter, d_vn2);
+  // Wt_n = G_(n) V_n^T from the injected state (the product the next Procrustes needs)
+  for (int n = 0; n < s->N; ++n) {
+    const ModeDev& m = s->modes[n];
+    const dim3 grid(m.nkc_w, m.nib_w);
+    switch (rpt_for(m.R)) {
+      case 2: k_contract_W<2><<<grid, kThreads, 0, st>>>(m, s->T, s->E[0], s->E[1], s->Y[n], s->d_ctl); break;
+      case 4: k_contract_W<4><<<grid, kThreads, 0, st>>>(m, s->T, s->E[0], s->E[1], s->Y[n], s->d_ctl); break;
+      case 8: k_contract_W<8><<<grid, kThreads, 0, st>>>(m, s->T, s->E[0], s->E[1], s->Y[n], s->d_ctl); break;
+      default: k_contract_W<16><<<grid, kThreads, 0, st>>>(m, s->T, s->E[0], s->E[1], s->Y[n], s->d_ctl); break;
+    }
+  }
+  CK(cudaGetLastError());
+  CK(cudaStreamSynchronize(st));
 }
 
 // Observer snapshot (recovery.hpp:38-48): host copies of e, z, y, u, v.
@@ -461,6 +556,36 @@ void run_solver(pasd_solver* s, int iters, pasd_observer_fn obs, void* user) {
     if (obs) deliver_observer(s, obs, user, hv);
     if (c.done) break;
   }
+}
+
+void profile_solver(pasd_solver* s, int iters, double* ms, int64_t* cnt, double* bytes, double* flops) {
+  if (!s->loaded) fail(PASD_ERR_STATE, "pasd_b200: no tensor loaded");
+  for (int k = 0; k < PASD_NUM_KERNEL_CLASSES; ++k) {
+    ms[k] = 0.0;
+    cnt[k] = 0;
+  }
+  std::vector<cudaEvent_t> ev;
+  std::vector<int> cls;
+  auto mark = [&](int c, bool begin) {
+    cudaEvent_t e;
+    CK(cudaEventCreate(&e));
+    CK(cudaEventRecord(e, s->stream));
+    ev.push_back(e);
+    if (begin) cls.push_back(c);
+  };
+  for (int it = 0; it < iters; ++it) launch_iteration_marked(s, s->stream, mark);
+  CK(cudaStreamSynchronize(s->stream));
+  for (size_t j = 0; j < cls.size(); ++j) {
+    float t = 0.f;
+    CK(cudaEventElapsedTime(&t, ev[2 * j], ev[2 * j + 1]));
+    ms[cls[j]] += t;
+    cnt[cls[j]] += 1;
+  }
+  for (cudaEvent_t e : ev) cudaEventDestroy(e);
+  kernel_work(s, bytes, flops);
+  sync_ctl(s);
+  if (s->h_ctl->nan_flag)
+    fail(PASD_ERR_NUMERICAL, "pasd: non-finite iterate at iteration " + std::to_string(s->h_ctl->iter));
 }
 
 void finalize_solver(pasd_solver* s, pasd_outputs* out) {
@@ -640,6 +765,25 @@ int pasd_b200_solver_finalize(pasd_solver* s, pasd_outputs* out, char* errbuf, s
     if (!s || !out) fail(PASD_ERR_ARGUMENT, "pasd_b200: null argument");
     CK(cudaSetDevice(s->device));
     finalize_solver(s, out);
+  });
+}
+
+int pasd_b200_solver_set_state(pasd_solver* s, const double* e, const double* const* y, const double* const* u,
+                               const double* const* v, double mu, int32_t iter, char* errbuf, size_t errlen) {
+  return guarded_call(errbuf, errlen, [&] {
+    if (!s) fail(PASD_ERR_ARGUMENT, "pasd_b200: null solver");
+    CK(cudaSetDevice(s->device));
+    set_state(s, e, y, u, v, mu, iter);
+  });
+}
+
+int pasd_b200_solver_profile(pasd_solver* s, int32_t iters, double* kernel_ms, int64_t* kernel_launches,
+                             double* kernel_bytes, double* kernel_flops, char* errbuf, size_t errlen) {
+  return guarded_call(errbuf, errlen, [&] {
+    if (!s || !kernel_ms || !kernel_launches || !kernel_bytes || !kernel_flops)
+      fail(PASD_ERR_ARGUMENT, "pasd_b200: null argument");
+    CK(cudaSetDevice(s->device));
+    profile_solver(s, iters, kernel_ms, kernel_launches, kernel_bytes, kernel_flops);
   });
 }
 

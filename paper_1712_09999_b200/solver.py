@@ -236,3 +236,50 @@ def procrustes(g, v, u_prev=None, *, device: int = 0):
                                 err, C.c_size_t(len(err)))
     raise_for_status(rc, err)
     return (None if deg.value else out), int(rank.value)
+
+
+def _solver_profile(self, iters: int):
+    """Eager run of `iters` iterations with CUDA events around every kernel
+    (pasd_b200_solver_profile).  Returns {class: {ms, launches, bytes, flops}}."""
+    K = len(_abi.PASD_KERNEL_CLASSES)
+    ms = (C.c_double * K)()
+    cnt = (C.c_int64 * K)()
+    by = (C.c_double * K)()
+    fl = (C.c_double * K)()
+    err = _err()
+    L = lib()
+    L.pasd_b200_solver_profile.restype = C.c_int
+    L.pasd_b200_solver_profile.argtypes = [C.c_void_p, C.c_int32, C.POINTER(C.c_double), C.POINTER(C.c_int64),
+                                           C.POINTER(C.c_double), C.POINTER(C.c_double), C.c_char_p, C.c_size_t]
+    rc = L.pasd_b200_solver_profile(self._h, int(iters), ms, cnt, by, fl, err, len(err))
+    raise_for_status(rc, err)
+    return {name: {"ms": ms[k], "launches": int(cnt[k]), "bytes": by[k], "flops": fl[k]}
+            for k, name in enumerate(_abi.PASD_KERNEL_CLASSES)}
+
+
+Solver.profile = _solver_profile
+
+
+def _solver_set_state(self, e, y, u, v, mu: float, iteration: int) -> None:
+    """Inject a reference iterate (PasdState, pasd.hpp:33-41); see
+    pasd_b200_solver_set_state.  e, y[n]: tensors; u[n]: I_n x R_n; v[n]:
+    R_n x J_n in the unfolding layout."""
+    n = len(self.dims)
+    ef = np.ravel(np.asarray(e, dtype=np.float64), order="F")
+    yf = [np.ravel(np.asarray(a, dtype=np.float64), order="F") for a in y]
+    uf = [np.ravel(np.asfortranarray(np.asarray(a, dtype=np.float64)), order="F") for a in u]
+    vf = [np.ravel(np.asfortranarray(np.asarray(a, dtype=np.float64)), order="F") for a in v]
+    if len(yf) != n or len(uf) != n or len(vf) != n:
+        raise ArgumentError("set_state: expected one y/u/v per mode")
+    err = _err()
+    L = lib()
+    L.pasd_b200_solver_set_state.restype = C.c_int
+    L.pasd_b200_solver_set_state.argtypes = [C.c_void_p, _abi.c_double_p, C.POINTER(_abi.c_double_p),
+                                             C.POINTER(_abi.c_double_p), C.POINTER(_abi.c_double_p), C.c_double,
+                                             C.c_int32, C.c_char_p, C.c_size_t]
+    rc = L.pasd_b200_solver_set_state(self._h, _abi.dptr(ef), _abi.ptr_array(yf), _abi.ptr_array(uf),
+                                      _abi.ptr_array(vf), C.c_double(mu), C.c_int32(iteration), err, len(err))
+    raise_for_status(rc, err)
+
+
+Solver.set_state = _solver_set_state
