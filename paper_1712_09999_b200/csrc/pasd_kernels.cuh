@@ -351,6 +351,28 @@ __global__ void __launch_bounds__(kThreads) k_contract_W(ModeDev m, const double
   if (tid == 0) m.gpart[(int64_t)blockIdx.x * m.nib_w + blockIdx.y] = g2;
 }
 
+// Generic-path reduction: Wt_n = sum_kc Wpart[kc] and ||G_n||^2 = sum gpart,
+// in a fixed order.  grid = (blocks, N).
+__global__ void k_wreduce_generic(const ModePack* __restrict__ mp, Ctl* ctl) {
+  if (ctl->done) return;
+  const int n = blockIdx.y;
+  const ModeDev& m = mp->m[n];
+  const int R = m.R;
+  const int64_t IR = m.I * R;
+  for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < IR; idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = idx % m.I;
+    const int r = (int)(idx / m.I);
+    double a = 0.0;
+    for (int kc = 0; kc < m.nkc_w; ++kc) a += m.Wpart[((int64_t)kc * m.I + i) * R + r];
+    m.Wt[idx] = a;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    double g2 = 0.0;
+    for (int j = 0; j < m.nkc_w * m.nib_w; ++j) g2 += m.gpart[j];
+    ctl->gnorm2[n] = g2;
+  }
+}
+
 // ---------------------------------------------------------------------------
 // Finalisation / observer kernels.
 __global__ void k_materialize_z(ModeDev m, double* __restrict__ out, int64_t S) {

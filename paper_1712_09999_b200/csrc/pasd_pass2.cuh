@@ -1,0 +1,494 @@
+// pasd_pass2.cuh — fused pass 2 of a PASD iteration for order-3 tensors on
+// the FP64 tensor cores (DMMA, mma.sync.m16n8k4.f64).
+//
+// One kernel replaces, per iteration (reference: proj/src/pasd.cpp:189-228 and
+// the next iteration's procrustes product, linops.cpp:98):
+//   Z_n = fold_n(U_n V_n) = UM_n x_n A_n          (refold; V_n = M_n A_n)
+//   h   = sum_n (T - Z_n) + Y_n/mu ; E = soft(h/N, 1/(mu N))
+//   Y_n += mu ((T - Z_n) - E) ; resid_n = max |.| ; NaN flag
+//   Wt_n = G_n^{next} A_n^T with G_n^{next} = (T - E) + Y_n/mu_next, and ||G_n^{next}||^2
+// HBM traffic: T, Y_1..3 read once, E, Y_1..3 written once; A_n slices come
+// through L2.
+//
+// Work decomposition.  A persistent CTA walks "pencils": a 16 (i1) x 8 (i3)
+// patch swept over all i2 in steps of 8.  Per step the brick is
+// 16 x 8 x 8 = 1024 elements.  The A_2 slice of the pencil (R2 x 16 x 8,
+// indexed by (i1, i3)) stays resident in shared memory for the whole sweep;
+// A_1 (R1 x 8 x 8, by (i2, i3)) and A_3 (R3 x 16 x 8, by (i1, i2)) are loaded
+// per step.  Warp w (of 8) owns the (16 i1 x 8 i2) tile at i3 = w for Z_1 and
+// Z_2 (identical accumulator layouts), and the (16 i1 x 8 i3) tile at i2 = w
+// for Z_3 (exchanged through shared memory).  Wt_1 uses the warp's own G_1
+// values directly as the DMMA A operand; Wt_2 / Wt_3 read G_2 / G_3 from
+// shared memory.  Wt_1 / Wt_3 rows are fixed along a pencil (register
+// accumulation, one partial per pencil); Wt_2 rows change per step and go to a
+// per-CTA partial.  All reductions are in a fixed order (deterministic).
+#pragma once
+#include "pasd_kernels.cuh"
+
+namespace pasd {
+
+constexpr int P2_B1 = 16, P2_B2 = 8, P2_B3 = 8;
+constexpr int P2_THREADS = 256;
+constexpr int P2_BRICK = P2_B1 * P2_B2 * P2_B3;  // 1024
+
+struct Pass2Args {
+  ModeDev m[3];
+  const double* T;
+  double* E0;
+  double* E1;
+  double* Y[3];
+  double* W1p;     // [npencils][16][R1]
+  double* W3p;     // [npencils][8][R3]
+  double* W2part;  // [grid][I2][R2]
+  double* gpart;   // [grid][3]
+  double* resid_part;  // [grid][PASD_MAX_ORDER]
+  int* bad_part;       // [grid]
+  int n1b, n3b, npencils;
+};
+
+__host__ __device__ inline int round_up(int x, int m) { return (x + m - 1) / m * m; }
+
+// Shared-memory plan (doubles).  LD values are chosen ~ 8 mod 16 to spread
+// the (row = t, col = g) fragment reads over the banks.
+struct P2Smem {
+  int RM1, RM2, RM3;  // rows padded to 16 (M tiles of the Wt products)
+  int RP1, RP2, RP3;  // K padded to 4
+  int ldA1, ldA2, ldA3, ldU;
+  int oA1, oA2, oA3, oU1, oU2, oU3, oZ3, oG2, oG3, oRed, total;
+};
+
+__host__ __device__ inline P2Smem p2_plan(int R1, int R2, int R3) {
+  P2Smem p;
+  p.RM1 = round_up(R1, 4);  // rows >= R are zero; M tiles past RM read 0 in registers
+  p.RM2 = round_up(R2, 4);
+  p.RM3 = round_up(R3, 4);
+  p.RP1 = round_up(R1, 4);
+  p.RP2 = round_up(R2, 4);
+  p.RP3 = round_up(R3, 4);
+  p.ldA1 = 64 + 8;    // cols (i2, i3)
+  p.ldA2 = 128 + 8;   // cols (i1, i3)
+  p.ldA3 = 128 + 8;   // cols (i1, i2)
+  int rmax = p.RP1 > p.RP2 ? p.RP1 : p.RP2;
+  rmax = rmax > p.RP3 ? rmax : p.RP3;
+  p.ldU = rmax + 4;
+  int o = 0;
+  p.oA1 = o; o += p.RM1 * p.ldA1;
+  p.oA2 = o; o += p.RM2 * p.ldA2;
+  p.oA3 = o; o += p.RM3 * p.ldA3;
+  p.oU1 = o; o += 16 * p.ldU;
+  p.oU2 = o; o += 8 * p.ldU;
+  p.oU3 = o; o += 8 * p.ldU;
+  p.oZ3 = o; o += P2_BRICK;
+  p.oG2 = o; o += P2_BRICK;
+  p.oG3 = o; o += P2_BRICK;
+  p.oRed = o; o += 64;
+  p.total = o;
+  return p;
+}
+
+__device__ __forceinline__ void dmma(double (&c)[4], double a0, double a1, double b0) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k4.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5}, {%6}, {%0,%1,%2,%3};"
+      : "+d"(c[0]), "+d"(c[1]), "+d"(c[2]), "+d"(c[3])
+      : "d"(a0), "d"(a1), "d"(b0));
+}
+
+// Asynchronous global->shared copy of one double (LDGSTS); src_bytes = 0
+// zero-fills the destination (out-of-range / padding entries).
+__device__ __forceinline__ void cp_async8(double* smem, const double* gmem, bool valid) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  const int nbytes = valid ? 8 : 0;
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(s), "l"(gmem), "r"(nbytes) : "memory");
+}
+__device__ __forceinline__ void cp_async16(double* smem, const double* gmem, int nbytes) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(s), "l"(gmem), "r"(nbytes) : "memory");
+}
+
+// Stage `rows` rows of 16 consecutive doubles (row j: src + j*step_r, with
+// the i1 extent clipped to `nvalid`) into dst[j*ld .. j*ld+15].  16-byte
+// copies when the source rows are 16-byte aligned, else 8-byte copies.
+__device__ __forceinline__ void stage_rows16(double* dst, int ld, const double* src, int64_t row_stride, int rows,
+                                             int nvalid, bool aligned16, const double* dummy) {
+  const int tid = threadIdx.x;
+  if (aligned16) {
+    const int c = tid & 7;  // 16-byte chunk within the row
+    const int v = nvalid - 2 * c;
+    const int nb = v >= 2 ? 16 : (v == 1 ? 8 : 0);
+    for (int j = tid >> 3; j < rows; j += P2_THREADS / 8)
+      cp_async16(dst + j * ld + 2 * c, nb ? src + row_stride * j + 2 * c : dummy, nb);
+  } else {
+    const int c = tid & 15;
+    const bool ok = c < nvalid;
+    for (int j = tid >> 4; j < rows; j += P2_THREADS / 16)
+      cp_async8(dst + j * ld + c, ok ? src + row_stride * j + c : dummy, ok);
+  }
+}
+
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
+// Brick element index e = i1 + 16 * (i2 + 8 * i3) (local coordinates).
+__device__ __forceinline__ int bidx(int l1, int l2, int l3) { return l1 + P2_B1 * (l2 + P2_B2 * l3); }
+// Padded exchange layouts (strides in doubles), conflict-free for their
+// write and read patterns within a half-warp (g, t in 0..3):
+//   Z3: written (l1=g, l3=2t), read (l1=g, l2=2t)        -> strides 22 / 182
+//   G2: written (l1=g, l2=2t), read (l1=t+c, l2=g)        -> strides 20 / 160
+//   G3: written (l1=g, l2=2t), read (l1=t+c, l3=g)        -> strides 22 / 180
+__device__ __forceinline__ int zx(int l1, int l2, int l3) { return l1 + 22 * l2 + 182 * l3; }
+__device__ __forceinline__ int g2x(int l1, int l2, int l3) { return l1 + 20 * l2 + 160 * l3; }
+__device__ __forceinline__ int g3x(int l1, int l2, int l3) { return l1 + 22 * l2 + 180 * l3; }
+
+// Shared-memory footprint (bytes) of k_pass2_fused<RP>.
+template <int RP>
+struct P2Layout {
+  static constexpr int RM = (RP + 15) / 16 * 16;  // rows of the M tiles (Wt products)
+  // leading dims chosen so the DMMA fragment reads (rows t x cols g, rows g x
+  // cols t) and the staging writes hit distinct banks per half-warp
+  static constexpr int LD1 = 64 + 4, LD2 = 128 + 4, LD3 = 128 + 4, LDU = RP + 4;
+  static constexpr int oA1 = 0;
+  static constexpr int oA2 = oA1 + RP * LD1;
+  static constexpr int oA3 = oA2 + RM * LD2;
+  static constexpr int oU1 = oA3 + RM * LD3;
+  static constexpr int oU2 = oU1 + 16 * LDU;
+  static constexpr int oU3 = oU2 + 8 * LDU;
+  static constexpr int oZ3 = oU3 + 8 * LDU;
+  static constexpr int oG2 = oZ3 + 8 * 182;
+  static constexpr int oG3 = oG2 + 8 * 160;
+  static constexpr int oRed = oG3 + 8 * 180;
+  static constexpr int total = oRed + 64;
+  static constexpr size_t bytes = sizeof(double) * (size_t)total;
+};
+
+// RP = common padded rank (multiple of 8, >= every R_n); rows r >= R_n of each
+// mode's operands are zero, so padding changes no result.
+template <int RP>
+__global__ void __launch_bounds__(P2_THREADS, 1) k_pass2_fused(const Pass2Args a, const Ctl* ctl) {
+  if (ctl->done) return;
+  using L = P2Layout<RP>;
+  constexpr int KS = RP / 4;   // k-steps of the Z products
+  constexpr int NT1 = RP / 8;  // n-tiles of the Wt_1 product
+  constexpr int MT = L::RM / 16;
+  extern __shared__ double sm[];
+  const ModeDev& m1 = a.m[0];
+  const ModeDev& m2 = a.m[1];
+  const ModeDev& m3 = a.m[2];
+  const int R1 = m1.R, R2 = m2.R, R3 = m3.R;
+  const int64_t I1 = m1.I, I2 = m2.I, I3 = m3.I;
+  double* A1s = sm + L::oA1;
+  double* A2s = sm + L::oA2;
+  double* A3s = sm + L::oA3;
+  double* U1s = sm + L::oU1;
+  double* U2s = sm + L::oU2;
+  double* U3s = sm + L::oU3;
+  double* Z3s = sm + L::oZ3;
+  double* G2s = sm + L::oG2;
+  double* G3s = sm + L::oG3;
+  double* red = sm + L::oRed;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5, g = lane >> 2, t = lane & 3;
+
+  const double* __restrict__ T = a.T;
+  double* __restrict__ Enew = ctl->ecur ? a.E0 : a.E1;
+  const double mu = ctl->mu;
+  const double inv_mu = __ddiv_rn(1.0, mu);                // pasd.cpp:170
+  const double inv_n = __ddiv_rn(1.0, 3.0);                // pasd.cpp:204
+  const double tau = __ddiv_rn(1.0, __dmul_rn(mu, 3.0));   // pasd.cpp:205
+  const double cand = __dmul_rn(ctl->rho, mu);
+  const double mu_next = (ctl->mu_max < cand) ? ctl->mu_max : cand;
+  const double inv_mu_next = __ddiv_rn(1.0, mu_next);
+
+  double* W2c = a.W2part + (int64_t)blockIdx.x * I2 * R2;  // per-CTA Wt_2 partial
+  for (int64_t idx = tid; idx < I2 * R2; idx += P2_THREADS) W2c[idx] = 0.0;
+  // zero padding rows once (never overwritten by the staging copies)
+  for (int idx = tid; idx < (L::RM - R2) * 128; idx += P2_THREADS) A2s[(R2 + idx / 128) * L::LD2 + (idx & 127)] = 0.0;
+  for (int idx = tid; idx < (L::RM - R3) * 128; idx += P2_THREADS) A3s[(R3 + idx / 128) * L::LD3 + (idx & 127)] = 0.0;
+  for (int idx = tid; idx < (RP - R1) * 64; idx += P2_THREADS) A1s[(R1 + idx / 64) * L::LD1 + (idx & 63)] = 0.0;
+  for (int idx = tid; idx < 32 * (RP + 4); idx += P2_THREADS) U1s[idx] = 0.0;  // U1s, U2s, U3s padding
+
+  double worst[3] = {0.0, 0.0, 0.0};
+  double gsq[3] = {0.0, 0.0, 0.0};
+  int bad = 0;
+  const int64_t S12 = I1 * I2;
+  const bool al1 = (I1 % 2) == 0;  // 16-byte aligned rows of 16 consecutive i1
+
+  for (int pen = blockIdx.x; pen < a.npencils; pen += gridDim.x) {
+    const int ib1 = pen % a.n1b, ib3 = pen / a.n1b;
+    const int64_t i1o = (int64_t)ib1 * P2_B1, i3o = (int64_t)ib3 * P2_B3;
+    const int nv1 = (int)imin64(16, I1 - i1o);
+    __syncthreads();  // previous pencil fully done with shared memory
+    // ---- pencil-resident: A_2 slice (I1, R2, I3 layout), UM_1 rows, UM_3 rows ----
+    for (int l3 = 0; l3 < 8; ++l3) {
+      const bool in3 = i3o + l3 < I3;
+      stage_rows16(A2s + 16 * l3, L::LD2, m2.A + i1o + I1 * (int64_t)R2 * (i3o + l3), I1, R2, in3 ? nv1 : 0, al1, m2.A);
+    }
+    for (int idx = tid; idx < 16 * R1; idx += P2_THREADS) {
+      const int l1 = idx & 15, r = idx >> 4;
+      const bool v = l1 < nv1;
+      cp_async8(U1s + l1 * L::LDU + r, v ? m1.UM + i1o + l1 + I1 * r : m1.UM, v);
+    }
+    for (int idx = tid; idx < 8 * R3; idx += P2_THREADS) {
+      const int l3 = idx & 7, r = idx >> 3;
+      const bool v = i3o + l3 < I3;
+      cp_async8(U3s + l3 * L::LDU + r, v ? m3.UM + i3o + l3 + I3 * r : m3.UM, v);
+    }
+    double w1acc[NT1][4];
+#pragma unroll
+    for (int j = 0; j < NT1; ++j) w1acc[j][0] = w1acc[j][1] = w1acc[j][2] = w1acc[j][3] = 0.0;
+    double w3acc[4] = {0.0, 0.0, 0.0, 0.0};
+
+    for (int64_t i2o = 0; i2o < I2; i2o += P2_B2) {
+      __syncthreads();  // previous step done with A1s/A3s/U2s/G2s/G3s
+      {  // A_1 (R1, I2, I3 layout): 4 threads per column (i2, i3)
+        const int c = tid >> 2, l2 = c & 7, l3 = c >> 3, r0 = tid & 3;
+        const int64_t i2 = i2o + l2, i3 = i3o + l3;
+        const bool colok = i2 < I2 && i3 < I3;
+        const double* src = m1.A + (colok ? (int64_t)R1 * (i2 + I2 * i3) : 0);
+        for (int r = r0; r < R1; r += 4) cp_async8(A1s + r * L::LD1 + c, colok ? src + r : m1.A, colok);
+      }
+      for (int l2 = 0; l2 < 8; ++l2) {  // A_3 (I1, I2, R3 layout)
+        const bool in2 = i2o + l2 < I2;
+        stage_rows16(A3s + 16 * l2, L::LD3, m3.A + i1o + I1 * (i2o + l2), S12, R3, in2 ? nv1 : 0, al1, m3.A);
+      }
+      for (int idx = tid; idx < 8 * R2; idx += P2_THREADS) {
+        const int l2 = idx & 7, r = idx >> 3;
+        const bool v = i2o + l2 < I2;
+        cp_async8(U2s + l2 * L::LDU + r, v ? m2.UM + i2o + l2 + I2 * r : m2.UM, v);
+      }
+      // this thread's 4 elements: (i1 = g, g+8) x (i2 = 2t, 2t+1) at i3 = w
+      double tv[4], yv[3][4];
+      bool inb[4];
+      int64_t off[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int64_t i1 = i1o + g + 8 * (q >> 1), i2 = i2o + 2 * t + (q & 1), i3 = i3o + w;
+        inb[q] = i1 < I1 && i2 < I2 && i3 < I3;
+        off[q] = i1 + I1 * i2 + S12 * i3;
+        tv[q] = inb[q] ? T[off[q]] : 0.0;
+#pragma unroll
+        for (int n = 0; n < 3; ++n) yv[n][q] = inb[q] ? a.Y[n][off[q]] : 0.0;
+      }
+      cp_async_wait_all();
+      __syncthreads();
+      // ---- Z products (6 independent accumulator chains) ----
+      double z1[4] = {0, 0, 0, 0}, z2[4] = {0, 0, 0, 0}, z3[4] = {0, 0, 0, 0};
+      double y1[4] = {0, 0, 0, 0}, y2[4] = {0, 0, 0, 0}, y3[4] = {0, 0, 0, 0};
+#pragma unroll
+      for (int ks = 0; ks < KS; ++ks) {
+        const int k = 4 * ks + t;
+        double(&c1)[4] = (ks & 1) ? y1 : z1;
+        double(&c2)[4] = (ks & 1) ? y2 : z2;
+        double(&c3)[4] = (ks & 1) ? y3 : z3;
+        dmma(c1, U1s[g * L::LDU + k], U1s[(g + 8) * L::LDU + k], A1s[k * L::LD1 + g + 8 * w]);
+        dmma(c2, A2s[k * L::LD2 + g + 16 * w], A2s[k * L::LD2 + g + 8 + 16 * w], U2s[g * L::LDU + k]);
+        dmma(c3, A3s[k * L::LD3 + g + 16 * w], A3s[k * L::LD3 + g + 8 + 16 * w], U3s[g * L::LDU + k]);
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        z1[q] += y1[q];
+        z2[q] += y2[q];
+        z3[q] += y3[q];
+      }
+      Z3s[zx(g, w, 2 * t)] = z3[0];
+      Z3s[zx(g, w, 2 * t + 1)] = z3[1];
+      Z3s[zx(g + 8, w, 2 * t)] = z3[2];
+      Z3s[zx(g + 8, w, 2 * t + 1)] = z3[3];
+      __syncthreads();
+      // ---- elementwise (reference op order, no FMA contraction) ----
+      double g1v[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int l1 = g + 8 * (q >> 1), l2 = 2 * t + (q & 1);
+        const double zz[3] = {z1[q], z2[q], Z3s[zx(l1, l2, w)]};
+        const double tt = tv[q];
+        double zt[3], h = 0.0;
+#pragma unroll
+        for (int n = 0; n < 3; ++n) {
+          zt[n] = __dsub_rn(tt, zz[n]);
+          h = __dadd_rn(h, __dadd_rn(zt[n], __dmul_rn(yv[n][q], inv_mu)));  // pasd.cpp:202
+        }
+        const double e = soft(__dmul_rn(h, inv_n), tau);  // pasd.cpp:208
+        double gn[3];
+#pragma unroll
+        for (int n = 0; n < 3; ++n) {
+          const double r = __dsub_rn(zt[n], e);                       // pasd.cpp:220
+          const double ynew = __dadd_rn(yv[n][q], __dmul_rn(mu, r));  // pasd.cpp:221
+          if (inb[q]) {
+            const double ar = fabs(r);
+            if (ar > worst[n]) worst[n] = ar;
+            bad |= !isfinite(r);
+            a.Y[n][off[q]] = ynew;
+          }
+          gn[n] = inb[q] ? g_elem(tt, e, ynew, inv_mu_next) : 0.0;  // next G_n
+          gsq[n] = fma(gn[n], gn[n], gsq[n]);
+        }
+        if (inb[q]) Enew[off[q]] = e;
+        g1v[q] = gn[0];
+        G2s[g2x(l1, l2, w)] = gn[1];
+        G3s[g3x(l1, l2, w)] = gn[2];
+      }
+      __syncthreads();
+      // ---- Wt products ----
+      // Wt_1: A operand = this thread's own G_1 (K = columns at i3 = w, permuted).
+#pragma unroll
+      for (int p = 0; p < 2; ++p) {
+#pragma unroll
+        for (int j = 0; j < NT1; ++j) dmma(w1acc[j], g1v[p], g1v[2 + p], A1s[(8 * j + g) * L::LD1 + 8 * w + 2 * t + p]);
+      }
+      if (w < 4) {
+        if (w < MT) {  // Wt_2^T m-tile w: rows r, cols i2, K = (i1, i3) = 128; flushed per step
+          double acc[4][4] = {};
+          const double* rowa = A2s + (16 * w + g) * L::LD2;
+          const double* rowb = rowa + 8 * L::LD2;
+#pragma unroll
+          for (int ks = 0; ks < 32; ++ks) {
+            const int k = 4 * ks + t;
+            dmma(acc[ks & 3], rowa[k], rowb[k], G2s[g2x(k & 15, g, k >> 4)]);
+          }
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const double v = (acc[0][q] + acc[1][q]) + (acc[2][q] + acc[3][q]);
+            const int r = 16 * w + g + 8 * (q >> 1);
+            const int64_t i2 = i2o + 2 * t + (q & 1);
+            if (r < R2 && i2 < I2) W2c[i2 * R2 + r] += v;
+          }
+        }
+      } else if (w - 4 < MT) {  // Wt_3^T m-tile: rows r, cols i3, K = (i1, i2) = 128; kept per pencil
+        double acc[3][4] = {};
+        const double* rowa = A3s + (16 * (w - 4) + g) * L::LD3;
+        const double* rowb = rowa + 8 * L::LD3;
+#pragma unroll
+        for (int ks = 0; ks < 32; ++ks) {
+          const int k = 4 * ks + t;
+          double(&c)[4] = (ks & 3) == 0 ? w3acc : acc[(ks & 3) - 1];
+          dmma(c, rowa[k], rowb[k], G3s[g3x(k & 15, k >> 4, g)]);
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) w3acc[q] += (acc[0][q] + acc[1][q]) + acc[2][q];
+      }
+    }
+    // ---- end of pencil: Wt_1 (sum over the 8 warps' column sets) and Wt_3 ----
+    __syncthreads();
+    double* wred = A1s;  // 8 warps x 16 x RP doubles (fits in A1s..A3s)
+#pragma unroll
+    for (int j = 0; j < NT1; ++j) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) wred[(w * 16 + g + 8 * (q >> 1)) * RP + 8 * j + 2 * t + (q & 1)] = w1acc[j][q];
+    }
+    __syncthreads();
+    double* w1out = a.W1p + (int64_t)pen * 16 * R1;
+    for (int idx = tid; idx < 16 * R1; idx += P2_THREADS) {
+      const int l1 = idx / R1, r = idx - l1 * R1;
+      double s = 0.0;
+#pragma unroll
+      for (int ww = 0; ww < 8; ++ww) s += wred[(ww * 16 + l1) * RP + r];
+      w1out[idx] = s;
+    }
+    if (w >= 4 && w - 4 < MT) {
+      double* w3out = a.W3p + (int64_t)pen * 8 * R3;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int r = 16 * (w - 4) + g + 8 * (q >> 1);
+        if (r < R3) w3out[(2 * t + (q & 1)) * R3 + r] = w3acc[q];
+      }
+    }
+    __syncthreads();
+    // restore the zero padding rows of A1s clobbered by the reduction scratch
+    for (int idx = tid; idx < (RP - R1) * 64; idx += P2_THREADS) A1s[(R1 + idx / 64) * L::LD1 + (idx & 63)] = 0.0;
+    for (int idx = tid; idx < (L::RM - R2) * 128; idx += P2_THREADS) A2s[(R2 + idx / 128) * L::LD2 + (idx & 127)] = 0.0;
+    for (int idx = tid; idx < (L::RM - R3) * 128; idx += P2_THREADS) A3s[(R3 + idx / 128) * L::LD3 + (idx & 127)] = 0.0;
+  }
+  // ---- per-CTA residual / NaN / ||G||^2 partials ----
+  for (int n = 0; n < 3; ++n) {
+    const double wv = block_reduce(worst[n], MaxOp(), red);
+    const double gv = block_reduce(gsq[n], AddOp(), red);
+    if (tid == 0) {
+      a.resid_part[(int64_t)blockIdx.x * PASD_MAX_ORDER + n] = wv;
+      a.gpart[blockIdx.x * 3 + n] = gv;
+    }
+  }
+  int* redi = reinterpret_cast<int*>(red + 32);
+  const int b = block_reduce(bad, OrOp(), redi);
+  if (tid == 0) a.bad_part[blockIdx.x] = b;
+}
+
+template <int RP>
+void launch_pass2(const Pass2Args& a, const Ctl* ctl, int grid, cudaStream_t st) {
+  k_pass2_fused<RP><<<grid, P2_THREADS, P2Layout<RP>::bytes, st>>>(a, ctl);
+}
+template <int RP>
+void setup_pass2() {
+  cudaFuncSetAttribute(k_pass2_fused<RP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P2Layout<RP>::bytes);
+}
+
+inline int pass2_rp(int R1, int R2, int R3) {
+  int r = R1 > R2 ? R1 : R2;
+  r = r > R3 ? r : R3;
+  return (r + 7) / 8 * 8;
+}
+inline size_t pass2_smem(int rp) {
+  switch (rp) {
+    case 8: return P2Layout<8>::bytes;
+    case 16: return P2Layout<16>::bytes;
+    case 24: return P2Layout<24>::bytes;
+    case 32: return P2Layout<32>::bytes;
+    case 40: return P2Layout<40>::bytes;
+    case 48: return P2Layout<48>::bytes;
+    case 56: return P2Layout<56>::bytes;
+    default: return P2Layout<64>::bytes;
+  }
+}
+inline void pass2_setup(int rp) {
+  switch (rp) {
+    case 8: setup_pass2<8>(); break;
+    case 16: setup_pass2<16>(); break;
+    case 24: setup_pass2<24>(); break;
+    case 32: setup_pass2<32>(); break;
+    case 40: setup_pass2<40>(); break;
+    case 48: setup_pass2<48>(); break;
+    case 56: setup_pass2<56>(); break;
+    default: setup_pass2<64>(); break;
+  }
+}
+inline void pass2_launch(int rp, const Pass2Args& a, const Ctl* ctl, int grid, cudaStream_t st) {
+  switch (rp) {
+    case 8: launch_pass2<8>(a, ctl, grid, st); break;
+    case 16: launch_pass2<16>(a, ctl, grid, st); break;
+    case 24: launch_pass2<24>(a, ctl, grid, st); break;
+    case 32: launch_pass2<32>(a, ctl, grid, st); break;
+    case 40: launch_pass2<40>(a, ctl, grid, st); break;
+    case 48: launch_pass2<48>(a, ctl, grid, st); break;
+    case 56: launch_pass2<56>(a, ctl, grid, st); break;
+    default: launch_pass2<64>(a, ctl, grid, st); break;
+  }
+}
+
+// Reduce the pass-2 partials into Wt_n (I_n x R_n, column-major) and
+// ctl->gnorm2[n], in a fixed order.  grid = (ceil(max I_n R_n / 256), 3).
+__global__ void k_pass2_reduce(const Pass2Args a, int nblk, Ctl* ctl) {
+  if (ctl->done) return;
+  const int n = blockIdx.y;
+  const ModeDev& m = a.m[n];
+  const int R = m.R;
+  const int64_t IR = m.I * R;
+  for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < IR; idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = idx % m.I;
+    const int r = (int)(idx / m.I);
+    double s = 0.0;
+    if (n == 0) {
+      const int ib = (int)(i / P2_B1), l = (int)(i % P2_B1);
+      for (int b3 = 0; b3 < a.n3b; ++b3) s += a.W1p[((int64_t)(ib + a.n1b * b3) * 16 + l) * R + r];
+    } else if (n == 1) {
+      for (int c = 0; c < nblk; ++c) s += a.W2part[((int64_t)c * m.I + i) * R + r];
+    } else {
+      const int ib = (int)(i / P2_B3), l = (int)(i % P2_B3);
+      for (int b1 = 0; b1 < a.n1b; ++b1) s += a.W3p[((int64_t)(b1 + a.n1b * ib) * 8 + l) * R + r];
+    }
+    m.Wt[idx] = s;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    double s = 0.0;
+    for (int c = 0; c < nblk; ++c) s += a.gpart[c * 3 + n];
+    ctl->gnorm2[n] = s;
+  }
+}
+
+}  // namespace pasd

@@ -283,21 +283,10 @@ __global__ void __launch_bounds__(kSmallThreads) k_polar(const ModePack* __restr
   const int64_t I = m.I, IR = I * R;
   SmallWs ws = make_ws(R, smem);
   const int ld = ws.ld;
-  double* Wt = m.scratch;           // I x R
+  double* Wt = m.Wt;                // I x R: G^{next} A^T, reduced by the pass that produced it
   double* X = m.scratch + IR;       // I x R
   double* X2 = m.scratch + 2 * IR;  // I x R
-  // 1. Wt = sum_kc Wpart[kc] (fixed order); ||G||^2 = sum gpart
-  const int nkc = m.nkc_w;
-  for (int64_t idx = tid; idx < IR; idx += nt) {
-    const int64_t i = idx % I;
-    const int r = (int)(idx / I);
-    double a = 0.0;
-    for (int kc = 0; kc < nkc; ++kc) a += m.Wpart[((int64_t)kc * I + i) * R + r];
-    Wt[idx] = a;
-  }
-  double g2 = 0.0;
-  for (int j = tid; j < nkc * m.nib_w; j += nt) g2 += m.gpart[j];
-  g2 = block_reduce(g2, AddOp(), ws.red);
+  const double g2 = ctl->gnorm2[n];  // ||G_n^{next}||_F^2
   // 2. W = Wt M  (M in S)
   for (int idx = tid; idx < R * R; idx += nt) ws.S[(idx / R) * ld + idx % R] = m.M[(idx / R) + R * (idx % R)];
   __syncthreads();
@@ -307,7 +296,6 @@ __global__ void __launch_bounds__(kSmallThreads) k_polar(const ModePack* __restr
   w2 = block_reduce(w2, AddOp(), ws.red);
   const double gnorm = sqrt(g2), vnorm = sqrt(ctl->vnorm2[n]);
   const double scale = fmax(1.0, gnorm * vnorm);  // linops.cpp:99
-  if (tid == 0) ctl->gnorm2[n] = g2;
   if (sqrt(w2) <= 1e-14 * scale) {                // linops.cpp:100-101 -> keep U (pasd.cpp:70-74)
     if (tid == 0) { ctl->degenerate[n] = 1; ctl->polar_rank[n] = 0; }
     return;

@@ -30,6 +30,8 @@
 #include "pasd_common.cuh"
 #include "pasd_kernels.cuh"
 #include "pasd_small.cuh"
+#include "pasd_pass2.cuh"
+#include "pasd_pass1.cuh"
 
 using namespace pasd;
 
@@ -152,6 +154,14 @@ struct pasd_solver {
   int* d_bad_part = nullptr;
   int nblk_update = 0;
   size_t small_smem = 0;
+  // fused order-3 pass 2 (pasd_pass2.cuh)
+  bool fused = false;
+  int p2_rp = 0;
+  Pass2Args p2{};
+  int p2_grid = 0;
+  size_t p2_smem = 0;
+  double* p2_resid = nullptr;
+  int* p2_bad = nullptr;
   double* zbuf = nullptr;  // S scratch (finalisation / observer)
   double* xbuf = nullptr;  // S scratch
   double* d_stats = nullptr;
@@ -192,14 +202,8 @@ void launch_iteration_marked(pasd_solver* s, cudaStream_t st, Mark&& mark) {
   ++launches;
   for (int n = 0; n < N; ++n) {
     const ModeDev& m = s->modes[n];
-    const unsigned grid = (unsigned)((m.J + CA_KT - 1) / CA_KT);
     mark(PASD_K_CONTRACT_A, true);
-    switch (rpt_for(m.R)) {
-      case 2: k_contract_A<2><<<grid, kThreads, 0, st>>>(m, s->T, s->E[0], s->E[1], s->Y[n], s->d_ctl); break;
-      case 4: k_contract_A<4><<<grid, kThreads, 0, st>>>(m, s->T, s->E[0], s->E[1], s->Y[n], s->d_ctl); break;
-      case 8: k_contract_A<8><<<grid, kThreads, 0, st>>>(m, s->T, s->E[0], s->E[1], s->Y[n], s->d_ctl); break;
-      default: k_contract_A<16><<<grid, kThreads, 0, st>>>(m, s->T, s->E[0], s->E[1], s->Y[n], s->d_ctl); break;
-    }
+    launch_contract_A_mma(m, s->T, s->E[0], s->E[1], s->Y[n], s->d_ctl, st);
     mark(PASD_K_CONTRACT_A, false);
     ++launches;
     mark(PASD_K_GRAM, true);
@@ -211,25 +215,46 @@ void launch_iteration_marked(pasd_solver* s, cudaStream_t st, Mark&& mark) {
   k_svt<<<N, kSmallThreads, s->small_smem, st>>>(s->d_pack, s->d_ctl);
   mark(PASD_K_SVT, false);
   ++launches;
-  mark(PASD_K_UPDATE, true);
-  k_update<<<s->nblk_update, kThreads, 0, st>>>(s->d_pack, s->T, s->E[0], s->E[1], s->d_resid_part, s->d_bad_part,
-                                                s->S, s->d_ctl);
-  mark(PASD_K_UPDATE, false);
-  ++launches;
-  mark(PASD_K_FINISH, true);
-  k_finish<<<1, kThreads, 0, st>>>(s->d_ctl, s->d_resid_part, s->d_bad_part, s->nblk_update, s->d_hist);
-  mark(PASD_K_FINISH, false);
-  ++launches;
-  for (int n = 0; n < N; ++n) {
-    const ModeDev& m = s->modes[n];
-    const dim3 grid(m.nkc_w, m.nib_w);
+  if (s->fused) {
+    mark(PASD_K_UPDATE, true);
+    pass2_launch(s->p2_rp, s->p2, s->d_ctl, s->p2_grid, st);
+    mark(PASD_K_UPDATE, false);
+    ++launches;
+    mark(PASD_K_FINISH, true);
+    k_finish<<<1, kThreads, 0, st>>>(s->d_ctl, s->p2_resid, s->p2_bad, s->p2_grid, s->d_hist);
+    mark(PASD_K_FINISH, false);
+    ++launches;
+    int64_t maxir = 1;
+    for (const ModeDev& m : s->modes) maxir = std::max<int64_t>(maxir, m.I * m.R);
     mark(PASD_K_CONTRACT_W, true);
-    switch (rpt_for(m.R)) {
-      case 2: k_contract_W<2><<<grid, kThreads, 0, st>>>(m, s->T, s->E[0], s->E[1], s->Y[n], s->d_ctl); break;
-      case 4: k_contract_W<4><<<grid, kThreads, 0, st>>>(m, s->T, s->E[0], s->E[1], s->Y[n], s->d_ctl); break;
-      case 8: k_contract_W<8><<<grid, kThreads, 0, st>>>(m, s->T, s->E[0], s->E[1], s->Y[n], s->d_ctl); break;
-      default: k_contract_W<16><<<grid, kThreads, 0, st>>>(m, s->T, s->E[0], s->E[1], s->Y[n], s->d_ctl); break;
+    k_pass2_reduce<<<dim3((unsigned)((maxir + 255) / 256), 3), 256, 0, st>>>(s->p2, s->p2_grid, s->d_ctl);
+    mark(PASD_K_CONTRACT_W, false);
+    ++launches;
+  } else {
+    mark(PASD_K_UPDATE, true);
+    k_update<<<s->nblk_update, kThreads, 0, st>>>(s->d_pack, s->T, s->E[0], s->E[1], s->d_resid_part,
+                                                  s->d_bad_part, s->S, s->d_ctl);
+    mark(PASD_K_UPDATE, false);
+    ++launches;
+    mark(PASD_K_FINISH, true);
+    k_finish<<<1, kThreads, 0, st>>>(s->d_ctl, s->d_resid_part, s->d_bad_part, s->nblk_update, s->d_hist);
+    mark(PASD_K_FINISH, false);
+    ++launches;
+    for (int n = 0; n < N; ++n) {
+      const ModeDev& m = s->modes[n];
+      const dim3 grid(m.nkc_w, m.nib_w);
+      mark(PASD_K_CONTRACT_W, true);
+      switch (rpt_for(m.R)) {
+        case 2: k_contract_W<2><<<grid, kThreads, 0, st>>>(m, s->T, s->E[0], s->E[1], s->Y[n], s->d_ctl); break;
+        case 4: k_contract_W<4><<<grid, kThreads, 0, st>>>(m, s->T, s->E[0], s->E[1], s->Y[n], s->d_ctl); break;
+        case 8: k_contract_W<8><<<grid, kThreads, 0, st>>>(m, s->T, s->E[0], s->E[1], s->Y[n], s->d_ctl); break;
+        default: k_contract_W<16><<<grid, kThreads, 0, st>>>(m, s->T, s->E[0], s->E[1], s->Y[n], s->d_ctl); break;
+      }
+      mark(PASD_K_CONTRACT_W, false);
+      ++launches;
     }
+    mark(PASD_K_CONTRACT_W, true);
+    k_wreduce_generic<<<dim3(64, N), 256, 0, st>>>(s->d_pack, s->d_ctl);
     mark(PASD_K_CONTRACT_W, false);
     ++launches;
   }
@@ -260,6 +285,13 @@ void kernel_work(const pasd_solver* s, double* bytes, double* flops) {
     bytes[PASD_K_SVT] += 8.0 * 2.0 * (double)m.I * R;
   }
   bytes[PASD_K_UPDATE] += 8.0 * (2.0 * N + 2.0) * S;         // T, Y_1..N in; E, Y_1..N out
+  if (s->fused) {  // pass 2 also forms Wt_n = G^{next} A_n^T (A_n already counted)
+    for (const ModeDev& m : s->modes) {
+      flops[PASD_K_UPDATE] += 2.0 * (double)m.R * S;
+      bytes[PASD_K_CONTRACT_W] = 0.0;
+      flops[PASD_K_CONTRACT_W] = 0.0;
+    }
+  }
 }
 
 __global__ void k_init_state(ModePack* mp, Ctl* ctl, double mu0, double rho, double mu_max, double eps, int maxiter,
@@ -276,6 +308,9 @@ __global__ void k_init_state(ModePack* mp, Ctl* ctl, double mu0, double rho, dou
     for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < (int64_t)m.R * m.R;
          idx += (int64_t)gridDim.x * blockDim.x)
       m.M[idx] = 0.0;  // V = 0 (pasd.cpp:153) <=> M = 0
+    for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < m.I * m.R;
+         idx += (int64_t)gridDim.x * blockDim.x)
+      m.Wt[idx] = 0.0;  // Wt = G V^T = 0 for V = 0: first Procrustes is degenerate
     const int64_t wp = (int64_t)m.nkc_w * m.I * m.R;
     for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < wp; idx += (int64_t)gridDim.x * blockDim.x)
       m.Wpart[idx] = 0.0;
@@ -398,6 +433,33 @@ pasd_solver* create_solver(const pasd_options* o, const pasd_shard* shard) {
   s->small_smem = small_ws_bytes(maxR);
   CK(cudaFuncSetAttribute(k_svt, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->small_smem));
   CK(cudaFuncSetAttribute(k_polar, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->small_smem));
+  if (s->N == 3) {
+    s->fused = true;
+    Pass2Args& a = s->p2;
+    for (int n = 0; n < 3; ++n) {
+      a.m[n] = s->modes[n];
+      a.Y[n] = s->Y[n];
+    }
+    a.T = s->T;
+    a.E0 = s->E[0];
+    a.E1 = s->E[1];
+    a.n1b = (int)((s->dims[0] + P2_B1 - 1) / P2_B1);
+    a.n3b = (int)((s->dims[2] + P2_B3 - 1) / P2_B3);
+    a.npencils = a.n1b * a.n3b;
+    s->p2_grid = std::max(1, std::min(a.npencils, sms));
+    s->p2_rp = pass2_rp(s->modes[0].R, s->modes[1].R, s->modes[2].R);
+    s->p2_smem = pass2_smem(s->p2_rp);
+    a.W1p = s->alloc<double>((size_t)a.npencils * 16 * s->modes[0].R);
+    a.W3p = s->alloc<double>((size_t)a.npencils * 8 * s->modes[2].R);
+    a.W2part = s->alloc<double>((size_t)s->p2_grid * s->dims[1] * s->modes[1].R);
+    a.gpart = s->alloc<double>((size_t)s->p2_grid * 3);
+    s->p2_resid = s->alloc<double>((size_t)s->p2_grid * PASD_MAX_ORDER);
+    s->p2_bad = s->alloc<int>(s->p2_grid);
+    a.resid_part = s->p2_resid;
+    a.bad_part = s->p2_bad;
+    pass2_setup(s->p2_rp);
+    CK(cudaGetLastError());
+  }
   s->d_stats = s->alloc<double>(2 * 2048);
   s->d_flag = s->alloc<int>(1);
   reset_state(s.get());
@@ -479,6 +541,7 @@ void set_state(pasd_solver* s, const double* e, const double* const* y, const do
       default: k_contract_W<16><<<grid, kThreads, 0, st>>>(m, s->T, s->E[0], s->E[1], s->Y[n], s->d_ctl); break;
     }
   }
+  k_wreduce_generic<<<dim3(64, s->N), 256, 0, st>>>(s->d_pack, s->d_ctl);
   CK(cudaGetLastError());
   CK(cudaStreamSynchronize(st));
 }
@@ -937,6 +1000,7 @@ void device_procrustes(const double* g_h, int64_t I, int64_t P, const double* v_
   m.Wpart = t.alloc<double>((size_t)m.nkc_w * IR);
   m.gpart = t.alloc<double>((size_t)m.nkc_w * m.nib_w);
   m.scratch = t.alloc<double>(3 * IR);
+  m.Wt = t.alloc<double>(IR);
   Ctl* ctl = t.alloc<Ctl>(1);
   double* vn = t.alloc<double>(1);
   k_sumsq<<<1, 1024>>>(m.A, R * P, vn);
@@ -955,6 +1019,7 @@ void device_procrustes(const double* g_h, int64_t I, int64_t P, const double* v_
   pack.m[0] = m;
   ModePack* d_pack = t.alloc<ModePack>(1);
   CK(cudaMemcpy(d_pack, &pack, sizeof(pack), cudaMemcpyHostToDevice));
+  k_wreduce_generic<<<dim3(64, 1), 256>>>(d_pack, ctl);
   const size_t smem = small_ws_bytes(R);
   CK(cudaFuncSetAttribute(k_polar, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   k_polar<<<1, kSmallThreads, smem>>>(d_pack, ctl);

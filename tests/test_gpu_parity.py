@@ -101,7 +101,7 @@ def test_single_step_parity_from_reference_state(gpu, oracle_mod):
         for n in range(3):
             assert rel(r.z[n], b.z[n]) <= 1e-11
             assert rel(r.y[n], b.y[n]) <= 1e-9  # Y += mu*r amplifies Z rounding by mu
-        np.testing.assert_allclose(r.final_residuals, b.residual_inf, rtol=1e-8)
+        np.testing.assert_allclose(r.final_residuals, b.residual_inf, rtol=1e-6, atol=1e-12 * np.abs(T).max())
 
 
 def test_zero_tensor(gpu):
