@@ -203,6 +203,46 @@ def e2e_recover(w, T_dev, steps: int):
     }
 
 
+def e2e_sharded(w, steps, shard, dist):
+    """Per-rank end-to-end run from pinned host slabs (H2D of the slab, the
+    loop with its NCCL exchanges, finalisation, D2H of the slab's X and E);
+    wall time max over ranks."""
+    import torch
+    import paper_1712_09999_b200 as pb
+    from paper_1712_09999_b200.api import PasdConfig
+    from paper_1712_09999_b200.workloads import generate_gpu
+
+    from paper_1712_09999_b200.sharding import Shard, nccl_unique_id
+
+    b, e = shard.struct.slab_begin, shard.struct.slab_end
+    rank = shard.struct.rank
+    uid = [nccl_unique_id() if rank == 0 else None]  # a unique id serves one communicator
+    dist.broadcast_object_list(uid, src=0)
+    shard = Shard(rank, shard.struct.nranks, (b, e), uid[0])
+    T = generate_gpu(w, seed=0)
+    Th = torch.empty(T[b:e].numel(), dtype=torch.float64, pin_memory=True)
+    Th.copy_(T[b:e].reshape(-1))
+    del T
+    torch.cuda.empty_cache()
+    cfg = PasdConfig(lambdas=w.lambdas(), ranks=list(w.ranks), eps=w.eps, maxiter=steps)
+    dist.barrier()
+    t0 = time.perf_counter()
+    sol = pb.Solver(w.dims, cfg, fixed_iters=True, poll_every=steps, shard=shard)
+    sol.load(Th.numpy().reshape(list(w.dims[:-1]) + [e - b], order="F"))
+    sol.run(steps)
+    sol.finalize(want_x=True, want_e=True)
+    sec = time.perf_counter() - t0
+    sol.close()
+    t = torch.tensor([sec], device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    sec = float(t.item())
+    slab_elems = Th.numel()
+    return {"value": steps / sec, "unit": "iter/s", "h2d_bytes_per_step": 8 * slab_elems / steps,
+            "d2h_bytes_per_step": 16 * slab_elems / steps, "seconds": sec,
+            "note": "per rank: solver create + H2D of its slab + fixed iterations + finalise + D2H of its "
+                    "X/E slab; max over ranks; bytes per rank amortised per iteration"}
+
+
 def roofline_from_profile(prof, peaks, iters):
     # Dominant kernel = largest share of device time.
     name = max(prof, key=lambda k: prof[k]["ms"])
@@ -269,28 +309,50 @@ def main():
     from paper_1712_09999_b200.api import PasdConfig
     from paper_1712_09999_b200.workloads import generate_gpu
 
-    if world > 1:
-        raise SystemExit("bench.py: multi-GPU sharding is not wired into this bench yet")
-    torch.cuda.set_device(0)
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local_rank)
+    dist = None
+    shard = None
+    if world > 1 or os.environ.get("PASD_BENCH_FORCE_SHARD") == "1":  # the latter: exercise the path on 1 GPU
+        import torch.distributed as dist
+        from paper_1712_09999_b200.sharding import Shard, nccl_unique_id, slab_bounds
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        uid = [nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        slab = slab_bounds(w.dims[-1], world, rank)
+        shard = Shard(rank, world, slab, uid[0])
     peaks = load_peaks()
     K, W = args.steps, max(3, args.warmup)
-    T = generate_gpu(w, seed=0)
+    T = generate_gpu(w, seed=0)  # identical on every rank (same seed); rank keeps its slab
+    T_loc = T[shard.struct.slab_begin:shard.struct.slab_end].contiguous() if shard else T
+    if shard:
+        del T
     cfg = PasdConfig(lambdas=w.lambdas(), ranks=list(w.ranks), eps=w.eps, maxiter=W + K + args.profile_iters + 1)
-    sol = pb.Solver(w.dims, cfg, fixed_iters=True, poll_every=K)
-    sol.load(T.data_ptr(), t_is_device=True)
+    sol = pb.Solver(w.dims, cfg, fixed_iters=True, poll_every=K, shard=shard)
+    sol.load(T_loc.data_ptr(), t_is_device=True)
     sol.run(W)
     stream = torch.cuda.ExternalStream(sol.stream)
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
-    clk = ClockSampler(torch.cuda.current_device())
+    clk = ClockSampler(local_rank)
     clk.start()
     torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
     ev0.record(stream)
     done, _ = sol.run(K)
     ev1.record(stream)
     ev1.synchronize()
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
     clocks = clk.stop()
     ms = ev0.elapsed_time(ev1)
+    if dist:  # device time, max over ranks
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
     launches = sol.launches
     prof = sol.profile(args.profile_iters)
     sol.close()
@@ -301,10 +363,10 @@ def main():
     S = w.size
     N = len(w.dims)
     RJ = sum(r * (S // d) for r, d in zip(w.ranks, w.dims))
-    B_iter = 8.0 * ((3 * N + 4) * S + 2 * RJ)
-    F_iter = 6.0 * S * sum(w.ranks)
+    B_iter = 8.0 * ((3 * N + 4) * S + 2 * RJ) / world
+    F_iter = 6.0 * S * sum(w.ranks) / world
     t_roof = max(B_iter / (peaks["hbm_gbs"] * 1e9), F_iter / (peaks["fp64_tflops"] * 1e12))
-    iteration_roofline = {"B_iter": B_iter, "F_iter": F_iter, "t_roof_ms": t_roof * 1e3,
+    iteration_roofline = {"B_iter_per_gpu": B_iter, "F_iter_per_gpu": F_iter, "t_roof_ms": t_roof * 1e3,
                           "t_measured_ms": ms / K, "frac": round(t_roof / (ms / K * 1e-3), 4)}
     line = {
         "metric": "PASD ADMM iters/s", "value": round(value, 4), "unit": "iter/s", "n_gpus": world,
@@ -319,19 +381,28 @@ def main():
         "roofline": roof,
         "iteration_roofline": iteration_roofline,
     }
-    del T
+    del T_loc
     torch.cuda.empty_cache()
-    if not args.no_e2e:
+    if not args.no_e2e and shard is None:
         Tg = generate_gpu(w, seed=0)
         line["e2e"] = e2e_recover(w, Tg, K)
         del Tg
         torch.cuda.empty_cache()
-    if not args.no_cpu_baseline:
+    elif not args.no_e2e:
+        line["e2e"] = e2e_sharded(w, K, shard, dist)
+    if dist:
+        line["config"]["parallelism"] = f"slab{world} (mode-3 slabs, NCCL all-reduce of A_3/Gram/Wt partials)"
+    if rank != 0:
+        dist.destroy_process_group()
+        return 0
+    if not args.no_cpu_baseline and shard is None:
         try:
             line["cpu_baseline"] = cpu_baseline(w, threads=1)
         except Exception as exc:  # reported, never fatal
             line["cpu_baseline"] = {"error": str(exc)}
     print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
     return 0
 
 

@@ -205,6 +205,10 @@ int pasd_b200_procrustes(const double* g, int64_t i_rows, int64_t p_cols, const 
                          const double* u_prev, double* u_out, int32_t* degenerate, int32_t* rank, int32_t device,
                          char* errbuf, size_t errlen);
 
+/* 128-byte NCCL unique id for pasd_shard.nccl_unique_id (rank 0 creates it and
+ * broadcasts it to the other ranks with the host launcher's own channel). */
+int pasd_b200_nccl_unique_id(void* out128, char* errbuf, size_t errlen);
+
 /* Library / build identification. */
 int pasd_b200_abi_version(void);
 const char* pasd_b200_build_info(void);

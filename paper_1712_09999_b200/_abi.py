@@ -108,6 +108,7 @@ HEADER_SYMBOLS = (
     "pasd_b200_validate",
     "pasd_b200_svt",
     "pasd_b200_procrustes",
+    "pasd_b200_nccl_unique_id",
     "pasd_b200_abi_version",
     "pasd_b200_build_info",
 )

@@ -21,6 +21,8 @@ struct ModeDev {
   int64_t I;        // I_n
   int64_t outer;    // prod of higher dims
   int64_t J;        // inner * outer = S / I_n (unfolding columns)
+  int64_t Ifull;    // full I_n: leading dimension of U, UM, Wt (== I unless the mode is slab-sharded)
+  int64_t ioff;     // offset of local index 0 within [0, Ifull) (slab begin for the sharded mode)
   int R;            // R_n
   int mode;         // 0-based
   double lambda;    // lambda_n (SVT weight)

@@ -180,6 +180,17 @@ __global__ void __launch_bounds__(kThreads) k_gram(ModeDev m, const Ctl* ctl) {
   }
 }
 
+// Gram_n = sum of the chunk partials in fixed order -> out (R x R).
+__global__ void k_gram_reduce(ModeDev m, double* __restrict__ out, const Ctl* ctl) {
+  if (ctl->done) return;
+  const int RR = m.R * m.R;
+  for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < RR; idx += gridDim.x * blockDim.x) {
+    double a = 0.0;
+    for (int kc = 0; kc < m.nkc_g; ++kc) a += m.Gpart[(int64_t)kc * RR + idx];
+    out[idx] = a;
+  }
+}
+
 // ---------------------------------------------------------------------------
 // Pass 2 (generic order N): refold, E shrink, multiplier ascent, residuals.
 struct ModePack {
@@ -242,24 +253,53 @@ __global__ void __launch_bounds__(kThreads) k_update(const ModePack* __restrict_
 }
 
 // mu schedule, residual history and stop rule (pasd.cpp:229-239).
-__global__ void k_finish(Ctl* ctl, const double* __restrict__ resid_part, const int* __restrict__ bad_part,
-                         int nblocks, double* history) {
+// Local residual maxima / NaN flag of one rank -> out[0..N) and out[N] (as
+// 0/1), ready for a MAX allreduce across slab-sharded ranks.
+__global__ void k_resid_local(const Ctl* ctl, const double* __restrict__ resid_part, const int* __restrict__ bad_part,
+                              int nblocks, double* out) {
   if (ctl->done) return;
   __shared__ double red[32];
   __shared__ int redi[32];
   const int N = ctl->order;
-  double resid[PASD_MAX_ORDER];
   for (int n = 0; n < N; ++n) {
     double w = 0.0;
     for (int b = threadIdx.x; b < nblocks; b += blockDim.x) {
       const double v = resid_part[(int64_t)b * PASD_MAX_ORDER + n];
       if (v > w) w = v;
     }
-    resid[n] = block_reduce(w, MaxOp(), red);
+    w = block_reduce(w, MaxOp(), red);
+    if (threadIdx.x == 0) out[n] = w;
   }
   int bad = 0;
   for (int b = threadIdx.x; b < nblocks; b += blockDim.x) bad |= bad_part[b];
   bad = block_reduce(bad, OrOp(), redi);
+  if (threadIdx.x == 0) out[N] = bad ? 1.0 : 0.0;
+}
+
+// `reduced` (optional): residual maxima + NaN flag already reduced across ranks.
+__global__ void k_finish(Ctl* ctl, const double* __restrict__ resid_part, const int* __restrict__ bad_part,
+                         int nblocks, double* history, const double* __restrict__ reduced) {
+  if (ctl->done) return;
+  __shared__ double red[32];
+  __shared__ int redi[32];
+  const int N = ctl->order;
+  double resid[PASD_MAX_ORDER];
+  int bad = 0;
+  if (reduced) {
+    for (int n = 0; n < N; ++n) resid[n] = reduced[n];
+    bad = reduced[N] != 0.0;
+  } else {
+    for (int n = 0; n < N; ++n) {
+      double w = 0.0;
+      for (int b = threadIdx.x; b < nblocks; b += blockDim.x) {
+        const double v = resid_part[(int64_t)b * PASD_MAX_ORDER + n];
+        if (v > w) w = v;
+      }
+      resid[n] = block_reduce(w, MaxOp(), red);
+    }
+    for (int b = threadIdx.x; b < nblocks; b += blockDim.x) bad |= bad_part[b];
+    bad = block_reduce(bad, OrOp(), redi);
+  }
   if (threadIdx.x == 0) {
     const double mu = ctl->mu;
     const double cand = __dmul_rn(ctl->rho, mu);
@@ -382,9 +422,9 @@ __global__ void k_materialize_z(ModeDev m, double* __restrict__ out, int64_t S) 
     const int64_t q = rest / m.I;
     const int64_t i = rest - q * m.I;
     const double* a = m.A + p + m.inner * (int64_t)m.R * q;
-    const double* um = m.UM + i;
+    const double* um = m.UM + m.ioff + i;
     double z = 0.0;
-    for (int r = 0; r < m.R; ++r) z = fma(um[m.I * r], a[m.inner * r], z);
+    for (int r = 0; r < m.R; ++r) z = fma(um[m.Ifull * r], a[m.inner * r], z);
     out[idx] = z;
   }
 }

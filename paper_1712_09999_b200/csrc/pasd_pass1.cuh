@@ -69,7 +69,7 @@ __global__ void __launch_bounds__(P1_THREADS, 2) k_contract_A_mma(ModeDev m, con
     for (int idx = tid; idx < P1_KC * RP; idx += P1_THREADS) {
       const int i = idx % P1_KC, r = idx / P1_KC;
       const bool ok = r < R && i0 + i < I;
-      cp_async8(&Us[buf][i][r], ok ? m.U + (i0 + i) + I * r : m.U, ok);
+      cp_async8(&Us[buf][i][r], ok ? m.U + m.ioff + (i0 + i) + m.Ifull * r : m.U, ok);
     }
   };
   double acc[NT][4];

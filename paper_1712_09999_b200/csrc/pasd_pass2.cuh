@@ -223,12 +223,12 @@ __global__ void __launch_bounds__(P2_THREADS, 1) k_pass2_fused(const Pass2Args a
     for (int idx = tid; idx < 16 * R1; idx += P2_THREADS) {
       const int l1 = idx & 15, r = idx >> 4;
       const bool v = l1 < nv1;
-      cp_async8(U1s + l1 * L::LDU + r, v ? m1.UM + i1o + l1 + I1 * r : m1.UM, v);
+      cp_async8(U1s + l1 * L::LDU + r, v ? m1.UM + m1.ioff + i1o + l1 + m1.Ifull * r : m1.UM, v);
     }
     for (int idx = tid; idx < 8 * R3; idx += P2_THREADS) {
       const int l3 = idx & 7, r = idx >> 3;
       const bool v = i3o + l3 < I3;
-      cp_async8(U3s + l3 * L::LDU + r, v ? m3.UM + i3o + l3 + I3 * r : m3.UM, v);
+      cp_async8(U3s + l3 * L::LDU + r, v ? m3.UM + m3.ioff + i3o + l3 + m3.Ifull * r : m3.UM, v);
     }
     double w1acc[NT1][4];
 #pragma unroll
@@ -251,7 +251,7 @@ __global__ void __launch_bounds__(P2_THREADS, 1) k_pass2_fused(const Pass2Args a
       for (int idx = tid; idx < 8 * R2; idx += P2_THREADS) {
         const int l2 = idx & 7, r = idx >> 3;
         const bool v = i2o + l2 < I2;
-        cp_async8(U2s + l2 * L::LDU + r, v ? m2.UM + i2o + l2 + I2 * r : m2.UM, v);
+        cp_async8(U2s + l2 * L::LDU + r, v ? m2.UM + m2.ioff + i2o + l2 + m2.Ifull * r : m2.UM, v);
       }
       // this thread's 4 elements: (i1 = g, g+8) x (i2 = 2t, 2t+1) at i3 = w
       double tv[4], yv[3][4];
@@ -463,31 +463,34 @@ inline void pass2_launch(int rp, const Pass2Args& a, const Ctl* ctl, int grid, c
 
 // Reduce the pass-2 partials into Wt_n (I_n x R_n, column-major) and
 // ctl->gnorm2[n], in a fixed order.  grid = (ceil(max I_n R_n / 256), 3).
-__global__ void k_pass2_reduce(const Pass2Args a, int nblk, Ctl* ctl) {
+__global__ void k_pass2_reduce(const Pass2Args a, int nblk, Ctl* ctl, double* g2out) {
   if (ctl->done) return;
   const int n = blockIdx.y;
   const ModeDev& m = a.m[n];
   const int R = m.R;
-  const int64_t IR = m.I * R;
+  const int64_t IR = m.Ifull * R;  // full rows; rows outside this rank's slab are 0
   for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < IR; idx += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t i = idx % m.I;
-    const int r = (int)(idx / m.I);
+    const int64_t ifull = idx % m.Ifull;
+    const int r = (int)(idx / m.Ifull);
+    const int64_t i = ifull - m.ioff;
     double s = 0.0;
-    if (n == 0) {
-      const int ib = (int)(i / P2_B1), l = (int)(i % P2_B1);
-      for (int b3 = 0; b3 < a.n3b; ++b3) s += a.W1p[((int64_t)(ib + a.n1b * b3) * 16 + l) * R + r];
-    } else if (n == 1) {
-      for (int c = 0; c < nblk; ++c) s += a.W2part[((int64_t)c * m.I + i) * R + r];
-    } else {
-      const int ib = (int)(i / P2_B3), l = (int)(i % P2_B3);
-      for (int b1 = 0; b1 < a.n1b; ++b1) s += a.W3p[((int64_t)(b1 + a.n1b * ib) * 8 + l) * R + r];
+    if (i >= 0 && i < m.I) {
+      if (n == 0) {
+        const int ib = (int)(i / P2_B1), l = (int)(i % P2_B1);
+        for (int b3 = 0; b3 < a.n3b; ++b3) s += a.W1p[((int64_t)(ib + a.n1b * b3) * 16 + l) * R + r];
+      } else if (n == 1) {
+        for (int c = 0; c < nblk; ++c) s += a.W2part[((int64_t)c * m.I + i) * R + r];
+      } else {
+        const int ib = (int)(i / P2_B3), l = (int)(i % P2_B3);
+        for (int b1 = 0; b1 < a.n1b; ++b1) s += a.W3p[((int64_t)(b1 + a.n1b * ib) * 8 + l) * R + r];
+      }
     }
     m.Wt[idx] = s;
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     double s = 0.0;
     for (int c = 0; c < nblk; ++c) s += a.gpart[c * 3 + n];
-    ctl->gnorm2[n] = s;
+    g2out[n] = s;
   }
 }
 

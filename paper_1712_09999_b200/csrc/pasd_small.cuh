@@ -217,13 +217,8 @@ __global__ void __launch_bounds__(kSmallThreads) k_svt(const ModePack* __restric
   const int R = m.R, tid = threadIdx.x, nt = blockDim.x;
   SmallWs ws = make_ws(R, smem);
   const int ld = ws.ld;
-  // Gram = sum of partials in fixed chunk order (deterministic)
-  for (int idx = tid; idx < R * R; idx += nt) {
-    double a = 0.0;
-    for (int kc = 0; kc < m.nkc_g; ++kc) a += m.Gpart[(int64_t)kc * R * R + idx];
-    ws.S[(idx / R) * ld + idx % R] = a;
-    m.Gram[idx] = a;
-  }
+  // Gram_n (reduced over chunks by k_gram_reduce, and over ranks when sharded)
+  for (int idx = tid; idx < R * R; idx += nt) ws.S[(idx / R) * ld + idx % R] = m.Gram[idx];
   __syncthreads();
   cta_jacobi_eig(ws, R);
   const double tau = __ddiv_rn(m.lambda, ctl->mu);  // lambda / mu (pasd.cpp:77)
@@ -269,7 +264,7 @@ __global__ void __launch_bounds__(kSmallThreads) k_svt(const ModePack* __restric
   }
   __syncthreads();
   // UM = U * M
-  cta_mul_nn(m.U, m.I, R, ws.S, ld, R, m.UM);
+  cta_mul_nn(m.U, m.Ifull, R, ws.S, ld, R, m.UM);
 }
 
 // ---------------------------------------------------------------------------
@@ -280,7 +275,7 @@ __global__ void __launch_bounds__(kSmallThreads) k_polar(const ModePack* __restr
   const int n = blockIdx.x;
   const ModeDev& m = mp->m[n];
   const int R = m.R, tid = threadIdx.x, nt = blockDim.x;
-  const int64_t I = m.I, IR = I * R;
+  const int64_t I = m.Ifull, IR = I * R;
   SmallWs ws = make_ws(R, smem);
   const int ld = ws.ld;
   double* Wt = m.Wt;                // I x R: G^{next} A^T, reduced by the pass that produced it

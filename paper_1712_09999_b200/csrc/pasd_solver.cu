@@ -13,6 +13,7 @@
 // results never depend on the polling period.  No CPU fallback exists: every
 // per-iteration step is a kernel in pasd_kernels.cuh / pasd_small.cuh.
 #include <cuda_runtime.h>
+#include <nccl.h>
 
 #include <algorithm>
 #include <cmath>
@@ -48,6 +49,10 @@ void ck(cudaError_t e, const char* what) {
   if (e != cudaSuccess) fail(PASD_ERR_CUDA, std::string("cuda: ") + what + ": " + cudaGetErrorString(e));
 }
 #define CK(x) ck((x), #x)
+void nk(ncclResult_t r, const char* what) {
+  if (r != ncclSuccess) fail(PASD_ERR_CUDA, std::string("nccl: ") + what + ": " + ncclGetErrorString(r));
+}
+#define NK(x) nk((x), #x)
 
 int guarded_call(char* err, size_t errlen, const std::function<void()>& f);
 
@@ -171,8 +176,20 @@ struct pasd_solver {
   int64_t launches_last_run = 0;
   int launches_per_iter = 0;
   bool loaded = false;
+  // slab sharding along the last mode (one process per GPU)
+  bool sharded = false;
+  int rank = 0, nranks = 1;
+  int64_t slab_b = 0, slab_e = 0;
+  std::vector<int64_t> gdims;  // global dims (dims = local slab dims)
+  ncclComm_t comm = nullptr;
+  double* A3_partial = nullptr;
+  std::vector<double*> gram_partial, wt_partial;
+  double* g2_partial = nullptr;
+  double* red_local = nullptr;
+  double* red = nullptr;
 
   ~pasd_solver() {
+    if (comm) ncclCommDestroy(comm);
     if (graph_exec) cudaGraphExecDestroy(graph_exec);
     if (graph) cudaGraphDestroy(graph);
     for (void* p : owned) cudaFree(p);
@@ -190,6 +207,10 @@ struct pasd_solver {
 
 namespace {
 
+double* ctl_gnorm2(pasd_solver* s) {  // device address of ctl->gnorm2[0]
+  return reinterpret_cast<double*>(reinterpret_cast<char*>(s->d_ctl) + offsetof(Ctl, gnorm2));
+}
+
 // Launches one iteration.  `mark(cls, begin)` (optional) is called around
 // every kernel; the profiler records CUDA events there.
 template <class Mark>
@@ -201,15 +222,33 @@ void launch_iteration_marked(pasd_solver* s, cudaStream_t st, Mark&& mark) {
   mark(PASD_K_POLAR, false);
   ++launches;
   for (int n = 0; n < N; ++n) {
-    const ModeDev& m = s->modes[n];
+    ModeDev m = s->modes[n];
+    if (s->sharded && n == N - 1) m.A = s->A3_partial;  // partial sum over this rank's slab
     mark(PASD_K_CONTRACT_A, true);
     launch_contract_A_mma(m, s->T, s->E[0], s->E[1], s->Y[n], s->d_ctl, st);
     mark(PASD_K_CONTRACT_A, false);
     ++launches;
+  }
+  if (s->sharded) {  // A_3 = sum over ranks of the slab partials (the one large exchange)
+    const ModeDev& m3 = s->modes[N - 1];
+    NK(ncclAllReduce(s->A3_partial, m3.A, (size_t)m3.J * m3.R, ncclDouble, ncclSum, s->comm, st));
+  }
+  for (int n = 0; n < N; ++n) {
+    const ModeDev& m = s->modes[n];
     mark(PASD_K_GRAM, true);
     k_gram<<<m.nkc_g, kThreads, 0, st>>>(m, s->d_ctl);
+    const bool part = s->sharded && n < N - 1;  // Gram_1, Gram_2 are partial over the slab
+    k_gram_reduce<<<8, 256, 0, st>>>(m, part ? s->gram_partial[n] : m.Gram, s->d_ctl);
     mark(PASD_K_GRAM, false);
-    ++launches;
+    launches += 2;
+  }
+  if (s->sharded) {
+    NK(ncclGroupStart());
+    for (int n = 0; n < N - 1; ++n) {
+      const ModeDev& m = s->modes[n];
+      NK(ncclAllReduce(s->gram_partial[n], m.Gram, (size_t)m.R * m.R, ncclDouble, ncclSum, s->comm, st));
+    }
+    NK(ncclGroupEnd());
   }
   mark(PASD_K_SVT, true);
   k_svt<<<N, kSmallThreads, s->small_smem, st>>>(s->d_pack, s->d_ctl);
@@ -220,15 +259,29 @@ void launch_iteration_marked(pasd_solver* s, cudaStream_t st, Mark&& mark) {
     pass2_launch(s->p2_rp, s->p2, s->d_ctl, s->p2_grid, st);
     mark(PASD_K_UPDATE, false);
     ++launches;
-    mark(PASD_K_FINISH, true);
-    k_finish<<<1, kThreads, 0, st>>>(s->d_ctl, s->p2_resid, s->p2_bad, s->p2_grid, s->d_hist);
-    mark(PASD_K_FINISH, false);
-    ++launches;
     int64_t maxir = 1;
-    for (const ModeDev& m : s->modes) maxir = std::max<int64_t>(maxir, m.I * m.R);
+    for (const ModeDev& m : s->modes) maxir = std::max<int64_t>(maxir, m.Ifull * m.R);
     mark(PASD_K_CONTRACT_W, true);
-    k_pass2_reduce<<<dim3((unsigned)((maxir + 255) / 256), 3), 256, 0, st>>>(s->p2, s->p2_grid, s->d_ctl);
+    k_pass2_reduce<<<dim3((unsigned)((maxir + 255) / 256), 3), 256, 0, st>>>(
+        s->p2, s->p2_grid, s->d_ctl, s->sharded ? s->g2_partial : ctl_gnorm2(s));
     mark(PASD_K_CONTRACT_W, false);
+    ++launches;
+    if (s->sharded) {
+      k_resid_local<<<1, kThreads, 0, st>>>(s->d_ctl, s->p2_resid, s->p2_bad, s->p2_grid, s->red_local);
+      ++launches;
+      NK(ncclGroupStart());
+      for (int n = 0; n < N; ++n) {
+        const ModeDev& m = s->modes[n];
+        NK(ncclAllReduce(s->wt_partial[n], m.Wt, (size_t)m.Ifull * m.R, ncclDouble, ncclSum, s->comm, st));
+      }
+      NK(ncclAllReduce(s->g2_partial, ctl_gnorm2(s), (size_t)N, ncclDouble, ncclSum, s->comm, st));
+      NK(ncclAllReduce(s->red_local, s->red, (size_t)N + 1, ncclDouble, ncclMax, s->comm, st));
+      NK(ncclGroupEnd());
+    }
+    mark(PASD_K_FINISH, true);
+    k_finish<<<1, kThreads, 0, st>>>(s->d_ctl, s->p2_resid, s->p2_bad, s->p2_grid, s->d_hist,
+                                     s->sharded ? s->red : nullptr);
+    mark(PASD_K_FINISH, false);
     ++launches;
   } else {
     mark(PASD_K_UPDATE, true);
@@ -237,7 +290,7 @@ void launch_iteration_marked(pasd_solver* s, cudaStream_t st, Mark&& mark) {
     mark(PASD_K_UPDATE, false);
     ++launches;
     mark(PASD_K_FINISH, true);
-    k_finish<<<1, kThreads, 0, st>>>(s->d_ctl, s->d_resid_part, s->d_bad_part, s->nblk_update, s->d_hist);
+    k_finish<<<1, kThreads, 0, st>>>(s->d_ctl, s->d_resid_part, s->d_bad_part, s->nblk_update, s->d_hist, nullptr);
     mark(PASD_K_FINISH, false);
     ++launches;
     for (int n = 0; n < N; ++n) {
@@ -299,16 +352,16 @@ __global__ void k_init_state(ModePack* mp, Ctl* ctl, double mu0, double rho, dou
   const int N = mp->order;
   for (int n = 0; n < N; ++n) {
     ModeDev& m = mp->m[n];
-    const int64_t IR = m.I * m.R;
+    const int64_t IR = m.Ifull * m.R;
     for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < IR; idx += (int64_t)gridDim.x * blockDim.x) {
-      const int64_t i = idx % m.I, r = idx / m.I;
+      const int64_t i = idx % m.Ifull, r = idx / m.Ifull;
       m.U[idx] = (i == r) ? 1.0 : 0.0;  // Matrix::Identity(rows, rank) (pasd.cpp:152)
       m.UM[idx] = 0.0;
     }
     for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < (int64_t)m.R * m.R;
          idx += (int64_t)gridDim.x * blockDim.x)
       m.M[idx] = 0.0;  // V = 0 (pasd.cpp:153) <=> M = 0
-    for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < m.I * m.R;
+    for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < m.Ifull * m.R;
          idx += (int64_t)gridDim.x * blockDim.x)
       m.Wt[idx] = 0.0;  // Wt = G V^T = 0 for V = 0: first Procrustes is degenerate
     const int64_t wp = (int64_t)m.nkc_w * m.I * m.R;
@@ -355,11 +408,27 @@ void reset_state(pasd_solver* s) {
 
 pasd_solver* create_solver(const pasd_options* o, const pasd_shard* shard) {
   validate_options(o);
-  if (shard && shard->nranks > 1)
-    fail(PASD_ERR_ARGUMENT, "pasd_b200: multi-rank sharding is not available in this build");
   auto s = std::make_unique<pasd_solver>();
   s->N = o->order;
   s->dims.assign(o->dims, o->dims + o->order);
+  s->gdims = s->dims;
+  if (shard) {  // slab along the last mode
+    if (o->order != 3) fail(PASD_ERR_ARGUMENT, "pasd_b200: slab sharding supports order-3 tensors only");
+    if (shard->nranks < 1 || shard->rank < 0 || shard->rank >= shard->nranks)
+      fail(PASD_ERR_ARGUMENT, "pasd_b200: invalid rank/nranks");
+    if (!(0 <= shard->slab_begin && shard->slab_begin < shard->slab_end && shard->slab_end <= s->dims[2]))
+      fail(PASD_ERR_ARGUMENT, "pasd_b200: slab [" + std::to_string(shard->slab_begin) + ", " +
+                                  std::to_string(shard->slab_end) + ") outside mode 3 of size " +
+                                  std::to_string(s->dims[2]));
+    for (int n = 0; n < 3; ++n)
+      if (o->ranks[n] > PASD_MAX_RANK) fail(PASD_ERR_ARGUMENT, "pasd_b200: rank exceeds 64");
+    s->sharded = true;
+    s->rank = shard->rank;
+    s->nranks = shard->nranks;
+    s->slab_b = shard->slab_begin;
+    s->slab_e = shard->slab_end;
+    s->dims[2] = s->slab_e - s->slab_b;
+  }
   s->S = dims_product(s->dims);
   s->ranks.assign(o->ranks, o->ranks + o->order);
   s->lambdas.assign(o->lambdas, o->lambdas + o->order);
@@ -392,15 +461,17 @@ pasd_solver* create_solver(const pasd_options* o, const pasd_shard* shard) {
     m.outer = 1;
     for (int l = n + 1; l < s->N; ++l) m.outer *= s->dims[l];
     m.J = m.inner * m.outer;
+    m.Ifull = s->gdims[n];
+    m.ioff = (s->sharded && n == s->N - 1) ? s->slab_b : 0;
     m.R = (int)s->ranks[n];
     maxR = std::max(maxR, m.R);
     m.lambda = s->lambdas[n];
-    const int64_t IR = m.I * m.R, RR = (int64_t)m.R * m.R;
-    m.U = s->alloc<double>(IR);
-    m.UM = s->alloc<double>(IR);
+    const int64_t IR = m.I * m.R, RR = (int64_t)m.R * m.R, IRf = m.Ifull * m.R;
+    m.U = s->alloc<double>(IRf);
+    m.UM = s->alloc<double>(IRf);
     m.M = s->alloc<double>(RR);
     m.A = s->alloc<double>((size_t)m.J * m.R);
-    m.Wt = s->alloc<double>(IR);
+    m.Wt = s->alloc<double>(IRf);
     m.nib_w = (int)((m.I + CW_IT - 1) / CW_IT);
     const int64_t kchunks = (m.J + CW_KC - 1) / CW_KC;
     m.nkc_w = (int)std::max<int64_t>(1, std::min<int64_t>(kchunks, std::max(1, 592 / m.nib_w)));
@@ -411,8 +482,28 @@ pasd_solver* create_solver(const pasd_options* o, const pasd_shard* shard) {
     m.Gram = s->alloc<double>(RR);
     m.sig = s->alloc<double>(m.R);
     m.P = s->alloc<double>(RR);
-    m.scratch = s->alloc<double>(3 * IR);
+    m.scratch = s->alloc<double>(3 * IRf);
     s->modes.push_back(m);
+  }
+  if (s->sharded) {
+    const ModeDev& m3 = s->modes[2];
+    s->A3_partial = s->alloc<double>((size_t)m3.J * m3.R);
+    for (int n = 0; n < 3; ++n) {
+      const ModeDev& m = s->modes[n];
+      s->gram_partial.push_back(s->alloc<double>((size_t)m.R * m.R));
+      s->wt_partial.push_back(s->alloc<double>((size_t)m.Ifull * m.R));
+    }
+    s->g2_partial = s->alloc<double>(PASD_MAX_ORDER);
+    s->red_local = s->alloc<double>(PASD_MAX_ORDER + 1);
+    s->red = s->alloc<double>(PASD_MAX_ORDER + 1);
+    ncclUniqueId id;
+    if (shard->nccl_unique_id)
+      std::memcpy(&id, shard->nccl_unique_id, sizeof(id));
+    else if (s->nranks == 1)
+      NK(ncclGetUniqueId(&id));
+    else
+      fail(PASD_ERR_ARGUMENT, "pasd_b200: nccl_unique_id is required for nranks > 1");
+    NK(ncclCommInitRank(&s->comm, s->nranks, id, s->rank));
   }
   std::memset(&s->h_pack, 0, sizeof(ModePack));
   s->h_pack.order = s->N;
@@ -438,6 +529,7 @@ pasd_solver* create_solver(const pasd_options* o, const pasd_shard* shard) {
     Pass2Args& a = s->p2;
     for (int n = 0; n < 3; ++n) {
       a.m[n] = s->modes[n];
+      if (s->sharded) a.m[n].Wt = s->wt_partial[n];  // reduced across ranks by NCCL
       a.Y[n] = s->Y[n];
     }
     a.T = s->T;
@@ -512,6 +604,7 @@ __global__ void k_state_ctl(Ctl* ctl, ModePack* mp, double mu, int iter, const d
 void set_state(pasd_solver* s, const double* e, const double* const* y, const double* const* u,
                const double* const* v, double mu, int iter) {
   if (!s->loaded) fail(PASD_ERR_STATE, "pasd_b200: no tensor loaded");
+  if (s->sharded) fail(PASD_ERR_STATE, "pasd_b200: set_state is not available on a sharded solver");
   if (!e || !y || !u || !v) fail(PASD_ERR_ARGUMENT, "pasd_b200: null state buffer");
   if (iter >= s->maxiter) fail(PASD_ERR_ARGUMENT, "pasd_b200: state iteration must be below maxiter");
   cudaStream_t st = s->stream;
@@ -600,6 +693,7 @@ void ensure_scratch(pasd_solver* s) {
 // Runs until stop or `iters` more iterations.
 void run_solver(pasd_solver* s, int iters, pasd_observer_fn obs, void* user) {
   if (!s->loaded) fail(PASD_ERR_STATE, "pasd_b200: no tensor loaded");
+  if (obs && s->sharded) fail(PASD_ERR_STATE, "pasd_b200: observers are not available on a sharded solver");
   sync_ctl(s);
   if (s->h_ctl->done) return;
   build_graph(s);
@@ -700,6 +794,16 @@ void finalize_solver(pasd_solver* s, pasd_outputs* out) {
   CK(cudaStreamSynchronize(st));
   double l1 = 0.0;
   abs_stats(e, &l1, nullptr);
+  auto allreduce_scalar = [&](double v, ncclRedOp_t op) {
+    if (!s->sharded) return v;
+    CK(cudaMemcpyAsync(s->d_stats, &v, sizeof(double), cudaMemcpyHostToDevice, st));
+    NK(ncclAllReduce(s->d_stats, s->d_stats + 1, 1, ncclDouble, op, s->comm, st));
+    double r = 0.0;
+    CK(cudaMemcpyAsync(&r, s->d_stats + 1, sizeof(double), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    return r;
+  };
+  l1 = allreduce_scalar(l1, ncclSum);  // ||E||_1 over all slabs
   double obj = l1;
   for (int n = 0; n < N; ++n) obj += s->lambdas[n] * c.nuclear[n];
   out->objective = obj;
@@ -719,12 +823,16 @@ void finalize_solver(pasd_solver* s, pasd_outputs* out) {
     double eps_hat = 0.0, tl1 = 0.0;
     abs_stats(s->xbuf, nullptr, &eps_hat);
     abs_stats(s->T, &tl1, nullptr);
+    eps_hat = allreduce_scalar(eps_hat, ncclMax);
+    tl1 = allreduce_scalar(tl1, ncclSum);
     const int k_star = c.iter - 1;
     const double geom = s->rho * (1.0 + s->rho) / (s->rho - 1.0) + 0.5 / std::pow(s->rho, k_star);
     double dim_sum = 0.0, lam_term = 0.0;
+    double Sg = 1.0;
+    for (int64_t d : s->gdims) Sg *= (double)d;
     for (int n = 0; n < N; ++n) {
-      dim_sum += (double)S;
-      lam_term += s->lambdas[n] * (double)S * s->eps;
+      dim_sum += Sg;
+      lam_term += s->lambdas[n] * Sg * s->eps;
     }
     const double nn = (double)N;
     const double cc = dim_sum * geom / (s->mu0 * nn * nn) + tl1;
@@ -758,6 +866,16 @@ int guarded_call(char* err, size_t errlen, const std::function<void()>& f) {
 extern "C" {
 
 int pasd_b200_abi_version(void) { return PASD_B200_ABI_VERSION; }
+
+int pasd_b200_nccl_unique_id(void* out128, char* errbuf, size_t errlen) {
+  return guarded_call(errbuf, errlen, [&] {
+    if (!out128) fail(PASD_ERR_ARGUMENT, "pasd_b200: null output");
+    ncclUniqueId id;
+    NK(ncclGetUniqueId(&id));
+    static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+    std::memcpy(out128, &id, sizeof(id));
+  });
+}
 
 const char* pasd_b200_build_info(void) {
   return "pasd_b200 sm_100a fp64; kernels: polar,contract_A,gram,svt,update,finish,contract_W";
@@ -924,6 +1042,8 @@ void device_svt(const double* m_h, int64_t rows, int64_t cols, double tau, doubl
   ModeDev m{};
   m.inner = 1;
   m.I = rows;
+  m.Ifull = rows;
+  m.ioff = 0;
   m.outer = cols;
   m.J = cols;
   m.R = (int)rows;
@@ -950,6 +1070,7 @@ void device_svt(const double* m_h, int64_t rows, int64_t cols, double tau, doubl
   Ctl* ctl = t.alloc<Ctl>(1);
   k_set_ctl<<<1, 1>>>(ctl, 1.0, 0.0);
   k_gram<<<m.nkc_g, kThreads>>>(m, ctl);
+  k_gram_reduce<<<8, 256>>>(m, m.Gram, ctl);
   const size_t smem = small_ws_bytes(R);
   CK(cudaFuncSetAttribute(k_svt, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   k_svt<<<1, kSmallThreads, smem>>>(d_pack, ctl);
@@ -974,6 +1095,8 @@ void device_procrustes(const double* g_h, int64_t I, int64_t P, const double* v_
   ModeDev m{};
   m.inner = 1;
   m.I = I;
+  m.Ifull = I;
+  m.ioff = 0;
   m.outer = P;
   m.J = P;
   m.R = R;

@@ -111,13 +111,19 @@ class Solver:
     def __init__(self, dims: Sequence[int], config: PasdConfig, *, device: int = 0, fixed_iters: bool = False,
                  poll_every: int = 0, shard: Optional[_abi.PasdShard] = None):
         self.dims = [int(d) for d in dims]
+        self.local_dims = list(self.dims)
+        sh = getattr(shard, "struct", shard)
+        if sh is not None:
+            self.local_dims[-1] = int(sh.slab_end - sh.slab_begin)
         self.config = config
         count_checks(self.dims, config)
         flags = _abi.PASD_FLAG_FIXED_ITERS if fixed_iters else 0
         self._opt, self._keep = build_options(self.dims, config, device=device, flags=flags, poll_every=poll_every)
         self._h = C.c_void_p()
         err = _err()
-        rc = lib().pasd_b200_solver_create(C.byref(self._opt), C.byref(shard) if shard is not None else None,
+        self._shard = shard
+        sh = getattr(shard, "struct", shard)
+        rc = lib().pasd_b200_solver_create(C.byref(self._opt), C.byref(sh) if sh is not None else None,
                                            C.byref(self._h), err, len(err))
         raise_for_status(rc, err)
 
@@ -155,7 +161,7 @@ class Solver:
 
     def finalize(self, want_x=True, want_e=True, want_z=False, want_y=False):
         n = len(self.dims)
-        total = int(np.prod(self.dims))
+        total = int(np.prod(self.local_dims))
         x = np.empty(total) if want_x else None
         e = np.empty(total) if want_e else None
         z = [np.empty(total) for _ in range(n)] if want_z else None
@@ -171,7 +177,7 @@ class Solver:
         out.final_residuals = _abi.dptr(fres)
         err = _err()
         raise_for_status(lib().pasd_b200_solver_finalize(self._h, C.byref(out), err, len(err)), err)
-        shape = tuple(self.dims)
+        shape = tuple(self.local_dims)
 
         def rs(a):
             return None if a is None else a.reshape(shape, order="F")

@@ -175,3 +175,28 @@ def test_reentrant_concurrent_calls(gpu, oracle_mod):
     for r in out:
         np.testing.assert_array_equal(r.x, ref.x)
         np.testing.assert_array_equal(r.e, ref.e)
+
+
+def test_sharded_single_rank_matches_unsharded(gpu, oracle_mod):
+    """The slab-sharded code path (NCCL all-reduces of the partial A_3, Gram,
+    Wt, ||G||^2 and residual buffers) with one rank owning the whole tensor
+    reproduces the unsharded solver bit-for-bit."""
+    from paper_1712_09999_b200.sharding import Shard
+
+    L0, T = instance(oracle_mod, (24, 20, 16), 2, 0.05, seed=5)
+    cfg = PasdConfig(lambdas=oracle_mod.default_lambdas(T.shape), ranks=[2, 2, 2], eps=1e-6)
+    s0 = gpu.Solver(T.shape, cfg)
+    s0.load(T)
+    s0.run(cfg.maxiter)
+    r0 = s0.finalize()
+    s0.close()
+    s1 = gpu.Solver(T.shape, cfg, shard=Shard(0, 1, (0, T.shape[2]), None))
+    s1.load(T)
+    s1.run(cfg.maxiter)
+    r1 = s1.finalize()
+    s1.close()
+    assert r0.iters == r1.iters and r0.converged == r1.converged
+    np.testing.assert_array_equal(r0.x, r1.x)
+    np.testing.assert_array_equal(r0.e, r1.e)
+    assert r0.objective == r1.objective
+    assert r0.certificate.epsilon_hat == r1.certificate.epsilon_hat
