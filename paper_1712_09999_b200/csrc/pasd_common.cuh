@@ -36,7 +36,8 @@ struct ModeDev {
   double* Gram;     // R x R   A_n A_n^T
   double* Gpart;    // [nkc][R][R] partial Gram
   double* sig;      // R       singular values of A_n (from the Gram eigen-solve)
-  double* P;        // R x R   eigenvectors of Gram_n (left singular vectors of A_n)
+  double* P;        // R x R   eigenvectors of Gram_n (left singular vectors of A_n); warm start
+  double* Qp;       // R x R   right rotation of the last Procrustes solve; warm start
   double* gpart;    // [nkc * nib] partial ||G||_F^2 of the W pass
   double* scratch;  // 3 x I x R scratch for the polar solve
   int nkc_w;        // kappa chunks of the W pass

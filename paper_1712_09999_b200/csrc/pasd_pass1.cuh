@@ -2,137 +2,238 @@
 //   A_n = U_n^T G_(n),  G_n = (T - E) + Y_n / mu          (proj/src/pasd.cpp:77,178-186)
 // for one mode n, directly on the strided tensor (no unfolding copy,
 // tensor.cpp:98-113).  As a GEMM: A (J x R) = G (J x I) * U (I x R), with
-// kappa = unfolding column (J, large), K = I_n, N = R_n <= 64.
+// kappa = unfolding column, K = I_n, N = R_n <= 64.
 //
-// CTA: 128 columns kappa x all R (RP = R padded to 8), 8 warps, warp w owns
-// the m16 tile of kappa rows 16w..16w+15 and all RP/8 n-tiles (the A
-// fragment is reused across them).  K runs over i in chunks of 16; the G
-// chunk is formed elementwise from T, E, Y_n (prefetched into registers one
-// chunk ahead, coalesced along the contiguous index) and double-buffered in
-// shared memory; the U chunk arrives by cp.async.
+// Persistent CTAs (one per SM, 8 warps) walk tiles of 128 columns kappa; K runs
+// over i in chunks of 16.  Raw T, E, Y_n chunks and the U chunk stream into a
+// 3-stage cp.async ring in shared memory (16-byte copies along the contiguous
+// index), so ~150 KB per SM is in flight while the DMMAs of the current chunk
+// run.  G is formed inside the DMMA A-fragment load (each G value feeds exactly
+// one fragment), warp w owns kappa rows 16w..16w+15 and all RP/8 n-tiles.
+// Tiles never cross an outer index q (for modes with inner > 1 a tile is 128
+// consecutive p at fixed q), so every staged row is one contiguous run.
 #pragma once
 #include "pasd_pass2.cuh"
 
 namespace pasd {
 
-constexpr int P1_MT = 128;  // kappa columns per CTA
-constexpr int P1_KC = 16;   // i rows per chunk
+constexpr int P1_MT = 128;     // kappa columns per tile
+constexpr int P1_KC = 16;      // i rows per chunk
+constexpr int P1_NST = 3;      // pipeline stages
 constexpr int P1_THREADS = 256;
-constexpr int P1_EPT = P1_MT * P1_KC / P1_THREADS;  // elements per thread per chunk (8)
 
-template <int RP>
-__global__ void __launch_bounds__(P1_THREADS, 2) k_contract_A_mma(ModeDev m, const double* __restrict__ T,
-                                                              const double* __restrict__ E0,
-                                                              const double* __restrict__ E1,
-                                                              const double* __restrict__ Y, const Ctl* ctl) {
+template <int RP, bool CONTIG>
+struct P1Layout {
+  // CONTIG (mode 1): raw[kappa][i] rows of 16 i;  else raw[i][kappa] rows of 128 kappa.
+  static constexpr int LDR = CONTIG ? (P1_KC + 4) : (P1_MT + 4);
+  static constexpr int RAW = CONTIG ? P1_MT * LDR : P1_KC * LDR;  // doubles per tensor per stage
+  static constexpr int LDU = RP + 4;
+  static constexpr int USZ = P1_KC * LDU;
+  static constexpr int STAGE = 3 * RAW + USZ;
+  static constexpr size_t bytes = sizeof(double) * (size_t)P1_NST * STAGE;
+};
+
+template <int RP, bool CONTIG>
+__global__ void __launch_bounds__(P1_THREADS, 1) k_pass1(ModeDev m, const double* __restrict__ T,
+                                                        const double* __restrict__ E0,
+                                                        const double* __restrict__ E1,
+                                                        const double* __restrict__ Y, const Ctl* ctl) {
   if (ctl->done) return;
-  constexpr int NT = RP / 8, LDG = P1_MT + 4, LDU = RP + 4;
+  using L = P1Layout<RP, CONTIG>;
+  constexpr int NT = RP / 8;
   extern __shared__ double p1sm[];
-  double(*Gs)[P1_KC][LDG] = reinterpret_cast<double(*)[P1_KC][LDG]>(p1sm);
-  double(*Us)[P1_KC][LDU] = reinterpret_cast<double(*)[P1_KC][LDU]>(p1sm + 2 * P1_KC * LDG);
   const double* __restrict__ E = ctl->ecur ? E1 : E0;
   const double inv_mu = __ddiv_rn(1.0, ctl->mu);  // pasd.cpp:170
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5, g = lane >> 2, t = lane & 3;
-  const int64_t k0 = (int64_t)blockIdx.x * P1_MT;
   const int64_t I = m.I, inner = m.inner;
   const int R = m.R;
-  const bool contig_i = inner == 1;  // mode 1: i is the contiguous index
-  // per-thread staging elements: (kk_j, ii_j) and base offsets
-  int kk[P1_EPT], ii[P1_EPT];
-  int64_t base[P1_EPT];
-  bool colok[P1_EPT];
+  // tiles: CONTIG -> 128 consecutive kappa; else (q, p-block of 128)
+  const int64_t pblocks = CONTIG ? 1 : (inner + P1_MT - 1) / P1_MT;
+  const int64_t ntiles = CONTIG ? (m.J + P1_MT - 1) / P1_MT : pblocks * m.outer;
+  const int nchunk = (int)((I + P1_KC - 1) / P1_KC);
+  const bool al = CONTIG ? (I % 2 == 0) : (inner % 2 == 0);  // 16-byte aligned rows
+  const int64_t my_tiles = ntiles > blockIdx.x ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  const int64_t total = my_tiles * nchunk;  // (tile, chunk) work items of this CTA
+
+  auto stage_ptr = [&](int s) { return p1sm + (size_t)s * L::STAGE; };
+  // issue the cp.async copies of work item `it` into stage s
+  auto issue = [&](int64_t it, int s) {
+    if (it >= total) return;
+    const int64_t tile = blockIdx.x + (it / nchunk) * gridDim.x;
+    const int64_t i0 = (it % nchunk) * P1_KC;
+    double* st = stage_ptr(s);
+    if (CONTIG) {
+      // 128 columns kappa, 16 consecutive i each (contiguous): row = column
+      const int64_t k0 = tile * P1_MT;
+      const int ni = (int)imin64(P1_KC, I - i0);
+      if (al) {
+        const int c = tid & 7;  // 16-byte chunk of the 16-double row
+        const int v = ni - 2 * c, nbc = v >= 2 ? 16 : (v == 1 ? 8 : 0);
 #pragma unroll
-  for (int j = 0; j < P1_EPT; ++j) {
-    const int e = tid + P1_THREADS * j;
-    if (contig_i) { ii[j] = e % P1_KC; kk[j] = e / P1_KC; }
-    else { kk[j] = e % P1_MT; ii[j] = e / P1_MT; }
-    const int64_t kap = k0 + kk[j];
-    colok[j] = kap < m.J;
-    const int64_t q = colok[j] ? kap / inner : 0;
-    const int64_t p = colok[j] ? kap - q * inner : 0;
-    base[j] = p + inner * ((int64_t)ii[j] + I * q);  // + inner * i0 per chunk
-  }
-  double tv[P1_EPT], ev[P1_EPT], yv[P1_EPT];
-  auto load_chunk = [&](int64_t i0) {
+        for (int k = 0; k < P1_MT / 32; ++k) {
+          const int j = (tid >> 3) + 32 * k;
+          const int64_t kap = k0 + j;
+          const int nb = kap < m.J ? nbc : 0;
+          const int64_t off = kap * I + i0 + 2 * c;
+          const int d = j * L::LDR + 2 * c;
+          cp_async16(st + d, nb ? T + off : T, nb);
+          cp_async16(st + L::RAW + d, nb ? E + off : T, nb);
+          cp_async16(st + 2 * L::RAW + d, nb ? Y + off : T, nb);
+        }
+      } else {
+        for (int idx = tid; idx < P1_MT * P1_KC; idx += P1_THREADS) {
+          const int j = idx / P1_KC, c = idx % P1_KC;
+          const int64_t kap = k0 + j;
+          const bool ok = kap < m.J && c < ni;
+          const int64_t off = kap * I + i0 + c;
+          const int d = j * L::LDR + c;
+          cp_async8(st + d, ok ? T + off : T, ok);
+          cp_async8(st + L::RAW + d, ok ? E + off : T, ok);
+          cp_async8(st + 2 * L::RAW + d, ok ? Y + off : T, ok);
+        }
+      }
+    } else {
+      const int64_t q = tile / pblocks, p0 = (tile % pblocks) * P1_MT;
+      const int np = (int)imin64(P1_MT, inner - p0);
+      const int ni = (int)imin64(P1_KC, I - i0);
+      const int64_t off0 = p0 + inner * (i0 + I * q);
+      if (al) {
+        // 64 16-byte chunks per 128-double row; thread -> (chunk c, rows rsub + 4k)
+        const int c = tid & 63, rsub = tid >> 6;
+        const int v = np - 2 * c, nbc = v >= 2 ? 16 : (v == 1 ? 8 : 0);
 #pragma unroll
-    for (int j = 0; j < P1_EPT; ++j) {
-      const bool ok = colok[j] && i0 + ii[j] < I;
-      const int64_t off = base[j] + inner * i0;
-      tv[j] = ok ? T[off] : 0.0;
-      ev[j] = ok ? E[off] : 0.0;
-      yv[j] = ok ? Y[off] : 0.0;
+        for (int k = 0; k < P1_KC / 4; ++k) {
+          const int ii = rsub + 4 * k;
+          const int nb = ii < ni ? nbc : 0;
+          const int64_t off = off0 + inner * ii + 2 * c;
+          const int d = ii * L::LDR + 2 * c;
+          cp_async16(st + d, nb ? T + off : T, nb);
+          cp_async16(st + L::RAW + d, nb ? E + off : T, nb);
+          cp_async16(st + 2 * L::RAW + d, nb ? Y + off : T, nb);
+        }
+      } else {
+        for (int idx = tid; idx < P1_KC * P1_MT; idx += P1_THREADS) {
+          const int ii = idx / P1_MT, c = idx % P1_MT;
+          const bool ok = ii < ni && c < np;
+          const int64_t off = off0 + inner * ii + c;
+          const int d = ii * L::LDR + c;
+          cp_async8(st + d, ok ? T + off : T, ok);
+          cp_async8(st + L::RAW + d, ok ? E + off : T, ok);
+          cp_async8(st + 2 * L::RAW + d, ok ? Y + off : T, ok);
+        }
+      }
     }
-  };
-  auto store_chunk = [&](int buf, int64_t i0) {
-#pragma unroll
-    for (int j = 0; j < P1_EPT; ++j) Gs[buf][ii[j]][kk[j]] = g_elem(tv[j], ev[j], yv[j], inv_mu);
+    double* us = st + 3 * L::RAW;
     for (int idx = tid; idx < P1_KC * RP; idx += P1_THREADS) {
       const int i = idx % P1_KC, r = idx / P1_KC;
       const bool ok = r < R && i0 + i < I;
-      cp_async8(&Us[buf][i][r], ok ? m.U + m.ioff + (i0 + i) + m.Ifull * r : m.U, ok);
+      cp_async8(us + i * L::LDU + r, ok ? m.U + m.ioff + (i0 + i) + m.Ifull * r : m.U, ok);
     }
   };
-  double acc[NT][4];
+
+  double acc[NT][4], acb[NT][4];  // even / odd k-steps (two independent DMMA chains per n-tile)
+  int64_t it = 0;
+  for (int s = 0; s < P1_NST - 1; ++s) {
+    issue(s, s);
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  }
+  for (; it < total; ++it) {
+    const int s = (int)(it % P1_NST);
+    const int ci = (int)(it % nchunk);
+    if (ci == 0) {
 #pragma unroll
-  for (int j = 0; j < NT; ++j) acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.0;
-  const int nchunks = (int)((I + P1_KC - 1) / P1_KC);
-  load_chunk(0);
-  store_chunk(0, 0);
-  for (int c = 0; c < nchunks; ++c) {
-    const int buf = c & 1;
-    if (c + 1 < nchunks) load_chunk((int64_t)(c + 1) * P1_KC);  // in flight during the MMAs
-    cp_async_wait_all();
-    __syncthreads();
+      for (int j = 0; j < NT; ++j) {
+        acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.0;
+        acb[j][0] = acb[j][1] = acb[j][2] = acb[j][3] = 0.0;
+      }
+    }
+    asm volatile("cp.async.wait_group %0;" ::"n"(P1_NST - 2) : "memory");
+    __syncthreads();  // stage s complete for all threads; stage of item it-1 free
+    issue(it + P1_NST - 1, (int)((it + P1_NST - 1) % P1_NST));
+    asm volatile("cp.async.commit_group;" ::: "memory");
+    const double* st = stage_ptr(s);
+    const double* Ts = st;
+    const double* Es = st + L::RAW;
+    const double* Ys = st + 2 * L::RAW;
+    const double* Us = st + 3 * L::RAW;
 #pragma unroll
     for (int ks = 0; ks < P1_KC / 4; ++ks) {
       const int k = 4 * ks + t;
-      const double a0 = Gs[buf][k][16 * w + g], a1 = Gs[buf][k][16 * w + g + 8];
+      const int r0 = 16 * w + g, r1 = r0 + 8;
+      const int o0 = CONTIG ? r0 * L::LDR + k : k * L::LDR + r0;
+      const int o1 = CONTIG ? r1 * L::LDR + k : k * L::LDR + r1;
+      const double a0 = g_elem(Ts[o0], Es[o0], Ys[o0], inv_mu);
+      const double a1 = g_elem(Ts[o1], Es[o1], Ys[o1], inv_mu);
 #pragma unroll
-      for (int j = 0; j < NT; ++j) dmma(acc[j], a0, a1, Us[buf][k][8 * j + g]);
+      for (int j = 0; j < NT; ++j) dmma((ks & 1) ? acb[j] : acc[j], a0, a1, Us[k * L::LDU + 8 * j + g]);
     }
-    if (c + 1 < nchunks) store_chunk(buf ^ 1, (int64_t)(c + 1) * P1_KC);
-  }
-  // epilogue: C rows kappa = 16w + g (+8), cols r = 8j + 2t (+1)
+    if (ci == nchunk - 1) {  // tile done: write A
+      const int64_t tile = blockIdx.x + (it / nchunk) * gridDim.x;
 #pragma unroll
-  for (int j = 0; j < NT; ++j) {
+      for (int j = 0; j < NT; ++j)
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int64_t kap = k0 + 16 * w + g + 8 * (q >> 1);
-      const int r = 8 * j + 2 * t + (q & 1);
-      if (kap < m.J && r < R) m.A[a_offset(m, kap, r)] = acc[j][q];
+        for (int q4 = 0; q4 < 4; ++q4) acc[j][q4] += acb[j][q4];
+#pragma unroll
+      for (int j = 0; j < NT; ++j) {
+#pragma unroll
+        for (int q4 = 0; q4 < 4; ++q4) {
+          const int row = 16 * w + g + 8 * (q4 >> 1);
+          const int r = 8 * j + 2 * t + (q4 & 1);
+          if (r >= R) continue;
+          if (CONTIG) {
+            const int64_t kap = tile * P1_MT + row;
+            if (kap < m.J) m.A[r + (int64_t)R * kap] = acc[j][q4];
+          } else {
+            const int64_t q = tile / pblocks, p = (tile % pblocks) * P1_MT + row;
+            if (p < inner) m.A[p + inner * ((int64_t)r + (int64_t)R * q)] = acc[j][q4];
+          }
+        }
+      }
     }
   }
+  asm volatile("cp.async.wait_all;" ::: "memory");
 }
 
-template <int RP>
-constexpr size_t p1_smem_bytes() {
-  return sizeof(double) * 2 * P1_KC * ((P1_MT + 4) + (RP + 4));
-}
-
-template <int RP>
+template <int RP, bool CONTIG>
 void launch_p1(const ModeDev& m, const double* T, const double* E0, const double* E1, const double* Y, const Ctl* ctl,
-               cudaStream_t st) {
-  static bool attr = false;  // idempotent attribute set (benign race)
+               int grid, cudaStream_t st) {
+  using L = P1Layout<RP, CONTIG>;
+  static bool attr = false;  // idempotent attribute set
   if (!attr) {
-    cudaFuncSetAttribute(k_contract_A_mma<RP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p1_smem_bytes<RP>());
+    cudaFuncSetAttribute(k_pass1<RP, CONTIG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::bytes);
     attr = true;
   }
-  const unsigned grid = (unsigned)((m.J + P1_MT - 1) / P1_MT);
-  k_contract_A_mma<RP><<<grid, P1_THREADS, p1_smem_bytes<RP>(), st>>>(m, T, E0, E1, Y, ctl);
+  k_pass1<RP, CONTIG><<<grid, P1_THREADS, L::bytes, st>>>(m, T, E0, E1, Y, ctl);
+}
+
+template <bool CONTIG>
+void launch_p1_rp(const ModeDev& m, const double* T, const double* E0, const double* E1, const double* Y,
+                  const Ctl* ctl, int grid, cudaStream_t st) {
+  switch ((m.R + 7) / 8 * 8) {
+    case 8: launch_p1<8, CONTIG>(m, T, E0, E1, Y, ctl, grid, st); break;
+    case 16: launch_p1<16, CONTIG>(m, T, E0, E1, Y, ctl, grid, st); break;
+    case 24: launch_p1<24, CONTIG>(m, T, E0, E1, Y, ctl, grid, st); break;
+    case 32: launch_p1<32, CONTIG>(m, T, E0, E1, Y, ctl, grid, st); break;
+    case 40: launch_p1<40, CONTIG>(m, T, E0, E1, Y, ctl, grid, st); break;
+    case 48: launch_p1<48, CONTIG>(m, T, E0, E1, Y, ctl, grid, st); break;
+    case 56: launch_p1<56, CONTIG>(m, T, E0, E1, Y, ctl, grid, st); break;
+    default: launch_p1<64, CONTIG>(m, T, E0, E1, Y, ctl, grid, st); break;
+  }
+}
+
+inline int pass1_grid(const ModeDev& m, int sms) {
+  const int64_t ntiles =
+      m.inner == 1 ? (m.J + P1_MT - 1) / P1_MT : ((m.inner + P1_MT - 1) / P1_MT) * m.outer;
+  return (int)imin64(ntiles, sms);
 }
 
 inline void launch_contract_A_mma(const ModeDev& m, const double* T, const double* E0, const double* E1,
-                                  const double* Y, const Ctl* ctl, cudaStream_t st) {
-  switch ((m.R + 7) / 8 * 8) {
-    case 8: launch_p1<8>(m, T, E0, E1, Y, ctl, st); break;
-    case 16: launch_p1<16>(m, T, E0, E1, Y, ctl, st); break;
-    case 24: launch_p1<24>(m, T, E0, E1, Y, ctl, st); break;
-    case 32: launch_p1<32>(m, T, E0, E1, Y, ctl, st); break;
-    case 40: launch_p1<40>(m, T, E0, E1, Y, ctl, st); break;
-    case 48: launch_p1<48>(m, T, E0, E1, Y, ctl, st); break;
-    case 56: launch_p1<56>(m, T, E0, E1, Y, ctl, st); break;
-    default: launch_p1<64>(m, T, E0, E1, Y, ctl, st); break;
-  }
+                                  const double* Y, const Ctl* ctl, int sms, cudaStream_t st) {
+  const int grid = pass1_grid(m, sms);
+  if (m.inner == 1)
+    launch_p1_rp<true>(m, T, E0, E1, Y, ctl, grid, st);
+  else
+    launch_p1_rp<false>(m, T, E0, E1, Y, ctl, grid, st);
 }
 
 }  // namespace pasd

@@ -165,6 +165,51 @@ __device__ void cta_jacobi_eig(SmallWs& ws, int n) {
   __syncthreads();
 }
 
+// Warm start: load the previous rotation Pg (R x R, global column-major) into
+// ws.Q and replace S by Q^T S Q (uses ws.Z).  After cta_jacobi_eig, call
+// cta_warm_finish to turn the Jacobi rotation V into Q V.
+__device__ void cta_warm_start(SmallWs& ws, int R, const double* Pg) {
+  const int tid = threadIdx.x, nt = blockDim.x, ld = ws.ld;
+  for (int idx = tid; idx < R * R; idx += nt) ws.Q[(idx % R) * ld + idx / R] = Pg[idx];
+  __syncthreads();
+  for (int idx = tid; idx < R * R; idx += nt) {  // Z = S Q
+    const int r = idx / R, c = idx % R;
+    double a = 0.0;
+    for (int k = 0; k < R; ++k) a = fma(ws.S[r * ld + k], ws.Q[k * ld + c], a);
+    ws.Z[r * ld + c] = a;
+  }
+  __syncthreads();
+  for (int idx = tid; idx < R * R; idx += nt) {  // S = Q^T Z
+    const int r = idx / R, c = idx % R;
+    double a = 0.0;
+    for (int k = 0; k < R; ++k) a = fma(ws.Q[k * ld + r], ws.Z[k * ld + c], a);
+    ws.S[r * ld + c] = a;
+  }
+  __syncthreads();
+  for (int idx = tid; idx < R * R; idx += nt) {  // exact symmetry
+    const int r = idx / R, c = idx % R;
+    if (r < c) {
+      const double v = 0.5 * (ws.S[r * ld + c] + ws.S[c * ld + r]);
+      ws.S[r * ld + c] = v;
+      ws.S[c * ld + r] = v;
+    }
+  }
+  __syncthreads();
+}
+
+__device__ void cta_warm_finish(SmallWs& ws, int R) {  // V <- Q V
+  const int tid = threadIdx.x, nt = blockDim.x, ld = ws.ld;
+  for (int idx = tid; idx < R * R; idx += nt) {
+    const int r = idx / R, c = idx % R;
+    double a = 0.0;
+    for (int k = 0; k < R; ++k) a = fma(ws.Q[r * ld + k], ws.V[k * ld + c], a);
+    ws.Z[r * ld + c] = a;
+  }
+  __syncthreads();
+  for (int idx = tid; idx < R * R; idx += nt) ws.V[(idx / R) * ld + idx % R] = ws.Z[(idx / R) * ld + idx % R];
+  __syncthreads();
+}
+
 // out(R x R2, smem row-major ld) = X^T Y with X (I x R), Y (I x R2) global column-major.
 __device__ void cta_gram_tn(const double* X, const double* Y, int64_t I, int R, int R2, double* out, int ld,
                             double* stage /* 2 x 32 x ld */) {
@@ -220,7 +265,9 @@ __global__ void __launch_bounds__(kSmallThreads) k_svt(const ModePack* __restric
   // Gram_n (reduced over chunks by k_gram_reduce, and over ranks when sharded)
   for (int idx = tid; idx < R * R; idx += nt) ws.S[(idx / R) * ld + idx % R] = m.Gram[idx];
   __syncthreads();
+  cta_warm_start(ws, R, m.P);  // previous eigenvectors: Gram changes slowly between iterations
   cta_jacobi_eig(ws, R);
+  cta_warm_finish(ws, R);
   const double tau = __ddiv_rn(m.lambda, ctl->mu);  // lambda / mu (pasd.cpp:77)
   if (tid == 0) {
     int keep = 0;
@@ -297,7 +344,9 @@ __global__ void __launch_bounds__(kSmallThreads) k_polar(const ModePack* __restr
   }
   // 3. first Gram/Jacobi pass: C = W^T W = Q1 L Q1^T ; X2 = W Q1
   cta_gram_tn(X, X, I, R, R, ws.S, ld, ws.T64);
+  cta_warm_start(ws, R, m.Qp);  // previous right rotation
   cta_jacobi_eig(ws, R);
+  cta_warm_finish(ws, R);
   for (int idx = tid; idx < R * R; idx += nt) ws.Q[(idx / R) * ld + idx % R] = ws.V[(idx / R) * ld + idx % R];
   __syncthreads();
   cta_mul_nn(X, I, R, ws.Q, ld, R, X2);
@@ -416,10 +465,11 @@ __global__ void __launch_bounds__(kSmallThreads) k_polar(const ModePack* __restr
       break;
     }
   }
-  // 7. U = Ut Q^T
+  // 7. U = Ut Q^T ; keep Q as the next warm start
   for (int idx = tid; idx < R * R; idx += nt) {
     const int r = idx / R, s = idx % R;
     ws.S[r * ld + s] = ws.Q[s * ld + r];
+    m.Qp[r + R * s] = ws.Q[r * ld + s];
   }
   __syncthreads();
   cta_mul_nn(X, I, R, ws.S, ld, R, m.U);

@@ -33,6 +33,7 @@
 #include "pasd_small.cuh"
 #include "pasd_pass2.cuh"
 #include "pasd_pass1.cuh"
+#include "pasd_gram.cuh"
 
 using namespace pasd;
 
@@ -158,6 +159,7 @@ struct pasd_solver {
   double* d_resid_part = nullptr;
   int* d_bad_part = nullptr;
   int nblk_update = 0;
+  int sms = 148;
   size_t small_smem = 0;
   // fused order-3 pass 2 (pasd_pass2.cuh)
   bool fused = false;
@@ -225,7 +227,7 @@ void launch_iteration_marked(pasd_solver* s, cudaStream_t st, Mark&& mark) {
     ModeDev m = s->modes[n];
     if (s->sharded && n == N - 1) m.A = s->A3_partial;  // partial sum over this rank's slab
     mark(PASD_K_CONTRACT_A, true);
-    launch_contract_A_mma(m, s->T, s->E[0], s->E[1], s->Y[n], s->d_ctl, st);
+    launch_contract_A_mma(m, s->T, s->E[0], s->E[1], s->Y[n], s->d_ctl, s->sms, st);
     mark(PASD_K_CONTRACT_A, false);
     ++launches;
   }
@@ -236,7 +238,7 @@ void launch_iteration_marked(pasd_solver* s, cudaStream_t st, Mark&& mark) {
   for (int n = 0; n < N; ++n) {
     const ModeDev& m = s->modes[n];
     mark(PASD_K_GRAM, true);
-    k_gram<<<m.nkc_g, kThreads, 0, st>>>(m, s->d_ctl);
+    launch_gram_mma(m, s->d_ctl, st);
     const bool part = s->sharded && n < N - 1;  // Gram_1, Gram_2 are partial over the slab
     k_gram_reduce<<<8, 256, 0, st>>>(m, part ? s->gram_partial[n] : m.Gram, s->d_ctl);
     mark(PASD_K_GRAM, false);
@@ -359,8 +361,12 @@ __global__ void k_init_state(ModePack* mp, Ctl* ctl, double mu0, double rho, dou
       m.UM[idx] = 0.0;
     }
     for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < (int64_t)m.R * m.R;
-         idx += (int64_t)gridDim.x * blockDim.x)
+         idx += (int64_t)gridDim.x * blockDim.x) {
       m.M[idx] = 0.0;  // V = 0 (pasd.cpp:153) <=> M = 0
+      const double id = (idx % (m.R + 1) == 0) ? 1.0 : 0.0;
+      m.P[idx] = id;   // warm starts of the eigen-solvers
+      m.Qp[idx] = id;
+    }
     for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < m.Ifull * m.R;
          idx += (int64_t)gridDim.x * blockDim.x)
       m.Wt[idx] = 0.0;  // Wt = G V^T = 0 for V = 0: first Procrustes is degenerate
@@ -477,11 +483,12 @@ pasd_solver* create_solver(const pasd_options* o, const pasd_shard* shard) {
     m.nkc_w = (int)std::max<int64_t>(1, std::min<int64_t>(kchunks, std::max(1, 592 / m.nib_w)));
     m.Wpart = s->alloc<double>((size_t)m.nkc_w * IR);
     m.gpart = s->alloc<double>((size_t)m.nkc_w * m.nib_w);
-    m.nkc_g = (int)std::max<int64_t>(1, std::min<int64_t>((m.J + GR_KC - 1) / GR_KC, 296));
+    m.nkc_g = (int)std::max<int64_t>(1, std::min<int64_t>((m.J + GM_KC - 1) / GM_KC, 148));
     m.Gpart = s->alloc<double>((size_t)m.nkc_g * RR);
     m.Gram = s->alloc<double>(RR);
     m.sig = s->alloc<double>(m.R);
     m.P = s->alloc<double>(RR);
+    m.Qp = s->alloc<double>(RR);
     m.scratch = s->alloc<double>(3 * IRf);
     s->modes.push_back(m);
   }
@@ -518,6 +525,7 @@ pasd_solver* create_solver(const pasd_options* o, const pasd_shard* shard) {
   s->d_hist = s->alloc<double>(std::max(1, s->maxiter));
   int sms = 148;
   CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, s->device));
+  s->sms = sms;
   s->nblk_update = (int)std::max<int64_t>(1, std::min<int64_t>((S + kThreads - 1) / kThreads, (int64_t)sms * 8));
   s->d_resid_part = s->alloc<double>((size_t)s->nblk_update * PASD_MAX_ORDER);
   s->d_bad_part = s->alloc<int>(s->nblk_update);
@@ -1055,12 +1063,14 @@ void device_svt(const double* m_h, int64_t rows, int64_t cols, double tau, doubl
   m.M = t.alloc<double>(R * R);
   m.Gram = t.alloc<double>(R * R);
   m.P = t.alloc<double>(R * R);
+  m.Qp = t.alloc<double>(R * R);
   m.sig = t.alloc<double>(R);
   m.nkc_g = (int)std::max<int64_t>(1, std::min<int64_t>((m.J + GR_KC - 1) / GR_KC, 296));
   m.Gpart = t.alloc<double>((size_t)m.nkc_g * R * R);
   std::vector<double> eye(R * R, 0.0);
   for (int i = 0; i < R; ++i) eye[i + R * i] = 1.0;
   CK(cudaMemcpy(m.U, eye.data(), sizeof(double) * R * R, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(m.P, eye.data(), sizeof(double) * R * R, cudaMemcpyHostToDevice));
   CK(cudaMemcpy(m.A, m_h, sizeof(double) * rows * cols, cudaMemcpyHostToDevice));
   ModePack pack{};
   pack.order = 1;
@@ -1118,6 +1128,8 @@ void device_procrustes(const double* g_h, int64_t I, int64_t P, const double* v_
   std::vector<double> eye(R * R, 0.0);
   for (int i = 0; i < R; ++i) eye[i + R * i] = 1.0;
   CK(cudaMemcpy(m.M, eye.data(), sizeof(double) * R * R, cudaMemcpyHostToDevice));
+  m.Qp = t.alloc<double>(R * R);
+  CK(cudaMemcpy(m.Qp, eye.data(), sizeof(double) * R * R, cudaMemcpyHostToDevice));
   m.nib_w = (int)((I + CW_IT - 1) / CW_IT);
   m.nkc_w = (int)std::max<int64_t>(1, std::min<int64_t>((P + CW_KC - 1) / CW_KC, std::max(1, 592 / m.nib_w)));
   m.Wpart = t.alloc<double>((size_t)m.nkc_w * IR);
