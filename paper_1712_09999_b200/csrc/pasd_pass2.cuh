@@ -137,6 +137,7 @@ __device__ __forceinline__ int bidx(int l1, int l2, int l3) { return l1 + P2_B1 
 __device__ __forceinline__ int zx(int l1, int l2, int l3) { return l1 + 22 * l2 + 182 * l3; }
 __device__ __forceinline__ int g2x(int l1, int l2, int l3) { return l1 + 20 * l2 + 160 * l3; }
 __device__ __forceinline__ int g3x(int l1, int l2, int l3) { return l1 + 22 * l2 + 180 * l3; }
+__device__ __forceinline__ bool mt_dummy_guard(int w, int MT) { return (w & 3) < MT; }
 
 // Shared-memory footprint (bytes) of k_pass2_fused<RP>.
 template <int RP>
@@ -233,30 +234,46 @@ __global__ void __launch_bounds__(P2_THREADS, 1) k_pass2_fused(const Pass2Args a
     double w1acc[NT1][4];
 #pragma unroll
     for (int j = 0; j < NT1; ++j) w1acc[j][0] = w1acc[j][1] = w1acc[j][2] = w1acc[j][3] = 0.0;
-    double w3acc[4] = {0.0, 0.0, 0.0, 0.0};
+    double w3acc[4] = {0.0, 0.0, 0.0, 0.0};  // Wt_3^T m-tile (w & 3), K-half (w >> 2)
 
-    for (int64_t i2o = 0; i2o < I2; i2o += P2_B2) {
-      __syncthreads();  // previous step done with A1s/A3s/U2s/G2s/G3s
+    // per-step staging (issued one step ahead, overlapping the Wt_2 products)
+    auto stage_step = [&](int64_t i2o) {
       {  // A_1 (R1, I2, I3 layout): 4 threads per column (i2, i3)
         const int c = tid >> 2, l2 = c & 7, l3 = c >> 3, r0 = tid & 3;
         const int64_t i2 = i2o + l2, i3 = i3o + l3;
         const bool colok = i2 < I2 && i3 < I3;
         const double* src = m1.A + (colok ? (int64_t)R1 * (i2 + I2 * i3) : 0);
-        for (int r = r0; r < R1; r += 4) cp_async8(A1s + r * L::LD1 + c, colok ? src + r : m1.A, colok);
+        double* dst = A1s + c;
+#pragma unroll 4
+        for (int r = r0; r < R1; r += 4) cp_async8(dst + r * L::LD1, colok ? src + r : m1.A, colok);
       }
-      for (int l2 = 0; l2 < 8; ++l2) {  // A_3 (I1, I2, R3 layout)
-        const bool in2 = i2o + l2 < I2;
-        stage_rows16(A3s + 16 * l2, L::LD3, m3.A + i1o + I1 * (i2o + l2), S12, R3, in2 ? nv1 : 0, al1, m3.A);
+      {  // A_3 (I1, I2, R3 layout): rows (r, l2) of 16 consecutive i1
+        const int c = tid & 7;
+        const int v = nv1 - 2 * c, nbc = v >= 2 ? 16 : (v == 1 ? 8 : 0);
+        for (int row = tid >> 3; row < 8 * R3; row += P2_THREADS / 8) {
+          const int l2 = row & 7, r = row >> 3;
+          const int nb = (i2o + l2 < I2) ? nbc : 0;
+          double* dst = A3s + r * L::LD3 + 16 * l2 + 2 * c;
+          const double* src = m3.A + i1o + 2 * c + I1 * (i2o + l2) + S12 * (int64_t)r;
+          if (al1)
+            cp_async16(dst, nb ? src : m3.A, nb);
+          else {
+            cp_async8(dst, nb >= 8 ? src : m3.A, nb >= 8);
+            cp_async8(dst + 1, nb >= 16 ? src + 1 : m3.A, nb >= 16);
+          }
+        }
       }
       for (int idx = tid; idx < 8 * R2; idx += P2_THREADS) {
         const int l2 = idx & 7, r = idx >> 3;
         const bool v = i2o + l2 < I2;
         cp_async8(U2s + l2 * L::LDU + r, v ? m2.UM + m2.ioff + i2o + l2 + m2.Ifull * r : m2.UM, v);
       }
-      // this thread's 4 elements: (i1 = g, g+8) x (i2 = 2t, 2t+1) at i3 = w
-      double tv[4], yv[3][4];
-      bool inb[4];
-      int64_t off[4];
+    };
+    // this thread's 4 elements: (i1 = g, g+8) x (i2 = 2t, 2t+1) at i3 = w
+    double tv[4], yv[3][4];
+    bool inb[4];
+    int64_t off[4];
+    auto load_elems = [&](int64_t i2o) {
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         const int64_t i1 = i1o + g + 8 * (q >> 1), i2 = i2o + 2 * t + (q & 1), i3 = i3o + w;
@@ -266,26 +283,33 @@ __global__ void __launch_bounds__(P2_THREADS, 1) k_pass2_fused(const Pass2Args a
 #pragma unroll
         for (int n = 0; n < 3; ++n) yv[n][q] = inb[q] ? a.Y[n][off[q]] : 0.0;
       }
+    };
+    stage_step(0);
+    load_elems(0);
+
+    for (int64_t i2o = 0; i2o < I2; i2o += P2_B2) {
       cp_async_wait_all();
-      __syncthreads();
+      __syncthreads();  // step data staged; previous step's smem consumers done
       // ---- Z products (6 independent accumulator chains) ----
       double z1[4] = {0, 0, 0, 0}, z2[4] = {0, 0, 0, 0}, z3[4] = {0, 0, 0, 0};
-      double y1[4] = {0, 0, 0, 0}, y2[4] = {0, 0, 0, 0}, y3[4] = {0, 0, 0, 0};
+      {
+        double y1[4] = {0, 0, 0, 0}, y2[4] = {0, 0, 0, 0}, y3[4] = {0, 0, 0, 0};
 #pragma unroll
-      for (int ks = 0; ks < KS; ++ks) {
-        const int k = 4 * ks + t;
-        double(&c1)[4] = (ks & 1) ? y1 : z1;
-        double(&c2)[4] = (ks & 1) ? y2 : z2;
-        double(&c3)[4] = (ks & 1) ? y3 : z3;
-        dmma(c1, U1s[g * L::LDU + k], U1s[(g + 8) * L::LDU + k], A1s[k * L::LD1 + g + 8 * w]);
-        dmma(c2, A2s[k * L::LD2 + g + 16 * w], A2s[k * L::LD2 + g + 8 + 16 * w], U2s[g * L::LDU + k]);
-        dmma(c3, A3s[k * L::LD3 + g + 16 * w], A3s[k * L::LD3 + g + 8 + 16 * w], U3s[g * L::LDU + k]);
-      }
+        for (int ks = 0; ks < KS; ++ks) {
+          const int k = 4 * ks + t;
+          double(&c1)[4] = (ks & 1) ? y1 : z1;
+          double(&c2)[4] = (ks & 1) ? y2 : z2;
+          double(&c3)[4] = (ks & 1) ? y3 : z3;
+          dmma(c1, U1s[g * L::LDU + k], U1s[(g + 8) * L::LDU + k], A1s[k * L::LD1 + g + 8 * w]);
+          dmma(c2, A2s[k * L::LD2 + g + 16 * w], A2s[k * L::LD2 + g + 8 + 16 * w], U2s[g * L::LDU + k]);
+          dmma(c3, A3s[k * L::LD3 + g + 16 * w], A3s[k * L::LD3 + g + 8 + 16 * w], U3s[g * L::LDU + k]);
+        }
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        z1[q] += y1[q];
-        z2[q] += y2[q];
-        z3[q] += y3[q];
+        for (int q = 0; q < 4; ++q) {
+          z1[q] += y1[q];
+          z2[q] += y2[q];
+          z3[q] += y3[q];
+        }
       }
       Z3s[zx(g, w, 2 * t)] = z3[0];
       Z3s[zx(g, w, 2 * t + 1)] = z3[1];
@@ -294,6 +318,8 @@ __global__ void __launch_bounds__(P2_THREADS, 1) k_pass2_fused(const Pass2Args a
       __syncthreads();
       // ---- elementwise (reference op order, no FMA contraction) ----
       double g1v[4];
+      int64_t offc[4];
+      bool inc[4];
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         const int l1 = g + 8 * (q >> 1), l2 = 2 * t + (q & 1);
@@ -324,46 +350,86 @@ __global__ void __launch_bounds__(P2_THREADS, 1) k_pass2_fused(const Pass2Args a
         g1v[q] = gn[0];
         G2s[g2x(l1, l2, w)] = gn[1];
         G3s[g3x(l1, l2, w)] = gn[2];
+        offc[q] = off[q];
+        inc[q] = inb[q];
       }
-      __syncthreads();
-      // ---- Wt products ----
-      // Wt_1: A operand = this thread's own G_1 (K = columns at i3 = w, permuted).
+      (void)offc;
+      (void)inc;
+      const bool more = i2o + P2_B2 < I2;
+      if (more) load_elems(i2o + P2_B2);  // next step's T, Y in flight during the Wt products
+      __syncthreads();  // G2s / G3s complete
+      // ---- W-a: Wt_1 (own G_1 as A operand) and half of Wt_3 ----
 #pragma unroll
       for (int p = 0; p < 2; ++p) {
 #pragma unroll
         for (int j = 0; j < NT1; ++j) dmma(w1acc[j], g1v[p], g1v[2 + p], A1s[(8 * j + g) * L::LD1 + 8 * w + 2 * t + p]);
       }
-      if (w < 4) {
-        if (w < MT) {  // Wt_2^T m-tile w: rows r, cols i2, K = (i1, i3) = 128; flushed per step
-          double acc[4][4] = {};
-          const double* rowa = A2s + (16 * w + g) * L::LD2;
-          const double* rowb = rowa + 8 * L::LD2;
-#pragma unroll
-          for (int ks = 0; ks < 32; ++ks) {
-            const int k = 4 * ks + t;
-            dmma(acc[ks & 3], rowa[k], rowb[k], G2s[g2x(k & 15, g, k >> 4)]);
-          }
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            const double v = (acc[0][q] + acc[1][q]) + (acc[2][q] + acc[3][q]);
-            const int r = 16 * w + g + 8 * (q >> 1);
-            const int64_t i2 = i2o + 2 * t + (q & 1);
-            if (r < R2 && i2 < I2) W2c[i2 * R2 + r] += v;
-          }
-        }
-      } else if (w - 4 < MT) {  // Wt_3^T m-tile: rows r, cols i3, K = (i1, i2) = 128; kept per pencil
+      const int mt = w & 3, kh = w >> 2;  // m-tile and K-half of the Wt_2 / Wt_3 products
+      if (mt < MT) {
         double acc[3][4] = {};
-        const double* rowa = A3s + (16 * (w - 4) + g) * L::LD3;
+        const double* rowa = A3s + (16 * mt + g) * L::LD3 + 64 * kh;
         const double* rowb = rowa + 8 * L::LD3;
+        const double* gcol = G3s + 180 * g;
 #pragma unroll
-        for (int ks = 0; ks < 32; ++ks) {
-          const int k = 4 * ks + t;
+        for (int ks = 0; ks < 16; ++ks) {
+          const int k = 64 * kh + 4 * ks + t;
           double(&c)[4] = (ks & 3) == 0 ? w3acc : acc[(ks & 3) - 1];
-          dmma(c, rowa[k], rowb[k], G3s[g3x(k & 15, k >> 4, g)]);
+          dmma(c, rowa[4 * ks + t], rowb[4 * ks + t], gcol[(k & 15) + 22 * (k >> 4)]);
         }
 #pragma unroll
         for (int q = 0; q < 4; ++q) w3acc[q] += (acc[0][q] + acc[1][q]) + acc[2][q];
       }
+      // prefetch this step's Wt_2 partial rows (read-modify-write below)
+      double w2old[4] = {0, 0, 0, 0};
+      if (kh == 0 && mt < MT) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int r = 16 * mt + g + 8 * (q >> 1);
+          const int64_t i2 = i2o + 2 * t + (q & 1);
+          if (r < R2 && i2 < I2) w2old[q] = W2c[i2 * R2 + r];
+        }
+      }
+      __syncthreads();  // A1s / A3s no longer needed this step
+      if (more) stage_step(i2o + P2_B2);
+      // ---- W-b: Wt_2^T (m-tile mt, K-half kh), K = (i1, i3) ----
+      double acc2[4] = {0, 0, 0, 0};
+      if (mt < MT) {
+        double acc[3][4] = {};
+        const double* rowa = A2s + (16 * mt + g) * L::LD2 + 64 * kh;
+        const double* rowb = rowa + 8 * L::LD2;
+#pragma unroll
+        for (int ks = 0; ks < 16; ++ks) {
+          const int k = 64 * kh + 4 * ks + t;
+          double(&c)[4] = (ks & 3) == 0 ? acc2 : acc[(ks & 3) - 1];
+          dmma(c, rowa[4 * ks + t], rowb[4 * ks + t], G2s[g2x(k & 15, g, k >> 4)]);
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) acc2[q] += (acc[0][q] + acc[1][q]) + acc[2][q];
+        if (kh == 1) {
+#pragma unroll
+          for (int q = 0; q < 4; ++q) Z3s[(mt * 32 + lane) * 4 + q] = acc2[q];  // exchange (Z3s free now)
+        }
+      }
+      __syncthreads();
+      if (kh == 0 && mt < MT) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int r = 16 * mt + g + 8 * (q >> 1);
+          const int64_t i2 = i2o + 2 * t + (q & 1);
+          if (r < R2 && i2 < I2) W2c[i2 * R2 + r] = w2old[q] + (acc2[q] + Z3s[(mt * 32 + lane) * 4 + q]);
+        }
+      }
+    }
+    // combine the two K-halves of Wt_3 through shared memory
+    __syncthreads();
+    if (w >= 4 && mt_dummy_guard(w, MT)) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) Z3s[((w & 3) * 32 + lane) * 4 + q] = w3acc[q];
+    }
+    __syncthreads();
+    if (w < 4 && w < MT) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) w3acc[q] += Z3s[(w * 32 + lane) * 4 + q];
     }
     // ---- end of pencil: Wt_1 (sum over the 8 warps' column sets) and Wt_3 ----
     __syncthreads();
@@ -382,11 +448,11 @@ __global__ void __launch_bounds__(P2_THREADS, 1) k_pass2_fused(const Pass2Args a
       for (int ww = 0; ww < 8; ++ww) s += wred[(ww * 16 + l1) * RP + r];
       w1out[idx] = s;
     }
-    if (w >= 4 && w - 4 < MT) {
+    if (w < 4 && w < MT) {
       double* w3out = a.W3p + (int64_t)pen * 8 * R3;
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
-        const int r = 16 * (w - 4) + g + 8 * (q >> 1);
+        const int r = 16 * w + g + 8 * (q >> 1);
         if (r < R3) w3out[(2 * t + (q & 1)) * R3 + r] = w3acc[q];
       }
     }
