@@ -211,8 +211,19 @@ __global__ void __launch_bounds__(P2_THREADS, 1) k_pass2_fused(const Pass2Args a
   const int64_t S12 = I1 * I2;
   const bool al1 = (I1 % 2) == 0;  // 16-byte aligned rows of 16 consecutive i1
 
-  for (int pen = blockIdx.x; pen < a.npencils; pen += gridDim.x) {
-    const int ib1 = pen % a.n1b, ib3 = pen / a.n1b;
+  for (int lin = blockIdx.x; lin < a.npencils; lin += gridDim.x) {
+    // Banded pencil order: the ~gridDim pencils processed concurrently form a
+    // ~12 x 12 patch of (i1-block, i3-block), so the A_3 slices (shared along
+    // i3) and A_1 slices (shared along i1) they stage each step are L2 hits.
+    int ib1, ib3;
+    {
+      const int BW = 12;
+      const int band = lin / (BW * a.n3b), lin_in = lin - band * BW * a.n3b;
+      const int bw = min(BW, a.n1b - band * BW);
+      ib1 = band * BW + lin_in % bw;
+      ib3 = lin_in / bw;
+    }
+    const int pen = ib1 + a.n1b * ib3;  // canonical index of the Wt_1 / Wt_3 partials
     const int64_t i1o = (int64_t)ib1 * P2_B1, i3o = (int64_t)ib3 * P2_B3;
     const int nv1 = (int)imin64(16, I1 - i1o);
     __syncthreads();  // previous pencil fully done with shared memory
