@@ -17,9 +17,12 @@
 
 namespace pasd {
 
-constexpr int P1_MT = 128;     // kappa columns per tile
+// 64 columns x 16 i per chunk, double-buffered, two CTAs per SM: one CTA's
+// DMMAs overlap the other's loads (a single CTA serialised them: measured
+// 4.6 ms compute-only + 4.6 ms load-only -> 7.6 ms combined per C5 mode).
+constexpr int P1_MT = 64;      // kappa columns per tile
 constexpr int P1_KC = 16;      // i rows per chunk
-constexpr int P1_NST = 3;      // pipeline stages
+constexpr int P1_NST = 2;      // pipeline stages
 constexpr int P1_THREADS = 256;
 
 template <int RP, bool CONTIG>
@@ -34,17 +37,21 @@ struct P1Layout {
 };
 
 template <int RP, bool CONTIG>
-__global__ void __launch_bounds__(P1_THREADS, 1) k_pass1(ModeDev m, const double* __restrict__ T,
+__global__ void __launch_bounds__(P1_THREADS, 2) k_pass1(ModeDev m, const double* __restrict__ T,
                                                         const double* __restrict__ E0,
                                                         const double* __restrict__ E1,
                                                         const double* __restrict__ Y, const Ctl* ctl) {
   if (ctl->done) return;
   using L = P1Layout<RP, CONTIG>;
-  constexpr int NT = RP / 8;
+  constexpr int MTILES = P1_MT / 16;                 // m16 tiles of kappa rows (4)
+  constexpr int NSPLIT = (P1_THREADS / 32) / MTILES;  // warps sharing an m-tile (2): split the n-tiles
+  constexpr int NTALL = RP / 8;
+  constexpr int NT = (NTALL + NSPLIT - 1) / NSPLIT;  // n-tiles per warp
   extern __shared__ double p1sm[];
   const double* __restrict__ E = ctl->ecur ? E1 : E0;
   const double inv_mu = __ddiv_rn(1.0, ctl->mu);  // pasd.cpp:170
-  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5, g = lane >> 2, t = lane & 3;
+  const int tid = threadIdx.x, lane = tid & 31, g = lane >> 2, t = lane & 3;
+  const int w = (tid >> 5) % MTILES, jbase = ((tid >> 5) / MTILES) * NT;  // m-tile, first n-tile
   const int64_t I = m.I, inner = m.inner;
   const int R = m.R;
   // tiles: CONTIG -> 128 consecutive kappa; else (q, p-block of 128)
@@ -70,8 +77,8 @@ __global__ void __launch_bounds__(P1_THREADS, 1) k_pass1(ModeDev m, const double
         const int c = tid & 7;  // 16-byte chunk of the 16-double row
         const int v = ni - 2 * c, nbc = v >= 2 ? 16 : (v == 1 ? 8 : 0);
 #pragma unroll
-        for (int k = 0; k < P1_MT / 32; ++k) {
-          const int j = (tid >> 3) + 32 * k;
+        for (int k = 0; k < P1_MT / (P1_THREADS / 8); ++k) {
+          const int j = (tid >> 3) + (P1_THREADS / 8) * k;
           const int64_t kap = k0 + j;
           const int nb = kap < m.J ? nbc : 0;
           const int64_t off = kap * I + i0 + 2 * c;
@@ -98,12 +105,13 @@ __global__ void __launch_bounds__(P1_THREADS, 1) k_pass1(ModeDev m, const double
       const int ni = (int)imin64(P1_KC, I - i0);
       const int64_t off0 = p0 + inner * (i0 + I * q);
       if (al) {
-        // 64 16-byte chunks per 128-double row; thread -> (chunk c, rows rsub + 4k)
-        const int c = tid & 63, rsub = tid >> 6;
+        // P1_MT/2 16-byte chunks per row; thread -> (chunk c, rows rsub + RG k)
+        constexpr int CPR = P1_MT / 2, RG = P1_THREADS / CPR;
+        const int c = tid % CPR, rsub = tid / CPR;
         const int v = np - 2 * c, nbc = v >= 2 ? 16 : (v == 1 ? 8 : 0);
 #pragma unroll
-        for (int k = 0; k < P1_KC / 4; ++k) {
-          const int ii = rsub + 4 * k;
+        for (int k = 0; k < P1_KC / RG; ++k) {
+          const int ii = rsub + RG * k;
           const int nb = ii < ni ? nbc : 0;
           const int64_t off = off0 + inner * ii + 2 * c;
           const int d = ii * L::LDR + 2 * c;
@@ -165,7 +173,8 @@ __global__ void __launch_bounds__(P1_THREADS, 1) k_pass1(ModeDev m, const double
       const double a0 = g_elem(Ts[o0], Es[o0], Ys[o0], inv_mu);
       const double a1 = g_elem(Ts[o1], Es[o1], Ys[o1], inv_mu);
 #pragma unroll
-      for (int j = 0; j < NT; ++j) dmma((ks & 1) ? acb[j] : acc[j], a0, a1, Us[k * L::LDU + 8 * j + g]);
+      for (int j = 0; j < NT; ++j)
+        if (jbase + j < NTALL) dmma((ks & 1) ? acb[j] : acc[j], a0, a1, Us[k * L::LDU + 8 * (jbase + j) + g]);
     }
     if (ci == nchunk - 1) {  // tile done: write A
       const int64_t tile = blockIdx.x + (it / nchunk) * gridDim.x;
@@ -178,7 +187,7 @@ __global__ void __launch_bounds__(P1_THREADS, 1) k_pass1(ModeDev m, const double
 #pragma unroll
         for (int q4 = 0; q4 < 4; ++q4) {
           const int row = 16 * w + g + 8 * (q4 >> 1);
-          const int r = 8 * j + 2 * t + (q4 & 1);
+          const int r = 8 * (jbase + j) + 2 * t + (q4 & 1);
           if (r >= R) continue;
           if (CONTIG) {
             const int64_t kap = tile * P1_MT + row;
@@ -224,7 +233,7 @@ void launch_p1_rp(const ModeDev& m, const double* T, const double* E0, const dou
 inline int pass1_grid(const ModeDev& m, int sms) {
   const int64_t ntiles =
       m.inner == 1 ? (m.J + P1_MT - 1) / P1_MT : ((m.inner + P1_MT - 1) / P1_MT) * m.outer;
-  return (int)imin64(ntiles, sms);
+  return (int)imin64(ntiles, 2 * sms);
 }
 
 inline void launch_contract_A_mma(const ModeDev& m, const double* T, const double* E0, const double* E1,
