@@ -44,6 +44,7 @@ struct Pass2Args {
   double* resid_part;  // [grid][PASD_MAX_ORDER]
   int* bad_part;       // [grid]
   int n1b, n3b, npencils;
+  int b1;  // i1 extent of a pencil (16 for k_pass2_fused, 8 for k_pass2_m8)
 };
 
 __host__ __device__ inline int round_up(int x, int m) { return (x + m - 1) / m * m; }
@@ -553,8 +554,8 @@ __global__ void k_pass2_reduce(const Pass2Args a, int nblk, Ctl* ctl, double* g2
     double s = 0.0;
     if (i >= 0 && i < m.I) {
       if (n == 0) {
-        const int ib = (int)(i / P2_B1), l = (int)(i % P2_B1);
-        for (int b3 = 0; b3 < a.n3b; ++b3) s += a.W1p[((int64_t)(ib + a.n1b * b3) * 16 + l) * R + r];
+        const int ib = (int)(i / a.b1), l = (int)(i % a.b1);
+        for (int b3 = 0; b3 < a.n3b; ++b3) s += a.W1p[((int64_t)(ib + a.n1b * b3) * a.b1 + l) * R + r];
       } else if (n == 1) {
         for (int c = 0; c < nblk; ++c) s += a.W2part[((int64_t)c * m.I + i) * R + r];
       } else {

@@ -19,6 +19,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <functional>
 #include <limits>
@@ -34,6 +35,7 @@
 #include "pasd_pass2.cuh"
 #include "pasd_pass1.cuh"
 #include "pasd_gram.cuh"
+#include "pasd_pass2m8.cuh"
 
 using namespace pasd;
 
@@ -163,6 +165,7 @@ struct pasd_solver {
   size_t small_smem = 0;
   // fused order-3 pass 2 (pasd_pass2.cuh)
   bool fused = false;
+  bool use_m8 = false;
   int p2_rp = 0;
   Pass2Args p2{};
   int p2_grid = 0;
@@ -258,7 +261,10 @@ void launch_iteration_marked(pasd_solver* s, cudaStream_t st, Mark&& mark) {
   ++launches;
   if (s->fused) {
     mark(PASD_K_UPDATE, true);
-    pass2_launch(s->p2_rp, s->p2, s->d_ctl, s->p2_grid, st);
+    if (s->use_m8)
+      m8_launch(s->p2_rp, s->p2, s->d_ctl, s->p2_grid, st);
+    else
+      pass2_launch(s->p2_rp, s->p2, s->d_ctl, s->p2_grid, st);
     mark(PASD_K_UPDATE, false);
     ++launches;
     int64_t maxir = 1;
@@ -543,13 +549,15 @@ pasd_solver* create_solver(const pasd_options* o, const pasd_shard* shard) {
     a.T = s->T;
     a.E0 = s->E[0];
     a.E1 = s->E[1];
-    a.n1b = (int)((s->dims[0] + P2_B1 - 1) / P2_B1);
+    s->p2_rp = pass2_rp(s->modes[0].R, s->modes[1].R, s->modes[2].R);
+    s->use_m8 = m8_supported(s->p2_rp) && std::getenv("PASD_PASS2_M16") == nullptr;
+    a.b1 = s->use_m8 ? M8_B : P2_B1;
+    a.n1b = (int)((s->dims[0] + a.b1 - 1) / a.b1);
     a.n3b = (int)((s->dims[2] + P2_B3 - 1) / P2_B3);
     a.npencils = a.n1b * a.n3b;
-    s->p2_grid = std::max(1, std::min(a.npencils, sms));
-    s->p2_rp = pass2_rp(s->modes[0].R, s->modes[1].R, s->modes[2].R);
-    s->p2_smem = pass2_smem(s->p2_rp);
-    a.W1p = s->alloc<double>((size_t)a.npencils * 16 * s->modes[0].R);
+    s->p2_grid = std::max(1, std::min(a.npencils, (s->use_m8 ? 2 : 1) * sms));
+    s->p2_smem = s->use_m8 ? 0 : pass2_smem(s->p2_rp);
+    a.W1p = s->alloc<double>((size_t)a.npencils * a.b1 * s->modes[0].R);
     a.W3p = s->alloc<double>((size_t)a.npencils * 8 * s->modes[2].R);
     a.W2part = s->alloc<double>((size_t)s->p2_grid * s->dims[1] * s->modes[1].R);
     a.gpart = s->alloc<double>((size_t)s->p2_grid * 3);
@@ -557,7 +565,10 @@ pasd_solver* create_solver(const pasd_options* o, const pasd_shard* shard) {
     s->p2_bad = s->alloc<int>(s->p2_grid);
     a.resid_part = s->p2_resid;
     a.bad_part = s->p2_bad;
-    pass2_setup(s->p2_rp);
+    if (s->use_m8)
+      m8_setup(s->p2_rp);
+    else
+      pass2_setup(s->p2_rp);
     CK(cudaGetLastError());
   }
   s->d_stats = s->alloc<double>(2 * 2048);
