@@ -1,5 +1,6 @@
 // pasd_pass1.cuh — pass 1 of a PASD iteration on the FP64 tensor cores:
 //   A_n = U_n^T G_(n),  G_n = (T - E) + Y_n / mu          (proj/src/pasd.cpp:77,178-186)
+// reading D = T - E (kept resident by the update pass, same rounded value) and Y_n.
 // for one mode n, directly on the strided tensor (no unfolding copy,
 // tensor.cpp:98-113).  As a GEMM: A (J x R) = G (J x I) * U (I x R), with
 // kappa = unfolding column, K = I_n, N = R_n <= 64.
@@ -20,9 +21,18 @@ namespace pasd {
 // 64 columns x 16 i per chunk, double-buffered, two CTAs per SM: one CTA's
 // DMMAs overlap the other's loads (a single CTA serialised them: measured
 // 4.6 ms compute-only + 4.6 ms load-only -> 7.6 ms combined per C5 mode).
-constexpr int P1_MT = 64;      // kappa columns per tile
-constexpr int P1_KC = 16;      // i rows per chunk
-constexpr int P1_NST = 2;      // pipeline stages
+#ifndef PASD_P1_MT
+#define PASD_P1_MT 128
+#endif
+constexpr int P1_MT = PASD_P1_MT;  // kappa columns per tile
+#ifndef PASD_P1_KC
+#define PASD_P1_KC 16
+#endif
+constexpr int P1_KC = PASD_P1_KC;  // i rows per chunk
+#ifndef PASD_P1_NST
+#define PASD_P1_NST 2
+#endif
+constexpr int P1_NST = PASD_P1_NST;  // pipeline stages
 constexpr int P1_THREADS = 256;
 
 template <int RP, bool CONTIG>
@@ -32,14 +42,12 @@ struct P1Layout {
   static constexpr int RAW = CONTIG ? P1_MT * LDR : P1_KC * LDR;  // doubles per tensor per stage
   static constexpr int LDU = RP + 4;
   static constexpr int USZ = P1_KC * LDU;
-  static constexpr int STAGE = 3 * RAW + USZ;
+  static constexpr int STAGE = 2 * RAW + USZ;  // D, Y_n, U chunk
   static constexpr size_t bytes = sizeof(double) * (size_t)P1_NST * STAGE;
 };
 
 template <int RP, bool CONTIG>
-__global__ void __launch_bounds__(P1_THREADS, 2) k_pass1(ModeDev m, const double* __restrict__ T,
-                                                        const double* __restrict__ E0,
-                                                        const double* __restrict__ E1,
+__global__ void __launch_bounds__(P1_THREADS, 2) k_pass1(ModeDev m, const double* __restrict__ D,
                                                         const double* __restrict__ Y, const Ctl* ctl) {
   if (ctl->done) return;
   using L = P1Layout<RP, CONTIG>;
@@ -48,7 +56,6 @@ __global__ void __launch_bounds__(P1_THREADS, 2) k_pass1(ModeDev m, const double
   constexpr int NTALL = RP / 8;
   constexpr int NT = (NTALL + NSPLIT - 1) / NSPLIT;  // n-tiles per warp
   extern __shared__ double p1sm[];
-  const double* __restrict__ E = ctl->ecur ? E1 : E0;
   const double inv_mu = __ddiv_rn(1.0, ctl->mu);  // pasd.cpp:170
   const int tid = threadIdx.x, lane = tid & 31, g = lane >> 2, t = lane & 3;
   const int w = (tid >> 5) % MTILES, jbase = ((tid >> 5) / MTILES) * NT;  // m-tile, first n-tile
@@ -83,9 +90,8 @@ __global__ void __launch_bounds__(P1_THREADS, 2) k_pass1(ModeDev m, const double
           const int nb = kap < m.J ? nbc : 0;
           const int64_t off = kap * I + i0 + 2 * c;
           const int d = j * L::LDR + 2 * c;
-          cp_async16(st + d, nb ? T + off : T, nb);
-          cp_async16(st + L::RAW + d, nb ? E + off : T, nb);
-          cp_async16(st + 2 * L::RAW + d, nb ? Y + off : T, nb);
+          cp_async16(st + d, nb ? D + off : D, nb);
+          cp_async16(st + L::RAW + d, nb ? Y + off : D, nb);
         }
       } else {
         for (int idx = tid; idx < P1_MT * P1_KC; idx += P1_THREADS) {
@@ -94,9 +100,8 @@ __global__ void __launch_bounds__(P1_THREADS, 2) k_pass1(ModeDev m, const double
           const bool ok = kap < m.J && c < ni;
           const int64_t off = kap * I + i0 + c;
           const int d = j * L::LDR + c;
-          cp_async8(st + d, ok ? T + off : T, ok);
-          cp_async8(st + L::RAW + d, ok ? E + off : T, ok);
-          cp_async8(st + 2 * L::RAW + d, ok ? Y + off : T, ok);
+          cp_async8(st + d, ok ? D + off : D, ok);
+          cp_async8(st + L::RAW + d, ok ? Y + off : D, ok);
         }
       }
     } else {
@@ -115,9 +120,8 @@ __global__ void __launch_bounds__(P1_THREADS, 2) k_pass1(ModeDev m, const double
           const int nb = ii < ni ? nbc : 0;
           const int64_t off = off0 + inner * ii + 2 * c;
           const int d = ii * L::LDR + 2 * c;
-          cp_async16(st + d, nb ? T + off : T, nb);
-          cp_async16(st + L::RAW + d, nb ? E + off : T, nb);
-          cp_async16(st + 2 * L::RAW + d, nb ? Y + off : T, nb);
+          cp_async16(st + d, nb ? D + off : D, nb);
+          cp_async16(st + L::RAW + d, nb ? Y + off : D, nb);
         }
       } else {
         for (int idx = tid; idx < P1_KC * P1_MT; idx += P1_THREADS) {
@@ -125,13 +129,12 @@ __global__ void __launch_bounds__(P1_THREADS, 2) k_pass1(ModeDev m, const double
           const bool ok = ii < ni && c < np;
           const int64_t off = off0 + inner * ii + c;
           const int d = ii * L::LDR + c;
-          cp_async8(st + d, ok ? T + off : T, ok);
-          cp_async8(st + L::RAW + d, ok ? E + off : T, ok);
-          cp_async8(st + 2 * L::RAW + d, ok ? Y + off : T, ok);
+          cp_async8(st + d, ok ? D + off : D, ok);
+          cp_async8(st + L::RAW + d, ok ? Y + off : D, ok);
         }
       }
     }
-    double* us = st + 3 * L::RAW;
+    double* us = st + 2 * L::RAW;
     for (int idx = tid; idx < P1_KC * RP; idx += P1_THREADS) {
       const int i = idx % P1_KC, r = idx / P1_KC;
       const bool ok = r < R && i0 + i < I;
@@ -139,7 +142,11 @@ __global__ void __launch_bounds__(P1_THREADS, 2) k_pass1(ModeDev m, const double
     }
   };
 
-  double acc[NT][4], acb[NT][4];  // even / odd k-steps (two independent DMMA chains per n-tile)
+  // even / odd k-steps in separate accumulators (two independent DMMA chains
+  // per n-tile) only when a warp has few n-tiles; NT >= 4 chains already keep
+  // the tensor pipe busy and the registers are needed by the staging.
+  constexpr bool TWO = NT < 4;
+  double acc[NT][4], acb[TWO ? NT : 1][4];
   int64_t it = 0;
   for (int s = 0; s < P1_NST - 1; ++s) {
     issue(s, s);
@@ -152,7 +159,7 @@ __global__ void __launch_bounds__(P1_THREADS, 2) k_pass1(ModeDev m, const double
 #pragma unroll
       for (int j = 0; j < NT; ++j) {
         acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.0;
-        acb[j][0] = acb[j][1] = acb[j][2] = acb[j][3] = 0.0;
+        if (TWO) acb[TWO ? j : 0][0] = acb[TWO ? j : 0][1] = acb[TWO ? j : 0][2] = acb[TWO ? j : 0][3] = 0.0;
       }
     }
     asm volatile("cp.async.wait_group %0;" ::"n"(P1_NST - 2) : "memory");
@@ -160,28 +167,28 @@ __global__ void __launch_bounds__(P1_THREADS, 2) k_pass1(ModeDev m, const double
     issue(it + P1_NST - 1, (int)((it + P1_NST - 1) % P1_NST));
     asm volatile("cp.async.commit_group;" ::: "memory");
     const double* st = stage_ptr(s);
-    const double* Ts = st;
-    const double* Es = st + L::RAW;
-    const double* Ys = st + 2 * L::RAW;
-    const double* Us = st + 3 * L::RAW;
+    const double* Ds = st;
+    const double* Ys = st + L::RAW;
+    const double* Us = st + 2 * L::RAW;
 #pragma unroll
     for (int ks = 0; ks < P1_KC / 4; ++ks) {
       const int k = 4 * ks + t;
       const int r0 = 16 * w + g, r1 = r0 + 8;
       const int o0 = CONTIG ? r0 * L::LDR + k : k * L::LDR + r0;
       const int o1 = CONTIG ? r1 * L::LDR + k : k * L::LDR + r1;
-      const double a0 = g_elem(Ts[o0], Es[o0], Ys[o0], inv_mu);
-      const double a1 = g_elem(Ts[o1], Es[o1], Ys[o1], inv_mu);
+      const double a0 = __dadd_rn(Ds[o0], __dmul_rn(Ys[o0], inv_mu));  // g_elem on D
+      const double a1 = __dadd_rn(Ds[o1], __dmul_rn(Ys[o1], inv_mu));
 #pragma unroll
       for (int j = 0; j < NT; ++j)
-        if (jbase + j < NTALL) dmma((ks & 1) ? acb[j] : acc[j], a0, a1, Us[k * L::LDU + 8 * (jbase + j) + g]);
+        if (jbase + j < NTALL) dmma((TWO && (ks & 1)) ? acb[TWO ? j : 0] : acc[j], a0, a1, Us[k * L::LDU + 8 * (jbase + j) + g]);
     }
     if (ci == nchunk - 1) {  // tile done: write A
       const int64_t tile = blockIdx.x + (it / nchunk) * gridDim.x;
 #pragma unroll
       for (int j = 0; j < NT; ++j)
 #pragma unroll
-        for (int q4 = 0; q4 < 4; ++q4) acc[j][q4] += acb[j][q4];
+        for (int q4 = 0; q4 < 4; ++q4)
+          if (TWO) acc[j][q4] += acb[TWO ? j : 0][q4];
 #pragma unroll
       for (int j = 0; j < NT; ++j) {
 #pragma unroll
@@ -204,7 +211,7 @@ __global__ void __launch_bounds__(P1_THREADS, 2) k_pass1(ModeDev m, const double
 }
 
 template <int RP, bool CONTIG>
-void launch_p1(const ModeDev& m, const double* T, const double* E0, const double* E1, const double* Y, const Ctl* ctl,
+void launch_p1(const ModeDev& m, const double* D, const double* Y, const Ctl* ctl,
                int grid, cudaStream_t st) {
   using L = P1Layout<RP, CONTIG>;
   static bool attr = false;  // idempotent attribute set
@@ -212,21 +219,21 @@ void launch_p1(const ModeDev& m, const double* T, const double* E0, const double
     cudaFuncSetAttribute(k_pass1<RP, CONTIG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::bytes);
     attr = true;
   }
-  k_pass1<RP, CONTIG><<<grid, P1_THREADS, L::bytes, st>>>(m, T, E0, E1, Y, ctl);
+  k_pass1<RP, CONTIG><<<grid, P1_THREADS, L::bytes, st>>>(m, D, Y, ctl);
 }
 
 template <bool CONTIG>
-void launch_p1_rp(const ModeDev& m, const double* T, const double* E0, const double* E1, const double* Y,
+void launch_p1_rp(const ModeDev& m, const double* D, const double* Y,
                   const Ctl* ctl, int grid, cudaStream_t st) {
   switch ((m.R + 7) / 8 * 8) {
-    case 8: launch_p1<8, CONTIG>(m, T, E0, E1, Y, ctl, grid, st); break;
-    case 16: launch_p1<16, CONTIG>(m, T, E0, E1, Y, ctl, grid, st); break;
-    case 24: launch_p1<24, CONTIG>(m, T, E0, E1, Y, ctl, grid, st); break;
-    case 32: launch_p1<32, CONTIG>(m, T, E0, E1, Y, ctl, grid, st); break;
-    case 40: launch_p1<40, CONTIG>(m, T, E0, E1, Y, ctl, grid, st); break;
-    case 48: launch_p1<48, CONTIG>(m, T, E0, E1, Y, ctl, grid, st); break;
-    case 56: launch_p1<56, CONTIG>(m, T, E0, E1, Y, ctl, grid, st); break;
-    default: launch_p1<64, CONTIG>(m, T, E0, E1, Y, ctl, grid, st); break;
+    case 8: launch_p1<8, CONTIG>(m, D, Y, ctl, grid, st); break;
+    case 16: launch_p1<16, CONTIG>(m, D, Y, ctl, grid, st); break;
+    case 24: launch_p1<24, CONTIG>(m, D, Y, ctl, grid, st); break;
+    case 32: launch_p1<32, CONTIG>(m, D, Y, ctl, grid, st); break;
+    case 40: launch_p1<40, CONTIG>(m, D, Y, ctl, grid, st); break;
+    case 48: launch_p1<48, CONTIG>(m, D, Y, ctl, grid, st); break;
+    case 56: launch_p1<56, CONTIG>(m, D, Y, ctl, grid, st); break;
+    default: launch_p1<64, CONTIG>(m, D, Y, ctl, grid, st); break;
   }
 }
 
@@ -236,13 +243,12 @@ inline int pass1_grid(const ModeDev& m, int sms) {
   return (int)imin64(ntiles, 2 * sms);
 }
 
-inline void launch_contract_A_mma(const ModeDev& m, const double* T, const double* E0, const double* E1,
-                                  const double* Y, const Ctl* ctl, int sms, cudaStream_t st) {
+inline void launch_contract_A_mma(const ModeDev& m, const double* D, const double* Y, const Ctl* ctl, int sms, cudaStream_t st) {
   const int grid = pass1_grid(m, sms);
   if (m.inner == 1)
-    launch_p1_rp<true>(m, T, E0, E1, Y, ctl, grid, st);
+    launch_p1_rp<true>(m, D, Y, ctl, grid, st);
   else
-    launch_p1_rp<false>(m, T, E0, E1, Y, ctl, grid, st);
+    launch_p1_rp<false>(m, D, Y, ctl, grid, st);
 }
 
 }  // namespace pasd

@@ -36,6 +36,7 @@ struct Pass2Args {
   const double* T;
   double* E0;
   double* E1;
+  double* D;   // T - E_new (pass 1's tensor operand)
   double* Y[3];
   double* W1p;     // [npencils][16][R1]
   double* W3p;     // [npencils][8][R3]
@@ -88,6 +89,9 @@ __host__ __device__ inline P2Smem p2_plan(int R1, int R2, int R3) {
 }
 
 __device__ __forceinline__ void dmma(double (&c)[4], double a0, double a1, double b0) {
+#if PASD_P2_EXP == 2
+  c[0] += a0 * b0; return;
+#endif
   asm volatile(
       "mma.sync.aligned.m16n8k4.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5}, {%6}, {%0,%1,%2,%3};"
       : "+d"(c[0]), "+d"(c[1]), "+d"(c[2]), "+d"(c[3])
@@ -126,6 +130,18 @@ __device__ __forceinline__ void stage_rows16(double* dst, int ld, const double* 
   }
 }
 
+// Same copies addressed by a 32-bit shared-window address (no per-copy
+// generic->shared conversion in the unrolled staging loops).
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void cp16s(unsigned s, const void* gmem, int nbytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(s), "l"(gmem), "r"(nbytes) : "memory");
+}
+__device__ __forceinline__ void cp8s(unsigned s, const void* gmem, int nbytes) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(s), "l"(gmem), "r"(nbytes) : "memory");
+}
+
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
 // Brick element index e = i1 + 16 * (i2 + 8 * i3) (local coordinates).
@@ -146,9 +162,13 @@ struct P2Layout {
   static constexpr int RM = (RP + 15) / 16 * 16;  // rows of the M tiles (Wt products)
   // leading dims chosen so the DMMA fragment reads (rows t x cols g, rows g x
   // cols t) and the staging writes hit distinct banks per half-warp
-  static constexpr int LD1 = 64 + 4, LD2 = 128 + 4, LD3 = 128 + 4, LDU = RP + 4;
+  // A1s is column-major: [column c = l2 + 8 l3][r], pitch LD1 = RP + 4 (4 or 12
+  // mod 16: the Z_1 reads (c = g, r = t) are conflict-free, the Wt_1 reads
+  // (c = 2t, r = g) 2-way), so each column's R1 contiguous values of A_1
+  // stage as 16-byte copies.
+  static constexpr int LD1 = RP + 4, LD2 = 128 + 4, LD3 = 128 + 4, LDU = RP + 4;
   static constexpr int oA1 = 0;
-  static constexpr int oA2 = oA1 + RP * LD1;
+  static constexpr int oA2 = oA1 + 64 * LD1;
   static constexpr int oA3 = oA2 + RM * LD2;
   static constexpr int oU1 = oA3 + RM * LD3;
   static constexpr int oU2 = oU1 + 16 * LDU;
@@ -203,7 +223,6 @@ __global__ void __launch_bounds__(P2_THREADS, 1) k_pass2_fused(const Pass2Args a
   // zero padding rows once (never overwritten by the staging copies)
   for (int idx = tid; idx < (L::RM - R2) * 128; idx += P2_THREADS) A2s[(R2 + idx / 128) * L::LD2 + (idx & 127)] = 0.0;
   for (int idx = tid; idx < (L::RM - R3) * 128; idx += P2_THREADS) A3s[(R3 + idx / 128) * L::LD3 + (idx & 127)] = 0.0;
-  for (int idx = tid; idx < (RP - R1) * 64; idx += P2_THREADS) A1s[(R1 + idx / 64) * L::LD1 + (idx & 63)] = 0.0;
   for (int idx = tid; idx < 32 * (RP + 4); idx += P2_THREADS) U1s[idx] = 0.0;  // U1s, U2s, U3s padding
 
   double worst[3] = {0.0, 0.0, 0.0};
@@ -227,6 +246,7 @@ __global__ void __launch_bounds__(P2_THREADS, 1) k_pass2_fused(const Pass2Args a
     const int pen = ib1 + a.n1b * ib3;  // canonical index of the Wt_1 / Wt_3 partials
     const int64_t i1o = (int64_t)ib1 * P2_B1, i3o = (int64_t)ib3 * P2_B3;
     const int nv1 = (int)imin64(16, I1 - i1o);
+    const int nbc1 = (nv1 - 2 * (tid & 7)) >= 2 ? 16 : ((nv1 - 2 * (tid & 7)) == 1 ? 8 : 0);  // A_3 chunk bytes
     __syncthreads();  // previous pencil fully done with shared memory
     // ---- pencil-resident: A_2 slice (I1, R2, I3 layout), UM_1 rows, UM_3 rows ----
     for (int l3 = 0; l3 < 8; ++l3) {
@@ -248,37 +268,80 @@ __global__ void __launch_bounds__(P2_THREADS, 1) k_pass2_fused(const Pass2Args a
     for (int j = 0; j < NT1; ++j) w1acc[j][0] = w1acc[j][1] = w1acc[j][2] = w1acc[j][3] = 0.0;
     double w3acc[4] = {0.0, 0.0, 0.0, 0.0};  // Wt_3^T m-tile (w & 3), K-half (w >> 2)
 
-    // per-step staging (issued one step ahead, overlapping the Wt_2 products)
+    // per-step staging (issued one step ahead, overlapping the Wt_2 products).
+    // Per-thread source/destination bases are fixed along the pencil; a step
+    // only advances them by 8 i2.
+    const int n3v = (int)imin64(8, I3 - i3o);  // valid i3 of the pencil
     auto stage_step = [&](int64_t i2o) {
-      {  // A_1 (R1, I2, I3 layout): 4 threads per column (i2, i3)
-        const int c = tid >> 2, l2 = c & 7, l3 = c >> 3, r0 = tid & 3;
-        const int64_t i2 = i2o + l2, i3 = i3o + l3;
-        const bool colok = i2 < I2 && i3 < I3;
-        const double* src = m1.A + (colok ? (int64_t)R1 * (i2 + I2 * i3) : 0);
-        double* dst = A1s + c;
-#pragma unroll 4
-        for (int r = r0; r < R1; r += 4) cp_async8(dst + r * L::LD1, colok ? src + r : m1.A, colok);
-      }
-      {  // A_3 (I1, I2, R3 layout): rows (r, l2) of 16 consecutive i1
-        const int c = tid & 7;
-        const int v = nv1 - 2 * c, nbc = v >= 2 ? 16 : (v == 1 ? 8 : 0);
-        for (int row = tid >> 3; row < 8 * R3; row += P2_THREADS / 8) {
-          const int l2 = row & 7, r = row >> 3;
-          const int nb = (i2o + l2 < I2) ? nbc : 0;
-          double* dst = A3s + r * L::LD3 + 16 * l2 + 2 * c;
-          const double* src = m3.A + i1o + 2 * c + I1 * (i2o + l2) + S12 * (int64_t)r;
-          if (al1)
-            cp_async16(dst, nb ? src : m3.A, nb);
-          else {
-            cp_async8(dst, nb >= 8 ? src : m3.A, nb >= 8);
-            cp_async8(dst + 1, nb >= 16 ? src + 1 : m3.A, nb >= 16);
+      {  // A_1 (R1, I2, I3 layout): warp w -> columns (l2 = w, l3 = k); lane -> r pair
+        const bool c2ok = i2o + w < I2;
+        const char* gp = reinterpret_cast<const char*>(m1.A + (int64_t)R1 * ((i2o + w) + I2 * i3o));
+        const int64_t kst = 8 * (int64_t)R1 * I2;  // bytes to the next l3
+        const unsigned sp = smem_u32(A1s + w * L::LD1);
+        if ((R1 & 1) == 0) {
+          if (lane < RP / 2) {
+            const int r = 2 * lane;
+            const bool rok = c2ok && r < R1;
+            gp += 16 * lane;
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+              const bool ok = rok && k < n3v;
+              cp16s(sp + 8 * (k * 8 * L::LD1 + r), ok ? (const void*)gp : (const void*)m1.A, ok ? 16 : 0);
+              gp += kst;
+            }
+          }
+        } else {
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int r = lane + 32 * h;
+            if (r < RP) {
+              const bool rok = c2ok && r < R1;
+              const char* gq = gp + 8 * r;
+#pragma unroll
+              for (int k = 0; k < 8; ++k) {
+                const bool ok = rok && k < n3v;
+                cp8s(sp + 8 * (k * 8 * L::LD1 + r), ok ? (const void*)gq : (const void*)m1.A, ok ? 8 : 0);
+                gq += kst;
+              }
+            }
           }
         }
       }
-      for (int idx = tid; idx < 8 * R2; idx += P2_THREADS) {
-        const int l2 = idx & 7, r = idx >> 3;
+      {  // A_3 (I1, I2, R3 layout): rows (r, l2) of 16 consecutive i1; thread ->
+         // 16-byte chunk c, l2, rows r = r0 + 4k (padding rows stay zero)
+        const int c = tid & 7, l2 = (tid >> 3) & 7, r0 = tid >> 6;
+        const bool ok2 = i2o + l2 < I2;
+        const int nb = ok2 ? nbc1 : 0;
+        const char* gp = reinterpret_cast<const char*>(nb ? m3.A + i1o + 2 * c + I1 * (i2o + l2) + S12 * (int64_t)r0 : m3.A);
+        const int64_t gst = nb ? 32 * S12 : 0;  // 4 rows r
+        const unsigned sp = smem_u32(A3s + r0 * L::LD3 + 16 * l2 + 2 * c);
+        if (al1) {
+#pragma unroll
+          for (int k = 0; k < L::RM / 4; ++k) {
+            if (r0 + 4 * k < R3) cp16s(sp + 32 * k * L::LD3, gp, nb);
+            gp += gst;
+          }
+        } else {
+          const int n0 = nb >= 8 ? 8 : 0, n1 = nb >= 16 ? 8 : 0;
+#pragma unroll
+          for (int k = 0; k < L::RM / 4; ++k) {
+            if (r0 + 4 * k < R3) {
+              cp8s(sp + 32 * k * L::LD3, n0 ? (const void*)gp : (const void*)m3.A, n0);
+              cp8s(sp + 32 * k * L::LD3 + 8, n1 ? (const void*)(gp + 8) : (const void*)m3.A, n1);
+            }
+            gp += gst;
+          }
+        }
+      }
+      {  // UM_2 rows of the step: thread -> (l2, r = tid / 8 + 32 k)
+        const int l2 = tid & 7;
         const bool v = i2o + l2 < I2;
-        cp_async8(U2s + l2 * L::LDU + r, v ? m2.UM + m2.ioff + i2o + l2 + m2.Ifull * r : m2.UM, v);
+        const double* src = m2.UM + m2.ioff + i2o + l2;
+#pragma unroll
+        for (int k = 0; k < (RP + 31) / 32; ++k) {
+          const int r = (tid >> 3) + 32 * k;
+          if (r < R2) cp8s(smem_u32(U2s + l2 * L::LDU + r), v ? (const void*)(src + m2.Ifull * r) : (const void*)m2.UM, v ? 8 : 0);
+        }
       }
     };
     // this thread's 4 elements: (i1 = g, g+8) x (i2 = 2t, 2t+1) at i3 = w
@@ -291,9 +354,13 @@ __global__ void __launch_bounds__(P2_THREADS, 1) k_pass2_fused(const Pass2Args a
         const int64_t i1 = i1o + g + 8 * (q >> 1), i2 = i2o + 2 * t + (q & 1), i3 = i3o + w;
         inb[q] = i1 < I1 && i2 < I2 && i3 < I3;
         off[q] = i1 + I1 * i2 + S12 * i3;
+#if PASD_P2_EXP == 3
+        tv[q] = off[q] * 1e-9; for (int n = 0; n < 3; ++n) yv[n][q] = tv[q] + n;
+#else
         tv[q] = inb[q] ? T[off[q]] : 0.0;
 #pragma unroll
         for (int n = 0; n < 3; ++n) yv[n][q] = inb[q] ? a.Y[n][off[q]] : 0.0;
+#endif
       }
     };
     stage_step(0);
@@ -312,7 +379,7 @@ __global__ void __launch_bounds__(P2_THREADS, 1) k_pass2_fused(const Pass2Args a
           double(&c1)[4] = (ks & 1) ? y1 : z1;
           double(&c2)[4] = (ks & 1) ? y2 : z2;
           double(&c3)[4] = (ks & 1) ? y3 : z3;
-          dmma(c1, U1s[g * L::LDU + k], U1s[(g + 8) * L::LDU + k], A1s[k * L::LD1 + g + 8 * w]);
+          dmma(c1, U1s[g * L::LDU + k], U1s[(g + 8) * L::LDU + k], A1s[(g + 8 * w) * L::LD1 + k]);
           dmma(c2, A2s[k * L::LD2 + g + 16 * w], A2s[k * L::LD2 + g + 8 + 16 * w], U2s[g * L::LDU + k]);
           dmma(c3, A3s[k * L::LD3 + g + 16 * w], A3s[k * L::LD3 + g + 8 + 16 * w], U3s[g * L::LDU + k]);
         }
@@ -353,12 +420,15 @@ __global__ void __launch_bounds__(P2_THREADS, 1) k_pass2_fused(const Pass2Args a
             const double ar = fabs(r);
             if (ar > worst[n]) worst[n] = ar;
             bad |= !isfinite(r);
-            a.Y[n][off[q]] = ynew;
+            if (PASD_P2_EXP != 3) a.Y[n][off[q]] = ynew;
           }
           gn[n] = inb[q] ? g_elem(tt, e, ynew, inv_mu_next) : 0.0;  // next G_n
           gsq[n] = fma(gn[n], gn[n], gsq[n]);
         }
-        if (inb[q]) Enew[off[q]] = e;
+        if (inb[q] && PASD_P2_EXP != 3) {
+          Enew[off[q]] = e;
+          a.D[off[q]] = __dsub_rn(tt, e);  // next pass 1 reads D = T - E
+        }
         g1v[q] = gn[0];
         G2s[g2x(l1, l2, w)] = gn[1];
         G3s[g3x(l1, l2, w)] = gn[2];
@@ -368,13 +438,12 @@ __global__ void __launch_bounds__(P2_THREADS, 1) k_pass2_fused(const Pass2Args a
       (void)offc;
       (void)inc;
       const bool more = i2o + P2_B2 < I2;
-      if (more) load_elems(i2o + P2_B2);  // next step's T, Y in flight during the Wt products
       __syncthreads();  // G2s / G3s complete
       // ---- W-a: Wt_1 (own G_1 as A operand) and half of Wt_3 ----
 #pragma unroll
       for (int p = 0; p < 2; ++p) {
 #pragma unroll
-        for (int j = 0; j < NT1; ++j) dmma(w1acc[j], g1v[p], g1v[2 + p], A1s[(8 * j + g) * L::LD1 + 8 * w + 2 * t + p]);
+        for (int j = 0; j < NT1; ++j) dmma(w1acc[j], g1v[p], g1v[2 + p], A1s[(8 * w + 2 * t + p) * L::LD1 + 8 * j + g]);
       }
       const int mt = w & 3, kh = w >> 2;  // m-tile and K-half of the Wt_2 / Wt_3 products
       if (mt < MT) {
@@ -402,7 +471,10 @@ __global__ void __launch_bounds__(P2_THREADS, 1) k_pass2_fused(const Pass2Args a
         }
       }
       __syncthreads();  // A1s / A3s no longer needed this step
+#if PASD_P2_EXP != 1
       if (more) stage_step(i2o + P2_B2);
+#endif
+      if (more) load_elems(i2o + P2_B2);  // next step's T, Y in flight during Wt_2 and Z
       // ---- W-b: Wt_2^T (m-tile mt, K-half kh), K = (i1, i3) ----
       double acc2[4] = {0, 0, 0, 0};
       if (mt < MT) {
@@ -469,8 +541,8 @@ __global__ void __launch_bounds__(P2_THREADS, 1) k_pass2_fused(const Pass2Args a
       }
     }
     __syncthreads();
-    // restore the zero padding rows of A1s clobbered by the reduction scratch
-    for (int idx = tid; idx < (RP - R1) * 64; idx += P2_THREADS) A1s[(R1 + idx / 64) * L::LD1 + (idx & 63)] = 0.0;
+    // restore the zero padding rows clobbered by the reduction scratch (A1s is
+    // fully rewritten, padding included, by every step's staging)
     for (int idx = tid; idx < (L::RM - R2) * 128; idx += P2_THREADS) A2s[(R2 + idx / 128) * L::LD2 + (idx & 127)] = 0.0;
     for (int idx = tid; idx < (L::RM - R3) * 128; idx += P2_THREADS) A3s[(R3 + idx / 128) * L::LD3 + (idx & 127)] = 0.0;
   }

@@ -244,7 +244,10 @@ __global__ void __launch_bounds__(M8_THREADS, 2) k_pass2_m8(const Pass2Args a, c
           gn[n] = inb[p] ? g_elem(tt, e, ynew, inv_mu_next) : 0.0;
           gsq[n] = fma(gn[n], gn[n], gsq[n]);
         }
-        if (inb[p]) Enew[off[p]] = e;
+        if (inb[p]) {
+          Enew[off[p]] = e;
+          a.D[off[p]] = __dsub_rn(tt, e);  // next pass 1 reads D = T - E
+        }
         g1v[p] = gn[0];
         G2x[g28x(g, l2, w)] = gn[1];
         G3x[g38x(g, l2, w)] = gn[2];

@@ -150,6 +150,7 @@ struct pasd_solver {
   cudaStream_t stream = nullptr;
   double* T = nullptr;
   double* E[2] = {nullptr, nullptr};
+  double* D = nullptr;  // T - E (pass 1 operand, written by the update pass)
   std::vector<double*> Y;
   std::vector<ModeDev> modes;
   std::vector<void*> owned;
@@ -230,7 +231,7 @@ void launch_iteration_marked(pasd_solver* s, cudaStream_t st, Mark&& mark) {
     ModeDev m = s->modes[n];
     if (s->sharded && n == N - 1) m.A = s->A3_partial;  // partial sum over this rank's slab
     mark(PASD_K_CONTRACT_A, true);
-    launch_contract_A_mma(m, s->T, s->E[0], s->E[1], s->Y[n], s->d_ctl, s->sms, st);
+    launch_contract_A_mma(m, s->D, s->Y[n], s->d_ctl, s->sms, st);
     mark(PASD_K_CONTRACT_A, false);
     ++launches;
   }
@@ -293,7 +294,7 @@ void launch_iteration_marked(pasd_solver* s, cudaStream_t st, Mark&& mark) {
     ++launches;
   } else {
     mark(PASD_K_UPDATE, true);
-    k_update<<<s->nblk_update, kThreads, 0, st>>>(s->d_pack, s->T, s->E[0], s->E[1], s->d_resid_part,
+    k_update<<<s->nblk_update, kThreads, 0, st>>>(s->d_pack, s->T, s->E[0], s->E[1], s->D, s->d_resid_part,
                                                   s->d_bad_part, s->S, s->d_ctl);
     mark(PASD_K_UPDATE, false);
     ++launches;
@@ -334,7 +335,7 @@ void kernel_work(const pasd_solver* s, double* bytes, double* flops) {
   for (int k = 0; k < PASD_NUM_KERNEL_CLASSES; ++k) bytes[k] = flops[k] = 0.0;
   for (const ModeDev& m : s->modes) {
     const double RJ = (double)m.R * (double)m.J, R = m.R;
-    bytes[PASD_K_CONTRACT_A] += 8.0 * (3.0 * S + RJ);        // T, E, Y_n in; A_n out
+    bytes[PASD_K_CONTRACT_A] += 8.0 * (2.0 * S + RJ);        // D = T - E, Y_n in; A_n out
     flops[PASD_K_CONTRACT_A] += 2.0 * R * S;
     bytes[PASD_K_GRAM] += 8.0 * RJ;                         // A_n in
     flops[PASD_K_GRAM] += 2.0 * R * RJ;
@@ -345,7 +346,7 @@ void kernel_work(const pasd_solver* s, double* bytes, double* flops) {
     bytes[PASD_K_POLAR] += 8.0 * 4.0 * (double)m.I * R;
     bytes[PASD_K_SVT] += 8.0 * 2.0 * (double)m.I * R;
   }
-  bytes[PASD_K_UPDATE] += 8.0 * (2.0 * N + 2.0) * S;         // T, Y_1..N in; E, Y_1..N out
+  bytes[PASD_K_UPDATE] += 8.0 * (2.0 * N + 3.0) * S;         // T, Y_1..N in; E, D, Y_1..N out
   if (s->fused) {  // pass 2 also forms Wt_n = G^{next} A_n^T (A_n already counted)
     for (const ModeDev& m : s->modes) {
       flops[PASD_K_UPDATE] += 2.0 * (double)m.R * S;
@@ -413,6 +414,7 @@ void reset_state(pasd_solver* s) {
   CK(cudaMemsetAsync(s->E[0], 0, s->S * sizeof(double), s->stream));
   CK(cudaMemsetAsync(s->E[1], 0, s->S * sizeof(double), s->stream));
   for (int n = 0; n < s->N; ++n) CK(cudaMemsetAsync(s->Y[n], 0, s->S * sizeof(double), s->stream));
+  CK(cudaMemcpyAsync(s->D, s->T, s->S * sizeof(double), cudaMemcpyDeviceToDevice, s->stream));  // D = T - 0
   k_init_state<<<64, 256, 0, s->stream>>>(s->d_pack, s->d_ctl, s->mu0, s->rho, s->mu_max, s->eps, s->maxiter,
                                           (s->flags & PASD_FLAG_FIXED_ITERS) ? 1 : 0);
   CK(cudaGetLastError());
@@ -462,6 +464,7 @@ pasd_solver* create_solver(const pasd_options* o, const pasd_shard* shard) {
   s->T = s->alloc<double>(S);
   s->E[0] = s->alloc<double>(S);
   s->E[1] = s->alloc<double>(S);
+  s->D = s->alloc<double>(S);
   for (int n = 0; n < s->N; ++n) s->Y.push_back(s->alloc<double>(S));
   int maxR = 1;
   for (int n = 0; n < s->N; ++n) {
@@ -549,6 +552,7 @@ pasd_solver* create_solver(const pasd_options* o, const pasd_shard* shard) {
     a.T = s->T;
     a.E0 = s->E[0];
     a.E1 = s->E[1];
+    a.D = s->D;
     s->p2_rp = pass2_rp(s->modes[0].R, s->modes[1].R, s->modes[2].R);
     s->use_m8 = m8_supported(s->p2_rp) && std::getenv("PASD_PASS2_M16") == nullptr;
     a.b1 = s->use_m8 ? M8_B : P2_B1;
@@ -598,6 +602,7 @@ void load_tensor(pasd_solver* s, const double* t, int is_device) {
                      s->stream));
   CK(cudaMemsetAsync(s->d_flag, 0, sizeof(int), s->stream));
   k_nonfinite<<<1184, 256, 0, s->stream>>>(s->T, s->S, s->d_flag);
+  k_tsub<<<1184, 256, 0, s->stream>>>(s->D, s->T, s->E[0], s->E[1], s->S, s->d_ctl);  // keep D = T - E
   int flag = 0;
   CK(cudaMemcpyAsync(&flag, s->d_flag, sizeof(int), cudaMemcpyDeviceToHost, s->stream));
   CK(cudaStreamSynchronize(s->stream));
@@ -630,6 +635,7 @@ void set_state(pasd_solver* s, const double* e, const double* const* y, const do
   const int64_t S = s->S;
   CK(cudaMemcpyAsync(s->E[0], e, S * sizeof(double), cudaMemcpyHostToDevice, st));
   CK(cudaMemcpyAsync(s->E[1], e, S * sizeof(double), cudaMemcpyHostToDevice, st));
+  k_tsub<<<1184, 256, 0, st>>>(s->D, s->T, s->E[0], s->E[1], S, s->d_ctl);
   std::vector<double> vn2(s->N, 0.0);
   double* d_vn2 = s->d_stats;  // scratch (finalisation reuses it later)
   ensure_scratch(s);

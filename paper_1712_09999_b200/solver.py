@@ -19,7 +19,7 @@ from .api import (ArgumentError, DeviceError, PasdConfig, RecoveryResult, as_ten
                   count_checks, raise_for_status, run_recover)
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libpasd_b200.so")
+LIB_PATH = os.environ.get("PASD_B200_LIB") or os.path.join(_HERE, "libpasd_b200.so")
 _LIB = None
 
 
