@@ -18,32 +18,32 @@
 
 namespace pasd {
 
-// 64 columns x 16 i per chunk, double-buffered, two CTAs per SM: one CTA's
-// DMMAs overlap the other's loads (a single CTA serialised them: measured
-// 4.6 ms compute-only + 4.6 ms load-only -> 7.6 ms combined per C5 mode).
-#ifndef PASD_P1_MT
-#define PASD_P1_MT 128
-#endif
-constexpr int P1_MT = PASD_P1_MT;  // kappa columns per tile
-#ifndef PASD_P1_KC
-#define PASD_P1_KC 16
-#endif
-constexpr int P1_KC = PASD_P1_KC;  // i rows per chunk
-#ifndef PASD_P1_NST
-#define PASD_P1_NST 2
-#endif
-constexpr int P1_NST = PASD_P1_NST;  // pipeline stages
+// 128 columns x 16 i per chunk, double-buffered, two CTAs per SM: one CTA's
+// DMMAs overlap the other's loads.  Warp w owns kappa rows 16w..16w+15 and
+// all n-tiles, so every G value is formed once.
+constexpr int P1_MT = 128;     // kappa columns per tile
+constexpr int P1_KC = 16;      // i rows per chunk
+constexpr int P1_NST = 2;      // pipeline stages
 constexpr int P1_THREADS = 256;
 
 template <int RP, bool CONTIG>
 struct P1Layout {
   // CONTIG (mode 1): raw[kappa][i] rows of 16 i;  else raw[i][kappa] rows of 128 kappa.
+  // Pitches are 4 mod 16 doubles: the fragment reads (row g, col t) hit 16
+  // distinct banks per half-warp.
   static constexpr int LDR = CONTIG ? (P1_KC + 4) : (P1_MT + 4);
   static constexpr int RAW = CONTIG ? P1_MT * LDR : P1_KC * LDR;  // doubles per tensor per stage
-  static constexpr int LDU = RP + 4;
-  static constexpr int USZ = P1_KC * LDU;
+  static constexpr int LDU = P1_KC + 4;                           // U chunk as [r][i]
+  static constexpr int USZ = RP * LDU;
   static constexpr int STAGE = 2 * RAW + USZ;  // D, Y_n, U chunk
   static constexpr size_t bytes = sizeof(double) * (size_t)P1_NST * STAGE;
+};
+
+// Work-item cursor: (tile, chunk) advanced without 64-bit divisions.  For
+// strided modes a tile is (q, p-block); `p0` / `q` track it incrementally.
+struct P1Cursor {
+  int64_t tile, q, pb;  // tile index, outer index, p-block
+  int chunk;
 };
 
 template <int RP, bool CONTIG>
@@ -51,111 +51,131 @@ __global__ void __launch_bounds__(P1_THREADS, 2) k_pass1(ModeDev m, const double
                                                         const double* __restrict__ Y, const Ctl* ctl) {
   if (ctl->done) return;
   using L = P1Layout<RP, CONTIG>;
-  constexpr int MTILES = P1_MT / 16;                 // m16 tiles of kappa rows (4)
-  constexpr int NSPLIT = (P1_THREADS / 32) / MTILES;  // warps sharing an m-tile (2): split the n-tiles
-  constexpr int NTALL = RP / 8;
-  constexpr int NT = (NTALL + NSPLIT - 1) / NSPLIT;  // n-tiles per warp
+  constexpr int NT = RP / 8;  // n-tiles per warp
   extern __shared__ double p1sm[];
   const double inv_mu = __ddiv_rn(1.0, ctl->mu);  // pasd.cpp:170
-  const int tid = threadIdx.x, lane = tid & 31, g = lane >> 2, t = lane & 3;
-  const int w = (tid >> 5) % MTILES, jbase = ((tid >> 5) / MTILES) * NT;  // m-tile, first n-tile
+  const int tid = threadIdx.x, lane = tid & 31, g = lane >> 2, t = lane & 3, w = tid >> 5;
   const int64_t I = m.I, inner = m.inner;
   const int R = m.R;
-  // tiles: CONTIG -> 128 consecutive kappa; else (q, p-block of 128)
   const int64_t pblocks = CONTIG ? 1 : (inner + P1_MT - 1) / P1_MT;
   const int64_t ntiles = CONTIG ? (m.J + P1_MT - 1) / P1_MT : pblocks * m.outer;
   const int nchunk = (int)((I + P1_KC - 1) / P1_KC);
-  const bool al = CONTIG ? (I % 2 == 0) : (inner % 2 == 0);  // 16-byte aligned rows
-  const int64_t my_tiles = ntiles > blockIdx.x ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
-  const int64_t total = my_tiles * nchunk;  // (tile, chunk) work items of this CTA
+  const bool al = CONTIG ? (I % 2 == 0) : (inner % 2 == 0);        // 16-byte aligned tensor rows
+  const bool alu = (m.Ifull % 2 == 0) && (m.ioff % 2 == 0);         // 16-byte aligned U columns
+  const int64_t gq = gridDim.x / pblocks, gpb = gridDim.x % pblocks;  // tile stride as (q, p-block)
+  const unsigned sbase = static_cast<unsigned>(__cvta_generic_to_shared(p1sm));
 
-  auto stage_ptr = [&](int s) { return p1sm + (size_t)s * L::STAGE; };
-  // issue the cp.async copies of work item `it` into stage s
-  auto issue = [&](int64_t it, int s) {
-    if (it >= total) return;
-    const int64_t tile = blockIdx.x + (it / nchunk) * gridDim.x;
-    const int64_t i0 = (it % nchunk) * P1_KC;
-    double* st = stage_ptr(s);
+  auto advance = [&](P1Cursor& c) {
+    if (++c.chunk == nchunk) {
+      c.chunk = 0;
+      c.tile += gridDim.x;
+      if (!CONTIG) {
+        c.q += gq;
+        c.pb += gpb;
+        if (c.pb >= pblocks) {
+          c.pb -= pblocks;
+          ++c.q;
+        }
+      }
+    }
+  };
+  // issue the cp.async copies of the work item at cursor c into stage s
+  auto issue = [&](const P1Cursor& c, int s) {
+    if (c.tile >= ntiles) return;
+    const int64_t i0 = (int64_t)c.chunk * P1_KC;
+    const unsigned st = sbase + 8u * (unsigned)(s * L::STAGE);
+    const int ni = (int)imin64(P1_KC, I - i0);
     if (CONTIG) {
       // 128 columns kappa, 16 consecutive i each (contiguous): row = column
-      const int64_t k0 = tile * P1_MT;
-      const int ni = (int)imin64(P1_KC, I - i0);
+      const int64_t k0 = c.tile * P1_MT;
       if (al) {
-        const int c = tid & 7;  // 16-byte chunk of the 16-double row
-        const int v = ni - 2 * c, nbc = v >= 2 ? 16 : (v == 1 ? 8 : 0);
+        const int cc = tid & 7;  // 16-byte chunk of the 16-double row
+        const int v = ni - 2 * cc, nbc = v >= 2 ? 16 : (v == 1 ? 8 : 0);
+        const int j0 = tid >> 3;
+        const int64_t off0 = (k0 + j0) * I + i0 + 2 * cc;
 #pragma unroll
-        for (int k = 0; k < P1_MT / (P1_THREADS / 8); ++k) {
-          const int j = (tid >> 3) + (P1_THREADS / 8) * k;
-          const int64_t kap = k0 + j;
-          const int nb = kap < m.J ? nbc : 0;
-          const int64_t off = kap * I + i0 + 2 * c;
-          const int d = j * L::LDR + 2 * c;
-          cp_async16(st + d, nb ? D + off : D, nb);
-          cp_async16(st + L::RAW + d, nb ? Y + off : D, nb);
+        for (int k = 0; k < P1_MT / 32; ++k) {
+          const int j = j0 + 32 * k;
+          const int nb = (k0 + j < m.J) ? nbc : 0;
+          const int64_t off = off0 + 32 * k * I;
+          const unsigned d = st + 8u * (unsigned)(j * L::LDR + 2 * cc);
+          cp16s(d, nb ? D + off : D, nb);
+          cp16s(d + 8u * L::RAW, nb ? Y + off : D, nb);
         }
       } else {
         for (int idx = tid; idx < P1_MT * P1_KC; idx += P1_THREADS) {
-          const int j = idx / P1_KC, c = idx % P1_KC;
-          const int64_t kap = k0 + j;
-          const bool ok = kap < m.J && c < ni;
-          const int64_t off = kap * I + i0 + c;
-          const int d = j * L::LDR + c;
-          cp_async8(st + d, ok ? D + off : D, ok);
-          cp_async8(st + L::RAW + d, ok ? Y + off : D, ok);
+          const int j = idx / P1_KC, cc = idx % P1_KC;
+          const bool ok = k0 + j < m.J && cc < ni;
+          const int64_t off = (k0 + j) * I + i0 + cc;
+          const unsigned d = st + 8u * (unsigned)(j * L::LDR + cc);
+          cp8s(d, ok ? D + off : D, ok ? 8 : 0);
+          cp8s(d + 8u * L::RAW, ok ? Y + off : D, ok ? 8 : 0);
         }
       }
     } else {
-      const int64_t q = tile / pblocks, p0 = (tile % pblocks) * P1_MT;
+      const int64_t p0 = c.pb * P1_MT;
       const int np = (int)imin64(P1_MT, inner - p0);
-      const int ni = (int)imin64(P1_KC, I - i0);
-      const int64_t off0 = p0 + inner * (i0 + I * q);
+      const int64_t off0 = p0 + inner * (i0 + I * c.q);
       if (al) {
-        // P1_MT/2 16-byte chunks per row; thread -> (chunk c, rows rsub + RG k)
-        constexpr int CPR = P1_MT / 2, RG = P1_THREADS / CPR;
-        const int c = tid % CPR, rsub = tid / CPR;
-        const int v = np - 2 * c, nbc = v >= 2 ? 16 : (v == 1 ? 8 : 0);
+        // 64 16-byte chunks per row; thread -> (chunk cc, rows rsub + 4k)
+        const int cc = tid & 63, rsub = tid >> 6;
+        const int v = np - 2 * cc, nbc = v >= 2 ? 16 : (v == 1 ? 8 : 0);
 #pragma unroll
-        for (int k = 0; k < P1_KC / RG; ++k) {
-          const int ii = rsub + RG * k;
+        for (int k = 0; k < P1_KC / 4; ++k) {
+          const int ii = rsub + 4 * k;
           const int nb = ii < ni ? nbc : 0;
-          const int64_t off = off0 + inner * ii + 2 * c;
-          const int d = ii * L::LDR + 2 * c;
-          cp_async16(st + d, nb ? D + off : D, nb);
-          cp_async16(st + L::RAW + d, nb ? Y + off : D, nb);
+          const int64_t off = off0 + inner * ii + 2 * cc;
+          const unsigned d = st + 8u * (unsigned)(ii * L::LDR + 2 * cc);
+          cp16s(d, nb ? D + off : D, nb);
+          cp16s(d + 8u * L::RAW, nb ? Y + off : D, nb);
         }
       } else {
         for (int idx = tid; idx < P1_KC * P1_MT; idx += P1_THREADS) {
-          const int ii = idx / P1_MT, c = idx % P1_MT;
-          const bool ok = ii < ni && c < np;
-          const int64_t off = off0 + inner * ii + c;
-          const int d = ii * L::LDR + c;
-          cp_async8(st + d, ok ? D + off : D, ok);
-          cp_async8(st + L::RAW + d, ok ? Y + off : D, ok);
+          const int ii = idx / P1_MT, cc = idx % P1_MT;
+          const bool ok = ii < ni && cc < np;
+          const int64_t off = off0 + inner * ii + cc;
+          const unsigned d = st + 8u * (unsigned)(ii * L::LDR + cc);
+          cp8s(d, ok ? D + off : D, ok ? 8 : 0);
+          cp8s(d + 8u * L::RAW, ok ? Y + off : D, ok ? 8 : 0);
         }
       }
     }
-    double* us = st + 2 * L::RAW;
-    for (int idx = tid; idx < P1_KC * RP; idx += P1_THREADS) {
-      const int i = idx % P1_KC, r = idx / P1_KC;
-      const bool ok = r < R && i0 + i < I;
-      cp_async8(us + i * L::LDU + r, ok ? m.U + m.ioff + (i0 + i) + m.Ifull * r : m.U, ok);
+    // U chunk as [r][i] (16 consecutive i of column r are contiguous in U)
+    const unsigned us = st + 8u * (unsigned)(2 * L::RAW);
+    const double* ub = m.U + m.ioff + i0;
+    if (alu) {
+      const int ip = tid & 7;
+      const int v = ni - 2 * ip, nbc = v >= 2 ? 16 : (v == 1 ? 8 : 0);
+#pragma unroll
+      for (int k = 0; k < (RP + 31) / 32; ++k) {
+        const int r = (tid >> 3) + 32 * k;
+        if (r < RP) {
+          const int nb = r < R ? nbc : 0;
+          cp16s(us + 8u * (unsigned)(r * L::LDU + 2 * ip), nb ? ub + 2 * ip + m.Ifull * r : m.U, nb);
+        }
+      }
+    } else {
+      for (int idx = tid; idx < P1_KC * RP; idx += P1_THREADS) {
+        const int i = idx & (P1_KC - 1), r = idx / P1_KC;
+        const bool ok = r < R && i < ni;
+        cp8s(us + 8u * (unsigned)(r * L::LDU + i), ok ? ub + i + m.Ifull * r : m.U, ok ? 8 : 0);
+      }
     }
   };
 
-  // even / odd k-steps in separate accumulators (two independent DMMA chains
-  // per n-tile) only when a warp has few n-tiles; NT >= 4 chains already keep
-  // the tensor pipe busy and the registers are needed by the staging.
+  // few n-tiles: even / odd k-steps in separate accumulators (independent chains)
   constexpr bool TWO = NT < 4;
   double acc[NT][4], acb[TWO ? NT : 1][4];
-  int64_t it = 0;
+  P1Cursor cur{(int64_t)blockIdx.x, (int64_t)blockIdx.x / pblocks, (int64_t)blockIdx.x % pblocks, 0};
+  P1Cursor nxt = cur;
   for (int s = 0; s < P1_NST - 1; ++s) {
-    issue(s, s);
+    issue(nxt, s);
+    advance(nxt);
     asm volatile("cp.async.commit_group;" ::: "memory");
   }
-  for (; it < total; ++it) {
+  for (int64_t it = 0; cur.tile < ntiles; ++it) {
     const int s = (int)(it % P1_NST);
-    const int ci = (int)(it % nchunk);
-    if (ci == 0) {
+    if (cur.chunk == 0) {
 #pragma unroll
       for (int j = 0; j < NT; ++j) {
         acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.0;
@@ -164,9 +184,10 @@ __global__ void __launch_bounds__(P1_THREADS, 2) k_pass1(ModeDev m, const double
     }
     asm volatile("cp.async.wait_group %0;" ::"n"(P1_NST - 2) : "memory");
     __syncthreads();  // stage s complete for all threads; stage of item it-1 free
-    issue(it + P1_NST - 1, (int)((it + P1_NST - 1) % P1_NST));
+    issue(nxt, (int)((it + P1_NST - 1) % P1_NST));
+    advance(nxt);
     asm volatile("cp.async.commit_group;" ::: "memory");
-    const double* st = stage_ptr(s);
+    const double* st = p1sm + (size_t)s * L::STAGE;
     const double* Ds = st;
     const double* Ys = st + L::RAW;
     const double* Us = st + 2 * L::RAW;
@@ -180,32 +201,33 @@ __global__ void __launch_bounds__(P1_THREADS, 2) k_pass1(ModeDev m, const double
       const double a1 = __dadd_rn(Ds[o1], __dmul_rn(Ys[o1], inv_mu));
 #pragma unroll
       for (int j = 0; j < NT; ++j)
-        if (jbase + j < NTALL) dmma((TWO && (ks & 1)) ? acb[TWO ? j : 0] : acc[j], a0, a1, Us[k * L::LDU + 8 * (jbase + j) + g]);
+        dmma((TWO && (ks & 1)) ? acb[TWO ? j : 0] : acc[j], a0, a1, Us[(8 * j + g) * L::LDU + k]);
     }
-    if (ci == nchunk - 1) {  // tile done: write A
-      const int64_t tile = blockIdx.x + (it / nchunk) * gridDim.x;
+    if (cur.chunk == nchunk - 1) {  // tile done: write A
+      if (TWO) {
 #pragma unroll
-      for (int j = 0; j < NT; ++j)
+        for (int j = 0; j < NT; ++j)
 #pragma unroll
-        for (int q4 = 0; q4 < 4; ++q4)
-          if (TWO) acc[j][q4] += acb[TWO ? j : 0][q4];
+          for (int q4 = 0; q4 < 4; ++q4) acc[j][q4] += acb[TWO ? j : 0][q4];
+      }
 #pragma unroll
       for (int j = 0; j < NT; ++j) {
 #pragma unroll
         for (int q4 = 0; q4 < 4; ++q4) {
           const int row = 16 * w + g + 8 * (q4 >> 1);
-          const int r = 8 * (jbase + j) + 2 * t + (q4 & 1);
+          const int r = 8 * j + 2 * t + (q4 & 1);
           if (r >= R) continue;
           if (CONTIG) {
-            const int64_t kap = tile * P1_MT + row;
+            const int64_t kap = cur.tile * P1_MT + row;
             if (kap < m.J) m.A[r + (int64_t)R * kap] = acc[j][q4];
           } else {
-            const int64_t q = tile / pblocks, p = (tile % pblocks) * P1_MT + row;
-            if (p < inner) m.A[p + inner * ((int64_t)r + (int64_t)R * q)] = acc[j][q4];
+            const int64_t p = cur.pb * P1_MT + row;
+            if (p < inner) m.A[p + inner * ((int64_t)r + (int64_t)R * cur.q)] = acc[j][q4];
           }
         }
       }
     }
+    advance(cur);
   }
   asm volatile("cp.async.wait_all;" ::: "memory");
 }

@@ -27,6 +27,9 @@
 
 namespace pasd {
 
+#ifndef PASD_P2_LOADPOS
+#define PASD_P2_LOADPOS 1
+#endif
 constexpr int P2_B1 = 16, P2_B2 = 8, P2_B3 = 8;
 constexpr int P2_THREADS = 256;
 constexpr int P2_BRICK = P2_B1 * P2_B2 * P2_B3;  // 1024
@@ -159,26 +162,46 @@ __device__ __forceinline__ bool mt_dummy_guard(int w, int MT) { return (w & 3) <
 // Shared-memory footprint (bytes) of k_pass2_fused<RP>.
 template <int RP>
 struct P2Layout {
-  static constexpr int RM = (RP + 15) / 16 * 16;  // rows of the M tiles (Wt products)
-  // leading dims chosen so the DMMA fragment reads (rows t x cols g, rows g x
-  // cols t) and the staging writes hit distinct banks per half-warp
+  // The Wt_2 / Wt_3 products read the A_2 / A_3 slices as 16-row M tiles
+  // covering RM rows; rows >= RP of the last tile run past the slice into the
+  // next buffer.  Those rows only feed output rows r >= RP, which are never
+  // stored, so the slices hold RP rows (rows R..RP-1 zero: the Z products use
+  // them along K).
+  static constexpr int RM = (RP + 15) / 16 * 16;
   // A1s is column-major: [column c = l2 + 8 l3][r], pitch LD1 = RP + 4 (4 or 12
   // mod 16: the Z_1 reads (c = g, r = t) are conflict-free, the Wt_1 reads
   // (c = 2t, r = g) 2-way), so each column's R1 contiguous values of A_1
-  // stage as 16-byte copies.
+  // stage as 16-byte copies.  Other pitches keep the fragment reads
+  // (rows t x cols g, rows g x cols t) on distinct banks per half-warp.
   static constexpr int LD1 = RP + 4, LD2 = 128 + 4, LD3 = 128 + 4, LDU = RP + 4;
+  static constexpr int A1SZ = 64 * LD1;
+  static constexpr int REST = RP * LD2 + RP * LD3 + 32 * LDU + 8 * 182 + 8 * 160 + 8 * 180 + 64;
+  // A_1 slice double-buffered (staged a whole step ahead) when it fits in 227 KB
+// Double-buffering A_1 (staged a whole step ahead) measured slower on B200:
+// 49.7 vs 43.2 ms per C5 launch.  Pass-2 time grows with the CTA's shared
+// memory footprint (an unused 8 KB pad: 43.2 -> 46.6 ms), so the single
+// buffer stays the default.
+#ifndef PASD_P2_DB
+#define PASD_P2_DB 0
+#endif
+  static constexpr bool DB = PASD_P2_DB && (2 * A1SZ + REST <= 227 * 1024 / 8);
   static constexpr int oA1 = 0;
-  static constexpr int oA2 = oA1 + 64 * LD1;
-  static constexpr int oA3 = oA2 + RM * LD2;
-  static constexpr int oU1 = oA3 + RM * LD3;
+  static constexpr int oA2 = oA1 + (DB ? 2 : 1) * A1SZ;
+  static constexpr int oA3 = oA2 + RP * LD2;
+  static constexpr int oU1 = oA3 + RP * LD3;
   static constexpr int oU2 = oU1 + 16 * LDU;
   static constexpr int oU3 = oU2 + 8 * LDU;
   static constexpr int oZ3 = oU3 + 8 * LDU;
   static constexpr int oG2 = oZ3 + 8 * 182;
   static constexpr int oG3 = oG2 + 8 * 160;
   static constexpr int oRed = oG3 + 8 * 180;
-  static constexpr int total = oRed + 64;
+#ifndef PASD_P2_PAD
+#define PASD_P2_PAD 0
+#endif
+  static constexpr int total = oRed + 64 + PASD_P2_PAD;
   static constexpr size_t bytes = sizeof(double) * (size_t)total;
+  static_assert((RM - RP) * LD3 <= total - oU1, "M-tile overrun must stay inside shared memory");
+  static_assert(128 * RP <= oA3, "end-of-pencil scratch must fit below A3s");
 };
 
 // RP = common padded rank (multiple of 8, >= every R_n); rows r >= R_n of each
@@ -221,9 +244,9 @@ __global__ void __launch_bounds__(P2_THREADS, 1) k_pass2_fused(const Pass2Args a
   double* W2c = a.W2part + (int64_t)blockIdx.x * I2 * R2;  // per-CTA Wt_2 partial
   for (int64_t idx = tid; idx < I2 * R2; idx += P2_THREADS) W2c[idx] = 0.0;
   // zero padding rows once (never overwritten by the staging copies)
-  for (int idx = tid; idx < (L::RM - R2) * 128; idx += P2_THREADS) A2s[(R2 + idx / 128) * L::LD2 + (idx & 127)] = 0.0;
-  for (int idx = tid; idx < (L::RM - R3) * 128; idx += P2_THREADS) A3s[(R3 + idx / 128) * L::LD3 + (idx & 127)] = 0.0;
-  for (int idx = tid; idx < 32 * (RP + 4); idx += P2_THREADS) U1s[idx] = 0.0;  // U1s, U2s, U3s padding
+  for (int idx = tid; idx < (RP - R2) * 128; idx += P2_THREADS) A2s[(R2 + idx / 128) * L::LD2 + (idx & 127)] = 0.0;
+  for (int idx = tid; idx < (RP - R3) * 128; idx += P2_THREADS) A3s[(R3 + idx / 128) * L::LD3 + (idx & 127)] = 0.0;
+  for (int idx = tid; idx < L::total - L::oU1; idx += P2_THREADS) U1s[idx] = 0.0;  // UM rows, exchange buffers
 
   double worst[3] = {0.0, 0.0, 0.0};
   double gsq[3] = {0.0, 0.0, 0.0};
@@ -272,12 +295,12 @@ __global__ void __launch_bounds__(P2_THREADS, 1) k_pass2_fused(const Pass2Args a
     // Per-thread source/destination bases are fixed along the pencil; a step
     // only advances them by 8 i2.
     const int n3v = (int)imin64(8, I3 - i3o);  // valid i3 of the pencil
-    auto stage_step = [&](int64_t i2o) {
+    auto stage_a1 = [&](int64_t i2o, double* A1b) {
       {  // A_1 (R1, I2, I3 layout): warp w -> columns (l2 = w, l3 = k); lane -> r pair
         const bool c2ok = i2o + w < I2;
         const char* gp = reinterpret_cast<const char*>(m1.A + (int64_t)R1 * ((i2o + w) + I2 * i3o));
         const int64_t kst = 8 * (int64_t)R1 * I2;  // bytes to the next l3
-        const unsigned sp = smem_u32(A1s + w * L::LD1);
+        const unsigned sp = smem_u32(A1b + w * L::LD1);
         if ((R1 & 1) == 0) {
           if (lane < RP / 2) {
             const int r = 2 * lane;
@@ -307,6 +330,8 @@ __global__ void __launch_bounds__(P2_THREADS, 1) k_pass2_fused(const Pass2Args a
           }
         }
       }
+    };
+    auto stage_a3u2 = [&](int64_t i2o) {
       {  // A_3 (I1, I2, R3 layout): rows (r, l2) of 16 consecutive i1; thread ->
          // 16-byte chunk c, l2, rows r = r0 + 4k (padding rows stay zero)
         const int c = tid & 7, l2 = (tid >> 3) & 7, r0 = tid >> 6;
@@ -317,14 +342,14 @@ __global__ void __launch_bounds__(P2_THREADS, 1) k_pass2_fused(const Pass2Args a
         const unsigned sp = smem_u32(A3s + r0 * L::LD3 + 16 * l2 + 2 * c);
         if (al1) {
 #pragma unroll
-          for (int k = 0; k < L::RM / 4; ++k) {
+          for (int k = 0; k < RP / 4; ++k) {
             if (r0 + 4 * k < R3) cp16s(sp + 32 * k * L::LD3, gp, nb);
             gp += gst;
           }
         } else {
           const int n0 = nb >= 8 ? 8 : 0, n1 = nb >= 16 ? 8 : 0;
 #pragma unroll
-          for (int k = 0; k < L::RM / 4; ++k) {
+          for (int k = 0; k < RP / 4; ++k) {
             if (r0 + 4 * k < R3) {
               cp8s(sp + 32 * k * L::LD3, n0 ? (const void*)gp : (const void*)m3.A, n0);
               cp8s(sp + 32 * k * L::LD3 + 8, n1 ? (const void*)(gp + 8) : (const void*)m3.A, n1);
@@ -363,11 +388,28 @@ __global__ void __launch_bounds__(P2_THREADS, 1) k_pass2_fused(const Pass2Args a
 #endif
       }
     };
-    stage_step(0);
+    stage_a1(0, A1s);
+    stage_a3u2(0);
+    if (L::DB) asm volatile("cp.async.commit_group;" ::: "memory");
+#if PASD_P2_LOADPOS == 0
     load_elems(0);
+#endif
 
-    for (int64_t i2o = 0; i2o < I2; i2o += P2_B2) {
-      cp_async_wait_all();
+    int sidx = 0;  // step index along the pencil (A_1 buffer parity)
+    for (int64_t i2o = 0; i2o < I2; i2o += P2_B2, ++sidx) {
+      const bool more = i2o + P2_B2 < I2;
+      double* A1c = A1s + ((L::DB && (sidx & 1)) ? L::A1SZ : 0);
+#if PASD_P2_LOADPOS == 1
+      load_elems(i2o);  // this step's T, Y: in flight while the staging lands and Z runs
+#endif
+      if (L::DB) {
+        // next step's A_1 slice into the other buffer: a whole step to land
+        if (more) stage_a1(i2o + P2_B2, A1s + ((sidx & 1) ? 0 : L::A1SZ));
+        asm volatile("cp.async.commit_group;" ::: "memory");
+        asm volatile("cp.async.wait_group 1;" ::: "memory");
+      } else {
+        cp_async_wait_all();
+      }
       __syncthreads();  // step data staged; previous step's smem consumers done
       // ---- Z products (6 independent accumulator chains) ----
       double z1[4] = {0, 0, 0, 0}, z2[4] = {0, 0, 0, 0}, z3[4] = {0, 0, 0, 0};
@@ -379,7 +421,7 @@ __global__ void __launch_bounds__(P2_THREADS, 1) k_pass2_fused(const Pass2Args a
           double(&c1)[4] = (ks & 1) ? y1 : z1;
           double(&c2)[4] = (ks & 1) ? y2 : z2;
           double(&c3)[4] = (ks & 1) ? y3 : z3;
-          dmma(c1, U1s[g * L::LDU + k], U1s[(g + 8) * L::LDU + k], A1s[(g + 8 * w) * L::LD1 + k]);
+          dmma(c1, U1s[g * L::LDU + k], U1s[(g + 8) * L::LDU + k], A1c[(g + 8 * w) * L::LD1 + k]);
           dmma(c2, A2s[k * L::LD2 + g + 16 * w], A2s[k * L::LD2 + g + 8 + 16 * w], U2s[g * L::LDU + k]);
           dmma(c3, A3s[k * L::LD3 + g + 16 * w], A3s[k * L::LD3 + g + 8 + 16 * w], U3s[g * L::LDU + k]);
         }
@@ -437,15 +479,22 @@ __global__ void __launch_bounds__(P2_THREADS, 1) k_pass2_fused(const Pass2Args a
       }
       (void)offc;
       (void)inc;
-      const bool more = i2o + P2_B2 < I2;
       __syncthreads();  // G2s / G3s complete
-      // ---- W-a: Wt_1 (own G_1 as A operand) and half of Wt_3 ----
+      // ---- Wt_1 uses the warp's own G_1 as the A operand (A_1 slice as B) ----
+      auto wt1 = [&]() {
 #pragma unroll
-      for (int p = 0; p < 2; ++p) {
+        for (int p = 0; p < 2; ++p) {
 #pragma unroll
-        for (int j = 0; j < NT1; ++j) dmma(w1acc[j], g1v[p], g1v[2 + p], A1s[(8 * w + 2 * t + p) * L::LD1 + 8 * j + g]);
-      }
+          for (int j = 0; j < NT1; ++j) dmma(w1acc[j], g1v[p], g1v[2 + p], A1c[(8 * w + 2 * t + p) * L::LD1 + 8 * j + g]);
+        }
+      };
       const int mt = w & 3, kh = w >> 2;  // m-tile and K-half of the Wt_2 / Wt_3 products
+#ifndef PASD_P2_W1LATE
+#define PASD_P2_W1LATE 1
+#endif
+      constexpr bool W1LATE = L::DB && PASD_P2_W1LATE;
+      if (!W1LATE) wt1();
+      // ---- Wt_3^T (m-tile mt, K-half kh), K = (i1, i2) ----
       if (mt < MT) {
         double acc[3][4] = {};
         const double* rowa = A3s + (16 * mt + g) * L::LD3 + 64 * kh;
@@ -470,11 +519,18 @@ __global__ void __launch_bounds__(P2_THREADS, 1) k_pass2_fused(const Pass2Args a
           if (r < R2 && i2 < I2) w2old[q] = W2c[i2 * R2 + r];
         }
       }
-      __syncthreads();  // A1s / A3s no longer needed this step
+      __syncthreads();  // A3s / U2s (and A1s when single-buffered) no longer needed this step
 #if PASD_P2_EXP != 1
-      if (more) stage_step(i2o + P2_B2);
+      if (more) {
+        if (!L::DB) stage_a1(i2o + P2_B2, A1s);
+        stage_a3u2(i2o + P2_B2);
+      }
+      if (L::DB) asm volatile("cp.async.commit_group;" ::: "memory");
 #endif
+#if PASD_P2_LOADPOS == 0
       if (more) load_elems(i2o + P2_B2);  // next step's T, Y in flight during Wt_2 and Z
+#endif
+      if (W1LATE) wt1();
       // ---- W-b: Wt_2^T (m-tile mt, K-half kh), K = (i1, i3) ----
       double acc2[4] = {0, 0, 0, 0};
       if (mt < MT) {
@@ -517,7 +573,7 @@ __global__ void __launch_bounds__(P2_THREADS, 1) k_pass2_fused(const Pass2Args a
     }
     // ---- end of pencil: Wt_1 (sum over the 8 warps' column sets) and Wt_3 ----
     __syncthreads();
-    double* wred = A1s;  // 8 warps x 16 x RP doubles (fits in A1s..A3s)
+    double* wred = A1s;  // 8 warps x 16 x RP doubles (fits below A3s)
 #pragma unroll
     for (int j = 0; j < NT1; ++j) {
 #pragma unroll
@@ -541,10 +597,11 @@ __global__ void __launch_bounds__(P2_THREADS, 1) k_pass2_fused(const Pass2Args a
       }
     }
     __syncthreads();
-    // restore the zero padding rows clobbered by the reduction scratch (A1s is
-    // fully rewritten, padding included, by every step's staging)
-    for (int idx = tid; idx < (L::RM - R2) * 128; idx += P2_THREADS) A2s[(R2 + idx / 128) * L::LD2 + (idx & 127)] = 0.0;
-    for (int idx = tid; idx < (L::RM - R3) * 128; idx += P2_THREADS) A3s[(R3 + idx / 128) * L::LD3 + (idx & 127)] = 0.0;
+    // restore the zero padding rows of A2s clobbered by the reduction scratch
+    // (single-buffered A_1 only; A1s itself is rewritten, padding included, by
+    // every step's staging)
+    if (!L::DB)
+      for (int idx = tid; idx < (RP - R2) * 128; idx += P2_THREADS) A2s[(R2 + idx / 128) * L::LD2 + (idx & 127)] = 0.0;
   }
   // ---- per-CTA residual / NaN / ||G||^2 partials ----
   for (int n = 0; n < 3; ++n) {
