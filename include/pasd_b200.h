@@ -124,9 +124,17 @@ typedef struct pasd_outputs {
 
 /* Full solve from a HOST tensor: H2D of t, the device-resident ADMM loop, the
  * finalisation and D2H of the requested outputs.  Returns PASD_OK or an error
- * code; errbuf receives the reference's exception message text. */
+ * code; errbuf receives the reference's exception message text.
+ * The last successful call's solver (device buffers and captured iteration
+ * graph) is kept, keyed on the full options struct, so a repeated solve of
+ * the same shape and options skips allocation and teardown; results do not
+ * depend on it.  Set PASD_B200_NO_CACHE in the environment to disable. */
 int pasd_b200_recover(const double* t, const pasd_options* opt, pasd_outputs* out,
                       pasd_observer_fn observer, void* user, char* errbuf, size_t errlen);
+
+/* Free the solver kept by pasd_b200_recover (device memory returns to the
+ * allocator).  Safe to call at any time. */
+void pasd_b200_release_cache(void);
 
 /* ---- device-resident solver handle (benchmarks, multi-GPU) -------------- */
 

@@ -7,10 +7,11 @@ Public API mirrors ``proj/include/tenrec`` of the reference:
 """
 from .api import (ArgumentError, Certificate, DeviceError, IoError, IterationView, NumericalError, PasdConfig,
                   RecoveryResult, StateError, TenrecError)
-from .solver import Solver, default_lambdas, default_rank_bound, lib, pasd_recover, validate_config
+from .solver import (Solver, default_lambdas, default_rank_bound, lib, pasd_recover, release_cache,
+                     validate_config)
 
 __all__ = [
     "ArgumentError", "Certificate", "DeviceError", "IoError", "IterationView", "NumericalError", "PasdConfig",
     "RecoveryResult", "StateError", "TenrecError", "Solver", "default_lambdas", "default_rank_bound", "lib",
-    "pasd_recover", "validate_config",
+    "pasd_recover", "release_cache", "validate_config",
 ]

@@ -92,6 +92,7 @@ class PasdOutputs(C.Structure):
 # Every symbol include/pasd_b200.h declares (checked by tests/test_abi.py).
 HEADER_SYMBOLS = (
     "pasd_b200_recover",
+    "pasd_b200_release_cache",
     "pasd_b200_solver_create",
     "pasd_b200_solver_load",
     "pasd_b200_solver_reset",

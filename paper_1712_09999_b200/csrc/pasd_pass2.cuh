@@ -193,8 +193,13 @@ struct P2Layout {
   static constexpr int oU3 = oU2 + 8 * LDU;
   static constexpr int oZ3 = oU3 + 8 * LDU;
   static constexpr int oG2 = oZ3 + 8 * 182;
+#if PASD_P2_EXP == 5
+  static constexpr int oG3 = oZ3;  // timing experiment only: alias (wrong results)
+  static constexpr int oRed = oG2 + 8 * 160;
+#else
   static constexpr int oG3 = oG2 + 8 * 160;
   static constexpr int oRed = oG3 + 8 * 180;
+#endif
 #ifndef PASD_P2_PAD
 #define PASD_P2_PAD 0
 #endif

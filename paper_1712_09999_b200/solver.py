@@ -33,6 +33,8 @@ def lib():
         L.pasd_b200_recover.restype = C.c_int
         L.pasd_b200_recover.argtypes = [_abi.c_double_p, C.POINTER(_abi.PasdOptions), C.POINTER(_abi.PasdOutputs),
                                         _abi.PasdObserverFn, C.c_void_p, C.c_char_p, C.c_size_t]
+        L.pasd_b200_release_cache.restype = None
+        L.pasd_b200_release_cache.argtypes = []
         L.pasd_b200_validate.restype = C.c_int
         L.pasd_b200_validate.argtypes = [C.POINTER(_abi.PasdOptions), C.c_char_p, C.c_size_t]
         L.pasd_b200_default_lambdas.restype = C.c_int
@@ -67,6 +69,11 @@ def lib():
 
 def _err():
     return C.create_string_buffer(1024)
+
+
+def release_cache() -> None:
+    """Free the solver pasd_recover keeps between calls of the same shape."""
+    lib().pasd_b200_release_cache()
 
 
 def validate_config(config: PasdConfig, dims: Sequence[int]) -> None:
