@@ -143,35 +143,51 @@ __global__ void __launch_bounds__(M8_THREADS, 2) k_pass2_m8(const Pass2Args a, c
     for (int j = 0; j < NT; ++j) w1acc[j][0] = w1acc[j][1] = 0.0;
     double w3acc[2][2] = {};  // Wt_3^T m-tiles (w-4) and (w), warps 4..7
 
+    // Per-step staging with per-thread address bases hoisted out of the copy
+    // loops (the swizzle term is fixed per thread, so a thread's copies are
+    // a constant stride apart in shared memory).
     auto stage_step = [&](int64_t i2o) {
-      {  // A_1 (R1, I2, I3): column (i2, i3) holds R1 contiguous values
+      {  // A_1 (R1, I2, I3): column (i2, i3) holds R1 contiguous values; thread -> column c, rows r0 + 4k
         const int c = tid >> 2, l2 = c & 7, l3 = c >> 3, r0 = tid & 3;
         const int64_t i2 = i2o + l2, i3 = i3o + l3;
         const bool colok = i2 < I2 && i3 < I3;
-        const double* src = m1.A + (colok ? (int64_t)R1 * (i2 + I2 * i3) : 0);
-#pragma unroll 4
-        for (int r = r0; r < R1; r += 4) cp_async8(A1s + sw(r, c), colok ? src + r : m1.A, colok);
+        const double* src = colok ? m1.A + (int64_t)R1 * (i2 + I2 * i3) + r0 : m1.A;
+        const int sst = colok ? 4 : 0;
+        const unsigned d0 = smem_u32(A1s + sw(r0, c));
+#pragma unroll
+        for (int k = 0; k < RP / 4; ++k)
+          if (r0 + 4 * k < R1) cp8s(d0 + 8u * 256u * k, src + k * sst, colok ? 8 : 0);
       }
-      {  // A_3 (I1, I2, R3): rows (r, l2) of 8 consecutive i1
-        const int c = tid & 3;
+      {  // A_3 (I1, I2, R3): rows (r, l2) of 8 consecutive i1; thread -> piece c, l2, rows r = tid/32 + 8k
+        const int c = tid & 3, l2 = (tid >> 2) & 7, rb = tid >> 5;
         const int v = nv1 - 2 * c, nbc = v >= 2 ? 16 : (v == 1 ? 8 : 0);
-        for (int row = tid >> 2; row < 8 * R3; row += M8_THREADS / 4) {
-          const int l2 = row & 7, r = row >> 3;
-          const int nb = (i2o + l2 < I2) ? nbc : 0;
-          double* dst = A3s + sw(r, 8 * l2 + 2 * c);
-          const double* src = m3.A + i1o + 2 * c + I1 * (i2o + l2) + S12 * (int64_t)r;
-          if (al1)
-            cp_async16(dst, nb ? src : m3.A, nb);
-          else {
-            cp_async8(dst, nb >= 8 ? src : m3.A, nb >= 8);
-            cp_async8(dst + 1, nb >= 16 ? src + 1 : m3.A, nb >= 16);
-          }
+        const int nb = (i2o + l2 < I2) ? nbc : 0;
+        const double* src = nb ? m3.A + i1o + 2 * c + I1 * (i2o + l2) + S12 * (int64_t)rb : m3.A;
+        const int64_t sst = nb ? 8 * S12 : 0;
+        const unsigned d0 = smem_u32(A3s + sw(rb, 8 * l2 + 2 * c));
+        if (al1) {
+#pragma unroll
+          for (int k = 0; k < (RP + 7) / 8; ++k)
+            if (rb + 8 * k < R3) cp16s(d0 + 8u * 512u * k, src + k * sst, nb);
+        } else {
+          const int n0 = nb >= 8 ? 8 : 0, n1 = nb >= 16 ? 8 : 0;
+#pragma unroll
+          for (int k = 0; k < (RP + 7) / 8; ++k)
+            if (rb + 8 * k < R3) {
+              cp8s(d0 + 8u * 512u * k, n0 ? src + k * sst : m3.A, n0);
+              cp8s(d0 + 8u * 512u * k + 8u, n1 ? src + k * sst + 1 : m3.A, n1);
+            }
         }
       }
-      for (int idx = tid; idx < 8 * R2; idx += M8_THREADS) {
-        const int l2 = idx & 7, r = idx >> 3;
+      {  // UM_2 rows of the step: thread -> (l2, r = tid / 8 + 32 k)
+        const int l2 = tid & 7, rb = tid >> 3;
         const bool v = i2o + l2 < I2;
-        cp_async8(U2s + swu<RP>(l2, r), v ? m2.UM + m2.ioff + i2o + l2 + m2.Ifull * r : m2.UM, v);
+        const double* src = v ? m2.UM + m2.ioff + i2o + l2 + m2.Ifull * rb : m2.UM;
+        const int64_t sst = v ? 32 * m2.Ifull : 0;
+        const unsigned d0 = smem_u32(U2s + swu<RP>(l2, rb));
+#pragma unroll
+        for (int k = 0; k < (RP + 31) / 32; ++k)
+          if (rb + 32 * k < R2) cp8s(d0 + 8u * 32u * k, src + k * sst, v ? 8 : 0);
       }
     };
     // this thread's 2 elements: i1 = g, i2 = 2t + p, i3 = w
