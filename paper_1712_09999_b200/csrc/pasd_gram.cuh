@@ -6,6 +6,7 @@
 // per-CTA partials in a fixed order.
 #pragma once
 #include "pasd_pass2.cuh"
+#include "pasd_small.cuh"
 
 namespace pasd {
 
@@ -20,13 +21,13 @@ struct GramLayout {
   static constexpr size_t bytes = sizeof(double) * 2 * GM_KC * LD;
 };
 
+// Partial Gram of the chunks cta, cta + ncta, ... of mode m into
+// m.Gpart[cta] (R x R).  RP >= round_up(R, 8).
 template <int RP>
-__global__ void __launch_bounds__(GM_THREADS) k_gram_mma(ModeDev m, const Ctl* ctl) {
-  if (ctl->done) return;
+__device__ void gram_partial(const ModeDev& m, int cta, int ncta, double* gsm) {
   using L = GramLayout<RP>;
   constexpr int TILES = L::MT * L::NT;
   constexpr int TPW = (TILES + 7) / 8;  // tiles per warp
-  extern __shared__ double gsm[];
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5, g = lane >> 2, t = lane & 3;
   const int R = m.R;
   const int64_t nchunks = (m.J + GM_KC - 1) / GM_KC;
@@ -51,12 +52,12 @@ __global__ void __launch_bounds__(GM_THREADS) k_gram_mma(ModeDev m, const Ctl* c
   double acc[TPW][4];
 #pragma unroll
   for (int j = 0; j < TPW; ++j) acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.0;
-  int64_t ch = blockIdx.x;
+  int64_t ch = cta;
   issue(ch, 0);
   asm volatile("cp.async.commit_group;" ::: "memory");
   int buf = 0;
-  for (; ch < nchunks; ch += gridDim.x, buf ^= 1) {
-    issue(ch + gridDim.x, buf ^ 1);
+  for (; ch < nchunks; ch += ncta, buf ^= 1) {
+    issue(ch + ncta, buf ^ 1);
     asm volatile("cp.async.commit_group;" ::: "memory");
     asm volatile("cp.async.wait_group 1;" ::: "memory");
     __syncthreads();
@@ -76,7 +77,7 @@ __global__ void __launch_bounds__(GM_THREADS) k_gram_mma(ModeDev m, const Ctl* c
     __syncthreads();  // buffer `buf` is refilled two chunks later
   }
   asm volatile("cp.async.wait_all;" ::: "memory");
-  double* out = m.Gpart + (int64_t)blockIdx.x * R * R;
+  double* out = m.Gpart + (int64_t)cta * R * R;
 #pragma unroll
   for (int j = 0; j < TPW; ++j) {
     const int tile = w + 8 * j;
@@ -88,6 +89,75 @@ __global__ void __launch_bounds__(GM_THREADS) k_gram_mma(ModeDev m, const Ctl* c
         if (r < R && c < R) out[r * R + c] = acc[j][q];
       }
     }
+  }
+}
+
+template <int RP>
+__global__ void __launch_bounds__(GM_THREADS) k_gram_mma(ModeDev m, const Ctl* ctl) {
+  if (ctl->done) return;
+  extern __shared__ double gsm[];
+  gram_partial<RP>(m, blockIdx.x, gridDim.x, gsm);
+}
+
+// All modes' Gram matrices and their SVTs in one launch (unsharded solves):
+// CTAs [base_n, base_n + nkc_g) form mode n's partials; the last of them to
+// finish (atomic ticket) sums the partials in index order (deterministic) and
+// runs the SVT of mode n in the same CTA.  Replaces k_gram_mma + k_gram_reduce
+// per mode and k_svt (7 launches at order 3).
+template <int RP>
+__global__ void __launch_bounds__(GM_THREADS) k_gram_svt(const ModePack* __restrict__ mp, Ctl* ctl, int* tickets) {
+  if (ctl->done) return;
+  extern __shared__ double gsm[];
+  __shared__ int last;
+  int n = 0, base = 0;
+  while (n + 1 < mp->order && (int)blockIdx.x >= base + mp->m[n].nkc_g) base += mp->m[n++].nkc_g;
+  const ModeDev& m = mp->m[n];
+  gram_partial<RP>(m, blockIdx.x - base, m.nkc_g, gsm);
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(&tickets[n], 1) == m.nkc_g - 1;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  if (threadIdx.x == 0) tickets[n] = 0;  // ready for the next replay
+  const int RR = m.R * m.R;
+  for (int idx = threadIdx.x; idx < RR; idx += blockDim.x) {
+    double a = 0.0;
+    for (int kc = 0; kc < m.nkc_g; ++kc) a += __ldcg(m.Gpart + (int64_t)kc * RR + idx);
+    m.Gram[idx] = a;
+  }
+  __syncthreads();
+  svt_mode(m, n, ctl, gsm);
+}
+
+template <int RP>
+void launch_gram_svt_rp(const ModePack* mp, Ctl* ctl, int* tickets, int grid, size_t smem, cudaStream_t st) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_gram_svt<RP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = true;
+  }
+  k_gram_svt<RP><<<grid, GM_THREADS, smem, st>>>(mp, ctl, tickets);
+}
+
+// smem of k_gram_svt<rp>: the larger of the chunk ring and the SVT workspace
+inline size_t gram_svt_smem(int rp, int maxR) {
+  const size_t ring = sizeof(double) * 2 * GM_KC * ((rp + 15) / 16 * 16 + 4);
+  const size_t ws = small_ws_bytes(maxR);
+  return ring > ws ? ring : ws;
+}
+
+inline void launch_gram_svt(int rp, const ModePack* mp, Ctl* ctl, int* tickets, int grid, size_t smem,
+                            cudaStream_t st) {
+  switch (rp) {
+    case 8: launch_gram_svt_rp<8>(mp, ctl, tickets, grid, smem, st); break;
+    case 16: launch_gram_svt_rp<16>(mp, ctl, tickets, grid, smem, st); break;
+    case 24: launch_gram_svt_rp<24>(mp, ctl, tickets, grid, smem, st); break;
+    case 32: launch_gram_svt_rp<32>(mp, ctl, tickets, grid, smem, st); break;
+    case 40: launch_gram_svt_rp<40>(mp, ctl, tickets, grid, smem, st); break;
+    case 48: launch_gram_svt_rp<48>(mp, ctl, tickets, grid, smem, st); break;
+    case 56: launch_gram_svt_rp<56>(mp, ctl, tickets, grid, smem, st); break;
+    default: launch_gram_svt_rp<64>(mp, ctl, tickets, grid, smem, st); break;
   }
 }
 

@@ -254,11 +254,10 @@ __device__ void cta_mul_nn(const double* X, int64_t I, int R, const double* B, i
 
 // ---------------------------------------------------------------------------
 // SVT factor: M_n = P diag(f) P^T, f_i = (sigma_i - tau)/sigma_i for sigma_i > tau.
-__global__ void __launch_bounds__(kSmallThreads) k_svt(const ModePack* __restrict__ mp, Ctl* ctl) {
-  if (ctl->done) return;
-  extern __shared__ double smem[];
-  const int n = blockIdx.x;
-  const ModeDev& m = mp->m[n];
+// SVT of mode n from its reduced Gram (one CTA): writes sig, M, P, UM and the
+// keep / vnorm2 / nuclear scalars.  Used by k_svt and by the last CTA of each
+// mode in k_gram_svt (pasd_gram.cuh).
+__device__ void svt_mode(const ModeDev& m, int n, Ctl* ctl, double* smem) {
   const int R = m.R, tid = threadIdx.x, nt = blockDim.x;
   SmallWs ws = make_ws(R, smem);
   const int ld = ws.ld;
@@ -312,6 +311,12 @@ __global__ void __launch_bounds__(kSmallThreads) k_svt(const ModePack* __restric
   __syncthreads();
   // UM = U * M
   cta_mul_nn(m.U, m.Ifull, R, ws.S, ld, R, m.UM);
+}
+
+__global__ void __launch_bounds__(kSmallThreads) k_svt(const ModePack* __restrict__ mp, Ctl* ctl) {
+  if (ctl->done) return;
+  extern __shared__ double smem[];
+  svt_mode(mp->m[blockIdx.x], blockIdx.x, ctl, smem);
 }
 
 // ---------------------------------------------------------------------------

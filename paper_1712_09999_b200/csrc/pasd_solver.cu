@@ -166,6 +166,10 @@ struct pasd_solver {
   int nblk_update = 0;
   int sms = 148;
   size_t small_smem = 0;
+  // fused Gram + SVT launch (unsharded)
+  int* d_tickets = nullptr;
+  int gram_rp = 0, gram_grid = 0;
+  size_t gram_smem = 0;
   // fused order-3 pass 2 (pasd_pass2.cuh)
   bool fused = false;
   bool use_m8 = false;
@@ -241,27 +245,33 @@ void launch_iteration_marked(pasd_solver* s, cudaStream_t st, Mark&& mark) {
     const ModeDev& m3 = s->modes[N - 1];
     NK(ncclAllReduce(s->A3_partial, m3.A, (size_t)m3.J * m3.R, ncclDouble, ncclSum, s->comm, st));
   }
-  for (int n = 0; n < N; ++n) {
-    const ModeDev& m = s->modes[n];
+  if (!s->sharded) {
+    // all Gram matrices and SVTs in one launch (pasd_gram.cuh k_gram_svt)
     mark(PASD_K_GRAM, true);
-    launch_gram_mma(m, s->d_ctl, st);
-    const bool part = s->sharded && n < N - 1;  // Gram_1, Gram_2 are partial over the slab
-    k_gram_reduce<<<8, 256, 0, st>>>(m, part ? s->gram_partial[n] : m.Gram, s->d_ctl);
+    launch_gram_svt(s->gram_rp, s->d_pack, s->d_ctl, s->d_tickets, s->gram_grid, s->gram_smem, st);
     mark(PASD_K_GRAM, false);
-    launches += 2;
-  }
-  if (s->sharded) {
+    ++launches;
+  } else {
+    for (int n = 0; n < N; ++n) {
+      const ModeDev& m = s->modes[n];
+      mark(PASD_K_GRAM, true);
+      launch_gram_mma(m, s->d_ctl, st);
+      const bool part = n < N - 1;  // Gram_1, Gram_2 are partial over the slab
+      k_gram_reduce<<<8, 256, 0, st>>>(m, part ? s->gram_partial[n] : m.Gram, s->d_ctl);
+      mark(PASD_K_GRAM, false);
+      launches += 2;
+    }
     NK(ncclGroupStart());
     for (int n = 0; n < N - 1; ++n) {
       const ModeDev& m = s->modes[n];
       NK(ncclAllReduce(s->gram_partial[n], m.Gram, (size_t)m.R * m.R, ncclDouble, ncclSum, s->comm, st));
     }
     NK(ncclGroupEnd());
+    mark(PASD_K_SVT, true);
+    k_svt<<<N, kSmallThreads, s->small_smem, st>>>(s->d_pack, s->d_ctl);
+    mark(PASD_K_SVT, false);
+    ++launches;
   }
-  mark(PASD_K_SVT, true);
-  k_svt<<<N, kSmallThreads, s->small_smem, st>>>(s->d_pack, s->d_ctl);
-  mark(PASD_K_SVT, false);
-  ++launches;
   if (s->fused) {
     mark(PASD_K_UPDATE, true);
     if (s->use_m8)
@@ -541,6 +551,12 @@ pasd_solver* create_solver(const pasd_options* o, const pasd_shard* shard) {
   s->d_resid_part = s->alloc<double>((size_t)s->nblk_update * PASD_MAX_ORDER);
   s->d_bad_part = s->alloc<int>(s->nblk_update);
   s->small_smem = small_ws_bytes(maxR);
+  s->d_tickets = s->alloc<int>(PASD_MAX_ORDER);
+  CK(cudaMemset(s->d_tickets, 0, sizeof(int) * PASD_MAX_ORDER));
+  s->gram_rp = (maxR + 7) / 8 * 8;
+  s->gram_grid = 0;
+  for (const ModeDev& m : s->modes) s->gram_grid += m.nkc_g;
+  s->gram_smem = gram_svt_smem(s->gram_rp, maxR);
   CK(cudaFuncSetAttribute(k_svt, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->small_smem));
   CK(cudaFuncSetAttribute(k_polar, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->small_smem));
   if (s->N == 3) {
