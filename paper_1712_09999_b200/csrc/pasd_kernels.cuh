@@ -191,13 +191,19 @@ __global__ void __launch_bounds__(kThreads) k_gram(ModeDev m, const Ctl* ctl) {
 }
 
 // Gram_n = sum of the chunk partials in fixed order -> out (R x R).
+// Sum of the per-CTA Gram partials: one warp per entry, lanes take partials
+// l, l+32, ..., then a fixed xor-shuffle tree -- the same order as the fused
+// k_gram_reduce_all, so sharded and unsharded solves agree bit for bit.
 __global__ void k_gram_reduce(ModeDev m, double* __restrict__ out, const Ctl* ctl) {
   if (ctl->done) return;
-  const int RR = m.R * m.R;
-  for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < RR; idx += gridDim.x * blockDim.x) {
+  const int RR = m.R * m.R, lane = threadIdx.x & 31;
+  const int wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+  for (int idx = wid; idx < RR; idx += nw) {
     double a = 0.0;
-    for (int kc = 0; kc < m.nkc_g; ++kc) a += m.Gpart[(int64_t)kc * RR + idx];
-    out[idx] = a;
+    for (int kc = lane; kc < m.nkc_g; kc += 32) a += m.Gpart[(int64_t)kc * RR + idx];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+    if (lane == 0) out[idx] = a;
   }
 }
 

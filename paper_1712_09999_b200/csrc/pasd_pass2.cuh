@@ -675,13 +675,18 @@ inline void pass2_launch(int rp, const Pass2Args& a, const Ctl* ctl, int grid, c
 
 // Reduce the pass-2 partials into Wt_n (I_n x R_n, column-major) and
 // ctl->gnorm2[n], in a fixed order.  grid = (ceil(max I_n R_n / 256), 3).
+// Wt_n = sum of the pass-2 partials, one warp per output entry: lane l sums
+// partials l, l+32, ... in order, then a fixed xor-shuffle tree (deterministic;
+// a per-thread serial sum was load-latency bound at small sizes).
 __global__ void k_pass2_reduce(const Pass2Args a, int nblk, Ctl* ctl, double* g2out) {
   if (ctl->done) return;
   const int n = blockIdx.y;
   const ModeDev& m = a.m[n];
-  const int R = m.R;
+  const int R = m.R, lane = threadIdx.x & 31;
   const int64_t IR = m.Ifull * R;  // full rows; rows outside this rank's slab are 0
-  for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < IR; idx += (int64_t)gridDim.x * blockDim.x) {
+  const int64_t wid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t idx = wid; idx < IR; idx += nw) {
     const int64_t ifull = idx % m.Ifull;
     const int r = (int)(idx / m.Ifull);
     const int64_t i = ifull - m.ioff;
@@ -689,20 +694,24 @@ __global__ void k_pass2_reduce(const Pass2Args a, int nblk, Ctl* ctl, double* g2
     if (i >= 0 && i < m.I) {
       if (n == 0) {
         const int ib = (int)(i / a.b1), l = (int)(i % a.b1);
-        for (int b3 = 0; b3 < a.n3b; ++b3) s += a.W1p[((int64_t)(ib + a.n1b * b3) * a.b1 + l) * R + r];
+        for (int b3 = lane; b3 < a.n3b; b3 += 32) s += a.W1p[((int64_t)(ib + a.n1b * b3) * a.b1 + l) * R + r];
       } else if (n == 1) {
-        for (int c = 0; c < nblk; ++c) s += a.W2part[((int64_t)c * m.I + i) * R + r];
+        for (int c = lane; c < nblk; c += 32) s += a.W2part[((int64_t)c * m.I + i) * R + r];
       } else {
         const int ib = (int)(i / P2_B3), l = (int)(i % P2_B3);
-        for (int b1 = 0; b1 < a.n1b; ++b1) s += a.W3p[((int64_t)(b1 + a.n1b * ib) * 8 + l) * R + r];
+        for (int b1 = lane; b1 < a.n1b; b1 += 32) s += a.W3p[((int64_t)(b1 + a.n1b * ib) * 8 + l) * R + r];
       }
     }
-    m.Wt[idx] = s;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) m.Wt[idx] = s;
   }
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
+  if (blockIdx.x == 0 && threadIdx.x < 32) {
     double s = 0.0;
-    for (int c = 0; c < nblk; ++c) s += a.gpart[c * 3 + n];
-    g2out[n] = s;
+    for (int c = lane; c < nblk; c += 32) s += a.gpart[c * 3 + n];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) g2out[n] = s;
   }
 }
 

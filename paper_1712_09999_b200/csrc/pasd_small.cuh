@@ -255,8 +255,7 @@ __device__ void cta_mul_nn(const double* X, int64_t I, int R, const double* B, i
 // ---------------------------------------------------------------------------
 // SVT factor: M_n = P diag(f) P^T, f_i = (sigma_i - tau)/sigma_i for sigma_i > tau.
 // SVT of mode n from its reduced Gram (one CTA): writes sig, M, P, UM and the
-// keep / vnorm2 / nuclear scalars.  Used by k_svt and by the last CTA of each
-// mode in k_gram_svt (pasd_gram.cuh).
+// keep / vnorm2 / nuclear scalars.
 __device__ void svt_mode(const ModeDev& m, int n, Ctl* ctl, double* smem) {
   const int R = m.R, tid = threadIdx.x, nt = blockDim.x;
   SmallWs ws = make_ws(R, smem);

@@ -166,10 +166,8 @@ struct pasd_solver {
   int nblk_update = 0;
   int sms = 148;
   size_t small_smem = 0;
-  // fused Gram + SVT launch (unsharded)
-  int* d_tickets = nullptr;
-  int gram_rp = 0, gram_grid = 0;
-  size_t gram_smem = 0;
+  // all-modes Gram launches (unsharded)
+  int gram_rp = 0, gram_grid = 0, gram_red_grid = 0;
   // fused order-3 pass 2 (pasd_pass2.cuh)
   bool fused = false;
   bool use_m8 = false;
@@ -246,11 +244,15 @@ void launch_iteration_marked(pasd_solver* s, cudaStream_t st, Mark&& mark) {
     NK(ncclAllReduce(s->A3_partial, m3.A, (size_t)m3.J * m3.R, ncclDouble, ncclSum, s->comm, st));
   }
   if (!s->sharded) {
-    // all Gram matrices and SVTs in one launch (pasd_gram.cuh k_gram_svt)
+    // all modes' Gram partials, then all reductions (pasd_gram.cuh), then the SVTs
     mark(PASD_K_GRAM, true);
-    launch_gram_svt(s->gram_rp, s->d_pack, s->d_ctl, s->d_tickets, s->gram_grid, s->gram_smem, st);
+    launch_gram_all(s->gram_rp, s->d_pack, s->d_ctl, s->gram_grid, st);
+    k_gram_reduce_all<<<s->gram_red_grid, 256, 0, st>>>(s->d_pack, s->d_ctl);
     mark(PASD_K_GRAM, false);
-    ++launches;
+    mark(PASD_K_SVT, true);
+    k_svt<<<N, kSmallThreads, s->small_smem, st>>>(s->d_pack, s->d_ctl);
+    mark(PASD_K_SVT, false);
+    launches += 3;
   } else {
     for (int n = 0; n < N; ++n) {
       const ModeDev& m = s->modes[n];
@@ -283,7 +285,7 @@ void launch_iteration_marked(pasd_solver* s, cudaStream_t st, Mark&& mark) {
     int64_t maxir = 1;
     for (const ModeDev& m : s->modes) maxir = std::max<int64_t>(maxir, m.Ifull * m.R);
     mark(PASD_K_CONTRACT_W, true);
-    k_pass2_reduce<<<dim3((unsigned)((maxir + 255) / 256), 3), 256, 0, st>>>(
+    k_pass2_reduce<<<dim3((unsigned)std::min<int64_t>((maxir + 7) / 8, 8 * s->sms), 3), 256, 0, st>>>(
         s->p2, s->p2_grid, s->d_ctl, s->sharded ? s->g2_partial : ctl_gnorm2(s));
     mark(PASD_K_CONTRACT_W, false);
     ++launches;
@@ -551,12 +553,14 @@ pasd_solver* create_solver(const pasd_options* o, const pasd_shard* shard) {
   s->d_resid_part = s->alloc<double>((size_t)s->nblk_update * PASD_MAX_ORDER);
   s->d_bad_part = s->alloc<int>(s->nblk_update);
   s->small_smem = small_ws_bytes(maxR);
-  s->d_tickets = s->alloc<int>(PASD_MAX_ORDER);
-  CK(cudaMemset(s->d_tickets, 0, sizeof(int) * PASD_MAX_ORDER));
   s->gram_rp = (maxR + 7) / 8 * 8;
   s->gram_grid = 0;
-  for (const ModeDev& m : s->modes) s->gram_grid += m.nkc_g;
-  s->gram_smem = gram_svt_smem(s->gram_rp, maxR);
+  int64_t gram_entries = 0;
+  for (const ModeDev& m : s->modes) {
+    s->gram_grid += m.nkc_g;
+    gram_entries += (int64_t)m.R * m.R;
+  }
+  s->gram_red_grid = (int)std::min<int64_t>((gram_entries + 7) / 8, 8 * s->sms);  // one warp per entry
   CK(cudaFuncSetAttribute(k_svt, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->small_smem));
   CK(cudaFuncSetAttribute(k_polar, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->small_smem));
   if (s->N == 3) {
