@@ -1,0 +1,20 @@
+#!/bin/bash
+# Round evidence on a B200 (run under gpurun from the repo root):
+#   tools/refresh_profiles.sh r01
+# Writes gpurun_out/prof/<round>_*: bench lines for C1-C5 and the reference arm,
+# the ncu launch list of a short C5 run and one `ncu --set full` capture of an
+# iteration's kernels.  Copy the ones to keep into profiles/.
+set -u
+R=${1:-r01}
+O=gpurun_out/prof
+mkdir -p $O
+python bench.py --steps 20 --warmup 3 > $O/${R}_bench_c5.json 2> $O/${R}_bench_c5.err
+python bench.py --impl reference --steps 3 --warmup 3 > $O/${R}_bench_reference_c5.json 2> $O/${R}_bench_reference_c5.err
+for c in c1 c2 c3 c4; do
+  python bench.py --config $c --steps 20 --warmup 3 > $O/${R}_bench_$c.json 2> $O/${R}_bench_$c.err
+done
+ncu --metrics gpu__time_duration.sum --clock-control none -k regex:'^k_' -c 60 --csv \
+  --log-file $O/${R}_launches_c5.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e > $O/ncu_launch.log 2>&1
+ncu --set full --import-source on --clock-control none -k regex:'^k_' --launch-skip 20 --launch-count 11 \
+  -o $O/${R}_c5_full python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e > $O/ncu_full.log 2>&1
+ls -la $O
