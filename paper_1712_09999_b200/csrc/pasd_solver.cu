@@ -576,7 +576,7 @@ pasd_solver* create_solver(const pasd_options* o, const pasd_shard* shard) {
     a.E1 = s->E[1];
     a.D = s->D;
     s->p2_rp = pass2_rp(s->modes[0].R, s->modes[1].R, s->modes[2].R);
-    s->use_m8 = m8_supported(s->p2_rp) && std::getenv("PASD_PASS2_M16") == nullptr;
+    s->use_m8 = (m8_supported(s->p2_rp) && std::getenv("PASD_PASS2_M16") == nullptr) || std::getenv("PASD_PASS2_M8") != nullptr;
     a.b1 = s->use_m8 ? M8_B : P2_B1;
     a.n1b = (int)((s->dims[0] + a.b1 - 1) / a.b1);
     a.n3b = (int)((s->dims[2] + P2_B3 - 1) / P2_B3);
