@@ -295,11 +295,14 @@ __global__ void k_resid_local(const Ctl* ctl, const double* __restrict__ resid_p
 }
 
 // `reduced` (optional): residual maxima + NaN flag already reduced across ranks.
-__global__ void k_finish(Ctl* ctl, const double* __restrict__ resid_part, const int* __restrict__ bad_part,
-                         int nblocks, double* history, const double* __restrict__ reduced) {
-  if (ctl->done) return;
-  __shared__ double red[32];
-  __shared__ int redi[32];
+// Body of k_finish; also run by the last CTA of the fused pass 2 (unsharded),
+// so partials written by other CTAs are read through L2 (__ldcg).
+// `red`: 64 doubles of shared scratch (the fused pass 2 passes its dynamic
+// buffer: static shared arrays would grow its footprint past the 196 KB
+// carve-out, measured 5 ms slower at C5).
+__device__ void finish_body(Ctl* ctl, const double* __restrict__ resid_part, const int* __restrict__ bad_part,
+                            int nblocks, double* history, const double* __restrict__ reduced, double* red) {
+  int* redi = reinterpret_cast<int*>(red + 32);
   const int N = ctl->order;
   double resid[PASD_MAX_ORDER];
   int bad = 0;
@@ -310,12 +313,12 @@ __global__ void k_finish(Ctl* ctl, const double* __restrict__ resid_part, const 
     for (int n = 0; n < N; ++n) {
       double w = 0.0;
       for (int b = threadIdx.x; b < nblocks; b += blockDim.x) {
-        const double v = resid_part[(int64_t)b * PASD_MAX_ORDER + n];
+        const double v = __ldcg(resid_part + (int64_t)b * PASD_MAX_ORDER + n);
         if (v > w) w = v;
       }
       resid[n] = block_reduce(w, MaxOp(), red);
     }
-    for (int b = threadIdx.x; b < nblocks; b += blockDim.x) bad |= bad_part[b];
+    for (int b = threadIdx.x; b < nblocks; b += blockDim.x) bad |= __ldcg(bad_part + b);
     bad = block_reduce(bad, OrOp(), redi);
   }
   if (threadIdx.x == 0) {
@@ -341,6 +344,27 @@ __global__ void k_finish(Ctl* ctl, const double* __restrict__ resid_part, const 
     if (bad) ctl->nan_flag = 1;
     if (bad || conv || iter >= ctl->maxiter) ctl->done = 1;
   }
+}
+
+__global__ void k_finish(Ctl* ctl, const double* __restrict__ resid_part, const int* __restrict__ bad_part,
+                         int nblocks, double* history, const double* __restrict__ reduced) {
+  if (ctl->done) return;
+  __shared__ double red[64];
+  finish_body(ctl, resid_part, bad_part, nblocks, history, reduced, red);
+}
+
+// Last-CTA ticket: returns true in exactly one CTA of the grid, after every
+// CTA's prior global writes are visible to it; resets the ticket for replay.
+// `flag`: one int of shared scratch.
+__device__ __forceinline__ bool last_cta(int* ticket, int* flag) {
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) *flag = atomicAdd(ticket, 1) == (int)(gridDim.x * gridDim.y * gridDim.z) - 1;
+  __syncthreads();
+  if (!*flag) return false;
+  __threadfence();
+  if (threadIdx.x == 0) *ticket = 0;
+  return true;
 }
 
 // ---------------------------------------------------------------------------

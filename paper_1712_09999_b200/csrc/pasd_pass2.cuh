@@ -49,6 +49,10 @@ struct Pass2Args {
   int* bad_part;       // [grid]
   int n1b, n3b, npencils;
   int b1;  // i1 extent of a pencil (16 for k_pass2_fused, 8 for k_pass2_m8)
+  // unsharded solves: the last CTA runs the iteration's finish (mu schedule,
+  // history, stop rule) -- one launch fewer per iteration
+  int* finish_ticket;  // nullptr: k_finish runs separately
+  double* history;
 };
 
 __host__ __device__ inline int round_up(int x, int m) { return (x + m - 1) / m * m; }
@@ -620,6 +624,9 @@ __global__ void __launch_bounds__(P2_THREADS, 1) k_pass2_fused(const Pass2Args a
   int* redi = reinterpret_cast<int*>(red + 32);
   const int b = block_reduce(bad, OrOp(), redi);
   if (tid == 0) a.bad_part[blockIdx.x] = b;
+  __syncthreads();  // the block reductions above are done with `red`
+  if (a.finish_ticket && last_cta(a.finish_ticket, reinterpret_cast<int*>(red + 48)))
+    finish_body(const_cast<Ctl*>(ctl), a.resid_part, a.bad_part, gridDim.x, a.history, nullptr, red);
 }
 
 template <int RP>

@@ -385,6 +385,9 @@ __global__ void __launch_bounds__(M8_THREADS, 2) k_pass2_m8(const Pass2Args a, c
   int* redi = reinterpret_cast<int*>(red + 32);
   const int b = block_reduce(bad, OrOp(), redi);
   if (tid == 0) a.bad_part[blockIdx.x] = b;
+  __syncthreads();  // the block reductions above are done with `red`
+  if (a.finish_ticket && last_cta(a.finish_ticket, reinterpret_cast<int*>(red + 48)))
+    finish_body(const_cast<Ctl*>(ctl), a.resid_part, a.bad_part, gridDim.x, a.history, nullptr, red);
 }
 
 template <int RP>

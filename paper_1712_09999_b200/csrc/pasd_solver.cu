@@ -301,11 +301,12 @@ void launch_iteration_marked(pasd_solver* s, cudaStream_t st, Mark&& mark) {
       NK(ncclAllReduce(s->red_local, s->red, (size_t)N + 1, ncclDouble, ncclMax, s->comm, st));
       NK(ncclGroupEnd());
     }
-    mark(PASD_K_FINISH, true);
-    k_finish<<<1, kThreads, 0, st>>>(s->d_ctl, s->p2_resid, s->p2_bad, s->p2_grid, s->d_hist,
-                                     s->sharded ? s->red : nullptr);
-    mark(PASD_K_FINISH, false);
-    ++launches;
+    if (s->sharded) {
+      mark(PASD_K_FINISH, true);
+      k_finish<<<1, kThreads, 0, st>>>(s->d_ctl, s->p2_resid, s->p2_bad, s->p2_grid, s->d_hist, s->red);
+      mark(PASD_K_FINISH, false);
+      ++launches;
+    }
   } else {
     mark(PASD_K_UPDATE, true);
     k_update<<<s->nblk_update, kThreads, 0, st>>>(s->d_pack, s->T, s->E[0], s->E[1], s->D, s->d_resid_part,
@@ -591,6 +592,11 @@ pasd_solver* create_solver(const pasd_options* o, const pasd_shard* shard) {
     s->p2_bad = s->alloc<int>(s->p2_grid);
     a.resid_part = s->p2_resid;
     a.bad_part = s->p2_bad;
+    a.history = s->d_hist;
+    if (!s->sharded) {  // the last pass-2 CTA runs the finish (sharded: after the NCCL max-reduce)
+      a.finish_ticket = s->alloc<int>(1);
+      CK(cudaMemset(a.finish_ticket, 0, sizeof(int)));
+    }
     if (s->use_m8)
       m8_setup(s->p2_rp);
     else
