@@ -111,33 +111,50 @@ __device__ void cta_jacobi_eig(SmallWs& ws, int n) {
         ws.pq[2 * j + 1] = q;
       }
       __syncthreads();
-      for (int idx = tid; idx < npairs * Rp; idx += nt) {  // rows p, q
-        const int j = idx / Rp, k = idx % Rp;
-        const double s = ws.sn[j];
-        if (s == 0.0) continue;
-        const int p = ws.pq[2 * j], q = ws.pq[2 * j + 1];
-        const double c = ws.cs[j];
-        const double a = S[p * ld + k], b = S[q * ld + k];
-        S[p * ld + k] = c * a - s * b;
-        S[q * ld + k] = s * a + c * b;
+      // Apply the round's disjoint rotations: S <- J^T S J block by block (the
+      // 2 x 2 block of pairs (ja, jb) depends only on itself; rows first, then
+      // columns, the same operation order as separate row and column passes)
+      // and V <- V J.  One barrier per round instead of two.
+      for (int bidx = tid; bidx < npairs * npairs; bidx += nt) {
+        const int ja = bidx / npairs, jb = bidx - ja * npairs;
+        const double sa = ws.sn[ja], sb = ws.sn[jb];
+        if (sa == 0.0 && sb == 0.0) continue;
+        const double ca = ws.cs[ja], cb = ws.cs[jb];
+        const int pa = ws.pq[2 * ja], qa = ws.pq[2 * ja + 1], pb = ws.pq[2 * jb], qb = ws.pq[2 * jb + 1];
+        double a00 = S[pa * ld + pb], a01 = S[pa * ld + qb], a10 = S[qa * ld + pb], a11 = S[qa * ld + qb];
+        if (sa != 0.0) {  // rows pa, qa
+          const double r00 = ca * a00 - sa * a10, r10 = sa * a00 + ca * a10;
+          const double r01 = ca * a01 - sa * a11, r11 = sa * a01 + ca * a11;
+          a00 = r00; a10 = r10; a01 = r01; a11 = r11;
+        }
+        if (sb != 0.0) {  // columns pb, qb
+          const double c00 = cb * a00 - sb * a01, c01 = sb * a00 + cb * a01;
+          const double c10 = cb * a10 - sb * a11, c11 = sb * a10 + cb * a11;
+          a00 = c00; a01 = c01; a10 = c10; a11 = c11;
+        }
+        S[pa * ld + pb] = a00;
+        S[pa * ld + qb] = a01;
+        S[qa * ld + pb] = a10;
+        S[qa * ld + qb] = a11;
       }
-      __syncthreads();
-      for (int idx = tid; idx < npairs * Rp; idx += nt) {  // columns p, q of S and V
-        const int j = idx / Rp, k = idx % Rp;
+      for (int idx = tid; idx < npairs * Rp; idx += nt) {  // columns p, q of V
+        const int j = idx / Rp, k = idx - j * Rp;
         const double s = ws.sn[j];
         if (s == 0.0) continue;
         const int p = ws.pq[2 * j], q = ws.pq[2 * j + 1];
         const double c = ws.cs[j];
-        const double a = S[k * ld + p], b = S[k * ld + q];
-        S[k * ld + p] = c * a - s * b;
-        S[k * ld + q] = s * a + c * b;
         const double va = V[k * ld + p], vb = V[k * ld + q];
         V[k * ld + p] = c * va - s * vb;
         V[k * ld + q] = s * va + c * vb;
       }
       __syncthreads();
     }
-    if (rotated == 0) break;
+    if (rotated == 0) {
+#ifdef PASD_DEBUG_SWEEPS
+      if (tid == 0) printf("jacobi n=%d block=%d sweeps=%d\n", n, blockIdx.x, sweep + 1);
+#endif
+      break;
+    }
     __syncthreads();
   }
   // sort descending (stable on index): perm[rank] = j
@@ -240,16 +257,39 @@ __device__ void cta_gram_tn(const double* X, const double* Y, int64_t I, int R, 
 }
 
 // out(I x R2, global col-major) = X (I x R, global col-major) * B (R x R2, smem row-major ld)
-__device__ void cta_mul_nn(const double* X, int64_t I, int R, const double* B, int ld, int R2, double* out) {
-  const int64_t total = I * R2;
-  for (int64_t idx = threadIdx.x; idx < total; idx += blockDim.x) {
-    const int64_t i = idx % I;
-    const int s = (int)(idx / I);
-    double a = 0.0;
-    for (int r = 0; r < R; ++r) a = fma(X[i + I * r], B[r * ld + s], a);
-    out[i + I * s] = a;
+// out (I x R2, col-major) = X (I x R, col-major) B (R x R2, smem row-major, ld).
+// 64-row chunks of X are staged in shared memory with coalesced loads; each
+// thread then forms one output column entry for 4 rows (B value reused).
+// The sum over r runs in index order from 0 (same result as the unstaged
+// loop).  `stage`: 64 x ld doubles.
+__device__ void cta_mul_nn(const double* X, int64_t I, int R, const double* B, int ld, int R2, double* out,
+                           double* stage) {
+  const int tid = threadIdx.x, nt = blockDim.x;
+  for (int64_t i0 = 0; i0 < I; i0 += 64) {
+    const int ic = (int)imin64(64, I - i0);
+    for (int idx = tid; idx < 64 * R; idx += nt) {
+      const int il = idx & 63, r = idx >> 6;
+      stage[il * ld + r] = il < ic ? X[i0 + il + I * r] : 0.0;
+    }
+    __syncthreads();
+    for (int idx = tid; idx < 16 * R2; idx += nt) {
+      const int q = idx & 15, c = idx >> 4;
+      double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+      for (int r = 0; r < R; ++r) {
+        const double b = B[r * ld + c];
+        a0 = fma(stage[q * ld + r], b, a0);
+        a1 = fma(stage[(q + 16) * ld + r], b, a1);
+        a2 = fma(stage[(q + 32) * ld + r], b, a2);
+        a3 = fma(stage[(q + 48) * ld + r], b, a3);
+      }
+      double* o = out + i0 + I * c;
+      if (q < ic) o[q] = a0;
+      if (q + 16 < ic) o[q + 16] = a1;
+      if (q + 32 < ic) o[q + 32] = a2;
+      if (q + 48 < ic) o[q + 48] = a3;
+    }
+    __syncthreads();
   }
-  __syncthreads();
 }
 
 // ---------------------------------------------------------------------------
@@ -309,7 +349,7 @@ __device__ void svt_mode(const ModeDev& m, int n, Ctl* ctl, double* smem) {
   }
   __syncthreads();
   // UM = U * M
-  cta_mul_nn(m.U, m.Ifull, R, ws.S, ld, R, m.UM);
+  cta_mul_nn(m.U, m.Ifull, R, ws.S, ld, R, m.UM, ws.T64);
 }
 
 __global__ void __launch_bounds__(kSmallThreads) k_svt(const ModePack* __restrict__ mp, Ctl* ctl) {
@@ -336,7 +376,7 @@ __global__ void __launch_bounds__(kSmallThreads) k_polar(const ModePack* __restr
   // 2. W = Wt M  (M in S)
   for (int idx = tid; idx < R * R; idx += nt) ws.S[(idx / R) * ld + idx % R] = m.M[(idx / R) + R * (idx % R)];
   __syncthreads();
-  cta_mul_nn(Wt, I, R, ws.S, ld, R, X);
+  cta_mul_nn(Wt, I, R, ws.S, ld, R, X, ws.T64);
   double w2 = 0.0;
   for (int64_t idx = tid; idx < IR; idx += nt) w2 += X[idx] * X[idx];
   w2 = block_reduce(w2, AddOp(), ws.red);
@@ -353,7 +393,7 @@ __global__ void __launch_bounds__(kSmallThreads) k_polar(const ModePack* __restr
   cta_warm_finish(ws, R);
   for (int idx = tid; idx < R * R; idx += nt) ws.Q[(idx / R) * ld + idx % R] = ws.V[(idx / R) * ld + idx % R];
   __syncthreads();
-  cta_mul_nn(X, I, R, ws.Q, ld, R, X2);
+  cta_mul_nn(X, I, R, ws.Q, ld, R, X2, ws.T64);
 #ifdef PASD_DEBUG_POLAR
   if (tid == 0) {
     printf("lam1:"); for (int j = 0; j < R; ++j) printf(" %g", ws.lam[j]); printf("\n");
@@ -366,7 +406,7 @@ __global__ void __launch_bounds__(kSmallThreads) k_polar(const ModePack* __restr
   // 4. second pass on the rotated columns: C2 = X2^T X2 = Q2 L2 Q2^T ; X = X2 Q2 ; Q = Q1 Q2
   cta_gram_tn(X2, X2, I, R, R, ws.S, ld, ws.T64);
   cta_jacobi_eig(ws, R);
-  cta_mul_nn(X2, I, R, ws.V, ld, R, X);
+  cta_mul_nn(X2, I, R, ws.V, ld, R, X, ws.T64);
   for (int idx = tid; idx < R * R; idx += nt) {
     const int r = idx / R, s = idx % R;
     double a = 0.0;
@@ -476,7 +516,7 @@ __global__ void __launch_bounds__(kSmallThreads) k_polar(const ModePack* __restr
     m.Qp[r + R * s] = ws.Q[r * ld + s];
   }
   __syncthreads();
-  cta_mul_nn(X, I, R, ws.S, ld, R, m.U);
+  cta_mul_nn(X, I, R, ws.S, ld, R, m.U, ws.T64);
 }
 
 }  // namespace pasd
