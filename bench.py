@@ -382,7 +382,7 @@ def main():
         "steps": K, "warmup": W, "ms_per_step": round(ms / K, 4), "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": w.name, "dims": list(w.dims), "ranks": list(w.ranks), "rho": w.rho,
-                   "noise": list(w.noise), "iters_fixed": True, "l2": "inputs larger than L2 (5 x 8 GB resident)"
+                   "noise": list(w.noise), "iters_fixed": True, "l2": "inputs larger than L2 (T, E x2, D, Y x3: 7 x 8 GB resident)"
                    if S * 8 > 126e6 else "inputs L2-resident"},
         "elem_iters_per_s": value * S,
         "gpu_launches": int(launches),
