@@ -12,11 +12,6 @@
 
 #define PASD_MAX_ORDER 8
 #define PASD_MAX_RANK 64
-// Timing experiments only (tools/, never the shipped build): 1 = no per-step
-// restaging in pass 2, 2 = no DMMAs in pass 2, 3 = no elementwise HBM traffic.
-#ifndef PASD_P2_EXP
-#define PASD_P2_EXP 0
-#endif
 
 namespace pasd {
 

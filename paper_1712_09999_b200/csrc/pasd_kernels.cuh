@@ -340,7 +340,6 @@ __device__ void finish_body(Ctl* ctl, const double* __restrict__ resid_part, con
     ctl->mu = mu_next;
     ctl->ecur ^= 1;
     ctl->converged = conv ? 1 : 0;
-    if (PASD_P2_EXP) bad = 0;  // timing experiments run on garbage
     if (bad) ctl->nan_flag = 1;
     if (bad || conv || iter >= ctl->maxiter) ctl->done = 1;
   }

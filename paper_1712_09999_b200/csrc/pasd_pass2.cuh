@@ -27,9 +27,6 @@
 
 namespace pasd {
 
-#ifndef PASD_P2_LOADPOS
-#define PASD_P2_LOADPOS 1
-#endif
 constexpr int P2_B1 = 16, P2_B2 = 8, P2_B3 = 8;
 constexpr int P2_THREADS = 256;
 constexpr int P2_BRICK = P2_B1 * P2_B2 * P2_B3;  // 1024
@@ -96,9 +93,6 @@ __host__ __device__ inline P2Smem p2_plan(int R1, int R2, int R3) {
 }
 
 __device__ __forceinline__ void dmma(double (&c)[4], double a0, double a1, double b0) {
-#if PASD_P2_EXP == 2
-  c[0] += a0 * b0; return;
-#endif
   asm volatile(
       "mma.sync.aligned.m16n8k4.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5}, {%6}, {%0,%1,%2,%3};"
       : "+d"(c[0]), "+d"(c[1]), "+d"(c[2]), "+d"(c[3])
@@ -197,17 +191,9 @@ struct P2Layout {
   static constexpr int oU3 = oU2 + 8 * LDU;
   static constexpr int oZ3 = oU3 + 8 * LDU;
   static constexpr int oG2 = oZ3 + 8 * 182;
-#if PASD_P2_EXP == 5
-  static constexpr int oG3 = oZ3;  // timing experiment only: alias (wrong results)
-  static constexpr int oRed = oG2 + 8 * 160;
-#else
   static constexpr int oG3 = oG2 + 8 * 160;
   static constexpr int oRed = oG3 + 8 * 180;
-#endif
-#ifndef PASD_P2_PAD
-#define PASD_P2_PAD 0
-#endif
-  static constexpr int total = oRed + 64 + PASD_P2_PAD;
+  static constexpr int total = oRed + 64;
   static constexpr size_t bytes = sizeof(double) * (size_t)total;
   static_assert((RM - RP) * LD3 <= total - oU1, "M-tile overrun must stay inside shared memory");
   static_assert(128 * RP <= oA3, "end-of-pencil scratch must fit below A3s");
@@ -388,29 +374,21 @@ __global__ void __launch_bounds__(P2_THREADS, 1) k_pass2_fused(const Pass2Args a
         const int64_t i1 = i1o + g + 8 * (q >> 1), i2 = i2o + 2 * t + (q & 1), i3 = i3o + w;
         inb[q] = i1 < I1 && i2 < I2 && i3 < I3;
         off[q] = i1 + I1 * i2 + S12 * i3;
-#if PASD_P2_EXP == 3
-        tv[q] = off[q] * 1e-9; for (int n = 0; n < 3; ++n) yv[n][q] = tv[q] + n;
-#else
         tv[q] = inb[q] ? T[off[q]] : 0.0;
 #pragma unroll
         for (int n = 0; n < 3; ++n) yv[n][q] = inb[q] ? a.Y[n][off[q]] : 0.0;
-#endif
       }
     };
     stage_a1(0, A1s);
     stage_a3u2(0);
     if (L::DB) asm volatile("cp.async.commit_group;" ::: "memory");
-#if PASD_P2_LOADPOS == 0
-    load_elems(0);
-#endif
 
     int sidx = 0;  // step index along the pencil (A_1 buffer parity)
     for (int64_t i2o = 0; i2o < I2; i2o += P2_B2, ++sidx) {
       const bool more = i2o + P2_B2 < I2;
       double* A1c = A1s + ((L::DB && (sidx & 1)) ? L::A1SZ : 0);
-#if PASD_P2_LOADPOS == 1
       load_elems(i2o);  // this step's T, Y: in flight while the staging lands and Z runs
-#endif
+                        // (measured 2 ms faster at C5 than prefetching them a step ahead)
       if (L::DB) {
         // next step's A_1 slice into the other buffer: a whole step to land
         if (more) stage_a1(i2o + P2_B2, A1s + ((sidx & 1) ? 0 : L::A1SZ));
@@ -471,12 +449,12 @@ __global__ void __launch_bounds__(P2_THREADS, 1) k_pass2_fused(const Pass2Args a
             const double ar = fabs(r);
             if (ar > worst[n]) worst[n] = ar;
             bad |= !isfinite(r);
-            if (PASD_P2_EXP != 3) a.Y[n][off[q]] = ynew;
+            a.Y[n][off[q]] = ynew;
           }
           gn[n] = inb[q] ? g_elem(tt, e, ynew, inv_mu_next) : 0.0;  // next G_n
           gsq[n] = fma(gn[n], gn[n], gsq[n]);
         }
-        if (inb[q] && PASD_P2_EXP != 3) {
+        if (inb[q]) {
           Enew[off[q]] = e;
           a.D[off[q]] = __dsub_rn(tt, e);  // next pass 1 reads D = T - E
         }
@@ -529,16 +507,11 @@ __global__ void __launch_bounds__(P2_THREADS, 1) k_pass2_fused(const Pass2Args a
         }
       }
       __syncthreads();  // A3s / U2s (and A1s when single-buffered) no longer needed this step
-#if PASD_P2_EXP != 1
       if (more) {
         if (!L::DB) stage_a1(i2o + P2_B2, A1s);
         stage_a3u2(i2o + P2_B2);
       }
       if (L::DB) asm volatile("cp.async.commit_group;" ::: "memory");
-#endif
-#if PASD_P2_LOADPOS == 0
-      if (more) load_elems(i2o + P2_B2);  // next step's T, Y in flight during Wt_2 and Z
-#endif
       if (W1LATE) wt1();
       // ---- W-b: Wt_2^T (m-tile mt, K-half kh), K = (i1, i3) ----
       double acc2[4] = {0, 0, 0, 0};
