@@ -23,6 +23,8 @@
 // accumulation, one partial per pencil); Wt_2 rows change per step and go to a
 // per-CTA partial.  All reductions are in a fixed order (deterministic).
 #pragma once
+#include <cuda.h>  // CUtensorMap (TMA descriptors, encoded on the host through the driver entry point)
+
 #include "pasd_kernels.cuh"
 
 namespace pasd {
@@ -50,6 +52,15 @@ struct Pass2Args {
   // history, stop rule) -- one launch fewer per iteration
   int* finish_ticket;  // nullptr: k_finish runs separately
   double* history;
+};
+
+// TMA descriptors of the element streams of k_pass2_fused<RP, true>: 3-D
+// float64 maps with a 16 x 8 x 8 box and 128-byte swizzle.  "A" maps are
+// (I1, I2, I3); the "B" map of Y_3 is (I1, I3, I2), so its brick lands in
+// shared memory as [l2][l3][l1] and the Wt_3 operand reads are conflict-free.
+struct P2Tmaps {
+  CUtensorMap t, y1, y2, y3b;  // loads
+  CUtensorMap e0, e1, d;       // stores (E double buffer: the kernel writes E[ecur ^ 1])
 };
 
 __host__ __device__ inline int round_up(int x, int m) { return (x + m - 1) / m * m; }
@@ -157,8 +168,8 @@ __device__ __forceinline__ int g2x(int l1, int l2, int l3) { return l1 + 20 * l2
 __device__ __forceinline__ int g3x(int l1, int l2, int l3) { return l1 + 22 * l2 + 180 * l3; }
 __device__ __forceinline__ bool mt_dummy_guard(int w, int MT) { return (w & 3) < MT; }
 
-// Shared-memory footprint (bytes) of k_pass2_fused<RP>.
-template <int RP>
+// Shared-memory footprint (bytes) of k_pass2_fused<RP, TIO>.
+template <int RP, bool TIO>
 struct P2Layout {
   // The Wt_2 / Wt_3 products read the A_2 / A_3 slices as 16-row M tiles
   // covering RM rows; rows >= RP of the last tile run past the slice into the
@@ -171,40 +182,81 @@ struct P2Layout {
   // (c = 2t, r = g) 2-way), so each column's R1 contiguous values of A_1
   // stage as 16-byte copies.  Other pitches keep the fragment reads
   // (rows t x cols g, rows g x cols t) on distinct banks per half-warp.
+  // (Double-buffering A_1 to stage it a whole step ahead measured slower:
+  // 49.7 vs 43.2 ms per C5 launch.)
   static constexpr int LD1 = RP + 4, LD2 = 128 + 4, LD3 = 128 + 4, LDU = RP + 4;
-  static constexpr int A1SZ = 64 * LD1;
-  static constexpr int REST = RP * LD2 + RP * LD3 + 32 * LDU + 8 * 182 + 8 * 160 + 8 * 180 + 64;
-  // A_1 slice double-buffered (staged a whole step ahead) when it fits in 227 KB
-// Double-buffering A_1 (staged a whole step ahead) measured slower on B200:
-// 49.7 vs 43.2 ms per C5 launch.  Pass-2 time grows with the CTA's shared
-// memory footprint (an unused 8 KB pad: 43.2 -> 46.6 ms), so the single
-// buffer stays the default.
-#ifndef PASD_P2_DB
-#define PASD_P2_DB 0
-#endif
-  static constexpr bool DB = PASD_P2_DB && (2 * A1SZ + REST <= 227 * 1024 / 8);
   static constexpr int oA1 = 0;
-  static constexpr int oA2 = oA1 + (DB ? 2 : 1) * A1SZ;
+  static constexpr int oA2 = oA1 + 64 * LD1;
   static constexpr int oA3 = oA2 + RP * LD2;
   static constexpr int oU1 = oA3 + RP * LD3;
   static constexpr int oU2 = oU1 + 16 * LDU;
   static constexpr int oU3 = oU2 + 8 * LDU;
   static constexpr int oZ3 = oU3 + 8 * LDU;
+  // plain I/O: G_2 / G_3 exchange buffers.  TMA I/O (TIO): six 16 x 8 x 8
+  // bricks (T->E, Y_1, Y_2, Y_3 [B layout], D, D [B layout]) read by the
+  // Wt_2 / Wt_3 products directly (G = D + Y/mu formed in the fragment load).
   static constexpr int oG2 = oZ3 + 8 * 182;
-  static constexpr int oG3 = oG2 + 8 * 160;
-  static constexpr int oRed = oG3 + 8 * 180;
-  static constexpr int total = oRed + 64;
+  static constexpr int oG3 = oG2 + (TIO ? 0 : 8 * 160);
+  static constexpr int oRed = oG3 + (TIO ? 0 : 8 * 180);
+  static constexpr int oBrick = oRed + 64;              // + runtime 1024-byte alignment
+  static constexpr int total = oBrick + (TIO ? 6 * P2_BRICK + 128 : 0);
   static constexpr size_t bytes = sizeof(double) * (size_t)total;
   static_assert((RM - RP) * LD3 <= total - oU1, "M-tile overrun must stay inside shared memory");
-  static_assert(128 * RP <= oA3, "end-of-pencil scratch must fit below A3s");
+  static_assert(128 * RP <= oA3 + RP * LD3, "end-of-pencil scratch must fit in A1s..A3s");
 };
+
+// Element (l1, l2, l3) of a 16 x 8 x 8 brick in the TMA SWIZZLE_128B layout:
+// 128-byte rows of 16 doubles, 16-byte chunks XOR-ed with (row mod 8).
+// Layout A: row = l2 + 8 l3; layout B: row = l3 + 8 l2.
+__device__ __forceinline__ int swz_row(int l1, int row) { return row * 16 + (((l1 >> 1) ^ (row & 7)) << 1) + (l1 & 1); }
+__device__ __forceinline__ int swzA(int l1, int l2, int l3) { return swz_row(l1, l2 + 8 * l3); }
+__device__ __forceinline__ int swzB(int l1, int l2, int l3) { return swz_row(l1, l3 + 8 * l2); }
+
+__device__ __forceinline__ void tma_load3(double* dst, const CUtensorMap* map, uint64_t* mbar, int c0, int c1, int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];"
+      :
+      : "r"(static_cast<unsigned>(__cvta_generic_to_shared(dst))), "l"(reinterpret_cast<uint64_t>(map)),
+        "r"(static_cast<unsigned>(__cvta_generic_to_shared(mbar))), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+__device__ __forceinline__ void tma_store3(const CUtensorMap* map, const double* src, int c0, int c1, int c2) {
+  asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];"
+               :
+               : "l"(reinterpret_cast<uint64_t>(map)), "r"(static_cast<unsigned>(__cvta_generic_to_shared(src))),
+                 "r"(c0), "r"(c1), "r"(c2)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_init(uint64_t* mbar) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(static_cast<unsigned>(__cvta_generic_to_shared(mbar)))
+               : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect(uint64_t* mbar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
+                   static_cast<unsigned>(__cvta_generic_to_shared(mbar))),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* mbar, unsigned parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@P1 bra DONE_%=;\n\t"
+      "bra WAIT_%=;\n"
+      "DONE_%=:\n\t}" ::"r"(static_cast<unsigned>(__cvta_generic_to_shared(mbar))),
+      "r"(parity)
+      : "memory");
+}
 
 // RP = common padded rank (multiple of 8, >= every R_n); rows r >= R_n of each
 // mode's operands are zero, so padding changes no result.
-template <int RP>
-__global__ void __launch_bounds__(P2_THREADS, 1) k_pass2_fused(const Pass2Args a, const Ctl* ctl) {
+template <int RP, bool TIO>
+__global__ void __launch_bounds__(P2_THREADS, 1) k_pass2_fused(const Pass2Args a, const Ctl* ctl,
+                                                                const __grid_constant__ P2Tmaps tm) {
   if (ctl->done) return;
-  using L = P2Layout<RP>;
+  using L = P2Layout<RP, TIO>;
   constexpr int KS = RP / 4;   // k-steps of the Z products
   constexpr int NT1 = RP / 8;  // n-tiles of the Wt_1 product
   constexpr int MT = L::RM / 16;
@@ -224,6 +276,10 @@ __global__ void __launch_bounds__(P2_THREADS, 1) k_pass2_fused(const Pass2Args a
   double* G2s = sm + L::oG2;
   double* G3s = sm + L::oG3;
   double* red = sm + L::oRed;
+  // TIO bricks: [0] T -> E, [1] Y_1, [2] Y_2, [3] Y_3 (layout B), [4] D, [5] D (layout B)
+  double* brk = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(sm + L::oBrick) + 1023) & ~uintptr_t(1023));
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(red + 56);
+  unsigned mph = 0;  // mbarrier phase parity of the next element-brick load
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5, g = lane >> 2, t = lane & 3;
 
   const double* __restrict__ T = a.T;
@@ -241,7 +297,21 @@ __global__ void __launch_bounds__(P2_THREADS, 1) k_pass2_fused(const Pass2Args a
   // zero padding rows once (never overwritten by the staging copies)
   for (int idx = tid; idx < (RP - R2) * 128; idx += P2_THREADS) A2s[(R2 + idx / 128) * L::LD2 + (idx & 127)] = 0.0;
   for (int idx = tid; idx < (RP - R3) * 128; idx += P2_THREADS) A3s[(R3 + idx / 128) * L::LD3 + (idx & 127)] = 0.0;
-  for (int idx = tid; idx < L::total - L::oU1; idx += P2_THREADS) U1s[idx] = 0.0;  // UM rows, exchange buffers
+  for (int idx = tid; idx < L::oBrick - L::oU1; idx += P2_THREADS) U1s[idx] = 0.0;  // UM rows, exchange buffers
+  if (TIO && tid == 0) mbar_init(mbar);
+  __syncthreads();
+  // TIO: the next brick's T, Y_1..3 (after the previous stores have read the bricks)
+  auto load_bricks = [&](int64_t i1o_, int64_t i2o_, int64_t i3o_) {
+    if (TIO && tid == 0) {
+      asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+      mbar_expect(mbar, 4u * P2_BRICK * sizeof(double));
+      const int c0 = (int)i1o_, c1 = (int)i2o_, c2 = (int)i3o_;
+      tma_load3(brk, &tm.t, mbar, c0, c1, c2);
+      tma_load3(brk + P2_BRICK, &tm.y1, mbar, c0, c1, c2);
+      tma_load3(brk + 2 * P2_BRICK, &tm.y2, mbar, c0, c1, c2);
+      tma_load3(brk + 3 * P2_BRICK, &tm.y3b, mbar, c0, c2, c1);
+    }
+  };
 
   double worst[3] = {0.0, 0.0, 0.0};
   double gsq[3] = {0.0, 0.0, 0.0};
@@ -266,6 +336,7 @@ __global__ void __launch_bounds__(P2_THREADS, 1) k_pass2_fused(const Pass2Args a
     const int nv1 = (int)imin64(16, I1 - i1o);
     const int nbc1 = (nv1 - 2 * (tid & 7)) >= 2 ? 16 : ((nv1 - 2 * (tid & 7)) == 1 ? 8 : 0);  // A_3 chunk bytes
     __syncthreads();  // previous pencil fully done with shared memory
+    load_bricks(i1o, 0, i3o);
     // ---- pencil-resident: A_2 slice (I1, R2, I3 layout), UM_1 rows, UM_3 rows ----
     for (int l3 = 0; l3 < 8; ++l3) {
       const bool in3 = i3o + l3 < I3;
@@ -381,22 +452,13 @@ __global__ void __launch_bounds__(P2_THREADS, 1) k_pass2_fused(const Pass2Args a
     };
     stage_a1(0, A1s);
     stage_a3u2(0);
-    if (L::DB) asm volatile("cp.async.commit_group;" ::: "memory");
 
-    int sidx = 0;  // step index along the pencil (A_1 buffer parity)
-    for (int64_t i2o = 0; i2o < I2; i2o += P2_B2, ++sidx) {
+    for (int64_t i2o = 0; i2o < I2; i2o += P2_B2) {
       const bool more = i2o + P2_B2 < I2;
-      double* A1c = A1s + ((L::DB && (sidx & 1)) ? L::A1SZ : 0);
-      load_elems(i2o);  // this step's T, Y: in flight while the staging lands and Z runs
-                        // (measured 2 ms faster at C5 than prefetching them a step ahead)
-      if (L::DB) {
-        // next step's A_1 slice into the other buffer: a whole step to land
-        if (more) stage_a1(i2o + P2_B2, A1s + ((sidx & 1) ? 0 : L::A1SZ));
-        asm volatile("cp.async.commit_group;" ::: "memory");
-        asm volatile("cp.async.wait_group 1;" ::: "memory");
-      } else {
-        cp_async_wait_all();
-      }
+      const double* A1c = A1s;
+      if (!TIO) load_elems(i2o);  // this step's T, Y: in flight while the staging lands and Z runs
+                                  // (measured 2 ms faster at C5 than prefetching them a step ahead)
+      cp_async_wait_all();
       __syncthreads();  // step data staged; previous step's smem consumers done
       // ---- Z products (6 independent accumulator chains) ----
       double z1[4] = {0, 0, 0, 0}, z2[4] = {0, 0, 0, 0}, z3[4] = {0, 0, 0, 0};
@@ -426,47 +488,97 @@ __global__ void __launch_bounds__(P2_THREADS, 1) k_pass2_fused(const Pass2Args a
       __syncthreads();
       // ---- elementwise (reference op order, no FMA contraction) ----
       double g1v[4];
-      int64_t offc[4];
-      bool inc[4];
+      if constexpr (!TIO) {
+        int64_t offc[4];
+        bool inc[4];
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const int l1 = g + 8 * (q >> 1), l2 = 2 * t + (q & 1);
-        const double zz[3] = {z1[q], z2[q], Z3s[zx(l1, l2, w)]};
-        const double tt = tv[q];
-        double zt[3], h = 0.0;
+        for (int q = 0; q < 4; ++q) {
+          const int l1 = g + 8 * (q >> 1), l2 = 2 * t + (q & 1);
+          const double zz[3] = {z1[q], z2[q], Z3s[zx(l1, l2, w)]};
+          const double tt = tv[q];
+          double zt[3], h = 0.0;
 #pragma unroll
-        for (int n = 0; n < 3; ++n) {
-          zt[n] = __dsub_rn(tt, zz[n]);
-          h = __dadd_rn(h, __dadd_rn(zt[n], __dmul_rn(yv[n][q], inv_mu)));  // pasd.cpp:202
-        }
-        const double e = soft(__dmul_rn(h, inv_n), tau);  // pasd.cpp:208
-        double gn[3];
+          for (int n = 0; n < 3; ++n) {
+            zt[n] = __dsub_rn(tt, zz[n]);
+            h = __dadd_rn(h, __dadd_rn(zt[n], __dmul_rn(yv[n][q], inv_mu)));  // pasd.cpp:202
+          }
+          const double e = soft(__dmul_rn(h, inv_n), tau);  // pasd.cpp:208
+          double gn[3];
 #pragma unroll
-        for (int n = 0; n < 3; ++n) {
-          const double r = __dsub_rn(zt[n], e);                       // pasd.cpp:220
-          const double ynew = __dadd_rn(yv[n][q], __dmul_rn(mu, r));  // pasd.cpp:221
+          for (int n = 0; n < 3; ++n) {
+            const double r = __dsub_rn(zt[n], e);                       // pasd.cpp:220
+            const double ynew = __dadd_rn(yv[n][q], __dmul_rn(mu, r));  // pasd.cpp:221
+            if (inb[q]) {
+              const double ar = fabs(r);
+              if (ar > worst[n]) worst[n] = ar;
+              bad |= !isfinite(r);
+              a.Y[n][off[q]] = ynew;
+            }
+            gn[n] = inb[q] ? g_elem(tt, e, ynew, inv_mu_next) : 0.0;  // next G_n
+            gsq[n] = fma(gn[n], gn[n], gsq[n]);
+          }
           if (inb[q]) {
+            Enew[off[q]] = e;
+            a.D[off[q]] = __dsub_rn(tt, e);  // next pass 1 reads D = T - E
+          }
+          g1v[q] = gn[0];
+          G2s[g2x(l1, l2, w)] = gn[1];
+          G3s[g3x(l1, l2, w)] = gn[2];
+          offc[q] = off[q];
+          inc[q] = inb[q];
+        }
+        (void)offc;
+        (void)inc;
+      } else {
+        // T, Y_n from the TMA bricks; E, D, Y_n written back in place.  Entries
+        // outside the tensor arrive as zeros (TMA fill) with zero Z, so they
+        // produce zeros everywhere and the stores clip them.
+        mbar_wait(mbar, mph);
+        mph ^= 1;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int l1 = g + 8 * (q >> 1), l2 = 2 * t + (q & 1);
+          const int pa = swzA(l1, l2, w), pb = swzB(l1, l2, w);
+          const double zz[3] = {z1[q], z2[q], Z3s[zx(l1, l2, w)]};
+          const double tt = brk[pa];
+          const double yq[3] = {brk[P2_BRICK + pa], brk[2 * P2_BRICK + pa], brk[3 * P2_BRICK + pb]};
+          double zt[3], h = 0.0;
+#pragma unroll
+          for (int n = 0; n < 3; ++n) {
+            zt[n] = __dsub_rn(tt, zz[n]);
+            h = __dadd_rn(h, __dadd_rn(zt[n], __dmul_rn(yq[n], inv_mu)));  // pasd.cpp:202
+          }
+          const double e = soft(__dmul_rn(h, inv_n), tau);  // pasd.cpp:208
+          const double dq = __dsub_rn(tt, e);              // D = T - E (next pass 1)
+          double gn[3];
+#pragma unroll
+          for (int n = 0; n < 3; ++n) {
+            const double r = __dsub_rn(zt[n], e);                  // pasd.cpp:220
+            const double ynew = __dadd_rn(yq[n], __dmul_rn(mu, r));  // pasd.cpp:221
             const double ar = fabs(r);
             if (ar > worst[n]) worst[n] = ar;
             bad |= !isfinite(r);
-            a.Y[n][off[q]] = ynew;
+            gn[n] = __dadd_rn(dq, __dmul_rn(ynew, inv_mu_next));  // = g_elem(tt, e, ynew, inv_mu_next)
+            gsq[n] = fma(gn[n], gn[n], gsq[n]);
+            brk[(1 + n) * P2_BRICK + (n == 2 ? pb : pa)] = ynew;
           }
-          gn[n] = inb[q] ? g_elem(tt, e, ynew, inv_mu_next) : 0.0;  // next G_n
-          gsq[n] = fma(gn[n], gn[n], gsq[n]);
+          brk[pa] = e;
+          brk[4 * P2_BRICK + pa] = dq;
+          brk[5 * P2_BRICK + pb] = dq;
+          g1v[q] = gn[0];
         }
-        if (inb[q]) {
-          Enew[off[q]] = e;
-          a.D[off[q]] = __dsub_rn(tt, e);  // next pass 1 reads D = T - E
-        }
-        g1v[q] = gn[0];
-        G2s[g2x(l1, l2, w)] = gn[1];
-        G3s[g3x(l1, l2, w)] = gn[2];
-        offc[q] = off[q];
-        inc[q] = inb[q];
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // bricks -> TMA (async proxy)
       }
-      (void)offc;
-      (void)inc;
-      __syncthreads();  // G2s / G3s complete
+      __syncthreads();  // G exchange / bricks complete
+      if (TIO && tid == 0) {  // E, Y_1..3, D of this brick: TMA tensor stores
+        const int c0 = (int)i1o, c1 = (int)i2o, c2 = (int)i3o;
+        tma_store3(ctl->ecur ? &tm.e0 : &tm.e1, brk, c0, c1, c2);
+        tma_store3(&tm.y1, brk + P2_BRICK, c0, c1, c2);
+        tma_store3(&tm.y2, brk + 2 * P2_BRICK, c0, c1, c2);
+        tma_store3(&tm.y3b, brk + 3 * P2_BRICK, c0, c2, c1);
+        tma_store3(&tm.d, brk + 4 * P2_BRICK, c0, c1, c2);
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      }
       // ---- Wt_1 uses the warp's own G_1 as the A operand (A_1 slice as B) ----
       auto wt1 = [&]() {
 #pragma unroll
@@ -476,11 +588,7 @@ __global__ void __launch_bounds__(P2_THREADS, 1) k_pass2_fused(const Pass2Args a
         }
       };
       const int mt = w & 3, kh = w >> 2;  // m-tile and K-half of the Wt_2 / Wt_3 products
-#ifndef PASD_P2_W1LATE
-#define PASD_P2_W1LATE 1
-#endif
-      constexpr bool W1LATE = L::DB && PASD_P2_W1LATE;
-      if (!W1LATE) wt1();
+      wt1();
       // ---- Wt_3^T (m-tile mt, K-half kh), K = (i1, i2) ----
       if (mt < MT) {
         double acc[3][4] = {};
@@ -491,7 +599,14 @@ __global__ void __launch_bounds__(P2_THREADS, 1) k_pass2_fused(const Pass2Args a
         for (int ks = 0; ks < 16; ++ks) {
           const int k = 64 * kh + 4 * ks + t;
           double(&c)[4] = (ks & 3) == 0 ? w3acc : acc[(ks & 3) - 1];
-          dmma(c, rowa[4 * ks + t], rowb[4 * ks + t], gcol[(k & 15) + 22 * (k >> 4)]);
+          double b3;
+          if constexpr (TIO) {  // G_3 at (i1 = k & 15, i2 = k >> 4, i3 = g) from the B-layout bricks
+            const int pb = swzB(k & 15, k >> 4, g);
+            b3 = __dadd_rn(brk[5 * P2_BRICK + pb], __dmul_rn(brk[3 * P2_BRICK + pb], inv_mu_next));
+          } else {
+            b3 = gcol[(k & 15) + 22 * (k >> 4)];
+          }
+          dmma(c, rowa[4 * ks + t], rowb[4 * ks + t], b3);
         }
 #pragma unroll
         for (int q = 0; q < 4; ++q) w3acc[q] += (acc[0][q] + acc[1][q]) + acc[2][q];
@@ -506,13 +621,11 @@ __global__ void __launch_bounds__(P2_THREADS, 1) k_pass2_fused(const Pass2Args a
           if (r < R2 && i2 < I2) w2old[q] = W2c[i2 * R2 + r];
         }
       }
-      __syncthreads();  // A3s / U2s (and A1s when single-buffered) no longer needed this step
+      __syncthreads();  // A1s / A3s / U2s no longer needed this step
       if (more) {
-        if (!L::DB) stage_a1(i2o + P2_B2, A1s);
+        stage_a1(i2o + P2_B2, A1s);
         stage_a3u2(i2o + P2_B2);
       }
-      if (L::DB) asm volatile("cp.async.commit_group;" ::: "memory");
-      if (W1LATE) wt1();
       // ---- W-b: Wt_2^T (m-tile mt, K-half kh), K = (i1, i3) ----
       double acc2[4] = {0, 0, 0, 0};
       if (mt < MT) {
@@ -523,7 +636,14 @@ __global__ void __launch_bounds__(P2_THREADS, 1) k_pass2_fused(const Pass2Args a
         for (int ks = 0; ks < 16; ++ks) {
           const int k = 64 * kh + 4 * ks + t;
           double(&c)[4] = (ks & 3) == 0 ? acc2 : acc[(ks & 3) - 1];
-          dmma(c, rowa[4 * ks + t], rowb[4 * ks + t], G2s[g2x(k & 15, g, k >> 4)]);
+          double b2;
+          if constexpr (TIO) {  // G_2 at (i1 = k & 15, i2 = g, i3 = k >> 4) from the A-layout bricks
+            const int pa = swzA(k & 15, g, k >> 4);
+            b2 = __dadd_rn(brk[4 * P2_BRICK + pa], __dmul_rn(brk[2 * P2_BRICK + pa], inv_mu_next));
+          } else {
+            b2 = G2s[g2x(k & 15, g, k >> 4)];
+          }
+          dmma(c, rowa[4 * ks + t], rowb[4 * ks + t], b2);
         }
 #pragma unroll
         for (int q = 0; q < 4; ++q) acc2[q] += (acc[0][q] + acc[1][q]) + acc[2][q];
@@ -533,6 +653,7 @@ __global__ void __launch_bounds__(P2_THREADS, 1) k_pass2_fused(const Pass2Args a
         }
       }
       __syncthreads();
+      if (more) load_bricks(i1o, i2o + P2_B2, i3o);  // the bricks are free: next step's T, Y (TIO)
       if (kh == 0 && mt < MT) {
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
@@ -580,11 +701,10 @@ __global__ void __launch_bounds__(P2_THREADS, 1) k_pass2_fused(const Pass2Args a
     }
     __syncthreads();
     // restore the zero padding rows of A2s clobbered by the reduction scratch
-    // (single-buffered A_1 only; A1s itself is rewritten, padding included, by
-    // every step's staging)
-    if (!L::DB)
-      for (int idx = tid; idx < (RP - R2) * 128; idx += P2_THREADS) A2s[(R2 + idx / 128) * L::LD2 + (idx & 127)] = 0.0;
+    // (A1s itself is rewritten, padding included, by every step's staging)
+    for (int idx = tid; idx < (RP - R2) * 128; idx += P2_THREADS) A2s[(R2 + idx / 128) * L::LD2 + (idx & 127)] = 0.0;
   }
+  if (TIO && tid == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // element stores done
   // ---- per-CTA residual / NaN / ||G||^2 partials ----
   for (int n = 0; n < 3; ++n) {
     const double wv = block_reduce(worst[n], MaxOp(), red);
@@ -602,13 +722,17 @@ __global__ void __launch_bounds__(P2_THREADS, 1) k_pass2_fused(const Pass2Args a
     finish_body(const_cast<Ctl*>(ctl), a.resid_part, a.bad_part, gridDim.x, a.history, nullptr, red);
 }
 
-template <int RP>
-void launch_pass2(const Pass2Args& a, const Ctl* ctl, int grid, cudaStream_t st) {
-  k_pass2_fused<RP><<<grid, P2_THREADS, P2Layout<RP>::bytes, st>>>(a, ctl);
+template <int RP, bool TIO>
+void launch_pass2(const Pass2Args& a, const Ctl* ctl, const P2Tmaps& tm, int grid, cudaStream_t st) {
+  k_pass2_fused<RP, TIO><<<grid, P2_THREADS, P2Layout<RP, TIO>::bytes, st>>>(a, ctl, tm);
 }
 template <int RP>
 void setup_pass2() {
-  cudaFuncSetAttribute(k_pass2_fused<RP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P2Layout<RP>::bytes);
+  cudaFuncSetAttribute(k_pass2_fused<RP, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)P2Layout<RP, false>::bytes);
+  if (P2Layout<RP, true>::bytes <= 227u * 1024u)
+    cudaFuncSetAttribute(k_pass2_fused<RP, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)P2Layout<RP, true>::bytes);
 }
 
 inline int pass2_rp(int R1, int R2, int R3) {
@@ -616,16 +740,20 @@ inline int pass2_rp(int R1, int R2, int R3) {
   r = r > R3 ? r : R3;
   return (r + 7) / 8 * 8;
 }
-inline size_t pass2_smem(int rp) {
+template <int RP>
+size_t pass2_smem_rp(bool tio) {
+  return tio ? P2Layout<RP, true>::bytes : P2Layout<RP, false>::bytes;
+}
+inline size_t pass2_smem(int rp, bool tio) {
   switch (rp) {
-    case 8: return P2Layout<8>::bytes;
-    case 16: return P2Layout<16>::bytes;
-    case 24: return P2Layout<24>::bytes;
-    case 32: return P2Layout<32>::bytes;
-    case 40: return P2Layout<40>::bytes;
-    case 48: return P2Layout<48>::bytes;
-    case 56: return P2Layout<56>::bytes;
-    default: return P2Layout<64>::bytes;
+    case 8: return pass2_smem_rp<8>(tio);
+    case 16: return pass2_smem_rp<16>(tio);
+    case 24: return pass2_smem_rp<24>(tio);
+    case 32: return pass2_smem_rp<32>(tio);
+    case 40: return pass2_smem_rp<40>(tio);
+    case 48: return pass2_smem_rp<48>(tio);
+    case 56: return pass2_smem_rp<56>(tio);
+    default: return pass2_smem_rp<64>(tio);
   }
 }
 inline void pass2_setup(int rp) {
@@ -640,16 +768,24 @@ inline void pass2_setup(int rp) {
     default: setup_pass2<64>(); break;
   }
 }
-inline void pass2_launch(int rp, const Pass2Args& a, const Ctl* ctl, int grid, cudaStream_t st) {
+template <int RP>
+void pass2_launch_rp(bool tio, const Pass2Args& a, const Ctl* ctl, const P2Tmaps& tm, int grid, cudaStream_t st) {
+  if (tio)
+    launch_pass2<RP, true>(a, ctl, tm, grid, st);
+  else
+    launch_pass2<RP, false>(a, ctl, tm, grid, st);
+}
+inline void pass2_launch(int rp, bool tio, const Pass2Args& a, const Ctl* ctl, const P2Tmaps& tm, int grid,
+                         cudaStream_t st) {
   switch (rp) {
-    case 8: launch_pass2<8>(a, ctl, grid, st); break;
-    case 16: launch_pass2<16>(a, ctl, grid, st); break;
-    case 24: launch_pass2<24>(a, ctl, grid, st); break;
-    case 32: launch_pass2<32>(a, ctl, grid, st); break;
-    case 40: launch_pass2<40>(a, ctl, grid, st); break;
-    case 48: launch_pass2<48>(a, ctl, grid, st); break;
-    case 56: launch_pass2<56>(a, ctl, grid, st); break;
-    default: launch_pass2<64>(a, ctl, grid, st); break;
+    case 8: pass2_launch_rp<8>(tio, a, ctl, tm, grid, st); break;
+    case 16: pass2_launch_rp<16>(tio, a, ctl, tm, grid, st); break;
+    case 24: pass2_launch_rp<24>(tio, a, ctl, tm, grid, st); break;
+    case 32: pass2_launch_rp<32>(tio, a, ctl, tm, grid, st); break;
+    case 40: pass2_launch_rp<40>(tio, a, ctl, tm, grid, st); break;
+    case 48: pass2_launch_rp<48>(tio, a, ctl, tm, grid, st); break;
+    case 56: pass2_launch_rp<56>(tio, a, ctl, tm, grid, st); break;
+    default: pass2_launch_rp<64>(tio, a, ctl, tm, grid, st); break;
   }
 }
 

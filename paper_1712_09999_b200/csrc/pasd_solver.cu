@@ -175,6 +175,8 @@ struct pasd_solver {
   Pass2Args p2{};
   int p2_grid = 0;
   size_t p2_smem = 0;
+  bool p2_tio = false;  // element streams through TMA (k_pass2_fused<RP, true>)
+  P2Tmaps p2_tmaps{};
   double* p2_resid = nullptr;
   int* p2_bad = nullptr;
   double* zbuf = nullptr;  // S scratch (finalisation / observer)
@@ -279,7 +281,7 @@ void launch_iteration_marked(pasd_solver* s, cudaStream_t st, Mark&& mark) {
     if (s->use_m8)
       m8_launch(s->p2_rp, s->p2, s->d_ctl, s->p2_grid, st);
     else
-      pass2_launch(s->p2_rp, s->p2, s->d_ctl, s->p2_grid, st);
+      pass2_launch(s->p2_rp, s->p2_tio, s->p2, s->d_ctl, s->p2_tmaps, s->p2_grid, st);
     mark(PASD_K_UPDATE, false);
     ++launches;
     int64_t maxir = 1;
@@ -435,6 +437,34 @@ void reset_state(pasd_solver* s) {
   CK(cudaGetLastError());
 }
 
+// 3-D float64 tensor map with a 16 x 8 x 8 box and 128-byte swizzle (pass-2
+// element bricks); dims / byte strides as given (dimension 0 contiguous).
+// cuTensorMapEncodeTiled comes from the driver entry point, so the library
+// does not link libcuda.
+void encode_brick_map(CUtensorMap* map, double* base, const std::vector<int64_t>& dims,
+                      const std::vector<int64_t>& strides) {
+  using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+  static EncodeFn encode = nullptr;
+  if (!encode) {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    CK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
+    if (q != cudaDriverEntryPointSuccess || !fn) fail(PASD_ERR_CUDA, "pasd_b200: cuTensorMapEncodeTiled unavailable");
+    encode = reinterpret_cast<EncodeFn>(fn);
+  }
+  const cuuint64_t gdim[3] = {(cuuint64_t)dims[0], (cuuint64_t)dims[1], (cuuint64_t)dims[2]};
+  const cuuint64_t gstride[2] = {(cuuint64_t)strides[0], (cuuint64_t)strides[1]};
+  const cuuint32_t box[3] = {P2_B1, P2_B2, P2_B3};
+  const cuuint32_t estride[3] = {1, 1, 1};
+  const CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, base, gdim, gstride, box, estride,
+                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                            CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    fail(PASD_ERR_CUDA, "pasd_b200: cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
+}
+
 pasd_solver* create_solver(const pasd_options* o, const pasd_shard* shard) {
   validate_options(o);
   auto s = std::make_unique<pasd_solver>();
@@ -583,7 +613,26 @@ pasd_solver* create_solver(const pasd_options* o, const pasd_shard* shard) {
     a.n3b = (int)((s->dims[2] + P2_B3 - 1) / P2_B3);
     a.npencils = a.n1b * a.n3b;
     s->p2_grid = std::max(1, std::min(a.npencils, (s->use_m8 ? 2 : 1) * sms));
-    s->p2_smem = s->use_m8 ? 0 : pass2_smem(s->p2_rp);
+    // TMA element streams (PASD_P2_TIO=1; needs 16-byte global strides, i.e. I1 even, and the
+    // bricks within 227 KB).  Parity-green but slower at C5 (45.7 vs 42.3 ms per launch: the
+    // CTA moves to the 228 KB carve-out, the Wt_2/Wt_3 operands are formed from D and Y in the
+    // fragment load, and L2 re-fetches of the A slices grow by 8.5 GB), so LDG/STG is the default.
+    const char* tio_env = std::getenv("PASD_P2_TIO");
+    s->p2_tio = !s->use_m8 && (s->dims[0] % 2 == 0) && pass2_smem(s->p2_rp, true) <= 227u * 1024u &&
+                (tio_env && tio_env[0] == '1');
+    if (s->p2_tio) {
+      const int64_t I1 = s->dims[0], I2 = s->dims[1], I3 = s->dims[2];
+      const std::vector<int64_t> da = {I1, I2, I3}, db = {I1, I3, I2};
+      const std::vector<int64_t> sa = {I1 * 8, I1 * I2 * 8}, sb = {I1 * I2 * 8, I1 * 8};
+      encode_brick_map(&s->p2_tmaps.t, s->T, da, sa);
+      encode_brick_map(&s->p2_tmaps.y1, s->Y[0], da, sa);
+      encode_brick_map(&s->p2_tmaps.y2, s->Y[1], da, sa);
+      encode_brick_map(&s->p2_tmaps.y3b, s->Y[2], db, sb);
+      encode_brick_map(&s->p2_tmaps.e0, s->E[0], da, sa);
+      encode_brick_map(&s->p2_tmaps.e1, s->E[1], da, sa);
+      encode_brick_map(&s->p2_tmaps.d, s->D, da, sa);
+    }
+    s->p2_smem = s->use_m8 ? 0 : pass2_smem(s->p2_rp, s->p2_tio);
     a.W1p = s->alloc<double>((size_t)a.npencils * a.b1 * s->modes[0].R);
     a.W3p = s->alloc<double>((size_t)a.npencils * 8 * s->modes[2].R);
     a.W2part = s->alloc<double>((size_t)s->p2_grid * s->dims[1] * s->modes[1].R);

@@ -200,3 +200,26 @@ def test_sharded_single_rank_matches_unsharded(gpu, oracle_mod):
     np.testing.assert_array_equal(r0.e, r1.e)
     assert r0.objective == r1.objective
     assert r0.certificate.epsilon_hat == r1.certificate.epsilon_hat
+
+
+def test_tma_element_streams_match_plain(monkeypatch):
+    """k_pass2_fused<RP, true> (T/Y loads and E/D/Y stores through TMA bricks)
+    gives bit-identical iterates to the LDG/STG variant."""
+    import paper_1712_09999_b200 as pb
+    from paper_1712_09999_b200.api import PasdConfig
+
+    rng = np.random.default_rng(7)
+    dims = (50, 44, 41)  # I1 even (TMA strides), ragged bricks in every mode
+    X = rng.standard_normal(dims)
+    cfg = PasdConfig(lambdas=[1.0, 1.0, 1.0], ranks=[40, 36, 33], maxiter=12)
+    monkeypatch.setenv("PASD_PASS2_M16", "1")
+    monkeypatch.setenv("PASD_P2_TIO", "0")
+    pb.release_cache()  # solvers read the variant switches when they are built
+    plain = pb.pasd_recover(X, cfg)
+    pb.release_cache()
+    monkeypatch.setenv("PASD_P2_TIO", "1")
+    tio = pb.pasd_recover(X, cfg)
+    pb.release_cache()
+    assert plain.iters == tio.iters
+    np.testing.assert_array_equal(plain.x, tio.x)
+    np.testing.assert_array_equal(plain.e, tio.e)
