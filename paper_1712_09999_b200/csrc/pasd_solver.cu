@@ -42,6 +42,8 @@
 using namespace pasd;
 
 namespace {
+// SMs left to NCCL while pass 1 of modes 1 and 2 overlaps the A_3 all-reduce
+constexpr int kNcclSms = 16;
 
 struct PasdError : std::runtime_error {
   int code;
@@ -194,6 +196,8 @@ struct pasd_solver {
   int64_t slab_b = 0, slab_e = 0;
   std::vector<int64_t> gdims;  // global dims (dims = local slab dims)
   ncclComm_t comm = nullptr;
+  cudaStream_t side = nullptr;  // A_3 all-reduce, overlapped with pass 1 of modes 1 and 2
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   double* A3_partial = nullptr;
   std::vector<double*> gram_partial, wt_partial;
   double* g2_partial = nullptr;
@@ -202,6 +206,9 @@ struct pasd_solver {
 
   ~pasd_solver() {
     if (comm) ncclCommDestroy(comm);
+    if (ev_fork) cudaEventDestroy(ev_fork);
+    if (ev_join) cudaEventDestroy(ev_join);
+    if (side) cudaStreamDestroy(side);
     if (graph_exec) cudaGraphExecDestroy(graph_exec);
     if (graph) cudaGraphDestroy(graph);
     for (void* p : owned) cudaFree(p);
@@ -233,17 +240,35 @@ void launch_iteration_marked(pasd_solver* s, cudaStream_t st, Mark&& mark) {
   k_polar<<<N, kSmallThreads, s->small_smem, st>>>(s->d_pack, s->d_ctl);
   mark(PASD_K_POLAR, false);
   ++launches;
-  for (int n = 0; n < N; ++n) {
-    ModeDev m = s->modes[n];
-    if (s->sharded && n == N - 1) m.A = s->A3_partial;  // partial sum over this rank's slab
+  if (!s->sharded) {
+    for (int n = 0; n < N; ++n) {
+      mark(PASD_K_CONTRACT_A, true);
+      launch_contract_A_mma(s->modes[n], s->D, s->Y[n], s->d_ctl, s->sms, st);
+      mark(PASD_K_CONTRACT_A, false);
+      ++launches;
+    }
+  } else {
+    // Mode 3 first: its slab partial A_3 (the one large exchange, R_3 I_1 I_2 doubles) is
+    // all-reduced on the side stream while pass 1 of modes 1 and 2 runs on SMs left free
+    // for NCCL's kernel; the main stream joins before the Gram products.
+    ModeDev m3 = s->modes[N - 1];
+    m3.A = s->A3_partial;
     mark(PASD_K_CONTRACT_A, true);
-    launch_contract_A_mma(m, s->D, s->Y[n], s->d_ctl, s->sms, st);
+    launch_contract_A_mma(m3, s->D, s->Y[N - 1], s->d_ctl, s->sms, st);
     mark(PASD_K_CONTRACT_A, false);
     ++launches;
-  }
-  if (s->sharded) {  // A_3 = sum over ranks of the slab partials (the one large exchange)
-    const ModeDev& m3 = s->modes[N - 1];
-    NK(ncclAllReduce(s->A3_partial, m3.A, (size_t)m3.J * m3.R, ncclDouble, ncclSum, s->comm, st));
+    CK(cudaEventRecord(s->ev_fork, st));
+    CK(cudaStreamWaitEvent(s->side, s->ev_fork, 0));
+    NK(ncclAllReduce(s->A3_partial, s->modes[N - 1].A, (size_t)m3.J * m3.R, ncclDouble, ncclSum, s->comm, s->side));
+    CK(cudaEventRecord(s->ev_join, s->side));
+    const int sms_p1 = std::max(1, s->sms - kNcclSms);
+    for (int n = 0; n < N - 1; ++n) {
+      mark(PASD_K_CONTRACT_A, true);
+      launch_contract_A_mma(s->modes[n], s->D, s->Y[n], s->d_ctl, sms_p1, st);
+      mark(PASD_K_CONTRACT_A, false);
+      ++launches;
+    }
+    CK(cudaStreamWaitEvent(st, s->ev_join, 0));
   }
   if (!s->sharded) {
     // all modes' Gram partials, then all reductions (pasd_gram.cuh), then the SVTs
@@ -565,6 +590,9 @@ pasd_solver* create_solver(const pasd_options* o, const pasd_shard* shard) {
     else
       fail(PASD_ERR_ARGUMENT, "pasd_b200: nccl_unique_id is required for nranks > 1");
     NK(ncclCommInitRank(&s->comm, s->nranks, id, s->rank));
+    CK(cudaStreamCreateWithFlags(&s->side, cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&s->ev_fork, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&s->ev_join, cudaEventDisableTiming));
   }
   std::memset(&s->h_pack, 0, sizeof(ModePack));
   s->h_pack.order = s->N;

@@ -166,11 +166,21 @@ class Solver:
     def launches(self) -> int:
         return int(lib().pasd_b200_solver_launches(self._h))
 
-    def finalize(self, want_x=True, want_e=True, want_z=False, want_y=False):
+    def finalize(self, want_x=True, want_e=True, want_z=False, want_y=False, out_x=None, out_e=None):
+        """Finalise into new arrays, or into `out_x` / `out_e` (contiguous float64
+        buffers of the local slab's size, e.g. views of pinned host memory)."""
         n = len(self.dims)
         total = int(np.prod(self.local_dims))
-        x = np.empty(total) if want_x else None
-        e = np.empty(total) if want_e else None
+
+        def dest(buf, want):
+            if buf is None:
+                return np.empty(total) if want else None
+            buf = np.asarray(buf)
+            if buf.dtype != np.float64 or buf.size != total or not buf.flags.c_contiguous:
+                raise ValueError("finalize: output buffers must be contiguous float64 of the slab's size")
+            return buf.reshape(-1)
+        x = dest(out_x, want_x)
+        e = dest(out_e, want_e)
         z = [np.empty(total) for _ in range(n)] if want_z else None
         y = [np.empty(total) for _ in range(n)] if want_y else None
         yh = [np.empty(total) for _ in range(n)] if want_y else None
