@@ -22,21 +22,36 @@ namespace pasd {
 // DMMAs overlap the other's loads.  Warp w owns kappa rows 16w..16w+15 and
 // all n-tiles, so every G value is formed once.
 constexpr int P1_MT = 128;     // kappa columns per tile
-constexpr int P1_KC = 16;      // i rows per chunk
-constexpr int P1_NST = 2;      // pipeline stages
 constexpr int P1_THREADS = 256;
+#ifndef PASD_P1_KCS
+#define PASD_P1_KCS 8
+#endif
+#ifndef PASD_P1_NSTS
+#define PASD_P1_NSTS 4
+#endif
+// chunk depth (i rows) and pipeline stages: mode 1 (CONTIG) stages 16 i per
+// column (128-byte runs); the strided modes stage 1 KB rows of 128 kappa, so
+// they take 8-row chunks in a 4-deep ring (more bytes in flight at two CTAs
+// per SM; measured at C5: KC/NST 16/2 -> 8/4 takes the two strided modes from
+// 4.7 to 4.2 ms each, 8/3 and 8/5 in between, 4/6 and 4/8 slower).
+template <bool CONTIG>
+struct P1Cfg {
+  static constexpr int KC = CONTIG ? 16 : PASD_P1_KCS;
+  static constexpr int NST = CONTIG ? 2 : PASD_P1_NSTS;
+};
 
 template <int RP, bool CONTIG>
 struct P1Layout {
   // CONTIG (mode 1): raw[kappa][i] rows of 16 i;  else raw[i][kappa] rows of 128 kappa.
   // Pitches are 4 mod 16 doubles: the fragment reads (row g, col t) hit 16
   // distinct banks per half-warp.
-  static constexpr int LDR = CONTIG ? (P1_KC + 4) : (P1_MT + 4);
-  static constexpr int RAW = CONTIG ? P1_MT * LDR : P1_KC * LDR;  // doubles per tensor per stage
-  static constexpr int LDU = P1_KC + 4;                           // U chunk as [r][i]
+  static constexpr int KC = P1Cfg<CONTIG>::KC, NST = P1Cfg<CONTIG>::NST;
+  static constexpr int LDR = CONTIG ? (KC + 4) : (P1_MT + 4);
+  static constexpr int RAW = CONTIG ? P1_MT * LDR : KC * LDR;  // doubles per tensor per stage
+  static constexpr int LDU = KC + 4;                           // U chunk as [r][i]
   static constexpr int USZ = RP * LDU;
   static constexpr int STAGE = 2 * RAW + USZ;  // D, Y_n, U chunk
-  static constexpr size_t bytes = sizeof(double) * (size_t)P1_NST * STAGE;
+  static constexpr size_t bytes = sizeof(double) * (size_t)NST * STAGE;
 };
 
 // Work-item cursor: (tile, chunk) advanced without 64-bit divisions.  For
@@ -52,6 +67,7 @@ __global__ void __launch_bounds__(P1_THREADS, 2) k_pass1(ModeDev m, const double
   if (ctl->done) return;
   using L = P1Layout<RP, CONTIG>;
   constexpr int NT = RP / 8;  // n-tiles per warp
+  constexpr int P1_KC = L::KC, P1_NST = L::NST;
   extern __shared__ double p1sm[];
   const double inv_mu = __ddiv_rn(1.0, ctl->mu);  // pasd.cpp:170
   const int tid = threadIdx.x, lane = tid & 31, g = lane >> 2, t = lane & 3, w = tid >> 5;
@@ -144,11 +160,12 @@ __global__ void __launch_bounds__(P1_THREADS, 2) k_pass1(ModeDev m, const double
     const unsigned us = st + 8u * (unsigned)(2 * L::RAW);
     const double* ub = m.U + m.ioff + i0;
     if (alu) {
-      const int ip = tid & 7;
+      constexpr int PAIRS = P1_KC / 2, RSTEP = P1_THREADS / PAIRS;
+      const int ip = tid % PAIRS;
       const int v = ni - 2 * ip, nbc = v >= 2 ? 16 : (v == 1 ? 8 : 0);
 #pragma unroll
-      for (int k = 0; k < (RP + 31) / 32; ++k) {
-        const int r = (tid >> 3) + 32 * k;
+      for (int k = 0; k < (RP + RSTEP - 1) / RSTEP; ++k) {
+        const int r = tid / PAIRS + RSTEP * k;
         if (r < RP) {
           const int nb = r < R ? nbc : 0;
           cp16s(us + 8u * (unsigned)(r * L::LDU + 2 * ip), nb ? ub + 2 * ip + m.Ifull * r : m.U, nb);
