@@ -23,21 +23,27 @@ namespace pasd {
 // all n-tiles, so every G value is formed once.
 constexpr int P1_MT = 128;     // kappa columns per tile
 constexpr int P1_THREADS = 256;
+#ifndef PASD_P1_KCC
+#define PASD_P1_KCC 8
+#endif
+#ifndef PASD_P1_NSTC
+#define PASD_P1_NSTC 3
+#endif
 #ifndef PASD_P1_KCS
 #define PASD_P1_KCS 8
 #endif
 #ifndef PASD_P1_NSTS
 #define PASD_P1_NSTS 4
 #endif
-// chunk depth (i rows) and pipeline stages: mode 1 (CONTIG) stages 16 i per
-// column (128-byte runs); the strided modes stage 1 KB rows of 128 kappa, so
-// they take 8-row chunks in a 4-deep ring (more bytes in flight at two CTAs
-// per SM; measured at C5: KC/NST 16/2 -> 8/4 takes the two strided modes from
-// 4.7 to 4.2 ms each, 8/3 and 8/5 in between, 4/6 and 4/8 slower).
+// chunk depth (i rows) and pipeline stages at two CTAs per SM.  Mode 1
+// (CONTIG) stages KC consecutive i per column, the strided modes 1 KB rows of
+// 128 kappa.  Measured at C5 (KC/NST): strided 16/2 -> 8/4 takes each strided
+// mode from 4.7 to 4.2 ms (8/3, 8/5 in between; 4/6, 4/8 slower); mode 1
+// 16/2 -> 8/3 saves 0.4 ms (8/4 no longer fits two CTAs per SM).
 template <bool CONTIG>
 struct P1Cfg {
-  static constexpr int KC = CONTIG ? 16 : PASD_P1_KCS;
-  static constexpr int NST = CONTIG ? 2 : PASD_P1_NSTS;
+  static constexpr int KC = CONTIG ? PASD_P1_KCC : PASD_P1_KCS;
+  static constexpr int NST = CONTIG ? PASD_P1_NSTC : PASD_P1_NSTS;
 };
 
 template <int RP, bool CONTIG>
@@ -105,15 +111,16 @@ __global__ void __launch_bounds__(P1_THREADS, 2) k_pass1(ModeDev m, const double
       // 128 columns kappa, 16 consecutive i each (contiguous): row = column
       const int64_t k0 = c.tile * P1_MT;
       if (al) {
-        const int cc = tid & 7;  // 16-byte chunk of the 16-double row
+        constexpr int CPR = P1_KC / 2, RPP = P1_THREADS / CPR;  // 16-byte chunks per row, rows per pass
+        const int cc = tid % CPR;  // 16-byte chunk of the KC-double row
         const int v = ni - 2 * cc, nbc = v >= 2 ? 16 : (v == 1 ? 8 : 0);
-        const int j0 = tid >> 3;
+        const int j0 = tid / CPR;
         const int64_t off0 = (k0 + j0) * I + i0 + 2 * cc;
 #pragma unroll
-        for (int k = 0; k < P1_MT / 32; ++k) {
-          const int j = j0 + 32 * k;
+        for (int k = 0; k < P1_MT / RPP; ++k) {
+          const int j = j0 + RPP * k;
           const int nb = (k0 + j < m.J) ? nbc : 0;
-          const int64_t off = off0 + 32 * k * I;
+          const int64_t off = off0 + (int64_t)RPP * k * I;
           const unsigned d = st + 8u * (unsigned)(j * L::LDR + 2 * cc);
           cp16s(d, nb ? D + off : D, nb);
           cp16s(d + 8u * L::RAW, nb ? Y + off : D, nb);
