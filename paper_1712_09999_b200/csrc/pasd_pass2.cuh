@@ -317,6 +317,7 @@ __global__ void __launch_bounds__(P2_THREADS, 1) k_pass2_fused(const Pass2Args a
   double gsq[3] = {0.0, 0.0, 0.0};
   int bad = 0;
   const int64_t S12 = I1 * I2;
+  const int ksz = (max(R1, max(R2, R3)) + 3) / 4;  // Z k-steps that touch a nonzero rank row
   const bool al1 = (I1 % 2) == 0;  // 16-byte aligned rows of 16 consecutive i1
 
   for (int lin = blockIdx.x; lin < a.npencils; lin += gridDim.x) {
@@ -466,6 +467,7 @@ __global__ void __launch_bounds__(P2_THREADS, 1) k_pass2_fused(const Pass2Args a
         double y1[4] = {0, 0, 0, 0}, y2[4] = {0, 0, 0, 0}, y3[4] = {0, 0, 0, 0};
 #pragma unroll
         for (int ks = 0; ks < KS; ++ks) {
+          if (ks >= ksz) break;  // k-steps past max R_n only multiply zero padding
           const int k = 4 * ks + t;
           double(&c1)[4] = (ks & 1) ? y1 : z1;
           double(&c2)[4] = (ks & 1) ? y2 : z2;

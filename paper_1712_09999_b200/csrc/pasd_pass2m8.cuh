@@ -96,6 +96,7 @@ __global__ void __launch_bounds__(M8_THREADS, 2) k_pass2_m8(const Pass2Args a, c
   double gsq[3] = {0.0, 0.0, 0.0};
   int bad = 0;
   const int64_t S12 = I1 * I2;
+  const int ksz = (max(R1, max(R2, R3)) + 3) / 4;  // Z k-steps that touch a nonzero rank row
   const bool al1 = (I1 % 2) == 0;
 
   for (int lin = blockIdx.x; lin < a.npencils; lin += gridDim.x) {
@@ -217,6 +218,7 @@ __global__ void __launch_bounds__(M8_THREADS, 2) k_pass2_m8(const Pass2Args a, c
         double y1[2] = {0, 0}, y2[2] = {0, 0}, y3[2] = {0, 0};
 #pragma unroll
         for (int ks = 0; ks < KS; ++ks) {
+          if (ks >= ksz) break;  // k-steps past max R_n only multiply zero padding
           const int k = 4 * ks + t;
           double(&c1)[2] = (ks & 1) ? y1 : z1;
           double(&c2)[2] = (ks & 1) ? y2 : z2;
