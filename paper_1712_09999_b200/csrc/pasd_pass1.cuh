@@ -21,8 +21,16 @@ namespace pasd {
 // 128 columns x 16 i per chunk, double-buffered, two CTAs per SM: one CTA's
 // DMMAs overlap the other's loads.  Warp w owns kappa rows 16w..16w+15 and
 // all n-tiles, so every G value is formed once.
-constexpr int P1_MT = 128;     // kappa columns per tile
-constexpr int P1_THREADS = 256;
+// (64-column tiles at 4 CTAs per SM measured slower: 13.5-14.1 vs 12.6 ms per C5 iteration.)
+#ifndef PASD_P1_MT
+#define PASD_P1_MT 128
+#endif
+#ifndef PASD_P1_CTAS
+#define PASD_P1_CTAS 2
+#endif
+constexpr int P1_MT = PASD_P1_MT;           // kappa columns per tile (16 per warp)
+constexpr int P1_THREADS = 2 * P1_MT;       // one warp per 16-column m-tile
+constexpr int P1_CTAS = PASD_P1_CTAS;       // resident CTAs per SM
 #ifndef PASD_P1_KCC
 #define PASD_P1_KCC 8
 #endif
@@ -68,7 +76,7 @@ struct P1Cursor {
 };
 
 template <int RP, bool CONTIG>
-__global__ void __launch_bounds__(P1_THREADS, 2) k_pass1(ModeDev m, const double* __restrict__ D,
+__global__ void __launch_bounds__(P1_THREADS, P1_CTAS) k_pass1(ModeDev m, const double* __restrict__ D,
                                                         const double* __restrict__ Y, const Ctl* ctl) {
   if (ctl->done) return;
   using L = P1Layout<RP, CONTIG>;
@@ -140,12 +148,13 @@ __global__ void __launch_bounds__(P1_THREADS, 2) k_pass1(ModeDev m, const double
       const int np = (int)imin64(P1_MT, inner - p0);
       const int64_t off0 = p0 + inner * (i0 + I * c.q);
       if (al) {
-        // 64 16-byte chunks per row; thread -> (chunk cc, rows rsub + 4k)
-        const int cc = tid & 63, rsub = tid >> 6;
+        // MT/2 16-byte chunks per row; thread -> (chunk cc, rows rsub + RG k)
+        constexpr int CPR = P1_MT / 2, RG = P1_THREADS / CPR;
+        const int cc = tid % CPR, rsub = tid / CPR;
         const int v = np - 2 * cc, nbc = v >= 2 ? 16 : (v == 1 ? 8 : 0);
 #pragma unroll
-        for (int k = 0; k < P1_KC / 4; ++k) {
-          const int ii = rsub + 4 * k;
+        for (int k = 0; k < P1_KC / RG; ++k) {
+          const int ii = rsub + RG * k;
           const int nb = ii < ni ? nbc : 0;
           const int64_t off = off0 + inner * ii + 2 * cc;
           const unsigned d = st + 8u * (unsigned)(ii * L::LDR + 2 * cc);
@@ -286,7 +295,7 @@ void launch_p1_rp(const ModeDev& m, const double* D, const double* Y,
 inline int pass1_grid(const ModeDev& m, int sms) {
   const int64_t ntiles =
       m.inner == 1 ? (m.J + P1_MT - 1) / P1_MT : ((m.inner + P1_MT - 1) / P1_MT) * m.outer;
-  return (int)imin64(ntiles, 2 * sms);
+  return (int)imin64(ntiles, P1_CTAS * sms);
 }
 
 inline void launch_contract_A_mma(const ModeDev& m, const double* D, const double* Y, const Ctl* ctl, int sms, cudaStream_t st) {
