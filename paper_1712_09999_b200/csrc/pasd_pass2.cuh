@@ -29,6 +29,9 @@
 
 namespace pasd {
 
+#ifndef PASD_P2_BW
+#define PASD_P2_BW 12  // i1-block band width of the pencil order
+#endif
 constexpr int P2_B1 = 16, P2_B2 = 8, P2_B3 = 8;
 constexpr int P2_THREADS = 256;
 constexpr int P2_BRICK = P2_B1 * P2_B2 * P2_B3;  // 1024
@@ -326,7 +329,7 @@ __global__ void __launch_bounds__(P2_THREADS, 1) k_pass2_fused(const Pass2Args a
     // i3) and A_1 slices (shared along i1) they stage each step are L2 hits.
     int ib1, ib3;
     {
-      const int BW = 12;
+      const int BW = PASD_P2_BW;
       const int band = lin / (BW * a.n3b), lin_in = lin - band * BW * a.n3b;
       const int bw = min(BW, a.n1b - band * BW);
       ib1 = band * BW + lin_in % bw;
