@@ -400,9 +400,10 @@ template <int RP>
 void setup_m8() {
   cudaFuncSetAttribute(k_pass2_m8<RP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)M8Layout<RP>::bytes);
 }
-// Measured on B200 (profiles/): the 8x8x8 two-CTA variant wins for R <= 32
-// (C2, C4), the 16x8x8 variant for R >= 40 (C3, C5).
-inline bool m8_supported(int rp) { return rp <= 32; }
+// Measured on B200 (profiles/): the 8x8x8 two-CTA variant wins for R <= 24
+// (C1: 0.122 vs 0.129 ms, C2: 0.516 vs 0.565 ms per iteration), the 16x8x8
+// variant from R = 32 on (C4: 3.04 vs 3.09 ms; C3, C5).
+inline bool m8_supported(int rp) { return rp <= 24; }
 inline void m8_setup(int rp) {
   switch (rp) {
     case 8: setup_m8<8>(); break;
