@@ -130,8 +130,8 @@ __global__ void __launch_bounds__(P1_THREADS, P1_CTAS) k_pass1(ModeDev m, const 
           const int nb = (k0 + j < m.J) ? nbc : 0;
           const int64_t off = off0 + (int64_t)RPP * k * I;
           const unsigned d = st + 8u * (unsigned)(j * L::LDR + 2 * cc);
-          cp16s(d, nb ? D + off : D, nb);
-          cp16s(d + 8u * L::RAW, nb ? Y + off : D, nb);
+          cp16z(d, nb ? D + off : D, nb != 0);  // even I: chunks wholly in or out
+          cp16z(d + 8u * L::RAW, nb ? Y + off : D, nb != 0);
         }
       } else {
         for (int idx = tid; idx < P1_MT * P1_KC; idx += P1_THREADS) {
@@ -158,8 +158,8 @@ __global__ void __launch_bounds__(P1_THREADS, P1_CTAS) k_pass1(ModeDev m, const 
           const int nb = ii < ni ? nbc : 0;
           const int64_t off = off0 + inner * ii + 2 * cc;
           const unsigned d = st + 8u * (unsigned)(ii * L::LDR + 2 * cc);
-          cp16s(d, nb ? D + off : D, nb);
-          cp16s(d + 8u * L::RAW, nb ? Y + off : D, nb);
+          cp16z(d, nb ? D + off : D, nb != 0);  // even inner: chunks wholly in or out
+          cp16z(d + 8u * L::RAW, nb ? Y + off : D, nb != 0);
         }
       } else {
         for (int idx = tid; idx < P1_KC * P1_MT; idx += P1_THREADS) {

@@ -157,6 +157,24 @@ __device__ __forceinline__ void cp8s(unsigned s, const void* gmem, int nbytes) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(s), "l"(gmem), "r"(nbytes) : "memory");
 }
 
+// Same copies with an all-or-nothing zero fill: the ignore-src predicate form
+// (LDGSTS.ZFILL with a predicate) needs no per-copy src-size arithmetic.
+// `gmem` must still be a valid address when !valid (it is not read).
+__device__ __forceinline__ void cp16z(unsigned s, const void* gmem, bool valid) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.eq.u32 p, %2, 0;\n\t"
+      "cp.async.cg.shared.global [%0], [%1], 16, p;\n\t}" ::"r"(s),
+      "l"(gmem), "r"((unsigned)valid)
+      : "memory");
+}
+__device__ __forceinline__ void cp8z(unsigned s, const void* gmem, bool valid) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.eq.u32 p, %2, 0;\n\t"
+      "cp.async.ca.shared.global [%0], [%1], 8, p;\n\t}" ::"r"(s),
+      "l"(gmem), "r"((unsigned)valid)
+      : "memory");
+}
+
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
 // Brick element index e = i1 + 16 * (i2 + 8 * i3) (local coordinates).
@@ -379,7 +397,7 @@ __global__ void __launch_bounds__(P2_THREADS, 1) k_pass2_fused(const Pass2Args a
 #pragma unroll
             for (int k = 0; k < 8; ++k) {
               const bool ok = rok && k < n3v;
-              cp16s(sp + 8 * (k * 8 * L::LD1 + r), ok ? (const void*)gp : (const void*)m1.A, ok ? 16 : 0);
+              cp16z(sp + 8 * (k * 8 * L::LD1 + r), ok ? (const void*)gp : (const void*)m1.A, ok);
               gp += kst;
             }
           }
@@ -410,10 +428,10 @@ __global__ void __launch_bounds__(P2_THREADS, 1) k_pass2_fused(const Pass2Args a
         const char* gp = reinterpret_cast<const char*>(nb ? m3.A + i1o + 2 * c + I1 * (i2o + l2) + S12 * (int64_t)r0 : m3.A);
         const int64_t gst = nb ? 32 * S12 : 0;  // 4 rows r
         const unsigned sp = smem_u32(A3s + r0 * L::LD3 + 16 * l2 + 2 * c);
-        if (al1) {
+        if (al1) {  // even I1: every 16-byte chunk is wholly inside or outside
 #pragma unroll
           for (int k = 0; k < RP / 4; ++k) {
-            if (r0 + 4 * k < R3) cp16s(sp + 32 * k * L::LD3, gp, nb);
+            if (r0 + 4 * k < R3) cp16z(sp + 32 * k * L::LD3, gp, nb != 0);
             gp += gst;
           }
         } else {
@@ -435,7 +453,7 @@ __global__ void __launch_bounds__(P2_THREADS, 1) k_pass2_fused(const Pass2Args a
 #pragma unroll
         for (int k = 0; k < (RP + 31) / 32; ++k) {
           const int r = (tid >> 3) + 32 * k;
-          if (r < R2) cp8s(smem_u32(U2s + l2 * L::LDU + r), v ? (const void*)(src + m2.Ifull * r) : (const void*)m2.UM, v ? 8 : 0);
+          if (r < R2) cp8z(smem_u32(U2s + l2 * L::LDU + r), v ? (const void*)(src + m2.Ifull * r) : (const void*)m2.UM, v);
         }
       }
     };
