@@ -29,6 +29,12 @@
 
 namespace pasd {
 
+#ifndef PASD_P2_ILV
+#define PASD_P2_ILV 1  // next-step staging interleaved with the Wt_2 DMMAs
+#endif
+#ifndef PASD_P2_PAIRBAR
+#define PASD_P2_PAIRBAR 1  // Wt_2 K-half exchange synchronised per warp pair (named barrier)
+#endif
 #ifndef PASD_P2_BW
 #define PASD_P2_BW 12  // i1-block band width of the pencil order
 #endif
@@ -50,6 +56,7 @@ struct Pass2Args {
   double* resid_part;  // [grid][PASD_MAX_ORDER]
   int* bad_part;       // [grid]
   int n1b, n3b, npencils;
+  int nw2;  // Wt_2 partial slices in W2part (fused: 2 per CTA, one per K-half; m8: 1 per CTA)
   int b1;  // i1 extent of a pencil (16 for k_pass2_fused, 8 for k_pass2_m8)
   // unsharded solves: the last CTA runs the iteration's finish (mu schedule,
   // history, stop rule) -- one launch fewer per iteration
@@ -313,8 +320,13 @@ __global__ void __launch_bounds__(P2_THREADS, 1) k_pass2_fused(const Pass2Args a
   const double mu_next = (ctl->mu_max < cand) ? ctl->mu_max : cand;
   const double inv_mu_next = __ddiv_rn(1.0, mu_next);
 
-  double* W2c = a.W2part + (int64_t)blockIdx.x * I2 * R2;  // per-CTA Wt_2 partial
-  for (int64_t idx = tid; idx < I2 * R2; idx += P2_THREADS) W2c[idx] = 0.0;
+  // Wt_2 partials: one per K-half (no exchange after the Wt_2 product) when the
+  // solver sized them so (small I_2 R_2: they stay in L2), else one per CTA
+  // with the two K-halves exchanged through shared memory.
+  const bool w2s = a.nw2 == 2 * (int)gridDim.x;
+  const int NW2 = w2s ? 2 : 1;
+  double* W2c = a.W2part + (int64_t)blockIdx.x * NW2 * I2 * R2;  // per-CTA Wt_2 partial(s)
+  for (int64_t idx = tid; idx < NW2 * I2 * R2; idx += P2_THREADS) W2c[idx] = 0.0;
   // zero padding rows once (never overwritten by the staging copies)
   for (int idx = tid; idx < (RP - R2) * 128; idx += P2_THREADS) A2s[(R2 + idx / 128) * L::LD2 + (idx & 127)] = 0.0;
   for (int idx = tid; idx < (RP - R3) * 128; idx += P2_THREADS) A3s[(R3 + idx / 128) * L::LD3 + (idx & 127)] = 0.0;
@@ -636,19 +648,52 @@ __global__ void __launch_bounds__(P2_THREADS, 1) k_pass2_fused(const Pass2Args a
       }
       // prefetch this step's Wt_2 partial rows (read-modify-write below)
       double w2old[4] = {0, 0, 0, 0};
-      if (kh == 0 && mt < MT) {
+      double* W2k = W2c + (w2s ? (int64_t)kh * I2 * R2 : 0);
+      if ((w2s || kh == 0) && mt < MT) {
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
           const int r = 16 * mt + g + 8 * (q >> 1);
           const int64_t i2 = i2o + 2 * t + (q & 1);
-          if (r < R2 && i2 < I2) w2old[q] = W2c[i2 * R2 + r];
+          if (r < R2 && i2 < I2) w2old[q] = W2k[i2 * R2 + r];
         }
       }
       __syncthreads();  // A1s / A3s / U2s no longer needed this step
-      if (more) {
+      // Next step's staging.  Common case (even R_1 and I_1, every warp in the
+      // Wt_2 product): the copies are issued one or two per Wt_2 k-step, so
+      // their issue overlaps the DMMAs instead of forming a phase of its own.
+      const bool ilv = PASD_P2_ILV && more && (R1 % 2 == 0) && al1 && MT == 4;
+      if (more && !ilv) {
         stage_a1(i2o + P2_B2, A1s);
         stage_a3u2(i2o + P2_B2);
       }
+      // per-thread sources of the interleaved copies (see stage_a1 / stage_a3u2)
+      const int64_t i2n = i2o + P2_B2;
+      const char* ga1 = reinterpret_cast<const char*>(m1.A + (int64_t)R1 * ((i2n + w) + I2 * i3o) + 2 * lane);
+      const bool a1ok = lane < RP / 2 && i2n + w < I2 && 2 * lane < R1;
+      const unsigned sa1 = smem_u32(A1s + w * L::LD1 + 2 * lane);
+      const int c3 = tid & 7, l23 = (tid >> 3) & 7, r03 = tid >> 6;
+      const bool a3ok = i2n + l23 < I2 && nbc1 != 0;
+      const char* ga3 =
+          reinterpret_cast<const char*>(a3ok ? m3.A + i1o + 2 * c3 + I1 * (i2n + l23) + S12 * (int64_t)r03 : m3.A);
+      const int64_t gst3 = a3ok ? 32 * S12 : 0;
+      const unsigned sa3 = smem_u32(A3s + r03 * L::LD3 + 16 * l23 + 2 * c3);
+      const int lu2 = tid & 7;
+      const bool u2ok = i2n + lu2 < I2;
+      const double* gu2 = m2.UM + m2.ioff + i2n + lu2;
+      auto issue_copy = [&](int ks) {  // k-step ks of Wt_2: A_3 row ks, A_1 l3 = ks / 2, UM_2 at the end
+        if (ks < RP / 4 && r03 + 4 * ks < R3) cp16z(sa3 + 32 * ks * L::LD3, ga3 + ks * gst3, a3ok);
+        if ((ks & 1) == 0) {
+          const int k = ks >> 1;
+          if (lane < RP / 2) {
+            const bool ok = a1ok && k < n3v;
+            cp16z(sa1 + 8 * (k * 8 * L::LD1), ok ? (const void*)(ga1 + k * (int64_t)R1 * I2 * 8) : (const void*)m1.A, ok);
+          }
+        }
+        if (ks >= 14) {
+          const int r = (tid >> 3) + 32 * (ks - 14);
+          if (r < R2 && r < RP) cp8z(smem_u32(U2s + lu2 * L::LDU + r), u2ok ? (const void*)(gu2 + m2.Ifull * r) : (const void*)m2.UM, u2ok);
+        }
+      };
       // ---- W-b: Wt_2^T (m-tile mt, K-half kh), K = (i1, i3) ----
       double acc2[4] = {0, 0, 0, 0};
       if (mt < MT) {
@@ -657,6 +702,7 @@ __global__ void __launch_bounds__(P2_THREADS, 1) k_pass2_fused(const Pass2Args a
         const double* rowb = rowa + 8 * L::LD2;
 #pragma unroll
         for (int ks = 0; ks < 16; ++ks) {
+          if (ilv) issue_copy(ks);
           const int k = 64 * kh + 4 * ks + t;
           double(&c)[4] = (ks & 3) == 0 ? acc2 : acc[(ks & 3) - 1];
           double b2;
@@ -670,14 +716,25 @@ __global__ void __launch_bounds__(P2_THREADS, 1) k_pass2_fused(const Pass2Args a
         }
 #pragma unroll
         for (int q = 0; q < 4; ++q) acc2[q] += (acc[0][q] + acc[1][q]) + acc[2][q];
-        if (kh == 1) {
+        if (!w2s && kh == 1) {
 #pragma unroll
           for (int q = 0; q < 4; ++q) Z3s[(mt * 32 + lane) * 4 + q] = acc2[q];  // exchange (Z3s free now)
         }
       }
-      __syncthreads();
+      if (TIO || (!w2s && !PASD_P2_PAIRBAR)) {
+        __syncthreads();
+      } else if (!w2s && mt < MT) {  // only the two K-half warps of m-tile mt exchange
+        asm volatile("bar.sync %0, 64;" ::"r"(1 + mt) : "memory");
+      }
       if (more) load_bricks(i1o, i2o + P2_B2, i3o);  // the bricks are free: next step's T, Y (TIO)
-      if (kh == 0 && mt < MT) {
+      if (w2s && mt < MT) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int r = 16 * mt + g + 8 * (q >> 1);
+          const int64_t i2 = i2o + 2 * t + (q & 1);
+          if (r < R2 && i2 < I2) W2k[i2 * R2 + r] = w2old[q] + acc2[q];
+        }
+      } else if (!w2s && kh == 0 && mt < MT) {
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
           const int r = 16 * mt + g + 8 * (q >> 1);
@@ -835,7 +892,7 @@ __global__ void k_pass2_reduce(const Pass2Args a, int nblk, Ctl* ctl, double* g2
         const int ib = (int)(i / a.b1), l = (int)(i % a.b1);
         for (int b3 = lane; b3 < a.n3b; b3 += 32) s += a.W1p[((int64_t)(ib + a.n1b * b3) * a.b1 + l) * R + r];
       } else if (n == 1) {
-        for (int c = lane; c < nblk; c += 32) s += a.W2part[((int64_t)c * m.I + i) * R + r];
+        for (int c = lane; c < a.nw2; c += 32) s += a.W2part[((int64_t)c * m.I + i) * R + r];
       } else {
         const int ib = (int)(i / P2_B3), l = (int)(i % P2_B3);
         for (int b1 = lane; b1 < a.n1b; b1 += 32) s += a.W3p[((int64_t)(b1 + a.n1b * ib) * 8 + l) * R + r];

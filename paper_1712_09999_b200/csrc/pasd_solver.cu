@@ -663,7 +663,12 @@ pasd_solver* create_solver(const pasd_options* o, const pasd_shard* shard) {
     s->p2_smem = s->use_m8 ? 0 : pass2_smem(s->p2_rp, s->p2_tio);
     a.W1p = s->alloc<double>((size_t)a.npencils * a.b1 * s->modes[0].R);
     a.W3p = s->alloc<double>((size_t)a.npencils * 8 * s->modes[2].R);
-    a.W2part = s->alloc<double>((size_t)s->p2_grid * s->dims[1] * s->modes[1].R);
+    // Wt_2 partials: one per K-half of each CTA while they stay small next to L2
+    // (C3 38 MB, C4 18 MB: one barrier per step fewer, -2..5% pass 2); at C5 the
+    // 118 MB they would take thrash L2 (+1 ms), so one per CTA there.
+    const double w2_split_bytes = 2.0 * s->p2_grid * (double)s->dims[1] * s->modes[1].R * sizeof(double);
+    a.nw2 = (!s->use_m8 && !s->p2_tio && w2_split_bytes <= 48e6) ? 2 * s->p2_grid : s->p2_grid;
+    a.W2part = s->alloc<double>((size_t)a.nw2 * s->dims[1] * s->modes[1].R);
     a.gpart = s->alloc<double>((size_t)s->p2_grid * 3);
     s->p2_resid = s->alloc<double>((size_t)s->p2_grid * PASD_MAX_ORDER);
     s->p2_bad = s->alloc<int>(s->p2_grid);
