@@ -223,3 +223,95 @@ def test_tma_element_streams_match_plain(monkeypatch):
     assert plain.iters == tio.iters
     np.testing.assert_array_equal(plain.x, tio.x)
     np.testing.assert_array_equal(plain.e, tio.e)
+
+
+def _oracle_pair(oracle_mod, dims, ranks, k, seed=3, rho=0.05):
+    """Oracle iterates k and k+1 of a low-rank instance (full-rank phase)."""
+    L0 = oracle_mod.gen_tucker(dims, list(ranks), seed=seed)
+    T = oracle_mod.corrupt_sparse(L0, rho, seed=seed)
+    cfg = PasdConfig(lambdas=oracle_mod.default_lambdas(dims), ranks=list(ranks), eps=1e-12, maxiter=k + 1)
+    snaps = {}
+
+    def obs(v):
+        if v.iter in (k, k + 1):
+            snaps[v.iter] = v
+
+    oracle_mod.pasd_recover(T, cfg, observer=obs, fixed_iters=True, threads=8)
+    a, b = snaps[k], snaps[k + 1]
+    for n, x in enumerate(a.v):  # Procrustes is unique only with full-rank V_n
+        assert np.linalg.matrix_rank(x) == ranks[n]
+    return T, cfg, a, b
+
+
+@pytest.mark.parametrize("dims,ranks,variant", [((50, 44, 41), (34, 34, 34), "M16"),  # RP 40 (C3's template)
+                                                ((64, 60, 40), (30, 30, 15), "M16"),  # RP 32, mixed ranks (C4-like)
+                                                ((66, 60, 57), (50, 50, 50), "M16"),  # RP 56 (C5's template)
+                                                ((72, 64, 60), (20, 20, 20), "M16"),  # RP 24 on both pass-2 variants
+                                                ((72, 64, 60), (20, 20, 20), "M8")])
+def test_single_step_parity_dmma_pass2(gpu, oracle_mod, monkeypatch, dims, ranks, variant):
+    """The DMMA pass 2 (k_pass2_fused 16x8x8, the bench's dominant kernel, and
+    k_pass2_m8 8x8x8) and the DMMA pass 1 at the BASELINE padded ranks, on
+    ragged bricks: inject the oracle's iterate k (full-rank phase), run one GPU
+    iteration, compare with the oracle's iterate k+1."""
+    T, cfg, a, b = _oracle_pair(oracle_mod, dims, ranks, k=130)
+    monkeypatch.setenv("PASD_PASS2_" + variant, "1")
+    s = gpu.Solver(T.shape, cfg, fixed_iters=True)
+    s.load(T)
+    s.set_state(a.e, a.y, a.u, a.v, a.mu_next, a.iter)
+    s.run(1)
+    r = s.finalize(want_z=True, want_y=True)
+    s.close()
+    assert r.iters == 131
+    assert rel(r.e, b.e) <= 1e-10
+    assert np.flatnonzero((r.e != 0) != (b.e != 0)).size <= 2
+    for n in range(3):
+        assert rel(r.z[n], b.z[n]) <= 1e-11
+        assert rel(r.y[n], b.y[n]) <= 1e-9
+    np.testing.assert_allclose(r.final_residuals, b.residual_inf, rtol=1e-6, atol=1e-12 * np.abs(T).max())
+
+
+@pytest.mark.parametrize("config", ["c3", "c4"])
+def test_full_size_trivial_phase_bit_exact(gpu, config):
+    """BASELINE full sizes (C3 400^3 R=40, C4 256x256x1024 R=(30,30,15)) through a
+    size-independent property: in the V = 0 phase (Z_n = 0) every entry of E
+    and Y_n follows the reference's elementwise recurrence (pasd.cpp:170-229,
+    SURVEY Appendix A), so a 2^20-entry sample recomputed in numpy (IEEE, no
+    FMA) must match the GPU bit for bit after 30 iterations."""
+    import torch
+
+    from paper_1712_09999_b200.workloads import WORKLOADS, generate_gpu
+
+    w = WORKLOADS[config]
+    K = 30
+    T = generate_gpu(w, seed=0)
+    cfg = PasdConfig(lambdas=w.lambdas(), ranks=list(w.ranks), maxiter=K)
+    s = gpu.Solver(w.dims, cfg, fixed_iters=True)
+    s.load(T.data_ptr(), t_is_device=True)
+    s.run(K)
+    r = s.finalize(want_x=False, want_e=True, want_y=True)
+    s.close()
+    assert r.iters == K
+    flat = T.reshape(-1)  # torch (i1 fastest, like the solver) -- same flat order as r.e
+    idx = np.random.default_rng(1).choice(flat.numel(), 1 << 20, replace=False)
+    t = flat[torch.from_numpy(idx).to(flat.device)].cpu().numpy().astype(np.float64)
+    del T, flat
+    torch.cuda.empty_cache()
+    N = 3
+    y = [np.zeros_like(t) for _ in range(N)]
+    e = np.zeros_like(t)
+    mu = cfg.mu0
+    for _ in range(K):
+        inv_mu = 1.0 / mu
+        h = np.zeros_like(t)
+        for n in range(N):
+            h = h + ((t - 0.0) + y[n] * inv_mu)
+        x = h * (1.0 / N)
+        tau = 1.0 / (mu * N)
+        e = np.where(x > tau, x - tau, np.where(x < -tau, x + tau, 0.0))
+        for n in range(N):
+            y[n] = y[n] + mu * ((t - 0.0) - e)
+        mu = min(cfg.rho * mu, cfg.mu_max)
+    np.testing.assert_array_equal(r.e.reshape(-1, order="F")[idx], e)  # solver order: i1 fastest
+    for n in range(N):
+        np.testing.assert_array_equal(r.y[n].reshape(-1, order="F")[idx], y[n])
+    assert r.objective == pytest.approx(np.abs(r.e).sum(), rel=1e-12)  # V_n = 0: objective = ||E||_1
