@@ -471,6 +471,24 @@ __global__ void k_materialize_z(ModeDev m, double* __restrict__ out, int64_t S) 
   }
 }
 
+// Z_n materialised and accumulated straight into x (no Z_n buffer): the same
+// fma chain as k_materialize_z, then x = x + c * z as k_accum_x (bit-identical
+// to the two-kernel sequence, one tensor write instead of three passes).
+__global__ void k_materialize_accum_x(ModeDev m, double* __restrict__ x, double c, int first, int64_t S) {
+  for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < S; idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t rest = idx / m.inner;
+    const int64_t p = idx - rest * m.inner;
+    const int64_t q = rest / m.I;
+    const int64_t i = rest - q * m.I;
+    const double* a = m.A + p + m.inner * (int64_t)m.R * q;
+    const double* um = m.UM + m.ioff + i;
+    double z = 0.0;
+    for (int r = 0; r < m.R; ++r) z = fma(um[m.Ifull * r], a[m.inner * r], z);
+    const double prev = first ? 0.0 : x[idx];
+    x[idx] = __dadd_rn(prev, __dmul_rn(c, z));
+  }
+}
+
 // x = x + (w_n / wsum) * z_n, accumulated from zero in mode order (recovery.cpp:12-23).
 __global__ void k_accum_x(double* __restrict__ x, const double* __restrict__ z, double c, int first, int64_t S) {
   for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < S; idx += (int64_t)gridDim.x * blockDim.x) {

@@ -198,6 +198,9 @@ struct pasd_solver {
   ncclComm_t comm = nullptr;
   cudaStream_t side = nullptr;  // A_3 all-reduce, overlapped with pass 1 of modes 1 and 2
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  // finalisation: D2H of E on its own stream, overlapping the X materialisation
+  cudaStream_t xfer = nullptr;
+  cudaEvent_t ev_xfork = nullptr, ev_xjoin = nullptr;
   double* A3_partial = nullptr;
   std::vector<double*> gram_partial, wt_partial;
   double* g2_partial = nullptr;
@@ -209,6 +212,9 @@ struct pasd_solver {
     if (ev_fork) cudaEventDestroy(ev_fork);
     if (ev_join) cudaEventDestroy(ev_join);
     if (side) cudaStreamDestroy(side);
+    if (ev_xfork) cudaEventDestroy(ev_xfork);
+    if (ev_xjoin) cudaEventDestroy(ev_xjoin);
+    if (xfer) cudaStreamDestroy(xfer);
     if (graph_exec) cudaGraphExecDestroy(graph_exec);
     if (graph) cudaGraphDestroy(graph);
     for (void* p : owned) cudaFree(p);
@@ -452,11 +458,13 @@ __global__ void k_init_state(ModePack* mp, Ctl* ctl, double mu0, double rho, dou
   }
 }
 
-void reset_state(pasd_solver* s) {
+// copy_d = false when a new tensor is loaded next (load_tensor forms D = T - E itself)
+void reset_state(pasd_solver* s, bool copy_d = true) {
   CK(cudaMemsetAsync(s->E[0], 0, s->S * sizeof(double), s->stream));
   CK(cudaMemsetAsync(s->E[1], 0, s->S * sizeof(double), s->stream));
   for (int n = 0; n < s->N; ++n) CK(cudaMemsetAsync(s->Y[n], 0, s->S * sizeof(double), s->stream));
-  CK(cudaMemcpyAsync(s->D, s->T, s->S * sizeof(double), cudaMemcpyDeviceToDevice, s->stream));  // D = T - 0
+  if (copy_d)
+    CK(cudaMemcpyAsync(s->D, s->T, s->S * sizeof(double), cudaMemcpyDeviceToDevice, s->stream));  // D = T - 0
   k_init_state<<<64, 256, 0, s->stream>>>(s->d_pack, s->d_ctl, s->mu0, s->rho, s->mu_max, s->eps, s->maxiter,
                                           (s->flags & PASD_FLAG_FIXED_ITERS) ? 1 : 0);
   CK(cudaGetLastError());
@@ -530,6 +538,9 @@ pasd_solver* create_solver(const pasd_options* o, const pasd_shard* shard) {
   s->device = o->device;
   CK(cudaSetDevice(s->device));
   CK(cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking));
+  CK(cudaStreamCreateWithFlags(&s->xfer, cudaStreamNonBlocking));
+  CK(cudaEventCreateWithFlags(&s->ev_xfork, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&s->ev_xjoin, cudaEventDisableTiming));
   const int64_t S = s->S;
   s->T = s->alloc<double>(S);
   s->E[0] = s->alloc<double>(S);
@@ -707,9 +718,22 @@ void sync_ctl(pasd_solver* s) {
   CK(cudaStreamSynchronize(s->stream));
 }
 
-void load_tensor(pasd_solver* s, const double* t, int is_device) {
-  CK(cudaMemcpyAsync(s->T, t, s->S * sizeof(double), is_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
-                     s->stream));
+// Upload T on the transfer stream (forked from the solver stream's current
+// point), so state resets queued on the solver stream afterwards overlap it.
+void begin_upload(pasd_solver* s, const double* t) {
+  CK(cudaEventRecord(s->ev_xfork, s->stream));
+  CK(cudaStreamWaitEvent(s->xfer, s->ev_xfork, 0));
+  CK(cudaMemcpyAsync(s->T, t, s->S * sizeof(double), cudaMemcpyHostToDevice, s->xfer));
+  CK(cudaEventRecord(s->ev_xjoin, s->xfer));
+}
+
+// uploaded: T already issued by begin_upload (the solver stream joins it here)
+void load_tensor(pasd_solver* s, const double* t, int is_device, bool uploaded = false) {
+  if (uploaded)
+    CK(cudaStreamWaitEvent(s->stream, s->ev_xjoin, 0));
+  else
+    CK(cudaMemcpyAsync(s->T, t, s->S * sizeof(double), is_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
+                       s->stream));
   CK(cudaMemsetAsync(s->d_flag, 0, sizeof(int), s->stream));
   k_nonfinite<<<1184, 256, 0, s->stream>>>(s->T, s->S, s->d_flag);
   k_tsub<<<1184, 256, 0, s->stream>>>(s->D, s->T, s->E[0], s->E[1], s->S, s->d_ctl);  // keep D = T - E
@@ -902,15 +926,25 @@ void finalize_solver(pasd_solver* s, pasd_outputs* out) {
   for (double w : s->alphas) wsum += w;
   const int blocks = 1184;
   const bool want_x = out->x != nullptr;
+  if (out->e) {  // E is final: its download overlaps the X materialisation below
+    CK(cudaEventRecord(s->ev_xfork, st));
+    CK(cudaStreamWaitEvent(s->xfer, s->ev_xfork, 0));
+    CK(cudaMemcpyAsync(out->e, e, S * sizeof(double), cudaMemcpyDeviceToHost, s->xfer));
+    CK(cudaEventRecord(s->ev_xjoin, s->xfer));
+  }
   for (int n = 0; n < N; ++n) {
     const bool want_z = out->z && out->z[n];
     if (!want_x && !want_z) continue;
-    k_materialize_z<<<blocks, 256, 0, st>>>(s->modes[n], s->zbuf, S);
-    if (want_x) k_accum_x<<<blocks, 256, 0, st>>>(s->xbuf, s->zbuf, s->alphas[n] / wsum, n == 0, S);
-    if (want_z) CK(cudaMemcpyAsync(out->z[n], s->zbuf, S * sizeof(double), cudaMemcpyDeviceToHost, st));
+    if (want_z) {
+      k_materialize_z<<<blocks, 256, 0, st>>>(s->modes[n], s->zbuf, S);
+      if (want_x) k_accum_x<<<blocks, 256, 0, st>>>(s->xbuf, s->zbuf, s->alphas[n] / wsum, n == 0, S);
+      CK(cudaMemcpyAsync(out->z[n], s->zbuf, S * sizeof(double), cudaMemcpyDeviceToHost, st));
+    } else {
+      k_materialize_accum_x<<<blocks, 256, 0, st>>>(s->modes[n], s->xbuf, s->alphas[n] / wsum, n == 0, S);
+    }
   }
   if (want_x) CK(cudaMemcpyAsync(out->x, s->xbuf, S * sizeof(double), cudaMemcpyDeviceToHost, st));
-  if (out->e) CK(cudaMemcpyAsync(out->e, e, S * sizeof(double), cudaMemcpyDeviceToHost, st));
+  if (out->e) CK(cudaStreamWaitEvent(st, s->ev_xjoin, 0));
   // objective = ||E||_1 + sum_n lambda_n ||V_n||_*  (pasd.cpp:263-266)
   std::vector<double> sums(blocks), maxs(blocks);
   auto abs_stats = [&](const double* x, double* sum, double* mx) {
@@ -1172,15 +1206,18 @@ int pasd_b200_recover(const double* t, const pasd_options* opt, pasd_outputs* ou
       std::lock_guard<std::mutex> lk(g_cache_mu);
       if (g_cache && key == g_cache_key) std::swap(s, g_cache);  // take it (concurrent calls build their own)
     }
+    bool uploaded = false;
     if (s) {
       validate_options(opt);
       CK(cudaSetDevice(s->device));
-      reset_state(s);
+      begin_upload(s, t);         // H2D of T ...
+      reset_state(s, false);      // ... overlaps the E / Y resets
+      uploaded = true;
     } else {
       s = create_solver(opt, nullptr);
     }
     const auto t1 = now();
-    load_tensor(s, t, 0);
+    load_tensor(s, t, 0, uploaded);
     const auto t2 = now();
     run_solver(s, s->maxiter, observer, user);
     const auto t3 = now();
