@@ -191,11 +191,7 @@ __global__ void k_gram_reduce_all(const ModePack* __restrict__ mp, const Ctl* ct
 
 template <int RP>
 void launch_gram_all_rp(const ModePack* mp, const Ctl* ctl, int grid, cudaStream_t st) {
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_gram_all<RP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GramLayout<RP>::bytes);
-    attr = true;
-  }
+  ensure_smem_attr<k_gram_all<RP>>(GramLayout<RP>::bytes);
   k_gram_all<RP><<<grid, GM_THREADS, GramLayout<RP>::bytes, st>>>(mp, ctl);
 }
 
@@ -215,11 +211,7 @@ inline void launch_gram_all(int rp, const ModePack* mp, const Ctl* ctl, int grid
 template <int RP>
 void launch_gram_rp(const ModeDev& m, const Ctl* ctl, cudaStream_t st) {
   using L = GramLayout<RP>;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_gram_mma<RP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::bytes);
-    attr = true;
-  }
+  ensure_smem_attr<k_gram_mma<RP>>(L::bytes);
   k_gram_mma<RP><<<m.nkc_g, GM_THREADS, L::bytes, st>>>(m, ctl);
 }
 

@@ -19,6 +19,24 @@
 
 #include "pasd_common.cuh"
 
+#include <atomic>
+
+namespace pasd {
+// cudaFuncAttributeMaxDynamicSharedMemorySize is per (kernel, device): set it
+// once per device a process launches on (a process may drive several GPUs).
+template <auto Kernel>
+inline void ensure_smem_attr(size_t bytes) {
+  static std::atomic<unsigned long long> done{0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const unsigned long long bit = 1ull << (dev & 63);
+  if (!(done.load(std::memory_order_acquire) & bit)) {
+    cudaFuncSetAttribute(Kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    done.fetch_or(bit, std::memory_order_acq_rel);
+  }
+}
+}  // namespace pasd
+
 namespace pasd {
 
 constexpr int kThreads = 256;

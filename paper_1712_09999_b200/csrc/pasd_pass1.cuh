@@ -269,11 +269,7 @@ template <int RP, bool CONTIG>
 void launch_p1(const ModeDev& m, const double* D, const double* Y, const Ctl* ctl,
                int grid, cudaStream_t st) {
   using L = P1Layout<RP, CONTIG>;
-  static bool attr = false;  // idempotent attribute set
-  if (!attr) {
-    cudaFuncSetAttribute(k_pass1<RP, CONTIG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::bytes);
-    attr = true;
-  }
+  ensure_smem_attr<k_pass1<RP, CONTIG>>(L::bytes);
   k_pass1<RP, CONTIG><<<grid, P1_THREADS, L::bytes, st>>>(m, D, Y, ctl);
 }
 

@@ -29,9 +29,6 @@
 
 namespace pasd {
 
-#ifndef PASD_P2_ILV
-#define PASD_P2_ILV 1  // next-step staging interleaved with the Wt_2 DMMAs
-#endif
 #ifndef PASD_P2_PAIRBAR
 #define PASD_P2_PAIRBAR 1  // Wt_2 K-half exchange synchronised per warp pair (named barrier)
 #endif
@@ -658,42 +655,10 @@ __global__ void __launch_bounds__(P2_THREADS, 1) k_pass2_fused(const Pass2Args a
         }
       }
       __syncthreads();  // A1s / A3s / U2s no longer needed this step
-      // Next step's staging.  Common case (even R_1 and I_1, every warp in the
-      // Wt_2 product): the copies are issued one or two per Wt_2 k-step, so
-      // their issue overlaps the DMMAs instead of forming a phase of its own.
-      const bool ilv = PASD_P2_ILV && more && (R1 % 2 == 0) && al1 && MT == 4;
-      if (more && !ilv) {
+      if (more) {
         stage_a1(i2o + P2_B2, A1s);
         stage_a3u2(i2o + P2_B2);
       }
-      // per-thread sources of the interleaved copies (see stage_a1 / stage_a3u2)
-      const int64_t i2n = i2o + P2_B2;
-      const char* ga1 = reinterpret_cast<const char*>(m1.A + (int64_t)R1 * ((i2n + w) + I2 * i3o) + 2 * lane);
-      const bool a1ok = lane < RP / 2 && i2n + w < I2 && 2 * lane < R1;
-      const unsigned sa1 = smem_u32(A1s + w * L::LD1 + 2 * lane);
-      const int c3 = tid & 7, l23 = (tid >> 3) & 7, r03 = tid >> 6;
-      const bool a3ok = i2n + l23 < I2 && nbc1 != 0;
-      const char* ga3 =
-          reinterpret_cast<const char*>(a3ok ? m3.A + i1o + 2 * c3 + I1 * (i2n + l23) + S12 * (int64_t)r03 : m3.A);
-      const int64_t gst3 = a3ok ? 32 * S12 : 0;
-      const unsigned sa3 = smem_u32(A3s + r03 * L::LD3 + 16 * l23 + 2 * c3);
-      const int lu2 = tid & 7;
-      const bool u2ok = i2n + lu2 < I2;
-      const double* gu2 = m2.UM + m2.ioff + i2n + lu2;
-      auto issue_copy = [&](int ks) {  // k-step ks of Wt_2: A_3 row ks, A_1 l3 = ks / 2, UM_2 at the end
-        if (ks < RP / 4 && r03 + 4 * ks < R3) cp16z(sa3 + 32 * ks * L::LD3, ga3 + ks * gst3, a3ok);
-        if ((ks & 1) == 0) {
-          const int k = ks >> 1;
-          if (lane < RP / 2) {
-            const bool ok = a1ok && k < n3v;
-            cp16z(sa1 + 8 * (k * 8 * L::LD1), ok ? (const void*)(ga1 + k * (int64_t)R1 * I2 * 8) : (const void*)m1.A, ok);
-          }
-        }
-        if (ks >= 14) {
-          const int r = (tid >> 3) + 32 * (ks - 14);
-          if (r < R2 && r < RP) cp8z(smem_u32(U2s + lu2 * L::LDU + r), u2ok ? (const void*)(gu2 + m2.Ifull * r) : (const void*)m2.UM, u2ok);
-        }
-      };
       // ---- W-b: Wt_2^T (m-tile mt, K-half kh), K = (i1, i3) ----
       double acc2[4] = {0, 0, 0, 0};
       if (mt < MT) {
@@ -702,7 +667,6 @@ __global__ void __launch_bounds__(P2_THREADS, 1) k_pass2_fused(const Pass2Args a
         const double* rowb = rowa + 8 * L::LD2;
 #pragma unroll
         for (int ks = 0; ks < 16; ++ks) {
-          if (ilv) issue_copy(ks);
           const int k = 64 * kh + 4 * ks + t;
           double(&c)[4] = (ks & 3) == 0 ? acc2 : acc[(ks & 3) - 1];
           double b2;
