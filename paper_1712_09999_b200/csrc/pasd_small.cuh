@@ -20,7 +20,10 @@
 
 namespace pasd {
 
-constexpr int kSmallThreads = 256;
+#ifndef PASD_SMALL_THREADS
+#define PASD_SMALL_THREADS 256
+#endif
+constexpr int kSmallThreads = PASD_SMALL_THREADS;
 
 // Shared-memory workspace of one small-solve CTA (dynamic smem).
 struct SmallWs {
@@ -73,7 +76,7 @@ __device__ __forceinline__ int rr_pos(int m, int round, int Rp) {
 // On exit diag(S) holds eigenvalues, ws.V (row-major) the eigenvectors as
 // columns: S_in = V diag V^T.  Then sorts eigenpairs descending into
 // lam[0..n) and the columns of V.
-__device__ void cta_jacobi_eig(SmallWs& ws, int n) {
+__device__ void cta_jacobi_eig(SmallWs& ws, int n, int tag = 0) {
   const int Rp = ws.Rp, ld = ws.ld, tid = threadIdx.x, nt = blockDim.x;
   double* S = ws.S;
   double* V = ws.V;
@@ -85,6 +88,22 @@ __device__ void cta_jacobi_eig(SmallWs& ws, int n) {
   }
   __syncthreads();
   const int npairs = Rp / 2;
+  // this thread's block items (ja, jb) and V items (pair j, row k), fixed for the call
+  constexpr int JB_MAX = (PASD_MAX_RANK / 2 * PASD_MAX_RANK / 2 + kSmallThreads - 1) / kSmallThreads;
+  constexpr int JV_MAX = (PASD_MAX_RANK / 2 * PASD_MAX_RANK + kSmallThreads - 1) / kSmallThreads;
+  int bja[JB_MAX], bjb[JB_MAX], vj[JV_MAX], vk[JV_MAX];
+#pragma unroll
+  for (int u = 0; u < JB_MAX; ++u) {
+    const int bidx = tid + u * nt;
+    bja[u] = bidx < npairs * npairs ? bidx / npairs : -1;
+    bjb[u] = bidx < npairs * npairs ? bidx % npairs : 0;
+  }
+#pragma unroll
+  for (int u = 0; u < JV_MAX; ++u) {
+    const int idx = tid + u * nt;
+    vj[u] = idx < npairs * Rp ? idx / Rp : -1;
+    vk[u] = idx < npairs * Rp ? idx % Rp : 0;
+  }
   __shared__ int rotated;
   for (int sweep = 0; sweep < 30 && Rp > 1; ++sweep) {
     if (tid == 0) rotated = 0;
@@ -114,9 +133,12 @@ __device__ void cta_jacobi_eig(SmallWs& ws, int n) {
       // Apply the round's disjoint rotations: S <- J^T S J block by block (the
       // 2 x 2 block of pairs (ja, jb) depends only on itself; rows first, then
       // columns, the same operation order as separate row and column passes)
-      // and V <- V J.  One barrier per round instead of two.
-      for (int bidx = tid; bidx < npairs * npairs; bidx += nt) {
-        const int ja = bidx / npairs, jb = bidx - ja * npairs;
+      // and V <- V J.  One barrier per round instead of two.  Work items are
+      // assigned once per call (no integer divisions inside the rounds).
+#pragma unroll
+      for (int u = 0; u < JB_MAX; ++u) {
+        if (bja[u] < 0) continue;
+        const int ja = bja[u], jb = bjb[u];
         const double sa = ws.sn[ja], sb = ws.sn[jb];
         if (sa == 0.0 && sb == 0.0) continue;
         const double ca = ws.cs[ja], cb = ws.cs[jb];
@@ -137,8 +159,10 @@ __device__ void cta_jacobi_eig(SmallWs& ws, int n) {
         S[qa * ld + pb] = a10;
         S[qa * ld + qb] = a11;
       }
-      for (int idx = tid; idx < npairs * Rp; idx += nt) {  // columns p, q of V
-        const int j = idx / Rp, k = idx - j * Rp;
+#pragma unroll
+      for (int u = 0; u < JV_MAX; ++u) {  // columns p, q of V
+        if (vj[u] < 0) continue;
+        const int j = vj[u], k = vk[u];
         const double s = ws.sn[j];
         if (s == 0.0) continue;
         const int p = ws.pq[2 * j], q = ws.pq[2 * j + 1];
@@ -151,7 +175,7 @@ __device__ void cta_jacobi_eig(SmallWs& ws, int n) {
     }
     if (rotated == 0) {
 #ifdef PASD_DEBUG_SWEEPS
-      if (tid == 0) printf("jacobi n=%d block=%d sweeps=%d\n", n, blockIdx.x, sweep + 1);
+      if (tid == 0) printf("jacobi n=%d block=%d tag=%d sweeps=%d\n", n, blockIdx.x, tag, sweep + 1);
 #endif
       break;
     }
@@ -228,13 +252,26 @@ __device__ void cta_warm_finish(SmallWs& ws, int R) {  // V <- Q V
 }
 
 // out(R x R2, smem row-major ld) = X^T Y with X (I x R), Y (I x R2) global column-major.
+// Rows of X and Y stream through shared memory in 32-row chunks; each thread
+// owns up to GT_MAX output entries (tid, tid + nt, ...) in registers, so the
+// FMA chains of different entries interleave (the small solves are latency
+// bound).  Per entry the sum still runs over i in ascending order from 0.
+constexpr int GT_MAX = (PASD_MAX_RANK * PASD_MAX_RANK + kSmallThreads - 1) / kSmallThreads;
 __device__ void cta_gram_tn(const double* X, const double* Y, int64_t I, int R, int R2, double* out, int ld,
                             double* stage /* 2 x 32 x ld */) {
   const int tid = threadIdx.x, nt = blockDim.x;
+  const int ne = R * R2;
   double* Xs = stage;
   double* Ys = stage + 32 * ld;
-  for (int idx = tid; idx < R * R2; idx += nt) out[(idx / R2) * ld + idx % R2] = 0.0;
-  __syncthreads();
+  double acc[GT_MAX];
+  int ro[GT_MAX], so[GT_MAX];
+#pragma unroll
+  for (int e = 0; e < GT_MAX; ++e) {
+    const int idx = tid + e * nt;
+    acc[e] = 0.0;
+    ro[e] = idx < ne ? idx / R2 : 0;
+    so[e] = idx < ne ? idx % R2 : 0;
+  }
   for (int64_t i0 = 0; i0 < I; i0 += 32) {
     const int ic = (int)imin64(32, I - i0);
     for (int idx = tid; idx < 32 * R; idx += nt) {
@@ -246,25 +283,31 @@ __device__ void cta_gram_tn(const double* X, const double* Y, int64_t I, int R, 
       Ys[il * ld + r] = il < ic ? Y[i0 + il + I * r] : 0.0;
     }
     __syncthreads();
-    for (int idx = tid; idx < R * R2; idx += nt) {
-      const int r = idx / R2, s = idx % R2;
-      double a = out[r * ld + s];
-      for (int il = 0; il < ic; ++il) a = fma(Xs[il * ld + r], Ys[il * ld + s], a);
-      out[r * ld + s] = a;
+    for (int il = 0; il < ic; ++il) {
+#pragma unroll
+      for (int e = 0; e < GT_MAX; ++e)
+        if (tid + e * nt < ne) acc[e] = fma(Xs[il * ld + ro[e]], Ys[il * ld + so[e]], acc[e]);
     }
     __syncthreads();
   }
+#pragma unroll
+  for (int e = 0; e < GT_MAX; ++e)
+    if (tid + e * nt < ne) out[ro[e] * ld + so[e]] = acc[e];
+  __syncthreads();
 }
 
-// out(I x R2, global col-major) = X (I x R, global col-major) * B (R x R2, smem row-major ld)
 // out (I x R2, col-major) = X (I x R, col-major) B (R x R2, smem row-major, ld).
-// 64-row chunks of X are staged in shared memory with coalesced loads; each
-// thread then forms one output column entry for 4 rows (B value reused).
-// The sum over r runs in index order from 0 (same result as the unstaged
-// loop).  `stage`: 64 x ld doubles.
+// 64-row chunks of X are staged in shared memory with coalesced loads; thread
+// (q = tid % 16, column group tid / 16) forms the 4 rows q, q+16, q+32, q+48
+// of up to MN_MAXC columns c, c + nt/16, ... (16 independent accumulators;
+// each X value is reused across its columns, each B value across its rows).
+// The sum over r runs in index order from 0 (same result as an unstaged loop).
+// `stage`: 64 x ld doubles.
+constexpr int MN_MAXC = (PASD_MAX_RANK + kSmallThreads / 16 - 1) / (kSmallThreads / 16);
 __device__ void cta_mul_nn(const double* X, int64_t I, int R, const double* B, int ld, int R2, double* out,
                            double* stage) {
   const int tid = threadIdx.x, nt = blockDim.x;
+  const int q = tid & 15, cg = tid >> 4, ncg = nt >> 4;
   for (int64_t i0 = 0; i0 < I; i0 += 64) {
     const int ic = (int)imin64(64, I - i0);
     for (int idx = tid; idx < 64 * R; idx += nt) {
@@ -272,21 +315,34 @@ __device__ void cta_mul_nn(const double* X, int64_t I, int R, const double* B, i
       stage[il * ld + r] = il < ic ? X[i0 + il + I * r] : 0.0;
     }
     __syncthreads();
-    for (int idx = tid; idx < 16 * R2; idx += nt) {
-      const int q = idx & 15, c = idx >> 4;
-      double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-      for (int r = 0; r < R; ++r) {
-        const double b = B[r * ld + c];
-        a0 = fma(stage[q * ld + r], b, a0);
-        a1 = fma(stage[(q + 16) * ld + r], b, a1);
-        a2 = fma(stage[(q + 32) * ld + r], b, a2);
-        a3 = fma(stage[(q + 48) * ld + r], b, a3);
+    double a[MN_MAXC][4];
+#pragma unroll
+    for (int k = 0; k < MN_MAXC; ++k) a[k][0] = a[k][1] = a[k][2] = a[k][3] = 0.0;
+    for (int r = 0; r < R; ++r) {
+      const double x0 = stage[q * ld + r], x1 = stage[(q + 16) * ld + r];
+      const double x2 = stage[(q + 32) * ld + r], x3 = stage[(q + 48) * ld + r];
+#pragma unroll
+      for (int k = 0; k < MN_MAXC; ++k) {
+        const int c = cg + k * ncg;
+        if (c < R2) {
+          const double b = B[r * ld + c];
+          a[k][0] = fma(x0, b, a[k][0]);
+          a[k][1] = fma(x1, b, a[k][1]);
+          a[k][2] = fma(x2, b, a[k][2]);
+          a[k][3] = fma(x3, b, a[k][3]);
+        }
       }
-      double* o = out + i0 + I * c;
-      if (q < ic) o[q] = a0;
-      if (q + 16 < ic) o[q + 16] = a1;
-      if (q + 32 < ic) o[q + 32] = a2;
-      if (q + 48 < ic) o[q + 48] = a3;
+    }
+#pragma unroll
+    for (int k = 0; k < MN_MAXC; ++k) {
+      const int c = cg + k * ncg;
+      if (c < R2) {
+        double* o = out + i0 + I * c;
+        if (q < ic) o[q] = a[k][0];
+        if (q + 16 < ic) o[q + 16] = a[k][1];
+        if (q + 32 < ic) o[q + 32] = a[k][2];
+        if (q + 48 < ic) o[q + 48] = a[k][3];
+      }
     }
     __syncthreads();
   }
@@ -304,7 +360,7 @@ __device__ void svt_mode(const ModeDev& m, int n, Ctl* ctl, double* smem) {
   for (int idx = tid; idx < R * R; idx += nt) ws.S[(idx / R) * ld + idx % R] = m.Gram[idx];
   __syncthreads();
   cta_warm_start(ws, R, m.P);  // previous eigenvectors: Gram changes slowly between iterations
-  cta_jacobi_eig(ws, R);
+  cta_jacobi_eig(ws, R, 1);
   cta_warm_finish(ws, R);
   const double tau = __ddiv_rn(m.lambda, ctl->mu);  // lambda / mu (pasd.cpp:77)
   if (tid == 0) {
@@ -389,7 +445,7 @@ __global__ void __launch_bounds__(kSmallThreads) k_polar(const ModePack* __restr
   // 3. first Gram/Jacobi pass: C = W^T W = Q1 L Q1^T ; X2 = W Q1
   cta_gram_tn(X, X, I, R, R, ws.S, ld, ws.T64);
   cta_warm_start(ws, R, m.Qp);  // previous right rotation
-  cta_jacobi_eig(ws, R);
+  cta_jacobi_eig(ws, R, 2);
   cta_warm_finish(ws, R);
   for (int idx = tid; idx < R * R; idx += nt) ws.Q[(idx / R) * ld + idx % R] = ws.V[(idx / R) * ld + idx % R];
   __syncthreads();
@@ -405,7 +461,7 @@ __global__ void __launch_bounds__(kSmallThreads) k_polar(const ModePack* __restr
 #endif
   // 4. second pass on the rotated columns: C2 = X2^T X2 = Q2 L2 Q2^T ; X = X2 Q2 ; Q = Q1 Q2
   cta_gram_tn(X2, X2, I, R, R, ws.S, ld, ws.T64);
-  cta_jacobi_eig(ws, R);
+  cta_jacobi_eig(ws, R, 3);
   cta_mul_nn(X2, I, R, ws.V, ld, R, X, ws.T64);
   for (int idx = tid; idx < R * R; idx += nt) {
     const int r = idx / R, s = idx % R;
@@ -417,11 +473,13 @@ __global__ void __launch_bounds__(kSmallThreads) k_polar(const ModePack* __restr
   for (int idx = tid; idx < R * R; idx += nt) ws.Q[(idx / R) * ld + idx % R] = ws.Z[(idx / R) * ld + idx % R];
   __syncthreads();
   // 5. column norms sigma_j of X (sorted descending by the Jacobi pass)
-  for (int j = 0; j < R; ++j) {
+  for (int j = tid >> 5; j < R; j += nt >> 5) {  // one warp per column, fixed-order reduction
+    const int lane = tid & 31;
     double a = 0.0;
-    for (int64_t i = tid; i < I; i += nt) a += X[i + I * j] * X[i + I * j];
-    a = block_reduce(a, AddOp(), ws.red);
-    if (tid == 0) ws.lam[j] = sqrt(a);
+    for (int64_t i = lane; i < I; i += 32) a = fma(X[i + I * j], X[i + I * j], a);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+    if (lane == 0) ws.lam[j] = sqrt(a);
   }
   __syncthreads();
 #ifdef PASD_DEBUG_POLAR
@@ -475,7 +533,7 @@ __global__ void __launch_bounds__(kSmallThreads) k_polar(const ModePack* __restr
         __syncthreads();
       }
       cta_gram_tn(B, B, I, mcols, mcols, ws.S, ld, ws.T64);
-      cta_jacobi_eig(ws, mcols);
+      cta_jacobi_eig(ws, mcols, 4);
       const bool ok = ws.lam[0] > 0.0 && ws.lam[mcols - 1] >= 1e-8 * ws.lam[0];
       if (!ok && attempt == 0) continue;
       // two symmetric-orthonormalisation passes: Y <- Y (Y^T Y)^{-1/2}
@@ -484,7 +542,7 @@ __global__ void __launch_bounds__(kSmallThreads) k_polar(const ModePack* __restr
         double* outp = pass == 0 ? Tm : X + I * k;
         if (pass == 1) {
           cta_gram_tn(Tm, Tm, I, mcols, mcols, ws.S, ld, ws.T64);
-          cta_jacobi_eig(ws, mcols);
+          cta_jacobi_eig(ws, mcols, 5);
         }
         for (int idx = tid; idx < mcols * mcols; idx += nt) {
           const int r = idx / mcols, c = idx % mcols;
