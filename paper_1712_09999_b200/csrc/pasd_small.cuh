@@ -16,12 +16,14 @@
 // Eigenproblems use a CTA-parallel cyclic Jacobi (round-robin ordering, R/2
 // disjoint rotations per step) in shared memory.
 #pragma once
+#include <cooperative_groups.h>
+
 #include "pasd_kernels.cuh"
 
 namespace pasd {
 
 #ifndef PASD_SMALL_THREADS
-#define PASD_SMALL_THREADS 256
+#define PASD_SMALL_THREADS 512
 #endif
 constexpr int kSmallThreads = PASD_SMALL_THREADS;
 
@@ -37,6 +39,7 @@ struct SmallWs {
   double* sn;   // Rp/2
   double* lam;  // Rp
   double* red;  // 32
+  double* cl;   // Rp + 8  vector partials of the cluster reductions (read remotely)
   int* pq;      // Rp
   int* perm;    // Rp
 };
@@ -44,8 +47,8 @@ struct SmallWs {
 __host__ __device__ inline size_t small_ws_bytes(int R) {
   const int Rp = R + (R & 1);
   const int ld = Rp + 1;
-  return sizeof(double) * (4 * (size_t)Rp * ld + 64 * (size_t)ld + Rp + Rp + 32) + sizeof(int) * (2 * (size_t)Rp) +
-         64;
+  return sizeof(double) * (4 * (size_t)Rp * ld + 64 * (size_t)ld + Rp + Rp + 32 + Rp + 8) +
+         sizeof(int) * (2 * (size_t)Rp) + 64;
 }
 
 __device__ inline SmallWs make_ws(int R, void* base) {
@@ -63,7 +66,8 @@ __device__ inline SmallWs make_ws(int R, void* base) {
   w.sn = w.cs + w.Rp / 2;
   w.lam = w.sn + w.Rp / 2;
   w.red = w.lam + w.Rp;
-  w.pq = reinterpret_cast<int*>(w.red + 32);
+  w.cl = w.red + 32;
+  w.pq = reinterpret_cast<int*>(w.cl + w.Rp + 8);
   w.perm = w.pq + w.Rp;
   return w;
 }
@@ -257,8 +261,9 @@ __device__ void cta_warm_finish(SmallWs& ws, int R) {  // V <- Q V
 // FMA chains of different entries interleave (the small solves are latency
 // bound).  Per entry the sum still runs over i in ascending order from 0.
 constexpr int GT_MAX = (PASD_MAX_RANK * PASD_MAX_RANK + kSmallThreads - 1) / kSmallThreads;
-__device__ void cta_gram_tn(const double* X, const double* Y, int64_t I, int R, int R2, double* out, int ld,
-                            double* stage /* 2 x 32 x ld */) {
+// X, Y: `I` rows with column stride ldg (a row block of an ldg-row matrix).
+__device__ void cta_gram_tn(const double* X, const double* Y, int64_t I, int64_t ldg, int R, int R2, double* out,
+                            int ld, double* stage /* 2 x 32 x ld */) {
   const int tid = threadIdx.x, nt = blockDim.x;
   const int ne = R * R2;
   double* Xs = stage;
@@ -276,11 +281,11 @@ __device__ void cta_gram_tn(const double* X, const double* Y, int64_t I, int R, 
     const int ic = (int)imin64(32, I - i0);
     for (int idx = tid; idx < 32 * R; idx += nt) {
       const int il = idx % 32, r = idx / 32;
-      Xs[il * ld + r] = il < ic ? X[i0 + il + I * r] : 0.0;
+      Xs[il * ld + r] = il < ic ? X[i0 + il + ldg * r] : 0.0;
     }
     for (int idx = tid; idx < 32 * R2; idx += nt) {
       const int il = idx % 32, r = idx / 32;
-      Ys[il * ld + r] = il < ic ? Y[i0 + il + I * r] : 0.0;
+      Ys[il * ld + r] = il < ic ? Y[i0 + il + ldg * r] : 0.0;
     }
     __syncthreads();
     for (int il = 0; il < ic; ++il) {
@@ -304,15 +309,16 @@ __device__ void cta_gram_tn(const double* X, const double* Y, int64_t I, int R, 
 // The sum over r runs in index order from 0 (same result as an unstaged loop).
 // `stage`: 64 x ld doubles.
 constexpr int MN_MAXC = (PASD_MAX_RANK + kSmallThreads / 16 - 1) / (kSmallThreads / 16);
-__device__ void cta_mul_nn(const double* X, int64_t I, int R, const double* B, int ld, int R2, double* out,
-                           double* stage) {
+// X and out: `I` rows with column stride ldg.
+__device__ void cta_mul_nn(const double* X, int64_t I, int64_t ldg, int R, const double* B, int ld, int R2,
+                           double* out, double* stage) {
   const int tid = threadIdx.x, nt = blockDim.x;
   const int q = tid & 15, cg = tid >> 4, ncg = nt >> 4;
   for (int64_t i0 = 0; i0 < I; i0 += 64) {
     const int ic = (int)imin64(64, I - i0);
     for (int idx = tid; idx < 64 * R; idx += nt) {
       const int il = idx & 63, r = idx >> 6;
-      stage[il * ld + r] = il < ic ? X[i0 + il + I * r] : 0.0;
+      stage[il * ld + r] = il < ic ? X[i0 + il + ldg * r] : 0.0;
     }
     __syncthreads();
     double a[MN_MAXC][4];
@@ -337,7 +343,7 @@ __device__ void cta_mul_nn(const double* X, int64_t I, int R, const double* B, i
     for (int k = 0; k < MN_MAXC; ++k) {
       const int c = cg + k * ncg;
       if (c < R2) {
-        double* o = out + i0 + I * c;
+        double* o = out + i0 + ldg * c;
         if (q < ic) o[q] = a[k][0];
         if (q + 16 < ic) o[q + 16] = a[k][1];
         if (q + 32 < ic) o[q + 32] = a[k][2];
@@ -349,17 +355,58 @@ __device__ void cta_mul_nn(const double* X, int64_t I, int R, const double* B, i
 }
 
 // ---------------------------------------------------------------------------
+// Cluster-parallel small solves.  Each mode is one thread-block cluster of
+// kSmallCluster CTAs (one per SM).  The tall-skinny I_n x R products run on
+// row blocks (CTA c owns rows [lo, hi)); R x R Gram matrices and column norms
+// are reduced through distributed shared memory in cluster-rank order, so every
+// CTA holds bit-identical totals and runs the same R x R Jacobi redundantly
+// (no broadcast needed, results independent of the cluster size only up to
+// the summation order of the partials).
+#ifndef PASD_SMALL_CLUSTER
+#define PASD_SMALL_CLUSTER 8
+#endif
+constexpr int kSmallCluster = PASD_SMALL_CLUSTER;
+
+struct RowBlock {
+  int64_t lo, rows;
+};
+__device__ inline RowBlock row_block(int64_t I, int crank) {
+  const int64_t chunk = (I + kSmallCluster - 1) / kSmallCluster;
+  const int64_t lo = imin64(I, chunk * crank), hi = imin64(I, lo + chunk);
+  return {lo, hi - lo};
+}
+
+// dst[r * ld + c] = sum over cluster ranks (in rank order) of src[r * ld + c]
+// (src: this CTA's partial in shared memory).  Ends with a cluster barrier, so
+// src may be reused afterwards.
+__device__ void cluster_sum_mat(const double* src, double* dst, int R, int R2, int ld) {
+  namespace cg = cooperative_groups;
+  cg::cluster_group cl = cg::this_cluster();
+  cl.sync();  // every partial written
+  for (int idx = threadIdx.x; idx < R * R2; idx += blockDim.x) {
+    const int r = idx / R2, c = idx - r * R2;
+    double a = 0.0;
+    for (int q = 0; q < kSmallCluster; ++q) a += cl.map_shared_rank(src, q)[r * ld + c];
+    dst[r * ld + c] = a;
+  }
+  cl.sync();  // every remote read done
+}
+
+// ---------------------------------------------------------------------------
 // SVT factor: M_n = P diag(f) P^T, f_i = (sigma_i - tau)/sigma_i for sigma_i > tau.
-// SVT of mode n from its reduced Gram (one CTA): writes sig, M, P, UM and the
-// keep / vnorm2 / nuclear scalars.
-__device__ void svt_mode(const ModeDev& m, int n, Ctl* ctl, double* smem) {
+// SVT of mode n from its reduced Gram (every CTA of the mode's cluster; rank 0
+// publishes sig, M, P and the keep / vnorm2 / nuclear scalars, each CTA forms
+// its rows of UM = U M).
+__device__ void svt_mode(const ModeDev& m, int n, Ctl* ctl, double* smem, int crank) {
   const int R = m.R, tid = threadIdx.x, nt = blockDim.x;
   SmallWs ws = make_ws(R, smem);
   const int ld = ws.ld;
+  const bool lead = crank == 0;
   // Gram_n (reduced over chunks by k_gram_reduce, and over ranks when sharded)
   for (int idx = tid; idx < R * R; idx += nt) ws.S[(idx / R) * ld + idx % R] = m.Gram[idx];
   __syncthreads();
   cta_warm_start(ws, R, m.P);  // previous eigenvectors: Gram changes slowly between iterations
+  cooperative_groups::this_cluster().sync();  // every CTA has read m.P before rank 0 rewrites it
   cta_jacobi_eig(ws, R, 1);
   cta_warm_finish(ws, R);
   const double tau = __ddiv_rn(m.lambda, ctl->mu);  // lambda / mu (pasd.cpp:77)
@@ -369,7 +416,7 @@ __device__ void svt_mode(const ModeDev& m, int n, Ctl* ctl, double* smem) {
     for (int j = 0; j < R; ++j) {
       const double sg = sqrt(fmax(ws.lam[j], 0.0));
       ws.lam[j] = sg;
-      m.sig[j] = sg;
+      if (lead) m.sig[j] = sg;
     }
     while (keep < R && ws.lam[keep] > tau) ++keep;  // linops.cpp:84-86
     for (int j = 0; j < R; ++j) {
@@ -382,9 +429,11 @@ __device__ void svt_mode(const ModeDev& m, int n, Ctl* ctl, double* smem) {
       }
       ws.Q[j] = f;  // row 0 of Q holds f_j
     }
-    ctl->keep[n] = keep;
-    ctl->vnorm2[n] = vn2;
-    ctl->nuclear[n] = nuc;
+    if (lead) {
+      ctl->keep[n] = keep;
+      ctl->vnorm2[n] = vn2;
+      ctl->nuclear[n] = nuc;
+    }
   }
   __syncthreads();
   // M = P diag(f) P^T  -> S (row-major) and global m.M (column-major == same, symmetric)
@@ -400,26 +449,37 @@ __device__ void svt_mode(const ModeDev& m, int n, Ctl* ctl, double* smem) {
     // symmetrise exactly
     const double a = 0.5 * (ws.Z[r * ld + s] + ws.Z[s * ld + r]);
     ws.S[r * ld + s] = a;
-    m.M[r + R * s] = a;
-    m.P[r + R * s] = ws.V[r * ld + s];
+    if (lead) {
+      m.M[r + R * s] = a;
+      m.P[r + R * s] = ws.V[r * ld + s];
+    }
   }
   __syncthreads();
-  // UM = U * M
-  cta_mul_nn(m.U, m.Ifull, R, ws.S, ld, R, m.UM, ws.T64);
+  // UM = U * M on this CTA's rows
+  const RowBlock rb = row_block(m.Ifull, crank);
+  if (rb.rows > 0) cta_mul_nn(m.U + rb.lo, rb.rows, m.Ifull, R, ws.S, ld, R, m.UM + rb.lo, ws.T64);
 }
 
-__global__ void __launch_bounds__(kSmallThreads) k_svt(const ModePack* __restrict__ mp, Ctl* ctl) {
+__global__ void __cluster_dims__(kSmallCluster, 1, 1) __launch_bounds__(kSmallThreads)
+    k_svt(const ModePack* __restrict__ mp, Ctl* ctl) {
   if (ctl->done) return;
   extern __shared__ double smem[];
-  svt_mode(mp->m[blockIdx.x], blockIdx.x, ctl, smem);
+  const int crank = (int)cooperative_groups::this_cluster().block_rank();
+  const int n = blockIdx.x / kSmallCluster;
+  svt_mode(mp->m[n], n, ctl, smem, crank);
 }
 
 // ---------------------------------------------------------------------------
 // Procrustes: U_n <- polar(Wt_n M_n) unless degenerate (linops.cpp:93-104).
-__global__ void __launch_bounds__(kSmallThreads) k_polar(const ModePack* __restrict__ mp, Ctl* ctl) {
+__global__ void __cluster_dims__(kSmallCluster, 1, 1) __launch_bounds__(kSmallThreads)
+    k_polar(const ModePack* __restrict__ mp, Ctl* ctl) {
   if (ctl->done) return;
   extern __shared__ double smem[];
-  const int n = blockIdx.x;
+  namespace cg = cooperative_groups;
+  cg::cluster_group cl = cg::this_cluster();
+  const int crank = (int)cl.block_rank();
+  const bool lead = crank == 0;
+  const int n = blockIdx.x / kSmallCluster;
   const ModeDev& m = mp->m[n];
   const int R = m.R, tid = threadIdx.x, nt = blockDim.x;
   const int64_t I = m.Ifull, IR = I * R;
@@ -428,41 +488,50 @@ __global__ void __launch_bounds__(kSmallThreads) k_polar(const ModePack* __restr
   double* Wt = m.Wt;                // I x R: G^{next} A^T, reduced by the pass that produced it
   double* X = m.scratch + IR;       // I x R
   double* X2 = m.scratch + 2 * IR;  // I x R
+  const RowBlock rb = row_block(I, crank);
+  const int64_t lo = rb.lo, rows = rb.rows;
   const double g2 = ctl->gnorm2[n];  // ||G_n^{next}||_F^2
-  // 2. W = Wt M  (M in S)
+  // 2. W = Wt M  (M in S), this CTA's rows; ||W||_F^2 over the cluster
   for (int idx = tid; idx < R * R; idx += nt) ws.S[(idx / R) * ld + idx % R] = m.M[(idx / R) + R * (idx % R)];
   __syncthreads();
-  cta_mul_nn(Wt, I, R, ws.S, ld, R, X, ws.T64);
+  if (rows > 0) cta_mul_nn(Wt + lo, rows, I, R, ws.S, ld, R, X + lo, ws.T64);
   double w2 = 0.0;
-  for (int64_t idx = tid; idx < IR; idx += nt) w2 += X[idx] * X[idx];
+  for (int64_t idx = tid; idx < rows * R; idx += nt) {
+    const double v = X[lo + (idx % rows) + I * (idx / rows)];
+    w2 += v * v;
+  }
   w2 = block_reduce(w2, AddOp(), ws.red);
+  if (tid == 0) ws.cl[0] = w2;
+  cluster_sum_mat(ws.cl, ws.lam, 1, 1, 1);
+  w2 = ws.lam[0];
   const double gnorm = sqrt(g2), vnorm = sqrt(ctl->vnorm2[n]);
   const double scale = fmax(1.0, gnorm * vnorm);  // linops.cpp:99
   if (sqrt(w2) <= 1e-14 * scale) {                // linops.cpp:100-101 -> keep U (pasd.cpp:70-74)
-    if (tid == 0) { ctl->degenerate[n] = 1; ctl->polar_rank[n] = 0; }
-    return;
+    if (lead && tid == 0) { ctl->degenerate[n] = 1; ctl->polar_rank[n] = 0; }
+    return;  // uniform over the cluster (identical w2)
   }
   // 3. first Gram/Jacobi pass: C = W^T W = Q1 L Q1^T ; X2 = W Q1
-  cta_gram_tn(X, X, I, R, R, ws.S, ld, ws.T64);
+  if (rows > 0) {
+    cta_gram_tn(X + lo, X + lo, rows, I, R, R, ws.Z, ld, ws.T64);
+  } else {
+    for (int idx = tid; idx < R * R; idx += nt) ws.Z[(idx / R) * ld + idx % R] = 0.0;
+  }
+  cluster_sum_mat(ws.Z, ws.S, R, R, ld);
   cta_warm_start(ws, R, m.Qp);  // previous right rotation
   cta_jacobi_eig(ws, R, 2);
   cta_warm_finish(ws, R);
   for (int idx = tid; idx < R * R; idx += nt) ws.Q[(idx / R) * ld + idx % R] = ws.V[(idx / R) * ld + idx % R];
   __syncthreads();
-  cta_mul_nn(X, I, R, ws.Q, ld, R, X2, ws.T64);
-#ifdef PASD_DEBUG_POLAR
-  if (tid == 0) {
-    printf("lam1:"); for (int j = 0; j < R; ++j) printf(" %g", ws.lam[j]); printf("\n");
-    printf("Q1:"); for (int r = 0; r < R; ++r) { for (int j = 0; j < R; ++j) printf(" %g", ws.Q[r * ld + j]); printf(" |"); } printf("\n");
-    printf("X row0:"); for (int j = 0; j < R; ++j) printf(" %g", X[I * j]); printf("\n");
-    printf("X2 row0:"); for (int j = 0; j < R; ++j) printf(" %g", X2[I * j]); printf("\n");
-  }
-  __syncthreads();
-#endif
+  if (rows > 0) cta_mul_nn(X + lo, rows, I, R, ws.Q, ld, R, X2 + lo, ws.T64);
   // 4. second pass on the rotated columns: C2 = X2^T X2 = Q2 L2 Q2^T ; X = X2 Q2 ; Q = Q1 Q2
-  cta_gram_tn(X2, X2, I, R, R, ws.S, ld, ws.T64);
+  if (rows > 0) {
+    cta_gram_tn(X2 + lo, X2 + lo, rows, I, R, R, ws.Z, ld, ws.T64);
+  } else {
+    for (int idx = tid; idx < R * R; idx += nt) ws.Z[(idx / R) * ld + idx % R] = 0.0;
+  }
+  cluster_sum_mat(ws.Z, ws.S, R, R, ld);
   cta_jacobi_eig(ws, R, 3);
-  cta_mul_nn(X2, I, R, ws.V, ld, R, X, ws.T64);
+  if (rows > 0) cta_mul_nn(X2 + lo, rows, I, R, ws.V, ld, R, X + lo, ws.T64);
   for (int idx = tid; idx < R * R; idx += nt) {
     const int r = idx / R, s = idx % R;
     double a = 0.0;
@@ -472,109 +541,111 @@ __global__ void __launch_bounds__(kSmallThreads) k_polar(const ModePack* __restr
   __syncthreads();
   for (int idx = tid; idx < R * R; idx += nt) ws.Q[(idx / R) * ld + idx % R] = ws.Z[(idx / R) * ld + idx % R];
   __syncthreads();
-  // 5. column norms sigma_j of X (sorted descending by the Jacobi pass)
-  for (int j = tid >> 5; j < R; j += nt >> 5) {  // one warp per column, fixed-order reduction
+  // 5. column norms sigma_j of X (sorted descending by the Jacobi pass): one
+  //    warp per column over this CTA's rows, then the cluster sum
+  for (int j = tid >> 5; j < R; j += nt >> 5) {
     const int lane = tid & 31;
     double a = 0.0;
-    for (int64_t i = lane; i < I; i += 32) a = fma(X[i + I * j], X[i + I * j], a);
+    for (int64_t i = lane; i < rows; i += 32) a = fma(X[lo + i + I * j], X[lo + i + I * j], a);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
-    if (lane == 0) ws.lam[j] = sqrt(a);
+    if (lane == 0) ws.cl[j] = a;
   }
+  cluster_sum_mat(ws.cl, ws.lam, 1, R, R);
+  for (int j = tid; j < R; j += nt) ws.lam[j] = sqrt(ws.lam[j]);
   __syncthreads();
-#ifdef PASD_DEBUG_POLAR
-  if (tid == 0) {
-    printf("sig:"); for (int j = 0; j < R; ++j) printf(" %g", ws.lam[j]); printf("\n");
-    printf("Q:"); for (int r = 0; r < R; ++r) { for (int j = 0; j < R; ++j) printf(" %g", ws.Q[r * ld + j]); printf(" |"); } printf("\n");
-    double d01 = 0; for (int64_t i = 0; i < I; ++i) d01 += X[i] * X[i + I]; printf("X col0.col1 = %g\n", d01);
-  }
-  __syncthreads();
-#endif
   const double smax = ws.lam[0] > 0.0 ? ws.lam[0] : 1.0;
   int k = 0;
   while (k < R && ws.lam[k] > 1e-12 * smax) ++k;
-  if (tid == 0) { ctl->degenerate[n] = 0; ctl->polar_rank[n] = k; }
-  // U_tilde columns j < k: X[:, j] / sigma_j   (written into X in place)
-  for (int64_t idx = tid; idx < I * k; idx += nt) {
-    const int j = (int)(idx / I);
-    X[idx] = X[idx] / ws.lam[j];
+  if (lead && tid == 0) { ctl->degenerate[n] = 0; ctl->polar_rank[n] = k; }
+  // U_tilde columns j < k: X[:, j] / sigma_j   (this CTA's rows, in place)
+  for (int64_t idx = tid; idx < rows * k; idx += nt) {
+    const int j = (int)(idx / rows);
+    const int64_t i = lo + idx % rows;
+    X[i + I * j] = X[i + I * j] / ws.lam[j];
   }
   __syncthreads();
   if (k < R) {
-    // 6. completion of the numerically null directions Q[:, k:].
-    //    Candidates: Wt Q[:, k:] = G^{next} A_prev^T Q_null (one subspace-
-    //    iteration step of G G^T on the sub-threshold directions), projected
-    //    off range(Ut) and symmetrically orthonormalised (polar).  If those are
-    //    ill-conditioned (e.g. at the first non-degenerate step), fall back to
-    //    the previous basis U_prev Q[:, k:] (for k = 0 that reproduces the
-    //    reference's keep-U rule, pasd.cpp:70-74).
-    const int mcols = R - k;
-    double* B = X2;  // I x mcols
-    double* Tm = Wt;  // I x mcols temp (Wt is consumed by attempt 0)
-    for (int attempt = 0; attempt < 2; ++attempt) {
-      const double* src = attempt == 0 ? Wt : m.U;
-      for (int64_t idx = tid; idx < I * mcols; idx += nt) {
-        const int64_t i = idx % I;
-        const int c = (int)(idx / I);
-        double a = 0.0;
-        for (int r = 0; r < R; ++r) a = fma(src[i + I * r], ws.Q[r * ld + k + c], a);
-        B[idx] = a;
-      }
-      __syncthreads();
-      for (int pass = 0; pass < 2 && k > 0; ++pass) {
-        cta_gram_tn(X, B, I, k, mcols, ws.S, ld, ws.T64);  // S (k x mcols) = Ut^T B
+    // The completion (transition iterations only) works on whole columns: rank 0
+    // runs it on all I rows while the cluster waits.
+    cl.sync();  // every CTA's rows of X, X2 written
+    if (lead) {
+      // 6. completion of the numerically null directions Q[:, k:].
+      //    Candidates: Wt Q[:, k:] = G^{next} A_prev^T Q_null (one subspace-
+      //    iteration step of G G^T on the sub-threshold directions), projected
+      //    off range(Ut) and symmetrically orthonormalised (polar).  If those are
+      //    ill-conditioned (e.g. at the first non-degenerate step), fall back to
+      //    the previous basis U_prev Q[:, k:] (for k = 0 that reproduces the
+      //    reference's keep-U rule, pasd.cpp:70-74).
+      const int mcols = R - k;
+      double* B = X2;  // I x mcols
+      double* Tm = Wt;  // I x mcols temp (Wt is consumed by attempt 0)
+      for (int attempt = 0; attempt < 2; ++attempt) {
+        const double* src = attempt == 0 ? Wt : m.U;
         for (int64_t idx = tid; idx < I * mcols; idx += nt) {
           const int64_t i = idx % I;
           const int c = (int)(idx / I);
-          double a = B[idx];
-          for (int j = 0; j < k; ++j) a = fma(-X[i + I * j], ws.S[j * ld + c], a);
+          double a = 0.0;
+          for (int r = 0; r < R; ++r) a = fma(src[i + I * r], ws.Q[r * ld + k + c], a);
           B[idx] = a;
         }
         __syncthreads();
-      }
-      cta_gram_tn(B, B, I, mcols, mcols, ws.S, ld, ws.T64);
-      cta_jacobi_eig(ws, mcols, 4);
-      const bool ok = ws.lam[0] > 0.0 && ws.lam[mcols - 1] >= 1e-8 * ws.lam[0];
-      if (!ok && attempt == 0) continue;
-      // two symmetric-orthonormalisation passes: Y <- Y (Y^T Y)^{-1/2}
-      for (int pass = 0; pass < 2; ++pass) {
-        const double* in = pass == 0 ? B : Tm;
-        double* outp = pass == 0 ? Tm : X + I * k;
-        if (pass == 1) {
-          cta_gram_tn(Tm, Tm, I, mcols, mcols, ws.S, ld, ws.T64);
-          cta_jacobi_eig(ws, mcols, 5);
-        }
-        for (int idx = tid; idx < mcols * mcols; idx += nt) {
-          const int r = idx / mcols, c = idx % mcols;
-          double a = 0.0;
-          for (int j = 0; j < mcols; ++j) {
-            const double l = ws.lam[j];
-            const double inv = l > 1e-280 ? 1.0 / sqrt(l) : 0.0;
-            a = fma(ws.V[r * ld + j] * inv, ws.V[c * ld + j], a);
+        for (int pass = 0; pass < 2 && k > 0; ++pass) {
+          cta_gram_tn(X, B, I, I, k, mcols, ws.S, ld, ws.T64);  // S (k x mcols) = Ut^T B
+          for (int64_t idx = tid; idx < I * mcols; idx += nt) {
+            const int64_t i = idx % I;
+            const int c = (int)(idx / I);
+            double a = B[idx];
+            for (int j = 0; j < k; ++j) a = fma(-X[i + I * j], ws.S[j * ld + c], a);
+            B[idx] = a;
           }
-          ws.Z[r * ld + c] = a;
+          __syncthreads();
         }
-        __syncthreads();
-        for (int64_t idx = tid; idx < I * mcols; idx += nt) {
-          const int64_t i = idx % I;
-          const int c = (int)(idx / I);
-          double a = 0.0;
-          for (int j = 0; j < mcols; ++j) a = fma(in[i + I * j], ws.Z[j * ld + c], a);
-          outp[i + I * c] = a;
+        cta_gram_tn(B, B, I, I, mcols, mcols, ws.S, ld, ws.T64);
+        cta_jacobi_eig(ws, mcols, 4);
+        const bool ok = ws.lam[0] > 0.0 && ws.lam[mcols - 1] >= 1e-8 * ws.lam[0];
+        if (!ok && attempt == 0) continue;
+        // two symmetric-orthonormalisation passes: Y <- Y (Y^T Y)^{-1/2}
+        for (int pass = 0; pass < 2; ++pass) {
+          const double* in = pass == 0 ? B : Tm;
+          double* outp = pass == 0 ? Tm : X + I * k;
+          if (pass == 1) {
+            cta_gram_tn(Tm, Tm, I, I, mcols, mcols, ws.S, ld, ws.T64);
+            cta_jacobi_eig(ws, mcols, 5);
+          }
+          for (int idx = tid; idx < mcols * mcols; idx += nt) {
+            const int r = idx / mcols, c = idx % mcols;
+            double a = 0.0;
+            for (int j = 0; j < mcols; ++j) {
+              const double l = ws.lam[j];
+              const double inv = l > 1e-280 ? 1.0 / sqrt(l) : 0.0;
+              a = fma(ws.V[r * ld + j] * inv, ws.V[c * ld + j], a);
+            }
+            ws.Z[r * ld + c] = a;
+          }
+          __syncthreads();
+          for (int64_t idx = tid; idx < I * mcols; idx += nt) {
+            const int64_t i = idx % I;
+            const int c = (int)(idx / I);
+            double a = 0.0;
+            for (int j = 0; j < mcols; ++j) a = fma(in[i + I * j], ws.Z[j * ld + c], a);
+            outp[i + I * c] = a;
+          }
+          __syncthreads();
         }
-        __syncthreads();
+        break;
       }
-      break;
     }
+    cl.sync();  // completed columns visible to every CTA
   }
-  // 7. U = Ut Q^T ; keep Q as the next warm start
+  // 7. U = Ut Q^T on this CTA's rows ; rank 0 keeps Q as the next warm start
   for (int idx = tid; idx < R * R; idx += nt) {
     const int r = idx / R, s = idx % R;
     ws.S[r * ld + s] = ws.Q[s * ld + r];
-    m.Qp[r + R * s] = ws.Q[r * ld + s];
+    if (lead) m.Qp[r + R * s] = ws.Q[r * ld + s];
   }
   __syncthreads();
-  cta_mul_nn(X, I, R, ws.S, ld, R, m.U, ws.T64);
+  if (rows > 0) cta_mul_nn(X + lo, rows, I, R, ws.S, ld, R, m.U + lo, ws.T64);
 }
 
 }  // namespace pasd

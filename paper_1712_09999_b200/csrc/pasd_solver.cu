@@ -243,7 +243,7 @@ void launch_iteration_marked(pasd_solver* s, cudaStream_t st, Mark&& mark) {
   const int N = s->N;
   int launches = 0;
   mark(PASD_K_POLAR, true);
-  k_polar<<<N, kSmallThreads, s->small_smem, st>>>(s->d_pack, s->d_ctl);
+  k_polar<<<N * kSmallCluster, kSmallThreads, s->small_smem, st>>>(s->d_pack, s->d_ctl);
   mark(PASD_K_POLAR, false);
   ++launches;
   if (!s->sharded) {
@@ -283,7 +283,7 @@ void launch_iteration_marked(pasd_solver* s, cudaStream_t st, Mark&& mark) {
     k_gram_reduce_all<<<s->gram_red_grid, 256, 0, st>>>(s->d_pack, s->d_ctl);
     mark(PASD_K_GRAM, false);
     mark(PASD_K_SVT, true);
-    k_svt<<<N, kSmallThreads, s->small_smem, st>>>(s->d_pack, s->d_ctl);
+    k_svt<<<N * kSmallCluster, kSmallThreads, s->small_smem, st>>>(s->d_pack, s->d_ctl);
     mark(PASD_K_SVT, false);
     launches += 3;
   } else {
@@ -303,7 +303,7 @@ void launch_iteration_marked(pasd_solver* s, cudaStream_t st, Mark&& mark) {
     }
     NK(ncclGroupEnd());
     mark(PASD_K_SVT, true);
-    k_svt<<<N, kSmallThreads, s->small_smem, st>>>(s->d_pack, s->d_ctl);
+    k_svt<<<N * kSmallCluster, kSmallThreads, s->small_smem, st>>>(s->d_pack, s->d_ctl);
     mark(PASD_K_SVT, false);
     ++launches;
   }
@@ -1330,7 +1330,7 @@ void device_svt(const double* m_h, int64_t rows, int64_t cols, double tau, doubl
   k_gram_reduce<<<8, 256>>>(m, m.Gram, ctl);
   const size_t smem = small_ws_bytes(R);
   CK(cudaFuncSetAttribute(k_svt, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  k_svt<<<1, kSmallThreads, smem>>>(d_pack, ctl);
+  k_svt<<<kSmallCluster, kSmallThreads, smem>>>(d_pack, ctl);
   double* V = t.alloc<double>(rows * cols);
   k_materialize_v<<<256, 256>>>(m, V);
   CK(cudaGetLastError());
@@ -1404,7 +1404,7 @@ void device_procrustes(const double* g_h, int64_t I, int64_t P, const double* v_
   k_wreduce_generic<<<dim3(64, 1), 256>>>(d_pack, ctl);
   const size_t smem = small_ws_bytes(R);
   CK(cudaFuncSetAttribute(k_polar, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  k_polar<<<1, kSmallThreads, smem>>>(d_pack, ctl);
+  k_polar<<<kSmallCluster, kSmallThreads, smem>>>(d_pack, ctl);
   CK(cudaGetLastError());
   Ctl hc;
   CK(cudaMemcpy(&hc, ctl, sizeof(Ctl), cudaMemcpyDeviceToHost));
