@@ -72,6 +72,10 @@ __device__ inline SmallWs make_ws(int R, void* base) {
   return w;
 }
 
+#ifndef PASD_JACOBI_QUAD
+#define PASD_JACOBI_QUAD 1e-10
+#endif
+
 __device__ __forceinline__ int rr_pos(int m, int round, int Rp) {
   return m == 0 ? 0 : 1 + (m - 1 + round) % (Rp - 1);
 }
@@ -108,9 +112,9 @@ __device__ void cta_jacobi_eig(SmallWs& ws, int n, int tag = 0) {
     vj[u] = idx < npairs * Rp ? idx / Rp : -1;
     vk[u] = idx < npairs * Rp ? idx % Rp : 0;
   }
-  __shared__ int rotated;
+  __shared__ int rotated, big;
   for (int sweep = 0; sweep < 30 && Rp > 1; ++sweep) {
-    if (tid == 0) rotated = 0;
+    if (tid == 0) rotated = big = 0;
     __syncthreads();
     for (int round = 0; round < Rp - 1; ++round) {
       for (int j = tid; j < npairs; j += nt) {
@@ -127,6 +131,7 @@ __device__ void cta_jacobi_eig(SmallWs& ws, int n, int tag = 0) {
           c = 1.0 / sqrt(1.0 + t * t);
           s = t * c;
           rotated = 1;
+          if (fabs(apq) > PASD_JACOBI_QUAD * sqrt(fabs(app) * fabs(aqq))) big = 1;
         }
         ws.cs[j] = c;
         ws.sn[j] = s;
@@ -177,7 +182,11 @@ __device__ void cta_jacobi_eig(SmallWs& ws, int n, int tag = 0) {
       }
       __syncthreads();
     }
-    if (rotated == 0) {
+    // Converged: no rotation at all, or only rotations so small (relative
+    // off-diagonal <= PASD_JACOBI_QUAD) that the quadratic convergence of the
+    // cyclic sweep leaves nothing above the rounding threshold for another one
+    // (saves the confirming sweep).
+    if (rotated == 0 || big == 0) {
 #ifdef PASD_DEBUG_SWEEPS
       if (tid == 0) printf("jacobi n=%d block=%d tag=%d sweeps=%d\n", n, blockIdx.x, tag, sweep + 1);
 #endif
