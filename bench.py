@@ -44,6 +44,8 @@ def parse_args():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--profile-iters", type=int, default=3)
+    ap.add_argument("--steady-after", type=int, default=140,
+                    help="N=1: also time 10 iterations after this many (the full-rank phase), 0 = skip")
     return ap.parse_args()
 
 
@@ -349,7 +351,9 @@ def main():
     T_loc = T[shard.struct.slab_begin:shard.struct.slab_end].contiguous() if shard else T
     if shard:
         del T
-    cfg = PasdConfig(lambdas=w.lambdas(), ranks=list(w.ranks), eps=w.eps, maxiter=W + K + args.profile_iters + 1)
+    steady_after = args.steady_after if world == 1 else 0
+    cfg = PasdConfig(lambdas=w.lambdas(), ranks=list(w.ranks), eps=w.eps,
+                     maxiter=max(W + K + args.profile_iters + 1, steady_after + 13))
     sol = pb.Solver(w.dims, cfg, fixed_iters=True, poll_every=K, shard=shard)
     sol.load(T_loc.data_ptr(), t_is_device=True)
     sol.run(W)
@@ -376,6 +380,27 @@ def main():
         ms = float(t.item())
     launches = sol.launches
     prof = sol.profile(args.profile_iters)
+    steady = None
+    if steady_after:
+        # The fixed-count BASELINE runs of C3-C5 stay in the V_n = 0 phase; this
+        # times the same solver later, with every V_n at full rank (non-degenerate
+        # Procrustes, longer Jacobi solves), as a representative steady state.
+        done_iters = W + K + args.profile_iters
+        if steady_after > done_iters:
+            sol.run(steady_after - done_iters)
+        keep, prank = sol.ranks()
+        s0 = torch.cuda.Event(enable_timing=True)
+        s1 = torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        s0.record(stream)
+        sol.run(10)
+        s1.record(stream)
+        s1.synchronize()
+        sms = s0.elapsed_time(s1) / 10
+        sprof = sol.profile(2)
+        steady = {"after_iters": max(steady_after, done_iters), "ms_per_step": round(sms, 4),
+                  "value": round(1e3 / sms, 4), "unit": "iter/s", "svt_keep": keep, "polar_rank": prank,
+                  "kernel_ms_per_iter": {k: round(v["ms"] / 2, 4) for k, v in sprof.items() if v["ms"] > 0}}
     sol.close()
     del sol
     value = K / (ms * 1e-3)
@@ -402,6 +427,8 @@ def main():
         "roofline": roof,
         "iteration_roofline": iteration_roofline,
     }
+    if steady:
+        line["steady_state"] = steady
     del T_loc
     torch.cuda.empty_cache()
     if not args.no_e2e and shard is None:

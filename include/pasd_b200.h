@@ -183,6 +183,12 @@ enum {
  * The iterate advances exactly as pasd_b200_solver_run would advance it. */
 int pasd_b200_solver_profile(pasd_solver* s, int32_t iters, double* kernel_ms, int64_t* kernel_launches,
                              double* kernel_bytes, double* kernel_flops, char* errbuf, size_t errlen);
+/* Ranks of the current iterate (diagnostics, e.g. to check that a run has
+ * reached the full-rank phase): svt_keep[n] = number of singular values of
+ * A_n kept by the last SVT (rank of V_n, linops.cpp:84-86), polar_rank[n] =
+ * numerical rank of W_n in the last Procrustes step (0 when it was degenerate
+ * and U_n was kept, pasd.cpp:70-74).  N entries each. */
+int pasd_b200_solver_ranks(pasd_solver* s, int32_t* svt_keep, int32_t* polar_rank, char* errbuf, size_t errlen);
 /* Number of kernel launches issued by the last pasd_b200_solver_run call. */
 int64_t pasd_b200_solver_launches(const pasd_solver* s);
 void pasd_b200_solver_destroy(pasd_solver* s);

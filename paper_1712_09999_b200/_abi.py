@@ -102,6 +102,7 @@ HEADER_SYMBOLS = (
     "pasd_b200_solver_device_e",
     "pasd_b200_solver_stream",
     "pasd_b200_solver_launches",
+    "pasd_b200_solver_ranks",
     "pasd_b200_solver_profile",
     "pasd_b200_solver_destroy",
     "pasd_b200_default_lambdas",

@@ -1146,6 +1146,18 @@ void* pasd_b200_solver_stream(const pasd_solver* s) { return s ? (void*)s->strea
 
 int64_t pasd_b200_solver_launches(const pasd_solver* s) { return s ? s->launches_last_run : 0; }
 
+int pasd_b200_solver_ranks(pasd_solver* s, int32_t* svt_keep, int32_t* polar_rank, char* errbuf, size_t errlen) {
+  return guarded_call(errbuf, errlen, [&] {
+    if (!s || !svt_keep || !polar_rank) fail(PASD_ERR_ARGUMENT, "pasd_b200: null argument");
+    CK(cudaSetDevice(s->device));
+    sync_ctl(s);
+    for (int n = 0; n < s->N; ++n) {
+      svt_keep[n] = s->h_ctl->keep[n];
+      polar_rank[n] = s->h_ctl->polar_rank[n];
+    }
+  });
+}
+
 void pasd_b200_solver_destroy(pasd_solver* s) {
   if (s) {
     cudaSetDevice(s->device);

@@ -166,6 +166,19 @@ class Solver:
     def launches(self) -> int:
         return int(lib().pasd_b200_solver_launches(self._h))
 
+    def ranks(self):
+        """(svt_keep, polar_rank) per mode of the current iterate (pasd_b200_solver_ranks)."""
+        n = len(self.dims)
+        keep = (C.c_int32 * n)()
+        prank = (C.c_int32 * n)()
+        err = _err()
+        L = lib()
+        L.pasd_b200_solver_ranks.restype = C.c_int
+        L.pasd_b200_solver_ranks.argtypes = [C.c_void_p, C.POINTER(C.c_int32), C.POINTER(C.c_int32), C.c_char_p,
+                                             C.c_size_t]
+        raise_for_status(L.pasd_b200_solver_ranks(self._h, keep, prank, err, len(err)), err)
+        return list(keep), list(prank)
+
     def finalize(self, want_x=True, want_e=True, want_z=False, want_y=False, out_x=None, out_e=None):
         """Finalise into new arrays, or into `out_x` / `out_e` (contiguous float64
         buffers of the local slab's size, e.g. views of pinned host memory)."""
