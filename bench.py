@@ -340,6 +340,8 @@ def main():
         import torch.distributed as dist
         from paper_1712_09999_b200.sharding import Shard, nccl_unique_id, slab_bounds
 
+        for k, v in (("RANK", "0"), ("WORLD_SIZE", "1"), ("MASTER_ADDR", "127.0.0.1"), ("MASTER_PORT", "29517")):
+            os.environ.setdefault(k, v)  # PASD_BENCH_FORCE_SHARD=1 without torchrun: a one-rank group
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
         uid = [nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(uid, src=0)
