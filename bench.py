@@ -299,6 +299,21 @@ def roofline_from_profile(prof, peaks, iters):
     r.update({"kernel": name, "traffic": traffic, "algorithmic_bytes_per_launch": bytes_per_launch,
               "algorithmic_flops_per_launch": flops_per_launch, "ms_per_launch": round(per_launch_ms, 4),
               "hbm_gbs": round(gbs, 1), "fp64_tflops": round(tfs, 3), "kernel_time_shares": shares})
+    # Every kernel class with algorithmic work: the same achieved / bound computation.
+    per = {}
+    for k, v in prof.items():
+        if v["ms"] <= 0 or (v["bytes"] <= 0 and v["flops"] <= 0):
+            continue
+        lpi = v["launches"] / max(1, iters)
+        ms_l = v["ms"] / max(1, v["launches"])
+        b_l, f_l = v["bytes"] / max(1.0, lpi), v["flops"] / max(1.0, lpi)
+        g = b_l / (ms_l * 1e-3) / 1e9
+        t = f_l / (ms_l * 1e-3) / 1e12
+        fp = f_l / max(1.0, b_l) > ridge
+        per[k] = {"ms_per_launch": round(ms_l, 4), "hbm_gbs": round(g, 1), "fp64_tflops": round(t, 3),
+                  "bound": "fp64" if fp else "hbm",
+                  "frac": round(t / peaks["fp64_tflops"] if fp else g / peaks["hbm_gbs"], 4)}
+    r["per_kernel"] = per
     return r
 
 
