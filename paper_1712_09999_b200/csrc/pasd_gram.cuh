@@ -16,6 +16,14 @@ template <int RP>
 struct GramLayout {
   static constexpr int RM = (RP + 15) / 16 * 16;  // rows covered by the m16 tiles
   static constexpr int MT = RM / 16, NT = RP / 8;
+  // Gram is symmetric: only the tiles that meet the upper triangle r <= c
+  // (n0 + 8 > m0, i.e. nt >= 2 mt) are formed; the reductions mirror the rest.
+  static constexpr int upper_tiles() {
+    int u = 0;
+    for (int mt = 0; mt < MT; ++mt) u += NT > 2 * mt ? NT - 2 * mt : 0;
+    return u;
+  }
+  static constexpr int UT = upper_tiles();
   // mode 1 (inner == 1): chunk as [kappa][r] (A_1 columns are contiguous in r);
   // other modes: [r][kappa] (64 contiguous kappa per r).  Both pitches are
   // 4 mod 16 doubles, so the fragment reads are conflict-free.
@@ -30,8 +38,18 @@ struct GramLayout {
 template <int RP, bool CONTIG>
 __device__ void gram_partial(const ModeDev& m, int cta, int ncta, double* gsm) {
   using L = GramLayout<RP>;
-  constexpr int TILES = L::MT * L::NT;
+  constexpr int TILES = L::UT;
   constexpr int TPW = (TILES + 7) / 8;  // tiles per warp
+  // upper tile index -> (m0, n0)
+  auto tile_mn = [](int tile, int& m0, int& n0) {
+    int mt = 0;
+    while (tile >= L::NT - 2 * mt) {
+      tile -= L::NT - 2 * mt;
+      ++mt;
+    }
+    m0 = 16 * mt;
+    n0 = 8 * (2 * mt + tile);
+  };
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5, g = lane >> 2, t = lane & 3;
   const int R = m.R;
   const int64_t inner = m.inner;
@@ -109,7 +127,8 @@ __device__ void gram_partial(const ModeDev& m, int cta, int ncta, double* gsm) {
     for (int j = 0; j < TPW; ++j) {
       const int tile = w + 8 * j;
       if (tile < TILES) {
-        const int m0 = 16 * (tile / L::NT), n0 = 8 * (tile % L::NT);
+        int m0, n0;
+        tile_mn(tile, m0, n0);
 #pragma unroll 4
         for (int ks = 0; ks < GM_KC / 4; ++ks) {
           const int kk = 4 * ks + t;
@@ -125,7 +144,8 @@ __device__ void gram_partial(const ModeDev& m, int cta, int ncta, double* gsm) {
   for (int j = 0; j < TPW; ++j) {
     const int tile = w + 8 * j;
     if (tile < TILES) {
-      const int m0 = 16 * (tile / L::NT), n0 = 8 * (tile % L::NT);
+      int m0, n0;
+      tile_mn(tile, m0, n0);
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         const int r = m0 + g + 8 * (q >> 1), c = n0 + 2 * t + (q & 1);
@@ -181,8 +201,10 @@ __global__ void k_gram_reduce_all(const ModePack* __restrict__ mp, const Ctl* ct
     while (idx >= (int64_t)mp->m[n].R * mp->m[n].R) idx -= (int64_t)mp->m[n].R * mp->m[n++].R;
     const ModeDev& m = mp->m[n];
     const int64_t RR = (int64_t)m.R * m.R;
+    const int64_t r = idx / m.R, c = idx - r * m.R;
+    const int64_t src = r <= c ? idx : c * m.R + r;  // partials hold the upper triangle
     double a = 0.0;
-    for (int kc = lane; kc < m.nkc_g; kc += 32) a += m.Gpart[kc * RR + idx];
+    for (int kc = lane; kc < m.nkc_g; kc += 32) a += m.Gpart[kc * RR + src];
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
     if (lane == 0) m.Gram[idx] = a;

@@ -217,8 +217,10 @@ __global__ void k_gram_reduce(ModeDev m, double* __restrict__ out, const Ctl* ct
   const int RR = m.R * m.R, lane = threadIdx.x & 31;
   const int wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
   for (int idx = wid; idx < RR; idx += nw) {
+    const int r = idx / m.R, c = idx - r * m.R;
+    const int src = r <= c ? idx : c * m.R + r;  // partials hold the upper triangle (pasd_gram.cuh)
     double a = 0.0;
-    for (int kc = lane; kc < m.nkc_g; kc += 32) a += m.Gpart[(int64_t)kc * RR + idx];
+    for (int kc = lane; kc < m.nkc_g; kc += 32) a += m.Gpart[(int64_t)kc * RR + src];
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
     if (lane == 0) out[idx] = a;
