@@ -72,44 +72,6 @@ struct P2Tmaps {
 
 __host__ __device__ inline int round_up(int x, int m) { return (x + m - 1) / m * m; }
 
-// Shared-memory plan (doubles).  LD values are chosen ~ 8 mod 16 to spread
-// the (row = t, col = g) fragment reads over the banks.
-struct P2Smem {
-  int RM1, RM2, RM3;  // rows padded to 16 (M tiles of the Wt products)
-  int RP1, RP2, RP3;  // K padded to 4
-  int ldA1, ldA2, ldA3, ldU;
-  int oA1, oA2, oA3, oU1, oU2, oU3, oZ3, oG2, oG3, oRed, total;
-};
-
-__host__ __device__ inline P2Smem p2_plan(int R1, int R2, int R3) {
-  P2Smem p;
-  p.RM1 = round_up(R1, 4);  // rows >= R are zero; M tiles past RM read 0 in registers
-  p.RM2 = round_up(R2, 4);
-  p.RM3 = round_up(R3, 4);
-  p.RP1 = round_up(R1, 4);
-  p.RP2 = round_up(R2, 4);
-  p.RP3 = round_up(R3, 4);
-  p.ldA1 = 64 + 8;    // cols (i2, i3)
-  p.ldA2 = 128 + 8;   // cols (i1, i3)
-  p.ldA3 = 128 + 8;   // cols (i1, i2)
-  int rmax = p.RP1 > p.RP2 ? p.RP1 : p.RP2;
-  rmax = rmax > p.RP3 ? rmax : p.RP3;
-  p.ldU = rmax + 4;
-  int o = 0;
-  p.oA1 = o; o += p.RM1 * p.ldA1;
-  p.oA2 = o; o += p.RM2 * p.ldA2;
-  p.oA3 = o; o += p.RM3 * p.ldA3;
-  p.oU1 = o; o += 16 * p.ldU;
-  p.oU2 = o; o += 8 * p.ldU;
-  p.oU3 = o; o += 8 * p.ldU;
-  p.oZ3 = o; o += P2_BRICK;
-  p.oG2 = o; o += P2_BRICK;
-  p.oG3 = o; o += P2_BRICK;
-  p.oRed = o; o += 64;
-  p.total = o;
-  return p;
-}
-
 __device__ __forceinline__ void dmma(double (&c)[4], double a0, double a1, double b0) {
   asm volatile(
       "mma.sync.aligned.m16n8k4.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5}, {%6}, {%0,%1,%2,%3};"
