@@ -497,12 +497,6 @@ __global__ void __cluster_dims__(kSmallCluster, 1, 1) __launch_bounds__(kSmallTh
   double* Wt = m.Wt;                // I x R: G^{next} A^T, reduced by the pass that produced it
   double* X = m.scratch + IR;       // I x R
   double* X2 = m.scratch + 2 * IR;  // I x R
-  if (ctl->vnorm2[n] == 0.0) {
-    // V_n = 0 (nothing kept by the last SVT): W = G V^T = 0 exactly, so the
-    // degenerate rule of linops.cpp:99-101 holds without forming it.
-    if (lead && tid == 0) { ctl->degenerate[n] = 1; ctl->polar_rank[n] = 0; }
-    return;  // uniform over the cluster, before any cluster barrier
-  }
   const RowBlock rb = row_block(I, crank);
   const int64_t lo = rb.lo, rows = rb.rows;
   const double g2 = ctl->gnorm2[n];  // ||G_n^{next}||_F^2
