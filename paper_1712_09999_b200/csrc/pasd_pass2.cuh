@@ -53,6 +53,7 @@ struct Pass2Args {
   double* resid_part;  // [grid][PASD_MAX_ORDER]
   int* bad_part;       // [grid]
   int n1b, n3b, npencils;
+  int nseg;  // i2 segments per pencil (Wt_1 / Wt_3 partials: npencils x nseg; k_pass2_m8 only, else 1)
   int nw2;  // Wt_2 partial slices in W2part (fused: 2 per CTA, one per K-half; m8: 1 per CTA)
   int b1;  // i1 extent of a pencil (16 for k_pass2_fused, 8 for k_pass2_m8)
   // unsharded solves: the last CTA runs the iteration's finish (mu schedule,
@@ -816,12 +817,18 @@ __global__ void k_pass2_reduce(const Pass2Args a, int nblk, Ctl* ctl, double* g2
     if (i >= 0 && i < m.I) {
       if (n == 0) {
         const int ib = (int)(i / a.b1), l = (int)(i % a.b1);
-        for (int b3 = lane; b3 < a.n3b; b3 += 32) s += a.W1p[((int64_t)(ib + a.n1b * b3) * a.b1 + l) * R + r];
+        for (int k = lane; k < a.n3b * a.nseg; k += 32) {
+          const int b3 = k % a.n3b, sg = k / a.n3b;
+          s += a.W1p[((int64_t)(ib + a.n1b * b3 + a.npencils * sg) * a.b1 + l) * R + r];
+        }
       } else if (n == 1) {
         for (int c = lane; c < a.nw2; c += 32) s += a.W2part[((int64_t)c * m.I + i) * R + r];
       } else {
         const int ib = (int)(i / P2_B3), l = (int)(i % P2_B3);
-        for (int b1 = lane; b1 < a.n1b; b1 += 32) s += a.W3p[((int64_t)(b1 + a.n1b * ib) * 8 + l) * R + r];
+        for (int k = lane; k < a.n1b * a.nseg; k += 32) {
+          const int b1 = k % a.n1b, sg = k / a.n1b;
+          s += a.W3p[((int64_t)(b1 + a.n1b * ib + a.npencils * sg) * 8 + l) * R + r];
+        }
       }
     }
 #pragma unroll

@@ -99,7 +99,12 @@ __global__ void __launch_bounds__(M8_THREADS, 2) k_pass2_m8(const Pass2Args a, c
   const int ksz = (max(R1, max(R2, R3)) + 3) / 4;  // Z k-steps that touch a nonzero rank row
   const bool al1 = (I1 % 2) == 0;
 
-  for (int lin = blockIdx.x; lin < a.npencils; lin += gridDim.x) {
+  // Work items: pencil x i2 segment (segments keep small tensors, where the
+  // pencil count is near the CTA count, from ending on a partial wave).
+  const int64_t seg_len = (((I2 + M8_B - 1) / M8_B + a.nseg - 1) / a.nseg) * M8_B;
+  for (int item = blockIdx.x; item < a.npencils * a.nseg; item += gridDim.x) {
+    const int seg = item / a.npencils, lin = item - seg * a.npencils;
+    const int64_t i2b = seg * seg_len, i2e = imin64(I2, i2b + seg_len);
     int ib1, ib3;
     {  // banded order: concurrent pencils form ~12 x 25 patches of (i1, i3) blocks
       const int BW = 12;
@@ -108,7 +113,7 @@ __global__ void __launch_bounds__(M8_THREADS, 2) k_pass2_m8(const Pass2Args a, c
       ib1 = band * BW + lin_in % bw;
       ib3 = lin_in / bw;
     }
-    const int pen = ib1 + a.n1b * ib3;
+    const int pen = ib1 + a.n1b * ib3 + a.npencils * seg;  // index of the Wt_1 / Wt_3 partials
     const int64_t i1o = (int64_t)ib1 * M8_B, i3o = (int64_t)ib3 * M8_B;
     const int nv1 = (int)imin64(M8_B, I1 - i1o);
     __syncthreads();
@@ -206,10 +211,10 @@ __global__ void __launch_bounds__(M8_THREADS, 2) k_pass2_m8(const Pass2Args a, c
         for (int n = 0; n < 3; ++n) yv[n][p] = inb[p] ? a.Y[n][off[p]] : 0.0;
       }
     };
-    stage_step(0);
-    load_elems(0);
+    stage_step(i2b);
+    load_elems(i2b);
 
-    for (int64_t i2o = 0; i2o < I2; i2o += M8_B) {
+    for (int64_t i2o = i2b; i2o < i2e; i2o += M8_B) {
       cp_async_wait_all();
       __syncthreads();
       // ---- Z products: three 8x8 tiles per warp, 2 chains each ----
@@ -270,7 +275,7 @@ __global__ void __launch_bounds__(M8_THREADS, 2) k_pass2_m8(const Pass2Args a, c
         G2x[g28x(g, l2, w)] = gn[1];
         G3x[g38x(g, l2, w)] = gn[2];
       }
-      const bool more = i2o + M8_B < I2;
+      const bool more = i2o + M8_B < i2e;
       if (more) load_elems(i2o + M8_B);  // next step's T, Y in flight during the Wt products
       __syncthreads();
       // ---- Wt_1: A operand = own G_1 (cols permuted: lane t supplies i2 = 2t + p) ----

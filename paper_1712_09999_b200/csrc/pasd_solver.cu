@@ -651,7 +651,26 @@ pasd_solver* create_solver(const pasd_options* o, const pasd_shard* shard) {
     a.n1b = (int)((s->dims[0] + a.b1 - 1) / a.b1);
     a.n3b = (int)((s->dims[2] + P2_B3 - 1) / P2_B3);
     a.npencils = a.n1b * a.n3b;
-    s->p2_grid = std::max(1, std::min(a.npencils, (s->use_m8 ? 2 : 1) * sms));
+    // k_pass2_m8 (small tensors): split each pencil's i2 sweep into nseg segments
+    // when the pencil count would leave the last wave of CTAs mostly empty (C1:
+    // 169 pencils on 296 CTA slots; C2: 625).  Segments keep >= 4 steps each so
+    // the pencil-resident A_2 slice is still reused.
+    a.nseg = 1;
+    if (s->use_m8) {
+      const int slots = 2 * sms;
+      const int64_t steps = (s->dims[1] + M8_B - 1) / M8_B;
+      double best = 0.0;
+      for (int sg = 1; sg <= 8 && (steps + sg - 1) / sg >= 4; ++sg) {
+        const double waves = (double)a.npencils * sg / slots;
+        const double eff = waves / std::ceil(waves);
+        if (eff > best + 0.02) {
+          best = eff;
+          a.nseg = sg;
+        }
+        if (eff >= 0.9) break;
+      }
+    }
+    s->p2_grid = std::max(1, (int)std::min<int64_t>((int64_t)a.npencils * a.nseg, (s->use_m8 ? 2 : 1) * sms));
     // TMA element streams (PASD_P2_TIO=1; needs 16-byte global strides, i.e. I1 even, and the
     // bricks within 227 KB).  Parity-green but slower at C5 (45.7 vs 42.3 ms per launch: the
     // CTA moves to the 228 KB carve-out, the Wt_2/Wt_3 operands are formed from D and Y in the
@@ -672,8 +691,8 @@ pasd_solver* create_solver(const pasd_options* o, const pasd_shard* shard) {
       encode_brick_map(&s->p2_tmaps.d, s->D, da, sa);
     }
     s->p2_smem = s->use_m8 ? 0 : pass2_smem(s->p2_rp, s->p2_tio);
-    a.W1p = s->alloc<double>((size_t)a.npencils * a.b1 * s->modes[0].R);
-    a.W3p = s->alloc<double>((size_t)a.npencils * 8 * s->modes[2].R);
+    a.W1p = s->alloc<double>((size_t)a.npencils * a.nseg * a.b1 * s->modes[0].R);
+    a.W3p = s->alloc<double>((size_t)a.npencils * a.nseg * 8 * s->modes[2].R);
     // Wt_2 partials: one per K-half of each CTA while they stay small next to L2
     // (C3 38 MB, C4 18 MB: one barrier per step fewer, -2..5% pass 2); at C5 the
     // 118 MB they would take thrash L2 (+1 ms), so one per CTA there.
