@@ -53,7 +53,7 @@ struct Pass2Args {
   double* resid_part;  // [grid][PASD_MAX_ORDER]
   int* bad_part;       // [grid]
   int n1b, n3b, npencils;
-  int nseg;  // i2 segments per pencil (Wt_1 / Wt_3 partials: npencils x nseg; k_pass2_m8 only, else 1)
+  int nseg;  // i2 segments per pencil (Wt_1 / Wt_3 partials: npencils x nseg)
   int nw2;  // Wt_2 partial slices in W2part (fused: 2 per CTA, one per K-half; m8: 1 per CTA)
   int b1;  // i1 extent of a pencil (16 for k_pass2_fused, 8 for k_pass2_m8)
   // unsharded solves: the last CTA runs the iteration's finish (mu schedule,
@@ -313,7 +313,11 @@ __global__ void __launch_bounds__(P2_THREADS, 1) k_pass2_fused(const Pass2Args a
   const int ksz = (max(R1, max(R2, R3)) + 3) / 4;  // Z k-steps that touch a nonzero rank row
   const bool al1 = (I1 % 2) == 0;  // 16-byte aligned rows of 16 consecutive i1
 
-  for (int lin = blockIdx.x; lin < a.npencils; lin += gridDim.x) {
+  // Work items: pencil x i2 segment (see the solver's choice of nseg).
+  const int64_t seg_len = (((I2 + P2_B2 - 1) / P2_B2 + a.nseg - 1) / a.nseg) * P2_B2;
+  for (int item = blockIdx.x; item < a.npencils * a.nseg; item += gridDim.x) {
+    const int seg = item / a.npencils, lin = item - seg * a.npencils;
+    const int64_t i2b = seg * seg_len, i2e = imin64(I2, i2b + seg_len);
     // Banded pencil order: the ~gridDim pencils processed concurrently form a
     // ~12 x 12 patch of (i1-block, i3-block), so the A_3 slices (shared along
     // i3) and A_1 slices (shared along i1) they stage each step are L2 hits.
@@ -325,12 +329,12 @@ __global__ void __launch_bounds__(P2_THREADS, 1) k_pass2_fused(const Pass2Args a
       ib1 = band * BW + lin_in % bw;
       ib3 = lin_in / bw;
     }
-    const int pen = ib1 + a.n1b * ib3;  // canonical index of the Wt_1 / Wt_3 partials
+    const int pen = ib1 + a.n1b * ib3 + a.npencils * seg;  // index of the Wt_1 / Wt_3 partials
     const int64_t i1o = (int64_t)ib1 * P2_B1, i3o = (int64_t)ib3 * P2_B3;
     const int nv1 = (int)imin64(16, I1 - i1o);
     const int nbc1 = (nv1 - 2 * (tid & 7)) >= 2 ? 16 : ((nv1 - 2 * (tid & 7)) == 1 ? 8 : 0);  // A_3 chunk bytes
     __syncthreads();  // previous pencil fully done with shared memory
-    load_bricks(i1o, 0, i3o);
+    load_bricks(i1o, i2b, i3o);
     // ---- pencil-resident: A_2 slice (I1, R2, I3 layout), UM_1 rows, UM_3 rows ----
     for (int l3 = 0; l3 < 8; ++l3) {
       const bool in3 = i3o + l3 < I3;
@@ -444,11 +448,11 @@ __global__ void __launch_bounds__(P2_THREADS, 1) k_pass2_fused(const Pass2Args a
         for (int n = 0; n < 3; ++n) yv[n][q] = inb[q] ? a.Y[n][off[q]] : 0.0;
       }
     };
-    stage_a1(0, A1s);
-    stage_a3u2(0);
+    stage_a1(i2b, A1s);
+    stage_a3u2(i2b);
 
-    for (int64_t i2o = 0; i2o < I2; i2o += P2_B2) {
-      const bool more = i2o + P2_B2 < I2;
+    for (int64_t i2o = i2b; i2o < i2e; i2o += P2_B2) {
+      const bool more = i2o + P2_B2 < i2e;
       const double* A1c = A1s;
       if (!TIO) load_elems(i2o);  // this step's T, Y: in flight while the staging lands and Z runs
                                   // (measured 2 ms faster at C5 than prefetching them a step ahead)

@@ -651,23 +651,26 @@ pasd_solver* create_solver(const pasd_options* o, const pasd_shard* shard) {
     a.n1b = (int)((s->dims[0] + a.b1 - 1) / a.b1);
     a.n3b = (int)((s->dims[2] + P2_B3 - 1) / P2_B3);
     a.npencils = a.n1b * a.n3b;
-    // k_pass2_m8 (small tensors): split each pencil's i2 sweep into nseg segments
-    // when the pencil count would leave the last wave of CTAs mostly empty (C1:
-    // 169 pencils on 296 CTA slots; C2: 625).  Segments keep >= 4 steps each so
-    // the pencil-resident A_2 slice is still reused.
+    // Split each pencil's i2 sweep into nseg segments when the pencil count
+    // would leave the last wave of CTAs mostly empty (C1: 169 pencils on 296
+    // slots of k_pass2_m8, C2: 625; C3: 1250 on 148 of k_pass2_fused).
+    // Segments keep >= 4 steps each so the pencil-resident A_2 slice is reused.
     a.nseg = 1;
-    if (s->use_m8) {
-      const int slots = 2 * sms;
-      const int64_t steps = (s->dims[1] + M8_B - 1) / M8_B;
-      double best = 0.0;
+    {
+      const int slots = (s->use_m8 ? 2 : 1) * sms;
+      const int64_t steps = (s->dims[1] + (s->use_m8 ? M8_B : P2_B2) - 1) / (s->use_m8 ? M8_B : P2_B2);
+      // modelled time ~ waves x (steps per item + per-item overhead), the
+      // overhead (pencil-resident staging, Wt_1 / Wt_3 partial reductions)
+      // measured at ~2 steps for the 16x8x8 kernel and ~1 for the 8x8x8 one
+      const double c0 = s->use_m8 ? 1.0 : 2.0;
+      double best = 1e300;
       for (int sg = 1; sg <= 8 && (steps + sg - 1) / sg >= 4; ++sg) {
-        const double waves = (double)a.npencils * sg / slots;
-        const double eff = waves / std::ceil(waves);
-        if (eff > best + 0.02) {
-          best = eff;
+        const double waves = std::ceil((double)a.npencils * sg / slots);
+        const double t = waves * ((double)((steps + sg - 1) / sg) + c0);
+        if (t < best * 0.99) {  // fewer segments unless clearly better
+          best = t;
           a.nseg = sg;
         }
-        if (eff >= 0.9) break;
       }
     }
     s->p2_grid = std::max(1, (int)std::min<int64_t>((int64_t)a.npencils * a.nseg, (s->use_m8 ? 2 : 1) * sms));
