@@ -315,3 +315,19 @@ def test_full_size_trivial_phase_bit_exact(gpu, config):
     for n in range(N):
         np.testing.assert_array_equal(r.y[n].reshape(-1, order="F")[idx], y[n])
     assert r.objective == pytest.approx(np.abs(r.e).sum(), rel=1e-12)  # V_n = 0: objective = ||E||_1
+
+
+def test_solver_ranks_report_the_phase(gpu, oracle_mod):
+    """pasd_b200_solver_ranks: V_n = 0 and a degenerate Procrustes in the first
+    iterations (pasd.cpp:70-74), full rank R once converged on a rank-R instance."""
+    L0, T = instance(oracle_mod, (24, 20, 16), 2, 0.05, seed=5)
+    cfg = PasdConfig(lambdas=oracle_mod.default_lambdas(T.shape), ranks=[2, 2, 2], eps=1e-7)
+    s = gpu.Solver(T.shape, cfg, poll_every=1)
+    s.load(T)
+    s.run(1)
+    assert s.ranks() == ([0, 0, 0], [0, 0, 0])
+    s.run(cfg.maxiter)
+    keep, prank = s.ranks()
+    r = s.finalize()
+    s.close()
+    assert r.converged and keep == [2, 2, 2] and prank == [2, 2, 2]
