@@ -72,6 +72,9 @@ __device__ inline SmallWs make_ws(int R, void* base) {
   return w;
 }
 
+#ifndef PASD_POLAR_ONEPASS
+#define PASD_POLAR_ONEPASS 1e-3  // max relative off-diagonal of (W Qp)^T (W Qp) for the one-pass Procrustes
+#endif
 #ifndef PASD_JACOBI_QUAD
 #define PASD_JACOBI_QUAD 1e-10
 #endif
@@ -519,37 +522,80 @@ __global__ void __cluster_dims__(kSmallCluster, 1, 1) __launch_bounds__(kSmallTh
     if (lead && tid == 0) { ctl->degenerate[n] = 1; ctl->polar_rank[n] = 0; }
     return;  // uniform over the cluster (identical w2)
   }
-  // 3. first Gram/Jacobi pass: C = W^T W = Q1 L Q1^T ; X2 = W Q1
-  if (rows > 0) {
-    cta_gram_tn(X + lo, X + lo, rows, I, R, R, ws.Z, ld, ws.T64);
-  } else {
-    for (int idx = tid; idx < R * R; idx += nt) ws.Z[(idx / R) * ld + idx % R] = 0.0;
+  // 3'. One pass from the previous rotation: X2 = W Qp, C = X2^T X2.  In the
+  //     steady state W's right singular vectors move little between iterations,
+  //     so C is nearly diagonal and a single relative-accuracy Jacobi on it
+  //     resolves every direction (the role of the two-pass scheme below).  When
+  //     C is not nearly diagonal (transitions), fall back to the two passes.
+  bool onepass = false;
+  if (PASD_POLAR_ONEPASS > 0.0) {
+    for (int idx = tid; idx < R * R; idx += nt) ws.Q[(idx % R) * ld + idx / R] = m.Qp[idx];
+    __syncthreads();
+    if (rows > 0) {
+      cta_mul_nn(X + lo, rows, I, R, ws.Q, ld, R, X2 + lo, ws.T64);
+      cta_gram_tn(X2 + lo, X2 + lo, rows, I, R, R, ws.Z, ld, ws.T64);
+    } else {
+      for (int idx = tid; idx < R * R; idx += nt) ws.Z[(idx / R) * ld + idx % R] = 0.0;
+    }
+    cluster_sum_mat(ws.Z, ws.S, R, R, ld);
+    double off = 0.0;  // max |C_ij| / sqrt(C_ii C_jj), i < j (identical in every CTA)
+    for (int idx = tid; idx < R * R; idx += nt) {
+      const int r = idx / R, c = idx % R;
+      if (r < c) {
+        const double d = sqrt(fabs(ws.S[r * ld + r]) * fabs(ws.S[c * ld + c]));
+        const double v = fabs(ws.S[r * ld + c]);
+        off = fmax(off, d > 0.0 ? v / d : (v > 0.0 ? 1.0 : 0.0));
+      }
+    }
+    off = block_reduce(off, MaxOp(), ws.red);
+    if (off <= PASD_POLAR_ONEPASS) {
+      onepass = true;
+      cta_jacobi_eig(ws, R, 3);
+      if (rows > 0) cta_mul_nn(X2 + lo, rows, I, R, ws.V, ld, R, X + lo, ws.T64);
+      for (int idx = tid; idx < R * R; idx += nt) {  // Q = Qp V
+        const int r = idx / R, s = idx % R;
+        double a = 0.0;
+        for (int j = 0; j < R; ++j) a = fma(ws.Q[r * ld + j], ws.V[j * ld + s], a);
+        ws.Z[r * ld + s] = a;
+      }
+      __syncthreads();
+      for (int idx = tid; idx < R * R; idx += nt) ws.Q[(idx / R) * ld + idx % R] = ws.Z[(idx / R) * ld + idx % R];
+      __syncthreads();
+    }
   }
-  cluster_sum_mat(ws.Z, ws.S, R, R, ld);
-  cta_warm_start(ws, R, m.Qp);  // previous right rotation
-  cta_jacobi_eig(ws, R, 2);
-  cta_warm_finish(ws, R);
-  for (int idx = tid; idx < R * R; idx += nt) ws.Q[(idx / R) * ld + idx % R] = ws.V[(idx / R) * ld + idx % R];
-  __syncthreads();
-  if (rows > 0) cta_mul_nn(X + lo, rows, I, R, ws.Q, ld, R, X2 + lo, ws.T64);
-  // 4. second pass on the rotated columns: C2 = X2^T X2 = Q2 L2 Q2^T ; X = X2 Q2 ; Q = Q1 Q2
-  if (rows > 0) {
-    cta_gram_tn(X2 + lo, X2 + lo, rows, I, R, R, ws.Z, ld, ws.T64);
-  } else {
-    for (int idx = tid; idx < R * R; idx += nt) ws.Z[(idx / R) * ld + idx % R] = 0.0;
+  if (!onepass) {
+    // 3. first Gram/Jacobi pass: C = W^T W = Q1 L Q1^T ; X2 = W Q1
+    if (rows > 0) {
+      cta_gram_tn(X + lo, X + lo, rows, I, R, R, ws.Z, ld, ws.T64);
+    } else {
+      for (int idx = tid; idx < R * R; idx += nt) ws.Z[(idx / R) * ld + idx % R] = 0.0;
+    }
+    cluster_sum_mat(ws.Z, ws.S, R, R, ld);
+    cta_warm_start(ws, R, m.Qp);  // previous right rotation
+    cta_jacobi_eig(ws, R, 2);
+    cta_warm_finish(ws, R);
+    for (int idx = tid; idx < R * R; idx += nt) ws.Q[(idx / R) * ld + idx % R] = ws.V[(idx / R) * ld + idx % R];
+    __syncthreads();
+    if (rows > 0) cta_mul_nn(X + lo, rows, I, R, ws.Q, ld, R, X2 + lo, ws.T64);
+    // 4. second pass on the rotated columns: C2 = X2^T X2 = Q2 L2 Q2^T ; X = X2 Q2 ; Q = Q1 Q2
+    if (rows > 0) {
+      cta_gram_tn(X2 + lo, X2 + lo, rows, I, R, R, ws.Z, ld, ws.T64);
+    } else {
+      for (int idx = tid; idx < R * R; idx += nt) ws.Z[(idx / R) * ld + idx % R] = 0.0;
+    }
+    cluster_sum_mat(ws.Z, ws.S, R, R, ld);
+    cta_jacobi_eig(ws, R, 3);
+    if (rows > 0) cta_mul_nn(X2 + lo, rows, I, R, ws.V, ld, R, X + lo, ws.T64);
+    for (int idx = tid; idx < R * R; idx += nt) {
+      const int r = idx / R, s = idx % R;
+      double a = 0.0;
+      for (int j = 0; j < R; ++j) a = fma(ws.Q[r * ld + j], ws.V[j * ld + s], a);
+      ws.Z[r * ld + s] = a;
+    }
+    __syncthreads();
+    for (int idx = tid; idx < R * R; idx += nt) ws.Q[(idx / R) * ld + idx % R] = ws.Z[(idx / R) * ld + idx % R];
+    __syncthreads();
   }
-  cluster_sum_mat(ws.Z, ws.S, R, R, ld);
-  cta_jacobi_eig(ws, R, 3);
-  if (rows > 0) cta_mul_nn(X2 + lo, rows, I, R, ws.V, ld, R, X + lo, ws.T64);
-  for (int idx = tid; idx < R * R; idx += nt) {
-    const int r = idx / R, s = idx % R;
-    double a = 0.0;
-    for (int j = 0; j < R; ++j) a = fma(ws.Q[r * ld + j], ws.V[j * ld + s], a);
-    ws.Z[r * ld + s] = a;
-  }
-  __syncthreads();
-  for (int idx = tid; idx < R * R; idx += nt) ws.Q[(idx / R) * ld + idx % R] = ws.Z[(idx / R) * ld + idx % R];
-  __syncthreads();
   // 5. column norms sigma_j of X (sorted descending by the Jacobi pass): one
   //    warp per column over this CTA's rows, then the cluster sum
   for (int j = tid >> 5; j < R; j += nt >> 5) {
