@@ -201,6 +201,10 @@ struct pasd_solver {
   // finalisation: D2H of E on its own stream, overlapping the X materialisation
   cudaStream_t xfer = nullptr;
   cudaEvent_t ev_xfork = nullptr, ev_xjoin = nullptr;
+  // unsharded graph: pass 1 of the N modes as concurrent branches (small tensors
+  // otherwise leave most SMs idle in each mode's single wave of tiles)
+  cudaStream_t p1s[PASD_MAX_ORDER] = {};
+  cudaEvent_t ev_p1fork = nullptr, ev_p1join[PASD_MAX_ORDER] = {};
   double* A3_partial = nullptr;
   std::vector<double*> gram_partial, wt_partial;
   double* g2_partial = nullptr;
@@ -215,6 +219,11 @@ struct pasd_solver {
     if (ev_xfork) cudaEventDestroy(ev_xfork);
     if (ev_xjoin) cudaEventDestroy(ev_xjoin);
     if (xfer) cudaStreamDestroy(xfer);
+    if (ev_p1fork) cudaEventDestroy(ev_p1fork);
+    for (int n = 0; n < PASD_MAX_ORDER; ++n) {
+      if (ev_p1join[n]) cudaEventDestroy(ev_p1join[n]);
+      if (p1s[n]) cudaStreamDestroy(p1s[n]);
+    }
     if (graph_exec) cudaGraphExecDestroy(graph_exec);
     if (graph) cudaGraphDestroy(graph);
     for (void* p : owned) cudaFree(p);
@@ -239,14 +248,25 @@ double* ctl_gnorm2(pasd_solver* s) {  // device address of ctl->gnorm2[0]
 // Launches one iteration.  `mark(cls, begin)` (optional) is called around
 // every kernel; the profiler records CUDA events there.
 template <class Mark>
-void launch_iteration_marked(pasd_solver* s, cudaStream_t st, Mark&& mark) {
+void launch_iteration_marked(pasd_solver* s, cudaStream_t st, Mark&& mark, bool concurrent = false) {
   const int N = s->N;
   int launches = 0;
   mark(PASD_K_POLAR, true);
   k_polar<<<N * kSmallCluster, kSmallThreads, s->small_smem, st>>>(s->d_pack, s->d_ctl);
   mark(PASD_K_POLAR, false);
   ++launches;
-  if (!s->sharded) {
+  if (!s->sharded && concurrent) {
+    // graph capture: the modes' pass-1 kernels are independent (each reads D, Y_n,
+    // U_n and writes A_n), so they run as concurrent branches and share the SMs
+    CK(cudaEventRecord(s->ev_p1fork, st));
+    for (int n = 0; n < N; ++n) {
+      CK(cudaStreamWaitEvent(s->p1s[n], s->ev_p1fork, 0));
+      launch_contract_A_mma(s->modes[n], s->D, s->Y[n], s->d_ctl, s->sms, s->p1s[n]);
+      CK(cudaEventRecord(s->ev_p1join[n], s->p1s[n]));
+      ++launches;
+    }
+    for (int n = 0; n < N; ++n) CK(cudaStreamWaitEvent(st, s->ev_p1join[n], 0));
+  } else if (!s->sharded) {
     for (int n = 0; n < N; ++n) {
       mark(PASD_K_CONTRACT_A, true);
       launch_contract_A_mma(s->modes[n], s->D, s->Y[n], s->d_ctl, s->sms, st);
@@ -373,7 +393,8 @@ void launch_iteration_marked(pasd_solver* s, cudaStream_t st, Mark&& mark) {
 }
 
 void launch_iteration(pasd_solver* s, cudaStream_t st) {
-  launch_iteration_marked(s, st, [](int, bool) {});
+  static const bool seq = std::getenv("PASD_P1_SEQUENTIAL") != nullptr;  // A/B switch
+  launch_iteration_marked(s, st, [](int, bool) {}, !seq);
 }
 
 // Algorithmic bytes / flops of one launch of each kernel class summed over
@@ -541,6 +562,11 @@ pasd_solver* create_solver(const pasd_options* o, const pasd_shard* shard) {
   CK(cudaStreamCreateWithFlags(&s->xfer, cudaStreamNonBlocking));
   CK(cudaEventCreateWithFlags(&s->ev_xfork, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&s->ev_xjoin, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&s->ev_p1fork, cudaEventDisableTiming));
+  for (int n = 0; n < s->N; ++n) {
+    CK(cudaStreamCreateWithFlags(&s->p1s[n], cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&s->ev_p1join[n], cudaEventDisableTiming));
+  }
   const int64_t S = s->S;
   s->T = s->alloc<double>(S);
   s->E[0] = s->alloc<double>(S);
