@@ -473,25 +473,25 @@ __device__ void svt_mode(const ModeDev& m, int n, Ctl* ctl, double* smem, int cr
 }
 
 __global__ void __cluster_dims__(kSmallCluster, 1, 1) __launch_bounds__(kSmallThreads)
-    k_svt(const ModePack* __restrict__ mp, Ctl* ctl) {
+    k_svt(const ModePack* __restrict__ mp, Ctl* ctl, int mode0 = 0) {
   if (ctl->done) return;
   extern __shared__ double smem[];
   const int crank = (int)cooperative_groups::this_cluster().block_rank();
-  const int n = blockIdx.x / kSmallCluster;
+  const int n = mode0 + blockIdx.x / kSmallCluster;  // mode0: per-mode launches
   svt_mode(mp->m[n], n, ctl, smem, crank);
 }
 
 // ---------------------------------------------------------------------------
 // Procrustes: U_n <- polar(Wt_n M_n) unless degenerate (linops.cpp:93-104).
 __global__ void __cluster_dims__(kSmallCluster, 1, 1) __launch_bounds__(kSmallThreads)
-    k_polar(const ModePack* __restrict__ mp, Ctl* ctl) {
+    k_polar(const ModePack* __restrict__ mp, Ctl* ctl, int mode0 = 0) {
   if (ctl->done) return;
   extern __shared__ double smem[];
   namespace cg = cooperative_groups;
   cg::cluster_group cl = cg::this_cluster();
   const int crank = (int)cl.block_rank();
   const bool lead = crank == 0;
-  const int n = blockIdx.x / kSmallCluster;
+  const int n = mode0 + blockIdx.x / kSmallCluster;  // mode0: per-mode launches
   const ModeDev& m = mp->m[n];
   const int R = m.R, tid = threadIdx.x, nt = blockDim.x;
   const int64_t I = m.Ifull, IR = I * R;

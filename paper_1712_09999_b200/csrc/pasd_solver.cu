@@ -251,22 +251,33 @@ template <class Mark>
 void launch_iteration_marked(pasd_solver* s, cudaStream_t st, Mark&& mark, bool concurrent = false) {
   const int N = s->N;
   int launches = 0;
+  if (!s->sharded && concurrent) {
+    // Graph capture, unsharded: the Procrustes step (U_n) and pass 1 (A_n from D,
+    // Y_n, U_n) are per mode, so each mode is one branch and the branches share
+    // the SMs (small tensors leave most SMs idle in any single mode's kernels).
+    CK(cudaEventRecord(s->ev_p1fork, st));
+    for (int n = 0; n < N; ++n) {
+      cudaStream_t bs = s->p1s[n];
+      const ModeDev& m = s->modes[n];
+      CK(cudaStreamWaitEvent(bs, s->ev_p1fork, 0));
+      k_polar<<<kSmallCluster, kSmallThreads, s->small_smem, bs>>>(s->d_pack, s->d_ctl, n);
+      launch_contract_A_mma(m, s->D, s->Y[n], s->d_ctl, s->sms, bs);
+      CK(cudaEventRecord(s->ev_p1join[n], bs));
+      launches += 2;
+    }
+    for (int n = 0; n < N; ++n) CK(cudaStreamWaitEvent(st, s->ev_p1join[n], 0));
+    // all modes' Gram partials, reductions and SVTs in three launches (per-mode
+    // Gram / SVT branches measured slower: more, smaller launches)
+    launch_gram_all(s->gram_rp, s->d_pack, s->d_ctl, s->gram_grid, st);
+    k_gram_reduce_all<<<s->gram_red_grid, 256, 0, st>>>(s->d_pack, s->d_ctl);
+    k_svt<<<N * kSmallCluster, kSmallThreads, s->small_smem, st>>>(s->d_pack, s->d_ctl);
+    launches += 3;
+  } else {
   mark(PASD_K_POLAR, true);
   k_polar<<<N * kSmallCluster, kSmallThreads, s->small_smem, st>>>(s->d_pack, s->d_ctl);
   mark(PASD_K_POLAR, false);
   ++launches;
-  if (!s->sharded && concurrent) {
-    // graph capture: the modes' pass-1 kernels are independent (each reads D, Y_n,
-    // U_n and writes A_n), so they run as concurrent branches and share the SMs
-    CK(cudaEventRecord(s->ev_p1fork, st));
-    for (int n = 0; n < N; ++n) {
-      CK(cudaStreamWaitEvent(s->p1s[n], s->ev_p1fork, 0));
-      launch_contract_A_mma(s->modes[n], s->D, s->Y[n], s->d_ctl, s->sms, s->p1s[n]);
-      CK(cudaEventRecord(s->ev_p1join[n], s->p1s[n]));
-      ++launches;
-    }
-    for (int n = 0; n < N; ++n) CK(cudaStreamWaitEvent(st, s->ev_p1join[n], 0));
-  } else if (!s->sharded) {
+  if (!s->sharded) {
     for (int n = 0; n < N; ++n) {
       mark(PASD_K_CONTRACT_A, true);
       launch_contract_A_mma(s->modes[n], s->D, s->Y[n], s->d_ctl, s->sms, st);
@@ -327,6 +338,7 @@ void launch_iteration_marked(pasd_solver* s, cudaStream_t st, Mark&& mark, bool 
     mark(PASD_K_SVT, false);
     ++launches;
   }
+  }  // per-mode branches / sequential launches
   if (s->fused) {
     mark(PASD_K_UPDATE, true);
     if (s->use_m8)
