@@ -273,71 +273,71 @@ void launch_iteration_marked(pasd_solver* s, cudaStream_t st, Mark&& mark, bool 
     k_svt<<<N * kSmallCluster, kSmallThreads, s->small_smem, st>>>(s->d_pack, s->d_ctl);
     launches += 3;
   } else {
-  mark(PASD_K_POLAR, true);
-  k_polar<<<N * kSmallCluster, kSmallThreads, s->small_smem, st>>>(s->d_pack, s->d_ctl);
-  mark(PASD_K_POLAR, false);
-  ++launches;
-  if (!s->sharded) {
-    for (int n = 0; n < N; ++n) {
-      mark(PASD_K_CONTRACT_A, true);
-      launch_contract_A_mma(s->modes[n], s->D, s->Y[n], s->d_ctl, s->sms, st);
-      mark(PASD_K_CONTRACT_A, false);
-      ++launches;
-    }
-  } else {
-    // Mode 3 first: its slab partial A_3 (the one large exchange, R_3 I_1 I_2 doubles) is
-    // all-reduced on the side stream while pass 1 of modes 1 and 2 runs on SMs left free
-    // for NCCL's kernel; the main stream joins before the Gram products.
-    ModeDev m3 = s->modes[N - 1];
-    m3.A = s->A3_partial;
-    mark(PASD_K_CONTRACT_A, true);
-    launch_contract_A_mma(m3, s->D, s->Y[N - 1], s->d_ctl, s->sms, st);
-    mark(PASD_K_CONTRACT_A, false);
+    mark(PASD_K_POLAR, true);
+    k_polar<<<N * kSmallCluster, kSmallThreads, s->small_smem, st>>>(s->d_pack, s->d_ctl);
+    mark(PASD_K_POLAR, false);
     ++launches;
-    CK(cudaEventRecord(s->ev_fork, st));
-    CK(cudaStreamWaitEvent(s->side, s->ev_fork, 0));
-    NK(ncclAllReduce(s->A3_partial, s->modes[N - 1].A, (size_t)m3.J * m3.R, ncclDouble, ncclSum, s->comm, s->side));
-    CK(cudaEventRecord(s->ev_join, s->side));
-    const int sms_p1 = std::max(1, s->sms - kNcclSms);
-    for (int n = 0; n < N - 1; ++n) {
+    if (!s->sharded) {
+      for (int n = 0; n < N; ++n) {
+        mark(PASD_K_CONTRACT_A, true);
+        launch_contract_A_mma(s->modes[n], s->D, s->Y[n], s->d_ctl, s->sms, st);
+        mark(PASD_K_CONTRACT_A, false);
+        ++launches;
+      }
+    } else {
+      // Mode 3 first: its slab partial A_3 (the one large exchange, R_3 I_1 I_2 doubles) is
+      // all-reduced on the side stream while pass 1 of modes 1 and 2 runs on SMs left free
+      // for NCCL's kernel; the main stream joins before the Gram products.
+      ModeDev m3 = s->modes[N - 1];
+      m3.A = s->A3_partial;
       mark(PASD_K_CONTRACT_A, true);
-      launch_contract_A_mma(s->modes[n], s->D, s->Y[n], s->d_ctl, sms_p1, st);
+      launch_contract_A_mma(m3, s->D, s->Y[N - 1], s->d_ctl, s->sms, st);
       mark(PASD_K_CONTRACT_A, false);
       ++launches;
+      CK(cudaEventRecord(s->ev_fork, st));
+      CK(cudaStreamWaitEvent(s->side, s->ev_fork, 0));
+      NK(ncclAllReduce(s->A3_partial, s->modes[N - 1].A, (size_t)m3.J * m3.R, ncclDouble, ncclSum, s->comm, s->side));
+      CK(cudaEventRecord(s->ev_join, s->side));
+      const int sms_p1 = std::max(1, s->sms - kNcclSms);
+      for (int n = 0; n < N - 1; ++n) {
+        mark(PASD_K_CONTRACT_A, true);
+        launch_contract_A_mma(s->modes[n], s->D, s->Y[n], s->d_ctl, sms_p1, st);
+        mark(PASD_K_CONTRACT_A, false);
+        ++launches;
+      }
+      CK(cudaStreamWaitEvent(st, s->ev_join, 0));
     }
-    CK(cudaStreamWaitEvent(st, s->ev_join, 0));
-  }
-  if (!s->sharded) {
-    // all modes' Gram partials, then all reductions (pasd_gram.cuh), then the SVTs
-    mark(PASD_K_GRAM, true);
-    launch_gram_all(s->gram_rp, s->d_pack, s->d_ctl, s->gram_grid, st);
-    k_gram_reduce_all<<<s->gram_red_grid, 256, 0, st>>>(s->d_pack, s->d_ctl);
-    mark(PASD_K_GRAM, false);
-    mark(PASD_K_SVT, true);
-    k_svt<<<N * kSmallCluster, kSmallThreads, s->small_smem, st>>>(s->d_pack, s->d_ctl);
-    mark(PASD_K_SVT, false);
-    launches += 3;
-  } else {
-    for (int n = 0; n < N; ++n) {
-      const ModeDev& m = s->modes[n];
+    if (!s->sharded) {
+      // all modes' Gram partials, then all reductions (pasd_gram.cuh), then the SVTs
       mark(PASD_K_GRAM, true);
-      launch_gram_mma(m, s->d_ctl, st);
-      const bool part = n < N - 1;  // Gram_1, Gram_2 are partial over the slab
-      k_gram_reduce<<<8, 256, 0, st>>>(m, part ? s->gram_partial[n] : m.Gram, s->d_ctl);
+      launch_gram_all(s->gram_rp, s->d_pack, s->d_ctl, s->gram_grid, st);
+      k_gram_reduce_all<<<s->gram_red_grid, 256, 0, st>>>(s->d_pack, s->d_ctl);
       mark(PASD_K_GRAM, false);
-      launches += 2;
+      mark(PASD_K_SVT, true);
+      k_svt<<<N * kSmallCluster, kSmallThreads, s->small_smem, st>>>(s->d_pack, s->d_ctl);
+      mark(PASD_K_SVT, false);
+      launches += 3;
+    } else {
+      for (int n = 0; n < N; ++n) {
+        const ModeDev& m = s->modes[n];
+        mark(PASD_K_GRAM, true);
+        launch_gram_mma(m, s->d_ctl, st);
+        const bool part = n < N - 1;  // Gram_1, Gram_2 are partial over the slab
+        k_gram_reduce<<<8, 256, 0, st>>>(m, part ? s->gram_partial[n] : m.Gram, s->d_ctl);
+        mark(PASD_K_GRAM, false);
+        launches += 2;
+      }
+      NK(ncclGroupStart());
+      for (int n = 0; n < N - 1; ++n) {
+        const ModeDev& m = s->modes[n];
+        NK(ncclAllReduce(s->gram_partial[n], m.Gram, (size_t)m.R * m.R, ncclDouble, ncclSum, s->comm, st));
+      }
+      NK(ncclGroupEnd());
+      mark(PASD_K_SVT, true);
+      k_svt<<<N * kSmallCluster, kSmallThreads, s->small_smem, st>>>(s->d_pack, s->d_ctl);
+      mark(PASD_K_SVT, false);
+      ++launches;
     }
-    NK(ncclGroupStart());
-    for (int n = 0; n < N - 1; ++n) {
-      const ModeDev& m = s->modes[n];
-      NK(ncclAllReduce(s->gram_partial[n], m.Gram, (size_t)m.R * m.R, ncclDouble, ncclSum, s->comm, st));
-    }
-    NK(ncclGroupEnd());
-    mark(PASD_K_SVT, true);
-    k_svt<<<N * kSmallCluster, kSmallThreads, s->small_smem, st>>>(s->d_pack, s->d_ctl);
-    mark(PASD_K_SVT, false);
-    ++launches;
-  }
   }  // per-mode branches / sequential launches
   if (s->fused) {
     mark(PASD_K_UPDATE, true);
