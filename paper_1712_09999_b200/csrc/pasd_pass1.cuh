@@ -11,8 +11,9 @@
 // index), so ~150 KB per SM is in flight while the DMMAs of the current chunk
 // run.  G is formed inside the DMMA A-fragment load (each G value feeds exactly
 // one fragment), warp w owns kappa rows 16w..16w+15 and all RP/8 n-tiles.
-// Tiles never cross an outer index q (for modes with inner > 1 a tile is 128
-// consecutive p at fixed q), so every staged row is one contiguous run.
+// A tile is 128 consecutive p at fixed q (every staged row one contiguous run),
+// or, where that wastes a mostly empty p-block per q, 128 consecutive unfolding
+// columns spanning two q (p1_cross).
 #pragma once
 #include "pasd_pass2.cuh"
 
@@ -68,6 +69,20 @@ struct P1Layout {
   static constexpr size_t bytes = sizeof(double) * (size_t)NST * STAGE;
 };
 
+// Strided modes whose inner extent leaves a mostly empty last 128-wide p-block
+// per q (> 5% of the tiles' width wasted: C1-C3, inner = 100, 200, 400) use
+// "crossing" tiles instead: 128 consecutive unfolding columns kappa = p + inner q
+// that may span two q.  (Measured: crossing tiles everywhere cost 7% at C5,
+// inner = 1000, so the q-aligned p-blocks stay where their waste is small.)
+__host__ __device__ inline bool p1_cross(int64_t inner) {
+  const int64_t pb = (inner + P1_MT - 1) / P1_MT;
+  return inner > 1 && (pb * P1_MT - inner) * 20 > pb * P1_MT;
+}
+__host__ __device__ inline int64_t p1_ntiles(const ModeDev& m) {
+  if (m.inner == 1 || p1_cross(m.inner)) return (m.J + P1_MT - 1) / P1_MT;
+  return ((m.inner + P1_MT - 1) / P1_MT) * m.outer;
+}
+
 // Work-item cursor: (tile, chunk) advanced without 64-bit divisions.  For
 // strided modes a tile is (q, p-block); `p0` / `q` track it incrementally.
 struct P1Cursor {
@@ -75,7 +90,7 @@ struct P1Cursor {
   int chunk;
 };
 
-template <int RP, bool CONTIG>
+template <int RP, bool CONTIG, bool CROSS = false>
 __global__ void __launch_bounds__(P1_THREADS, P1_CTAS) k_pass1(ModeDev m, const double* __restrict__ D,
                                                         const double* __restrict__ Y, const Ctl* ctl) {
   if (ctl->done) return;
@@ -88,7 +103,8 @@ __global__ void __launch_bounds__(P1_THREADS, P1_CTAS) k_pass1(ModeDev m, const 
   const int64_t I = m.I, inner = m.inner;
   const int R = m.R;
   const int64_t pblocks = CONTIG ? 1 : (inner + P1_MT - 1) / P1_MT;
-  const int64_t ntiles = CONTIG ? (m.J + P1_MT - 1) / P1_MT : pblocks * m.outer;
+  constexpr bool cross = !CONTIG && CROSS;  // compile-time: the q-aligned kernels carry no trace of it
+  const int64_t ntiles = (CONTIG || cross) ? (m.J + P1_MT - 1) / P1_MT : pblocks * m.outer;
   const int nchunk = (int)((I + P1_KC - 1) / P1_KC);
   const bool al = CONTIG ? (I % 2 == 0) : (inner % 2 == 0);        // 16-byte aligned tensor rows
   const bool alu = (m.Ifull % 2 == 0) && (m.ioff % 2 == 0);         // 16-byte aligned U columns
@@ -139,6 +155,36 @@ __global__ void __launch_bounds__(P1_THREADS, P1_CTAS) k_pass1(ModeDev m, const 
           const bool ok = k0 + j < m.J && cc < ni;
           const int64_t off = (k0 + j) * I + i0 + cc;
           const unsigned d = st + 8u * (unsigned)(j * L::LDR + cc);
+          cp8s(d, ok ? D + off : D, ok ? 8 : 0);
+          cp8s(d + 8u * L::RAW, ok ? Y + off : D, ok ? 8 : 0);
+        }
+      }
+    } else if (cross) {
+      // crossing tile: each column chunk locates its own (p, q)
+      if (al) {
+        constexpr int CPR = P1_MT / 2, RG = P1_THREADS / CPR;
+        const int cc = tid % CPR, rsub = tid / CPR;
+        const int64_t kap = c.tile * P1_MT + 2 * cc;
+        const bool cok = kap < m.J;
+        const int64_t q = kap / inner;
+        const int64_t off0 = (kap - q * inner) + inner * (i0 + I * q);
+#pragma unroll
+        for (int k = 0; k < P1_KC / RG; ++k) {
+          const int ii = rsub + RG * k;
+          const bool ok = cok && ii < ni;  // even inner: a 16-byte chunk never straddles q
+          const int64_t off = off0 + inner * ii;
+          const unsigned d = st + 8u * (unsigned)(ii * L::LDR + 2 * cc);
+          cp16z(d, ok ? D + off : D, ok);
+          cp16z(d + 8u * L::RAW, ok ? Y + off : D, ok);
+        }
+      } else {
+        for (int idx = tid; idx < P1_KC * P1_MT; idx += P1_THREADS) {
+          const int ii = idx / P1_MT, cc = idx % P1_MT;
+          const int64_t kap = c.tile * P1_MT + cc;
+          const bool ok = ii < ni && kap < m.J;
+          const int64_t q = kap / inner;
+          const int64_t off = (kap - q * inner) + inner * (i0 + ii + I * q);
+          const unsigned d = st + 8u * (unsigned)(ii * L::LDR + cc);
           cp8s(d, ok ? D + off : D, ok ? 8 : 0);
           cp8s(d + 8u * L::RAW, ok ? Y + off : D, ok ? 8 : 0);
         }
@@ -253,6 +299,12 @@ __global__ void __launch_bounds__(P1_THREADS, P1_CTAS) k_pass1(ModeDev m, const 
           if (CONTIG) {
             const int64_t kap = cur.tile * P1_MT + row;
             if (kap < m.J) m.A[r + (int64_t)R * kap] = acc[j][q4];
+          } else if (cross) {
+            const int64_t kap = cur.tile * P1_MT + row;
+            if (kap < m.J) {
+              const int64_t q = kap / inner;
+              m.A[(kap - q * inner) + inner * ((int64_t)r + (int64_t)R * q)] = acc[j][q4];
+            }
           } else {
             const int64_t p = cur.pb * P1_MT + row;
             if (p < inner) m.A[p + inner * ((int64_t)r + (int64_t)R * cur.q)] = acc[j][q4];
@@ -265,41 +317,41 @@ __global__ void __launch_bounds__(P1_THREADS, P1_CTAS) k_pass1(ModeDev m, const 
   asm volatile("cp.async.wait_all;" ::: "memory");
 }
 
-template <int RP, bool CONTIG>
+template <int RP, bool CONTIG, bool CROSS>
 void launch_p1(const ModeDev& m, const double* D, const double* Y, const Ctl* ctl,
                int grid, cudaStream_t st) {
   using L = P1Layout<RP, CONTIG>;
-  ensure_smem_attr<k_pass1<RP, CONTIG>>(L::bytes);
-  k_pass1<RP, CONTIG><<<grid, P1_THREADS, L::bytes, st>>>(m, D, Y, ctl);
+  ensure_smem_attr<k_pass1<RP, CONTIG, CROSS>>(L::bytes);
+  k_pass1<RP, CONTIG, CROSS><<<grid, P1_THREADS, L::bytes, st>>>(m, D, Y, ctl);
 }
 
-template <bool CONTIG>
+template <bool CONTIG, bool CROSS>
 void launch_p1_rp(const ModeDev& m, const double* D, const double* Y,
                   const Ctl* ctl, int grid, cudaStream_t st) {
   switch ((m.R + 7) / 8 * 8) {
-    case 8: launch_p1<8, CONTIG>(m, D, Y, ctl, grid, st); break;
-    case 16: launch_p1<16, CONTIG>(m, D, Y, ctl, grid, st); break;
-    case 24: launch_p1<24, CONTIG>(m, D, Y, ctl, grid, st); break;
-    case 32: launch_p1<32, CONTIG>(m, D, Y, ctl, grid, st); break;
-    case 40: launch_p1<40, CONTIG>(m, D, Y, ctl, grid, st); break;
-    case 48: launch_p1<48, CONTIG>(m, D, Y, ctl, grid, st); break;
-    case 56: launch_p1<56, CONTIG>(m, D, Y, ctl, grid, st); break;
-    default: launch_p1<64, CONTIG>(m, D, Y, ctl, grid, st); break;
+    case 8: launch_p1<8, CONTIG, CROSS>(m, D, Y, ctl, grid, st); break;
+    case 16: launch_p1<16, CONTIG, CROSS>(m, D, Y, ctl, grid, st); break;
+    case 24: launch_p1<24, CONTIG, CROSS>(m, D, Y, ctl, grid, st); break;
+    case 32: launch_p1<32, CONTIG, CROSS>(m, D, Y, ctl, grid, st); break;
+    case 40: launch_p1<40, CONTIG, CROSS>(m, D, Y, ctl, grid, st); break;
+    case 48: launch_p1<48, CONTIG, CROSS>(m, D, Y, ctl, grid, st); break;
+    case 56: launch_p1<56, CONTIG, CROSS>(m, D, Y, ctl, grid, st); break;
+    default: launch_p1<64, CONTIG, CROSS>(m, D, Y, ctl, grid, st); break;
   }
 }
 
 inline int pass1_grid(const ModeDev& m, int sms) {
-  const int64_t ntiles =
-      m.inner == 1 ? (m.J + P1_MT - 1) / P1_MT : ((m.inner + P1_MT - 1) / P1_MT) * m.outer;
-  return (int)imin64(ntiles, P1_CTAS * sms);
+  return (int)imin64(p1_ntiles(m), P1_CTAS * sms);
 }
 
 inline void launch_contract_A_mma(const ModeDev& m, const double* D, const double* Y, const Ctl* ctl, int sms, cudaStream_t st) {
   const int grid = pass1_grid(m, sms);
   if (m.inner == 1)
-    launch_p1_rp<true>(m, D, Y, ctl, grid, st);
+    launch_p1_rp<true, false>(m, D, Y, ctl, grid, st);
+  else if (p1_cross(m.inner))
+    launch_p1_rp<false, true>(m, D, Y, ctl, grid, st);
   else
-    launch_p1_rp<false>(m, D, Y, ctl, grid, st);
+    launch_p1_rp<false, false>(m, D, Y, ctl, grid, st);
 }
 
 }  // namespace pasd
