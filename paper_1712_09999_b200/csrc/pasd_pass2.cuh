@@ -20,8 +20,11 @@
 // for Z_3 (exchanged through shared memory).  Wt_1 uses the warp's own G_1
 // values directly as the DMMA A operand; Wt_2 / Wt_3 read G_2 / G_3 from
 // shared memory.  Wt_1 / Wt_3 rows are fixed along a pencil (register
-// accumulation, one partial per pencil); Wt_2 rows change per step and go to a
-// per-CTA partial.  All reductions are in a fixed order (deterministic).
+// accumulation, one partial per pencil, or per pencil segment when the solver
+// splits the i2 sweep, Pass2Args::nseg); Wt_2 rows change per step and go to a
+// per-CTA partial (its two K-halves exchanged by a warp-pair barrier, or kept as
+// two partials when they fit in L2, Pass2Args::nw2).  All reductions are in a
+// fixed order (deterministic).
 #pragma once
 #include <cuda.h>  // CUtensorMap (TMA descriptors, encoded on the host through the driver entry point)
 
