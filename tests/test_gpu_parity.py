@@ -333,13 +333,14 @@ def test_solver_ranks_report_the_phase(gpu, oracle_mod):
     assert r.converged and keep == [2, 2, 2] and prank == [2, 2, 2]
 
 
-def test_steady_state_procrustes_is_the_polar_factor(gpu, oracle_mod):
+@pytest.mark.parametrize("dims,r", [((30, 28, 26), 3), ((66, 60, 57), 50)])
+def test_steady_state_procrustes_is_the_polar_factor(gpu, oracle_mod, dims, r):
     """Full-rank phase (where the Procrustes takes its one-pass, warm-rotation
     route and the SVT its warm-started Jacobi): U_k = polar(W_k), W_k = G^(k)
     V_{k-1}^T, G^(k) = unfold_n(T - E_{k-1} + Y_{n,k-1} / mu_k) (pasd.cpp:178-187,
     linops.cpp:93-104), and V_k = SVT(U_k^T G^(k)), to 1e-10."""
-    L0, T = instance(oracle_mod, (30, 28, 26), 3, 0.05, seed=4)
-    cfg = PasdConfig(lambdas=oracle_mod.default_lambdas(T.shape), ranks=[3, 3, 3], eps=1e-14, maxiter=160)
+    L0, T = instance(oracle_mod, dims, r, 0.05, seed=4)
+    cfg = PasdConfig(lambdas=oracle_mod.default_lambdas(T.shape), ranks=[r] * 3, eps=1e-14, maxiter=160)
     K = 150
     views = {}
 
@@ -350,7 +351,7 @@ def test_steady_state_procrustes_is_the_polar_factor(gpu, oracle_mod):
     gpu.pasd_recover(T, cfg, observer=obs, fixed_iters=True)
     a, b = views[K - 1], views[K]
     for n in range(3):
-        assert np.linalg.matrix_rank(a.v[n]) == 3
+        assert np.linalg.matrix_rank(a.v[n]) == r
         G = oracle_mod.unfold((T - a.e) + a.y[n] * (1.0 / b.mu_used), n + 1)
         W = G @ a.v[n].T
         uw, _, vt = np.linalg.svd(W, full_matrices=False)
