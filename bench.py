@@ -369,8 +369,9 @@ def main():
     if shard:
         del T
     steady_after = args.steady_after if world == 1 else 0
+    steady_start = max(steady_after, W + K + args.profile_iters) if steady_after else 0
     cfg = PasdConfig(lambdas=w.lambdas(), ranks=list(w.ranks), eps=w.eps,
-                     maxiter=max(W + K + args.profile_iters + 1, steady_after + 13))
+                     maxiter=max(W + K + args.profile_iters + 1, steady_start + 13))
     sol = pb.Solver(w.dims, cfg, fixed_iters=True, poll_every=K, shard=shard)
     sol.load(T_loc.data_ptr(), t_is_device=True)
     sol.run(W)
