@@ -1,0 +1,36 @@
+"""BASELINE configs[0] as a whole solve: C1 (100^3, Tucker rank 10, 10% corruption),
+R = 10, run to eps = 1e-7 -- GPU (pasd_recover through the C-ABI, host buffers)
+vs the CPU restatement of the reference (oracle/, 1 thread and all threads).
+Prints one JSON line (run under gpurun; writes nothing else)."""
+import json
+import os
+import sys
+import time
+
+import numpy as np
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import oracle  # noqa: E402  (CPU baseline only)
+import paper_1712_09999_b200 as pb  # noqa: E402
+from paper_1712_09999_b200.api import PasdConfig  # noqa: E402
+
+dims = (100, 100, 100)
+L0 = oracle.gen_tucker(dims, [10, 10, 10], seed=0)
+T = oracle.corrupt_sparse(L0, 0.10, seed=0)
+cfg = PasdConfig(lambdas=oracle.default_lambdas(dims), ranks=[10, 10, 10], eps=1e-7)
+rse = lambda x: float(np.linalg.norm(x - L0) / np.linalg.norm(L0))  # noqa: E731
+out = {"workload": "c1_100cube_r10 solve to eps 1e-7 (BASELINE configs[0])"}
+pb.pasd_recover(T, cfg)  # warm-up (module load, solver cache)
+ts = []
+for _ in range(5):
+    t0 = time.perf_counter()
+    rg = pb.pasd_recover(T, cfg)
+    ts.append(time.perf_counter() - t0)
+out["gpu"] = {"seconds": float(np.median(ts)), "iters": rg.iters, "converged": rg.converged, "rse": rse(rg.x)}
+for threads in (1, os.cpu_count() or 1):
+    t0 = time.perf_counter()
+    ro = oracle.pasd_recover(T, cfg, threads=threads)
+    out[f"cpu_{threads}t"] = {"seconds": time.perf_counter() - t0, "iters": ro.iters, "converged": ro.converged,
+                             "rse": rse(ro.x)}
+out["speedup_vs_1t"] = out["cpu_1t"]["seconds"] / out["gpu"]["seconds"]
+print(json.dumps(out))
