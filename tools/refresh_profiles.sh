@@ -10,6 +10,7 @@ O=gpurun_out/prof
 mkdir -p $O
 python bench.py --steps 20 --warmup 3 > $O/${R}_bench_c5.json 2> $O/${R}_bench_c5.err
 python bench.py --impl reference --steps 3 --warmup 3 > $O/${R}_bench_reference_c5.json 2> $O/${R}_bench_reference_c5.err
+python tools/c1_solve.py > $O/${R}_c1_solve.json 2> $O/${R}_c1_solve.err
 for c in c1 c2 c3 c4; do
   python bench.py --config $c --steps 20 --warmup 3 > $O/${R}_bench_$c.json 2> $O/${R}_bench_$c.err
 done
