@@ -15,10 +15,12 @@
  * Tensors are dense float64 with the FIRST index varying fastest
  * (proj/include/tenrec/tensor.hpp:23-24).  Matrices are column-major.
  *
- * No global mutable state: every call owns its stream(s), device buffers and
- * (multi-GPU) NCCL communicator, so concurrent calls from several host threads
- * are safe (the reference harness calls the solver from a thread pool,
- * proj/src/bench.cpp:226-248).
+ * Every call owns its stream(s), device buffers and (multi-GPU) NCCL
+ * communicator, so concurrent calls from several host threads are safe (the
+ * reference harness calls the solver from a thread pool,
+ * proj/src/bench.cpp:226-248).  The only global mutable state is the opt-in
+ * solver reuse of pasd_b200_recover (PASD_FLAG_REUSE_SOLVER, mutex-guarded;
+ * see there for the HBM it retains).
  */
 #ifndef PASD_B200_H
 #define PASD_B200_H
@@ -52,7 +54,15 @@ enum {
   PASD_FLAG_NO_CERTIFICATE = 1u << 0,
   /* Deterministic fixed-iteration mode: ignore eps, run exactly maxiter
    * iterations (BASELINE "fixed N iters" runs).  converged is reported 0. */
-  PASD_FLAG_FIXED_ITERS = 1u << 1
+  PASD_FLAG_FIXED_ITERS = 1u << 1,
+  /* pasd_b200_recover only: keep this call's solver (device buffers + the
+   * captured iteration graph) for the next call with identical options, which
+   * then skips allocation, graph capture and teardown.  Results do not depend
+   * on it.  The kept solver holds its HBM -- about (N + 4) S doubles plus the
+   * A_n (R_n J_n doubles each): ~64 GB at 1000^3, R = 50 -- until
+   * pasd_b200_release_cache() or exit; a call with different options frees it
+   * before allocating its own. */
+  PASD_FLAG_REUSE_SOLVER = 1u << 2
 };
 
 /* Mirror of tenrec::PasdConfig (pasd.hpp:8-27) plus placement. */
@@ -124,16 +134,13 @@ typedef struct pasd_outputs {
 
 /* Full solve from a HOST tensor: H2D of t, the device-resident ADMM loop, the
  * finalisation and D2H of the requested outputs.  Returns PASD_OK or an error
- * code; errbuf receives the reference's exception message text.
- * The last successful call's solver (device buffers and captured iteration
- * graph) is kept, keyed on the full options struct, so a repeated solve of
- * the same shape and options skips allocation and teardown; results do not
- * depend on it.  Set PASD_B200_NO_CACHE in the environment to disable. */
+ * code; errbuf receives the reference's exception message text.  With
+ * PASD_FLAG_REUSE_SOLVER the solver is kept for the next identical call. */
 int pasd_b200_recover(const double* t, const pasd_options* opt, pasd_outputs* out,
                       pasd_observer_fn observer, void* user, char* errbuf, size_t errlen);
 
-/* Free the solver kept by pasd_b200_recover (device memory returns to the
- * allocator).  Safe to call at any time. */
+/* Free the solver kept by pasd_b200_recover under PASD_FLAG_REUSE_SOLVER
+ * (device memory returns to the allocator).  Safe to call at any time. */
 void pasd_b200_release_cache(void);
 
 /* ---- device-resident solver handle (benchmarks, multi-GPU) -------------- */
@@ -218,6 +225,43 @@ int pasd_b200_svt(const double* m, int64_t rows, int64_t cols, double tau, doubl
 int pasd_b200_procrustes(const double* g, int64_t i_rows, int64_t p_cols, const double* v, int64_t r_rows,
                          const double* u_prev, double* u_out, int32_t* degenerate, int32_t* rank, int32_t device,
                          char* errbuf, size_t errlen);
+
+/* ---- spec-shaped single-step API (pasd.hpp:43-58, 68-70) ----------------
+ * The reference's PasdState pieces as host buffers: t, e, y (S doubles each,
+ * first index fastest), u (I_n x R_n) and v (R_n x J_n, J_n = S / I_n,
+ * unfolding column order), all column-major; mode is 1-based like the
+ * reference (out of range -> ArgumentError "mode m out of range 1..N",
+ * tensor.cpp:133-137).  Device kernels compute every step; results go to
+ * caller-allocated host buffers.
+ *
+ * pasd_g_matrix (pasd.cpp:82-97): g_out (I_n x J_n) = unfold_n((T - E) + Y / mu),
+ * the reference's operation order (bit-exact). */
+int pasd_b200_g_matrix(int32_t order, const int64_t* dims, const double* t, const double* e, const double* y,
+                       double mu, int32_t mode, double* g_out, int32_t device, char* errbuf, size_t errlen);
+/* update_u (pasd.cpp:99-103 -> update_u_from, pasd.cpp:70-74): u_out (I_n x R_n)
+ * = polar(G_n V_n^T), or u_prev when the product is numerically zero
+ * (linops.cpp:99-101; *degenerate = 1). */
+int pasd_b200_update_u(int32_t order, const int64_t* dims, const double* t, const double* e, const double* y,
+                       double mu, int32_t mode, int64_t rank, const double* u_prev, const double* v, double* u_out,
+                       int32_t* degenerate, int32_t device, char* errbuf, size_t errlen);
+/* update_v (pasd.cpp:105-109 -> update_v_from, pasd.cpp:76-78): v_out (R_n x J_n)
+ * = svt(U_n^T G_n, lambda / mu); *kept = number of singular values kept. */
+int pasd_b200_update_v(int32_t order, const int64_t* dims, const double* t, const double* e, const double* y,
+                       double mu, int32_t mode, int64_t rank, const double* u, double lambda, double* v_out,
+                       int32_t* kept, int32_t device, char* errbuf, size_t errlen);
+/* update_e (pasd.cpp:111-130): e_out = soft(mean_n((T - fold_n(U_n V_n)) + Y_n / mu),
+ * 1 / (mu N)); u[N], v[N], y[N], ranks[N]. */
+int pasd_b200_update_e(int32_t order, const int64_t* dims, const int64_t* ranks, const double* t,
+                       const double* const* u, const double* const* v, const double* const* y, double mu,
+                       double* e_out, int32_t device, char* errbuf, size_t errlen);
+/* suboptimality_certificate (pasd.hpp:68-70, pasd.cpp:277-309) of a finished
+ * run: PASD_ERR_STATE "certificate requires a converged result" unless
+ * converged, "certificate requires the final multipliers" when y / y_hat
+ * (N host tensors each) are missing.  opt supplies dims, lambdas, mu0, rho,
+ * eps (and the device). */
+int pasd_b200_certificate(const double* t, const pasd_options* opt, int32_t iters, int32_t converged,
+                          const double* const* y, const double* const* y_hat, double* epsilon_hat, double* c,
+                          double* bound, char* errbuf, size_t errlen);
 
 /* 128-byte NCCL unique id for pasd_shard.nccl_unique_id (rank 0 creates it and
  * broadcasts it to the other ranks with the host launcher's own channel). */

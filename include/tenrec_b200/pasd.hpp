@@ -12,6 +12,7 @@
 // Eigen is not a dependency of this build; `data()` layouts are identical.
 #pragma once
 
+#include <algorithm>
 #include <cstdint>
 #include <functional>
 #include <optional>
@@ -101,15 +102,32 @@ struct RecoveryResult {
   std::vector<DenseTensor> y_hat;
 };
 
-// recovery.hpp:38-50 (u/v are column-major host copies).
+// recovery.hpp:38-50: the same members, typed.  The referenced objects are
+// host copies owned by the callback frame and valid only during the call
+// (pasd.cpp:241-242).
 struct IterationView {
-  int iter = 0;
-  double mu_used = 0;
-  double mu_next = 0;
-  std::vector<double> residual_inf;
-  const pasd_iteration_view* raw = nullptr;  // e, z, y, u, v pointers, valid during the callback
+  int iter = 0;        // 1-based count of completed iterations
+  double mu_used = 0;  // penalty used by this iteration's updates
+  double mu_next = 0;  // penalty after the schedule step
+  const std::vector<double>& residual_inf;
+  const DenseTensor& e;
+  const std::vector<DenseTensor>& z;
+  const std::vector<DenseTensor>& y;
+  const std::vector<Matrix>* u = nullptr;  // I_n x R_n
+  const std::vector<Matrix>* v = nullptr;  // R_n x J_n (unfolding column order)
 };
 using IterationObserver = std::function<void(const IterationView&)>;
+
+// pasd.hpp:33-41
+struct PasdState {
+  std::vector<Matrix> u;
+  std::vector<Matrix> v;
+  DenseTensor e;
+  std::vector<DenseTensor> y;
+  std::vector<DenseTensor> y_hat;
+  double mu = 0.0;
+  int iter = 0;
+};
 
 // pasd.hpp:8-27
 struct PasdConfig {
@@ -225,18 +243,33 @@ inline RecoveryResult pasd_recover(const DenseTensor& t, const PasdConfig& confi
   out.final_residuals = res.final_residuals.data();
   struct Ctx {
     const IterationObserver* obs;
-    std::size_t n;
-  } ctx{&observer, n};
+    const std::vector<Index>* dims;
+    const std::vector<Index>* ranks;
+  } ctx{&observer, &dims, &config.ranks};
   pasd_observer_fn fn = nullptr;
   if (observer) {
     fn = [](const pasd_iteration_view* v, void* user) {
       auto* c = static_cast<Ctx*>(user);
-      IterationView view;
-      view.iter = v->iter;
-      view.mu_used = v->mu_used;
-      view.mu_next = v->mu_next;
-      view.residual_inf.assign(v->residual_inf, v->residual_inf + c->n);
-      view.raw = v;
+      const std::vector<Index>& d = *c->dims;
+      const std::size_t N = d.size();
+      Index S = 1;
+      for (Index x : d) S *= x;
+      auto tensor = [&](const double* p) { return DenseTensor::from_data(d, std::vector<double>(p, p + S)); };
+      std::vector<double> resid(v->residual_inf, v->residual_inf + N);
+      const DenseTensor e = tensor(v->e);
+      std::vector<DenseTensor> z, y;
+      std::vector<Matrix> u, vv;
+      for (std::size_t k = 0; k < N; ++k) {
+        z.push_back(tensor(v->z[k]));
+        y.push_back(tensor(v->y[k]));
+        const Index I = d[k], R = (*c->ranks)[k], J = S / I;
+        Matrix um(I, R), vm(R, J);
+        std::copy(v->u[k], v->u[k] + I * R, um.data());
+        std::copy(v->v[k], v->v[k] + R * J, vm.data());
+        u.push_back(std::move(um));
+        vv.push_back(std::move(vm));
+      }
+      const IterationView view{v->iter, v->mu_used, v->mu_next, resid, e, z, y, &u, &vv};
       (*c->obs)(view);
     };
   }
@@ -248,6 +281,103 @@ inline RecoveryResult pasd_recover(const DenseTensor& t, const PasdConfig& confi
   res.objective = out.objective;
   if (out.has_certificate) res.certificate = Certificate{out.cert_epsilon_hat, out.cert_c, out.cert_bound};
   return res;
+}
+
+// ---- spec-shaped single-step API (pasd.hpp:43-58, 68-70) ------------------
+namespace detail {
+inline void check_state(const PasdState& st, const DenseTensor& t, Index mode) {
+  if (mode < 1 || mode > t.order())
+    throw ArgumentError("mode " + std::to_string(mode) + " out of range 1.." + std::to_string(t.order()));
+  const auto n = static_cast<std::size_t>(mode - 1);
+  if (st.u.size() <= n || st.v.size() <= n || st.y.size() <= n)
+    throw ArgumentError("pasd_b200: state has no basis / coefficients / multiplier for mode " + std::to_string(mode));
+}
+}  // namespace detail
+
+// pasd_g_matrix (pasd.cpp:82-97)
+inline Matrix pasd_g_matrix(const DenseTensor& t, const DenseTensor& e, const DenseTensor& y, double mu, Index mode,
+                            int device = 0) {
+  if (t.dims() != e.dims() || t.dims() != y.dims()) throw ArgumentError("g_matrix: dimension mismatch");
+  if (mode < 1 || mode > t.order())
+    throw ArgumentError("mode " + std::to_string(mode) + " out of range 1.." + std::to_string(t.order()));
+  Matrix g(t.dim(mode), t.size() / t.dim(mode));
+  char err[1024] = {0};
+  detail::check(pasd_b200_g_matrix(static_cast<int32_t>(t.order()), t.dims().data(), t.data(), e.data(), y.data(), mu,
+                                   static_cast<int32_t>(mode), g.data(), device, err, sizeof(err)),
+                err);
+  return g;
+}
+
+// update_u (pasd.cpp:99-103)
+inline Matrix update_u(const PasdState& state, const DenseTensor& t, Index mode, int device = 0) {
+  detail::check_state(state, t, mode);
+  const auto n = static_cast<std::size_t>(mode - 1);
+  const Matrix& up = state.u[n];
+  Matrix u(up.rows(), up.cols());
+  int32_t degenerate = 0;
+  char err[1024] = {0};
+  detail::check(pasd_b200_update_u(static_cast<int32_t>(t.order()), t.dims().data(), t.data(), state.e.data(),
+                                   state.y[n].data(), state.mu, static_cast<int32_t>(mode), up.cols(), up.data(),
+                                   state.v[n].data(), u.data(), &degenerate, device, err, sizeof(err)),
+                err);
+  return u;
+}
+
+// update_v (pasd.cpp:105-109)
+inline Matrix update_v(const PasdState& state, const DenseTensor& t, Index mode, double lambda, int device = 0) {
+  detail::check_state(state, t, mode);
+  const auto n = static_cast<std::size_t>(mode - 1);
+  const Index R = state.u[n].cols();
+  Matrix v(R, t.size() / t.dim(mode));
+  int32_t kept = 0;
+  char err[1024] = {0};
+  detail::check(pasd_b200_update_v(static_cast<int32_t>(t.order()), t.dims().data(), t.data(), state.e.data(),
+                                   state.y[n].data(), state.mu, static_cast<int32_t>(mode), R, state.u[n].data(),
+                                   lambda, v.data(), &kept, device, err, sizeof(err)),
+                err);
+  return v;
+}
+
+// update_e (pasd.cpp:111-130)
+inline DenseTensor update_e(const PasdState& state, const DenseTensor& t, int device = 0) {
+  const auto N = static_cast<std::size_t>(t.order());
+  if (state.u.size() != N || state.v.size() != N || state.y.size() != N)
+    throw ArgumentError("pasd_b200: state needs one basis / coefficient matrix / multiplier per mode");
+  std::vector<Index> ranks(N);
+  std::vector<const double*> u(N), v(N), y(N);
+  for (std::size_t k = 0; k < N; ++k) {
+    ranks[k] = state.u[k].cols();
+    u[k] = state.u[k].data();
+    v[k] = state.v[k].data();
+    y[k] = state.y[k].data();
+  }
+  DenseTensor e = DenseTensor::zeros(t.dims());
+  char err[1024] = {0};
+  detail::check(pasd_b200_update_e(static_cast<int32_t>(N), t.dims().data(), ranks.data(), t.data(), u.data(),
+                                   v.data(), y.data(), state.mu, e.data(), device, err, sizeof(err)),
+                err);
+  return e;
+}
+
+// suboptimality_certificate (pasd.cpp:277-309)
+inline Certificate suboptimality_certificate(const RecoveryResult& result, const DenseTensor& t,
+                                             const PasdConfig& config) {
+  if (!result.converged) throw StateError("certificate requires a converged result");
+  const auto N = static_cast<std::size_t>(t.order());
+  if (result.y.size() != N || result.y_hat.size() != N) throw StateError("certificate requires the final multipliers");
+  detail::count_checks(config, N);
+  pasd_options o = config.to_c(t.dims());
+  std::vector<const double*> y(N), h(N);
+  for (std::size_t k = 0; k < N; ++k) {
+    y[k] = result.y[k].data();
+    h[k] = result.y_hat[k].data();
+  }
+  Certificate c;
+  char err[1024] = {0};
+  detail::check(pasd_b200_certificate(t.data(), &o, result.iters, 1, y.data(), h.data(), &c.epsilon_hat, &c.c,
+                                      &c.bound, err, sizeof(err)),
+                err);
+  return c;
 }
 
 }  // namespace tenrec_b200

@@ -169,3 +169,37 @@ def default_lambdas(dims):
     total = int(np.prod([int(d) for d in dims]))
     n = float(len(dims))
     return [math.sqrt(float(max(int(d), total // int(d)))) / n for d in dims]
+
+
+def pasd_v0_phase(t, config: PasdConfig, iters: int, *, threads: int = 1, fixed_iters: bool = True,
+                  e_out=None, y_out=None):
+    """pasd_recover restricted to the V = 0 phase (pasd_oracle.cpp v0_phase).
+
+    Returns (e, y, history, final_residuals, min_margin, left_at, iters_done):
+    left_at is the first iteration whose SVT would keep a singular value (the
+    phase ends there and the run stops before it), 0 if the phase lasted.
+    e_out / y_out may be preallocated Fortran-ordered float64 tensors."""
+    from paper_1712_09999_b200.api import build_options
+    t = as_tensor(t)
+    dims = t.shape
+    opt, _keep = build_options(dims, config, flags=_abi.PASD_FLAG_FIXED_ITERS if fixed_iters else 0)
+    S = t.size
+    e = e_out if e_out is not None else np.empty(dims, order="F")
+    ys = y_out if y_out is not None else [np.empty(dims, order="F") for _ in dims]
+    for a in [e] + list(ys):
+        assert a.flags.f_contiguous and a.dtype == np.float64 and a.shape == dims
+    yp = (_abi.c_double_p * len(dims))(*[_abi.dptr(np.ravel(y, order="K")) for y in ys])
+    hist = np.zeros(max(1, iters))
+    resid = np.zeros(len(dims))
+    margin = C.c_double(0.0)
+    left = C.c_int(0)
+    done = C.c_int(0)
+    err = _err()
+    f = lib().oracle_pasd_v0_phase
+    f.restype = C.c_int
+    rc = f(_abi.dptr(np.ravel(t, order="K")), C.byref(opt), C.c_int(iters), C.c_int(threads),
+           _abi.dptr(np.ravel(e, order="K")), yp, _abi.dptr(hist), _abi.dptr(resid), C.byref(margin),
+           C.byref(left), C.byref(done), err, C.c_size_t(len(err)))
+    raise_for_status(rc, err)
+    assert e.size == S
+    return e, ys, hist[:done.value].tolist(), resid, margin.value, left.value, done.value

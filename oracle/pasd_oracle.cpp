@@ -158,11 +158,12 @@ static void unfold_into(const double* src, const std::vector<Index>& dims, Index
     std::memcpy(dst, src, size_t(slab * s.outer) * sizeof(double));
     return;
   }
-  par_for(s.outer, [&](Index qb, Index qe, int) {
-    for (Index q = qb; q < qe; ++q)
-      for (Index p = 0; p < s.inner; ++p)
-        for (Index r = 0; r < s.mode_dim; ++r)
-          dst[q * slab + r + s.mode_dim * p] = src[q * slab + p + s.inner * r];
+  // parallel over the unfolding columns j = p + inner*q (pure copies: any split is exact)
+  par_for(s.inner * s.outer, [&](Index jb, Index je, int) {
+    for (Index j = jb; j < je; ++j) {
+      const Index q = j / s.inner, p = j - q * s.inner;
+      for (Index r = 0; r < s.mode_dim; ++r) dst[q * slab + r + s.mode_dim * p] = src[q * slab + p + s.inner * r];
+    }
   });
 }
 
@@ -174,11 +175,11 @@ static void fold_into(const double* src, const std::vector<Index>& dims, Index m
     std::memcpy(dst, src, size_t(slab * s.outer) * sizeof(double));
     return;
   }
-  par_for(s.outer, [&](Index qb, Index qe, int) {
-    for (Index q = qb; q < qe; ++q)
-      for (Index r = 0; r < s.mode_dim; ++r)
-        for (Index p = 0; p < s.inner; ++p)
-          dst[q * slab + p + s.inner * r] = src[q * slab + r + s.mode_dim * p];
+  par_for(s.inner * s.outer, [&](Index jb, Index je, int) {
+    for (Index j = jb; j < je; ++j) {
+      const Index q = j / s.inner, p = j - q * s.inner;
+      for (Index r = 0; r < s.mode_dim; ++r) dst[q * slab + p + s.inner * r] = src[q * slab + r + s.mode_dim * p];
+    }
   });
 }
 
@@ -267,7 +268,14 @@ static Matrix svt(const Matrix& m, double tau, Index* kept = nullptr) {  // lino
 static bool procrustes(const Matrix& g, const Matrix& v, Matrix& u_out) {
   if (g.cols != v.cols) throw ArgumentError("procrustes: g and v must have the same number of columns");
   if (v.rows > g.rows) throw ArgumentError("procrustes: v has more rows than g (R must not exceed I)");
-  const Matrix w = gemm(g, false, v, true);
+  // W = G V^T, formed as (V G^T)^T: OpenBLAS's NT kernel with n = R and
+  // k = J ~ 1e5 runs at ~1 GF/s, the TN/NT product with the long dimension as
+  // k in the other operand order at full speed (same product, another
+  // summation order -- neither is Eigen's).
+  const Matrix wt = gemm(v, false, g, true);
+  Matrix w(g.rows, v.rows);
+  for (Index i = 0; i < w.rows; ++i)
+    for (Index r = 0; r < w.cols; ++r) w(i, r) = wt(r, i);
   const double scale = std::max(1.0, g.norm() * v.norm());
   if (w.norm() <= 1e-14 * scale) return false;
   const ThinSvd svd = thin_svd(w);
@@ -516,6 +524,135 @@ static Result pasd_recover(const double* td, const std::vector<Index>& dims, con
   res.y_hat = std::move(y_hat);
   if (converged) certificate(res, td, total, static_cast<size_t>(n_modes), cfg);
   return res;
+}
+
+// --------------------------------------------------- pasd.cpp, V = 0 phase
+// The same iteration as pasd_recover above, restricted to the phase in which
+// every V_n is still zero, for the full-size configs whose
+// complete solve does not fit a test (C3/C4 at 100 iterations, C5 at 50):
+//   * W = G V^T = 0, so procrustes is degenerate and U_n stays eye(I_n, R_n)
+//     (linops.cpp:99-101, pasd.cpp:70-74, init pasd.cpp:152);
+//   * A_n = U_n^T G_(n) is then rows 0..R_n-1 of the unfolding, and svt keeps
+//     nothing iff sigma_max(A_n) <= lambda_n / mu (linops.cpp:84-88), so
+//     V_n = 0 and Z_n = U_n V_n = 0 (pasd.cpp:188-190);
+//   * E, Y_n, the residuals and mu follow pasd.cpp:193-239 with Z_n = 0, in
+//     the reference's operation order (T - 0.0 == T exactly).
+// The precondition is CHECKED every iteration: sigma_max(A_n)^2 is the largest
+// eigenvalue of A_n A_n^T (dsyrk over column blocks + dsyev).  The function
+// stops at the first iteration whose SVT would keep a singular value (returned
+// in *left_at, 0 if none) and reports the smallest relative margin
+// (tau - sigma_max) / tau seen.  Bit-exact with pasd_recover while the phase
+// lasts (tests/test_oracle_kat.py::test_v0_phase_matches_full_oracle).
+extern "C" void scipy_dsyrk_(const char* uplo, const char* trans, const int* n, const int* k, const double* alpha,
+                             const double* a, const int* lda, const double* beta, double* c, const int* ldc, size_t,
+                             size_t);
+extern "C" int scipy_LAPACKE_dsyev(int layout, char jobz, char uplo, int n, double* a, int lda, double* w);
+
+static void v0_phase(const double* td, const std::vector<Index>& dims, const Config& cfg, int iters, double* ed,
+                     double* const* yd, double* hist, double* resid_out, double* min_margin, int* left_at,
+                     int* iters_done) {
+  validate(cfg, dims);
+  const Index total = dims_product(dims);
+  const size_t N = dims.size();
+  const int T = g_threads;
+  scipy_openblas_set_num_threads(1);  // dsyrk is called from every worker thread
+  std::fill(ed, ed + total, 0.0);
+  for (size_t n = 0; n < N; ++n) std::fill(yd[n], yd[n] + total, 0.0);
+  double mu = cfg.mu0;
+  *left_at = 0;
+  *min_margin = std::numeric_limits<double>::infinity();
+  std::vector<double> resid(N, std::numeric_limits<double>::infinity());
+  int iter = 0;
+  constexpr Index kBlk = 256;
+  while (iter < iters) {
+    const double inv_mu = 1.0 / mu;
+    // precondition of this iteration's SVT: sigma_max(rows 0..R-1 of G_(n)) <= lambda_n / mu
+    for (size_t n = 0; n < N; ++n) {
+      const ModeSplit sp = split_dims(dims, Index(n) + 1);
+      const int R = int(cfg.ranks[n]);
+      const Index J = sp.inner * sp.outer;
+      std::vector<std::vector<double>> part(size_t(std::max(1, T)), std::vector<double>(size_t(R) * R, 0.0));
+      const double* y = yd[n];
+      auto body = [&](Index b, Index e_, int k) {
+        std::vector<double> blk(size_t(R) * kBlk);
+        double* c = part[size_t(k)].data();
+        for (Index j0 = b; j0 < e_; j0 += kBlk) {
+          const int nb = int(std::min<Index>(kBlk, e_ - j0));
+          for (int jj = 0; jj < nb; ++jj) {
+            const Index j = j0 + jj, p = j % sp.inner, q = j / sp.inner;
+            for (int r = 0; r < R; ++r) {
+              const Index i = p + sp.inner * r + sp.inner * sp.mode_dim * q;
+              blk[size_t(r) + size_t(R) * jj] = td[i] - ed[i] + y[i] * inv_mu;  // pasd.cpp:183
+            }
+          }
+          const double one = 1.0;
+          scipy_dsyrk_("U", "N", &R, &nb, &one, blk.data(), &R, &one, c, &R, 1, 1);
+        }
+      };
+      if (T <= 1 || J < 4096) {
+        body(0, J, 0);
+      } else {
+        std::vector<std::thread> th;
+        for (int k = 0; k < T; ++k) th.emplace_back(body, J * k / T, J * (k + 1) / T, k);
+        for (auto& t : th) t.join();
+      }
+      std::vector<double> gram(size_t(R) * R, 0.0), w(size_t(R), 0.0);
+      for (auto& pk : part)
+        for (size_t i = 0; i < gram.size(); ++i) gram[i] += pk[i];
+      if (scipy_LAPACKE_dsyev(kColMajor, 'N', 'U', R, gram.data(), R, w.data()) != 0)
+        throw NumericalError("v0_phase: dsyev failed");
+      const double smax = std::sqrt(std::max(0.0, w[size_t(R - 1)]));
+      const double tau = cfg.lambdas[n] / mu;  // pasd.cpp:77
+      const double margin = (tau - smax) / tau;
+      *min_margin = std::min(*min_margin, margin);
+      if (!(smax <= tau)) {  // svt would keep sigma_1 (strict sigma > tau, linops.cpp:85)
+        *left_at = iter + 1;
+        *iters_done = iter;
+        for (size_t m = 0; m < N; ++m) resid_out[m] = resid[m];
+        return;
+      }
+    }
+    // E update with Z_n = 0 (pasd.cpp:193-209), multiplier ascent + residuals (pasd.cpp:211-228)
+    const double inv_n = 1.0 / double(N);
+    const double tau_e = 1.0 / (mu * double(N));
+    std::vector<std::vector<double>> worst(size_t(std::max(1, T)), std::vector<double>(N, 0.0));
+    std::vector<int> badv(size_t(std::max(1, T)), 0);
+    par_for(total, [&](Index b, Index e_, int k) {
+      double* wk = worst[size_t(k)].data();
+      int nbad = 0;
+      for (Index i = b; i < e_; ++i) {
+        double sd = 0.0;
+        for (size_t n = 0; n < N; ++n) sd += td[i] - 0.0 + yd[n][i] * inv_mu;
+        const double e = soft_threshold(sd * inv_n, tau_e);
+        ed[i] = e;
+        for (size_t n = 0; n < N; ++n) {
+          const double r = td[i] - 0.0 - e;
+          yd[n][i] += mu * r;
+          const double a = std::fabs(r);
+          if (a > wk[n]) wk[n] = a;
+          nbad |= !std::isfinite(r);
+        }
+      }
+      badv[size_t(k)] = nbad;
+    });
+    bool bad = false;
+    for (size_t n = 0; n < N; ++n) {
+      double w = 0.0;
+      for (size_t k = 0; k < worst.size(); ++k) w = std::max(w, worst[k][n]);
+      resid[n] = w;
+    }
+    for (int b : badv) bad = bad || b;
+    const double mu_next = std::min(cfg.rho * mu, cfg.mu_max);  // pasd.cpp:229
+    ++iter;
+    if (bad) throw NumericalError("pasd: non-finite iterate at iteration " + std::to_string(iter));
+    hist[iter - 1] = *std::max_element(resid.begin(), resid.end());
+    mu = mu_next;
+    bool converged = !cfg.fixed_iters;  // pasd.cpp:235-237
+    for (double r : resid) converged = converged && (r < cfg.eps);
+    if (converged) break;
+  }
+  *iters_done = iter;
+  for (size_t n = 0; n < N; ++n) resid_out[n] = resid[n];
 }
 
 // -------------------------------------------------------------- rng.hpp/synth
@@ -849,5 +986,32 @@ int oracle_procrustes(const double* g, int64_t i_rows, int64_t p_cols, const dou
   });
 }
 double oracle_soft_threshold(double x, double tau) { return soft_threshold(x, tau); }
+
+// V = 0 phase restatement (see v0_phase above).  e (S) and y[N] (S each) are
+// caller buffers that receive the iterate; hist has room for `iters` entries.
+int oracle_pasd_v0_phase(const double* t, const pasd_options* opt, int iters, int threads, double* e,
+                         double* const* y, double* hist, double* resid, double* min_margin, int* left_at,
+                         int* iters_done, char* err, size_t errlen) {
+  return guarded(err, errlen, [&] {
+    if (!opt || opt->order < 1) throw ArgumentError("tensor order must be at least 1");
+    g_threads = std::max(1, threads);
+    const std::vector<Index> dims = to_dims(opt->order, opt->dims);
+    Config cfg;
+    for (int n = 0; n < opt->order; ++n) {
+      cfg.lambdas.push_back(opt->lambdas[n]);
+      cfg.ranks.push_back(opt->ranks[n]);
+    }
+    cfg.mu0 = opt->mu0;
+    cfg.mu_max = opt->mu_max;
+    cfg.rho = opt->rho;
+    cfg.eps = opt->eps;
+    cfg.maxiter = opt->maxiter;
+    cfg.fixed_iters = (opt->flags & PASD_FLAG_FIXED_ITERS) != 0;
+    const Index total = dims_product(dims);
+    for (Index i = 0; i < total; ++i)
+      if (!std::isfinite(t[i])) throw ArgumentError("pasd: input tensor contains non-finite entries");
+    v0_phase(t, dims, cfg, std::min(iters, cfg.maxiter), e, y, hist, resid, min_margin, left_at, iters_done);
+  });
+}
 
 }  // extern "C"

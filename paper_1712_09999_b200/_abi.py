@@ -18,6 +18,7 @@ PASD_ERR_CUDA = 5
 PASD_FLAG_NONE = 0
 PASD_FLAG_NO_CERTIFICATE = 1 << 0
 PASD_FLAG_FIXED_ITERS = 1 << 1
+PASD_FLAG_REUSE_SOLVER = 1 << 2
 
 PASD_KERNEL_CLASSES = ("polar", "contract_A", "gram", "svt", "update", "finish", "contract_W")
 
@@ -110,6 +111,11 @@ HEADER_SYMBOLS = (
     "pasd_b200_validate",
     "pasd_b200_svt",
     "pasd_b200_procrustes",
+    "pasd_b200_g_matrix",
+    "pasd_b200_update_u",
+    "pasd_b200_update_v",
+    "pasd_b200_update_e",
+    "pasd_b200_certificate",
     "pasd_b200_nccl_unique_id",
     "pasd_b200_abi_version",
     "pasd_b200_build_info",

@@ -4,6 +4,7 @@
 * ``Certificate``     — ``tenrec::Certificate``     (recovery.hpp:14-18)
 * ``RecoveryResult``  — ``tenrec::RecoveryResult``  (recovery.hpp:20-34)
 * ``IterationView``   — ``tenrec::IterationView``   (recovery.hpp:38-48)
+* ``PasdState``       — ``tenrec::PasdState``       (pasd.hpp:33-41)
 * ``ArgumentError`` / ``IoError`` / ``NumericalError`` / ``StateError``
   — the exception taxonomy of errors.hpp:9-30.
 
@@ -137,6 +138,20 @@ class IterationView:
 
 
 IterationObserver = Callable[[IterationView], None]
+
+
+@dataclass
+class PasdState:
+    """Solver iterate (tenrec::PasdState, pasd.hpp:33-41): u[n] (I_n x R_n),
+    v[n] (R_n x J_n, unfolding column order), e, y[n], y_hat[n], mu, iter."""
+
+    u: List[np.ndarray]
+    v: List[np.ndarray]
+    e: np.ndarray
+    y: List[np.ndarray]
+    y_hat: List[np.ndarray] = field(default_factory=list)
+    mu: float = 0.0
+    iter: int = 0
 
 
 def as_tensor(t) -> np.ndarray:

@@ -135,6 +135,24 @@ T* dalloc(size_t count) {
 
 int rpt_for(int R) { return R <= 8 ? 2 : R <= 16 ? 4 : R <= 32 ? 8 : 16; }
 
+// The small solves' dynamic shared-memory cap is a per-(kernel, device)
+// attribute shared by every solver in the process: set it once per device to
+// the largest workspace this build supports (R = PASD_MAX_RANK), so a solver
+// created later with a smaller rank can never lower it under an earlier one.
+void ensure_small_smem_attr() {
+  static std::mutex mu;
+  static std::vector<char> done;
+  int dev = 0;
+  CK(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lk(mu);
+  if ((int)done.size() <= dev) done.resize(dev + 1, 0);
+  if (done[dev]) return;
+  const int bytes = (int)small_ws_bytes(PASD_MAX_RANK);
+  CK(cudaFuncSetAttribute(k_svt, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+  CK(cudaFuncSetAttribute(k_polar, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+  done[dev] = 1;
+}
+
 }  // namespace
 
 // ============================================================================
@@ -669,8 +687,7 @@ pasd_solver* create_solver(const pasd_options* o, const pasd_shard* shard) {
     gram_entries += (int64_t)m.R * m.R;
   }
   s->gram_red_grid = (int)std::min<int64_t>((gram_entries + 7) / 8, 8 * s->sms);  // one warp per entry
-  CK(cudaFuncSetAttribute(k_svt, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->small_smem));
-  CK(cudaFuncSetAttribute(k_polar, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->small_smem));
+  ensure_small_smem_attr();
   if (s->N == 3) {
     s->fused = true;
     Pass2Args& a = s->p2;
@@ -1225,11 +1242,14 @@ void pasd_b200_solver_destroy(pasd_solver* s) {
   }
 }
 
-// One-shot solves keep the last solver (device buffers, captured graph) keyed
-// on the complete options struct: a repeated call with the same problem shape
-// and options skips allocation, graph capture and teardown.  The cache holds
-// device memory until pasd_b200_release_cache() or process exit; set
-// PASD_B200_NO_CACHE to disable it.
+// Opt-in reuse (PASD_FLAG_REUSE_SOLVER): a one-shot solve may keep its solver
+// (device buffers, captured graph) keyed on the complete options struct, so a
+// repeated call with the same problem shape and options skips allocation,
+// graph capture and teardown.  This is the library's only global state; it
+// is never used unless the caller sets the flag, and it holds the solver's
+// HBM (about (N+4) S doubles plus A_n: ~64 GB at 1000^3, R = 50) until
+// pasd_b200_release_cache() or process exit.  On a miss the stale entry is
+// freed BEFORE the new solver is allocated, so peak HBM is one solver.
 namespace {
 std::mutex g_cache_mu;
 pasd_solver* g_cache = nullptr;
@@ -1264,8 +1284,8 @@ std::vector<char> options_key(const pasd_options* o) {
 
 int pasd_b200_recover(const double* t, const pasd_options* opt, pasd_outputs* out, pasd_observer_fn observer,
                       void* user, char* errbuf, size_t errlen) {
-  static const bool use_cache = std::getenv("PASD_B200_NO_CACHE") == nullptr;
   static const bool trace = std::getenv("PASD_B200_TRACE") != nullptr;
+  const bool use_cache = opt && (opt->flags & PASD_FLAG_REUSE_SOLVER);
   pasd_solver* s = nullptr;
   std::vector<char> key;
   const int rc = guarded_call(errbuf, errlen, [&] {
@@ -1275,8 +1295,18 @@ int pasd_b200_recover(const double* t, const pasd_options* opt, pasd_outputs* ou
     const auto t0 = now();
     if (use_cache) {
       key = options_key(opt);
-      std::lock_guard<std::mutex> lk(g_cache_mu);
-      if (g_cache && key == g_cache_key) std::swap(s, g_cache);  // take it (concurrent calls build their own)
+      pasd_solver* stale = nullptr;
+      {
+        std::lock_guard<std::mutex> lk(g_cache_mu);
+        if (g_cache && key == g_cache_key) {
+          std::swap(s, g_cache);  // take it (concurrent calls build their own)
+        } else if (g_cache) {
+          stale = g_cache;        // a miss: free the old solver before allocating a new one
+          g_cache = nullptr;
+          g_cache_key.clear();
+        }
+      }
+      pasd_b200_solver_destroy(stale);
     }
     bool uploaded = false;
     if (s) {
@@ -1352,13 +1382,29 @@ __global__ void k_set_ctl(Ctl* ctl, double mu, double vnorm2) {
   ctl->vnorm2[0] = vnorm2;
 }
 
-void device_svt(const double* m_h, int64_t rows, int64_t cols, double tau, double* out_h, int32_t* kept, int device) {
+// m_is_device: m is a device pointer on `device` (the spec helpers form U^T G there).
+void device_svt(const double* m_h, int64_t rows, int64_t cols, double tau, double* out_h, int32_t* kept, int device,
+                bool m_is_device = false) {
   if (tau < 0.0 || !std::isfinite(tau)) fail(PASD_ERR_ARGUMENT, "svt: threshold must be a nonnegative finite number");
   if (rows < 1 || cols < 1) fail(PASD_ERR_ARGUMENT, "thin_svd: matrix must be nonempty");
-  for (int64_t i = 0; i < rows * cols; ++i)
-    if (!std::isfinite(m_h[i])) fail(PASD_ERR_ARGUMENT, "thin_svd: input contains non-finite entries");
+  if (m_is_device) {
+    CK(cudaSetDevice(device));
+    TmpDev f;
+    int* flag = f.alloc<int>(1);
+    CK(cudaMemset(flag, 0, sizeof(int)));
+    k_nonfinite<<<256, 256>>>(m_h, rows * cols, flag);
+    int h = 0;
+    CK(cudaMemcpy(&h, flag, sizeof(int), cudaMemcpyDeviceToHost));
+    if (h) fail(PASD_ERR_ARGUMENT, "thin_svd: input contains non-finite entries");
+  } else {
+    for (int64_t i = 0; i < rows * cols; ++i)
+      if (!std::isfinite(m_h[i])) fail(PASD_ERR_ARGUMENT, "thin_svd: input contains non-finite entries");
+  }
   if (tau == 0.0) {  // linops.cpp:80-81
-    std::memcpy(out_h, m_h, sizeof(double) * rows * cols);
+    if (m_is_device)
+      CK(cudaMemcpy(out_h, m_h, sizeof(double) * rows * cols, cudaMemcpyDeviceToHost));
+    else
+      std::memcpy(out_h, m_h, sizeof(double) * rows * cols);
     if (kept) *kept = (int32_t)std::min(rows, cols);
     return;
   }
@@ -1390,7 +1436,7 @@ void device_svt(const double* m_h, int64_t rows, int64_t cols, double tau, doubl
   for (int i = 0; i < R; ++i) eye[i + R * i] = 1.0;
   CK(cudaMemcpy(m.U, eye.data(), sizeof(double) * R * R, cudaMemcpyHostToDevice));
   CK(cudaMemcpy(m.P, eye.data(), sizeof(double) * R * R, cudaMemcpyHostToDevice));
-  CK(cudaMemcpy(m.A, m_h, sizeof(double) * rows * cols, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(m.A, m_h, sizeof(double) * rows * cols, m_is_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice));
   ModePack pack{};
   pack.order = 1;
   pack.m[0] = m;
@@ -1401,7 +1447,7 @@ void device_svt(const double* m_h, int64_t rows, int64_t cols, double tau, doubl
   k_gram<<<m.nkc_g, kThreads>>>(m, ctl);
   k_gram_reduce<<<8, 256>>>(m, m.Gram, ctl);
   const size_t smem = small_ws_bytes(R);
-  CK(cudaFuncSetAttribute(k_svt, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  ensure_small_smem_attr();
   k_svt<<<kSmallCluster, kSmallThreads, smem>>>(d_pack, ctl);
   double* V = t.alloc<double>(rows * cols);
   k_materialize_v<<<256, 256>>>(m, V);
@@ -1413,7 +1459,7 @@ void device_svt(const double* m_h, int64_t rows, int64_t cols, double tau, doubl
 }
 
 void device_procrustes(const double* g_h, int64_t I, int64_t P, const double* v_h, int64_t R64, const double* u_prev,
-                       double* u_out, int32_t* degenerate, int32_t* rank, int device) {
+                       double* u_out, int32_t* degenerate, int32_t* rank, int device, bool g_is_device = false) {
   if (R64 > I) fail(PASD_ERR_ARGUMENT, "procrustes: v has more rows than g (R must not exceed I)");
   if (I < 1 || P < 1 || R64 < 1) fail(PASD_ERR_ARGUMENT, "thin_svd: matrix must be nonempty");
   if (R64 > PASD_MAX_RANK)
@@ -1433,7 +1479,7 @@ void device_procrustes(const double* g_h, int64_t I, int64_t P, const double* v_
   double* G = t.alloc<double>(I * P);
   double* Z0 = t.alloc<double>(I * P);
   CK(cudaMemset(Z0, 0, sizeof(double) * I * P));
-  CK(cudaMemcpy(G, g_h, sizeof(double) * I * P, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(G, g_h, sizeof(double) * I * P, g_is_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice));
   m.A = t.alloc<double>(R * P);
   CK(cudaMemcpy(m.A, v_h, sizeof(double) * R * P, cudaMemcpyHostToDevice));
   m.U = t.alloc<double>(IR);
@@ -1475,7 +1521,7 @@ void device_procrustes(const double* g_h, int64_t I, int64_t P, const double* v_
   CK(cudaMemcpy(d_pack, &pack, sizeof(pack), cudaMemcpyHostToDevice));
   k_wreduce_generic<<<dim3(64, 1), 256>>>(d_pack, ctl);
   const size_t smem = small_ws_bytes(R);
-  CK(cudaFuncSetAttribute(k_polar, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  ensure_small_smem_attr();
   k_polar<<<kSmallCluster, kSmallThreads, smem>>>(d_pack, ctl);
   CK(cudaGetLastError());
   Ctl hc;
@@ -1507,3 +1553,5 @@ int pasd_b200_procrustes(const double* g, int64_t i_rows, int64_t p_cols, const 
 }
 
 }  // extern "C"
+
+#include "pasd_spec.cuh"

@@ -103,9 +103,13 @@ def default_rank_bound(target_rank: int) -> int:
 
 
 def pasd_recover(t, config: PasdConfig, observer=None, *, device: int = 0, fixed_iters: bool = False,
-                 want_z: bool = True, want_y: bool = True, poll_every: int = 0) -> RecoveryResult:
-    """Drop-in for tenrec::pasd_recover (pasd.hpp:65-66) on a B200."""
-    flags = _abi.PASD_FLAG_FIXED_ITERS if fixed_iters else 0
+                 want_z: bool = True, want_y: bool = True, poll_every: int = 0,
+                 reuse_solver: bool = False) -> RecoveryResult:
+    """Drop-in for tenrec::pasd_recover (pasd.hpp:65-66) on a B200.
+
+    reuse_solver: keep the device solver for the next call with identical
+    options (PASD_FLAG_REUSE_SOLVER; frees with release_cache())."""
+    flags = (_abi.PASD_FLAG_FIXED_ITERS if fixed_iters else 0) | (_abi.PASD_FLAG_REUSE_SOLVER if reuse_solver else 0)
     return run_recover(lib().pasd_b200_recover, t, config, observer, flags=flags, want_z=want_z, want_y=want_y,
                        device=device, poll_every=poll_every)
 
@@ -179,9 +183,13 @@ class Solver:
         raise_for_status(L.pasd_b200_solver_ranks(self._h, keep, prank, err, len(err)), err)
         return list(keep), list(prank)
 
-    def finalize(self, want_x=True, want_e=True, want_z=False, want_y=False, out_x=None, out_e=None):
+    def finalize(self, want_x=True, want_e=True, want_z=False, want_y=False, out_x=None, out_e=None,
+                 want_y_hat=None):
         """Finalise into new arrays, or into `out_x` / `out_e` (contiguous float64
-        buffers of the local slab's size, e.g. views of pinned host memory)."""
+        buffers of the local slab's size, e.g. views of pinned host memory).
+        Y-hat is returned with Y unless want_y_hat says otherwise."""
+        if want_y_hat is None:
+            want_y_hat = want_y
         n = len(self.dims)
         total = int(np.prod(self.local_dims))
 
@@ -196,7 +204,7 @@ class Solver:
         e = dest(out_e, want_e)
         z = [np.empty(total) for _ in range(n)] if want_z else None
         y = [np.empty(total) for _ in range(n)] if want_y else None
-        yh = [np.empty(total) for _ in range(n)] if want_y else None
+        yh = [np.empty(total) for _ in range(n)] if want_y_hat else None
         hist = np.zeros(max(1, int(self.config.maxiter)))
         fres = np.zeros(n)
         out = _abi.PasdOutputs()
@@ -319,3 +327,123 @@ def _solver_set_state(self, e, y, u, v, mu: float, iteration: int) -> None:
 
 
 Solver.set_state = _solver_set_state
+
+
+# ---- spec-shaped single-step API (pasd.hpp:43-58, 68-70) -------------------
+def _f64(a):
+    return np.ravel(np.asfortranarray(np.asarray(a, dtype=np.float64)), order="F")
+
+
+def _dims_arg(t):
+    d = np.ascontiguousarray(np.asarray(t.shape, dtype=np.int64))
+    return d, d.ctypes.data_as(_abi.c_int64_p)
+
+
+def pasd_g_matrix(t, e, y, mu: float, mode: int, *, device: int = 0) -> np.ndarray:
+    """G_n = unfold_n(T - E + Y / mu) (pasd.cpp:82-97), on the device; mode 1-based."""
+    t = as_tensor(t)
+    if np.shape(e) != t.shape or np.shape(y) != t.shape:
+        raise ArgumentError("g_matrix: dimension mismatch")  # pasd.cpp:84-85
+    d, dp = _dims_arg(t)
+    rows = t.shape[mode - 1] if 1 <= mode <= t.ndim else 1
+    g = np.empty((rows, t.size // rows), order="F")
+    err = _err()
+    L = lib()
+    L.pasd_b200_g_matrix.restype = C.c_int
+    rc = L.pasd_b200_g_matrix(C.c_int32(t.ndim), dp, _abi.dptr(_f64(t)), _abi.dptr(_f64(e)), _abi.dptr(_f64(y)),
+                              C.c_double(mu), C.c_int32(mode), g.ctypes.data_as(_abi.c_double_p), C.c_int32(device),
+                              err, C.c_size_t(len(err)))
+    raise_for_status(rc, err)
+    return g
+
+
+def update_u(state, t, mode: int, *, device: int = 0) -> np.ndarray:
+    """Basis update (pasd.cpp:99-103): polar(G_n V_n^T), or the previous basis
+    when the product is numerically zero."""
+    t = as_tensor(t)
+    n = mode - 1
+    d, dp = _dims_arg(t)
+    u_prev = _f64(state.u[n]) if 0 <= n < t.ndim else np.zeros(1)
+    v = _f64(state.v[n]) if 0 <= n < t.ndim else np.zeros(1)
+    rank = np.asarray(state.u[n]).shape[1] if 0 <= n < t.ndim else 1
+    rows = t.shape[n] if 0 <= n < t.ndim else 1
+    out = np.empty((rows, rank), order="F")
+    deg = C.c_int32(0)
+    err = _err()
+    L = lib()
+    L.pasd_b200_update_u.restype = C.c_int
+    y = state.y[n] if 0 <= n < t.ndim else t
+    rc = L.pasd_b200_update_u(C.c_int32(t.ndim), dp, _abi.dptr(_f64(t)), _abi.dptr(_f64(state.e)),
+                              _abi.dptr(_f64(y)), C.c_double(state.mu), C.c_int32(mode), C.c_int64(rank),
+                              _abi.dptr(u_prev), _abi.dptr(v), out.ctypes.data_as(_abi.c_double_p), C.byref(deg),
+                              C.c_int32(device), err, C.c_size_t(len(err)))
+    raise_for_status(rc, err)
+    return out
+
+
+def update_v(state, t, mode: int, lam: float, *, device: int = 0) -> np.ndarray:
+    """Coefficient update (pasd.cpp:105-109): SVT_{lambda/mu}(U_n^T G_n)."""
+    t = as_tensor(t)
+    n = mode - 1
+    d, dp = _dims_arg(t)
+    ok = 0 <= n < t.ndim
+    rank = np.asarray(state.u[n]).shape[1] if ok else 1
+    cols = t.size // t.shape[n] if ok else 1
+    out = np.empty((rank, cols), order="F")
+    kept = C.c_int32(0)
+    err = _err()
+    L = lib()
+    L.pasd_b200_update_v.restype = C.c_int
+    rc = L.pasd_b200_update_v(C.c_int32(t.ndim), dp, _abi.dptr(_f64(t)), _abi.dptr(_f64(state.e)),
+                              _abi.dptr(_f64(state.y[n] if ok else t)), C.c_double(state.mu), C.c_int32(mode),
+                              C.c_int64(rank), _abi.dptr(_f64(state.u[n] if ok else np.zeros(1))), C.c_double(lam),
+                              out.ctypes.data_as(_abi.c_double_p), C.byref(kept), C.c_int32(device), err,
+                              C.c_size_t(len(err)))
+    raise_for_status(rc, err)
+    return out
+
+
+def update_e(state, t, *, device: int = 0) -> np.ndarray:
+    """Sparse update (pasd.cpp:111-130): shrink(mean_n(T - fold_n(U_n V_n) + Y_n / mu), 1 / (mu N))."""
+    t = as_tensor(t)
+    n = t.ndim
+    d, dp = _dims_arg(t)
+    if len(state.u) != n or len(state.v) != n or len(state.y) != n:
+        raise ArgumentError("update_e: expected one u/v/y per mode")
+    ranks = np.ascontiguousarray(np.asarray([np.asarray(u).shape[1] for u in state.u], dtype=np.int64))
+    uf = [_f64(u) for u in state.u]
+    vf = [_f64(v) for v in state.v]
+    yf = [_f64(y) for y in state.y]
+    out = np.empty(t.shape, order="F")
+    err = _err()
+    L = lib()
+    L.pasd_b200_update_e.restype = C.c_int
+    rc = L.pasd_b200_update_e(C.c_int32(n), dp, ranks.ctypes.data_as(_abi.c_int64_p), _abi.dptr(_f64(t)),
+                              _abi.ptr_array(uf), _abi.ptr_array(vf), _abi.ptr_array(yf), C.c_double(state.mu),
+                              out.ctypes.data_as(_abi.c_double_p), C.c_int32(device), err, C.c_size_t(len(err)))
+    raise_for_status(rc, err)
+    return out
+
+
+def suboptimality_certificate(result: RecoveryResult, t, config: PasdConfig, *, device: int = 0):
+    """Certificate of a converged run (pasd.cpp:277-309); StateError otherwise."""
+    from .api import Certificate, StateError
+
+    t = as_tensor(t)
+    count_checks(list(t.shape), config)
+    if not result.converged:
+        raise StateError("certificate requires a converged result")
+    if not result.y or not result.y_hat or len(result.y) != t.ndim or len(result.y_hat) != t.ndim:
+        raise StateError("certificate requires the final multipliers")
+    opt, keep = build_options(list(t.shape), config, device=device)
+    yf = [_f64(a) for a in result.y]
+    hf = [_f64(a) for a in result.y_hat]
+    eh, c, b = C.c_double(0), C.c_double(0), C.c_double(0)
+    err = _err()
+    L = lib()
+    L.pasd_b200_certificate.restype = C.c_int
+    rc = L.pasd_b200_certificate(_abi.dptr(_f64(t)), C.byref(opt), C.c_int32(result.iters),
+                                 C.c_int32(1 if result.converged else 0), _abi.ptr_array(yf), _abi.ptr_array(hf),
+                                 C.byref(eh), C.byref(c), C.byref(b), err, C.c_size_t(len(err)))
+    raise_for_status(rc, err)
+    return Certificate(eh.value, c.value, b.value)
