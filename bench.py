@@ -152,11 +152,14 @@ def cpu_baseline(w, threads: int, iters: int = 3):
     gaps = [b - a for a, b in zip(stamps[:-1], stamps[1:])]
     per_iter = statistics.median(gaps)
     elem_rate = total / per_iter
+    extrapolated = total != w.size
     return {
         "value": elem_rate / w.size,
         "unit": "iter/s",
         "cores": threads,
         "kind": "port",
+        "extrapolated": extrapolated,
+        "sample_dims": list(dims),
         "elem_iters_per_s": elem_rate,
         "sample": f"oracle/ (C++ restatement of proj/src/pasd.cpp, OpenBLAS dgesdd/dgemm) on dims {list(dims)} "
                   f"ranks {list(ranks)}, {iters} fixed iterations, per-iteration time = median gap between "
@@ -272,7 +275,7 @@ def e2e_sharded(w, steps, shard, dist):
                     "max over ranks; bytes per rank amortised per iteration"}
 
 
-def roofline_from_profile(prof, peaks, iters):
+def roofline_from_profile(prof, peaks, iters, workload):
     # Dominant kernel = largest share of device time.
     name = max(prof, key=lambda k: prof[k]["ms"])
     p = prof[name]
@@ -286,12 +289,12 @@ def roofline_from_profile(prof, peaks, iters):
     fp_frac = tfs / peaks["fp64_tflops"]
     intensity = flops_per_launch / max(1.0, bytes_per_launch)
     ridge = peaks["fp64_tflops"] * 1e12 / (peaks["hbm_gbs"] * 1e9)
-    traffic = None
+    traffic = None  # DRAM bytes per launch from an ncu --set full capture of THIS workload, else null
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tpath):
         try:
             with open(tpath) as f:
-                traffic = json.load(f).get(name)
+                traffic = json.load(f).get(workload, {}).get(name)
         except Exception:
             traffic = None
     total_ms = sum(v["ms"] for v in prof.values())
@@ -334,16 +337,27 @@ def main():
     if args.impl == "reference":
         if rank != 0:
             return 0
+        # The reference runs single-threaded: Eigen without OpenMP and OpenBLAS
+        # pinned to one thread (linops.cpp:17-23), so its stock setting -- the
+        # line's value -- is 1 thread; the restatement on every host thread is
+        # reported beside it.
+        cb = cpu_baseline(w, 1, iters=max(3, min(args.steps, 6)))
         threads = os.cpu_count() or 1
-        cb = cpu_baseline(w, threads, iters=max(3, min(args.steps, 6)))
+        try:
+            cb_all = cpu_baseline(w, threads, iters=max(3, min(args.steps, 6)))
+            all_threads = {k: cb_all[k] for k in ("value", "unit", "cores", "extrapolated", "sample")}
+        except Exception as exc:  # reported, never fatal
+            all_threads = {"error": str(exc)}
         line = {
             "impl": "reference", "metric": "PASD ADMM iters/s", "value": cb["value"], "unit": "iter/s",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": w.name, "dims": list(w.dims), "ranks": list(w.ranks)},
-            "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
+            "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "extrapolated", "sample_dims",
+                                                 "sample")},
             "e2e": {"value": cb["value"], "unit": "iter/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
             "elem_iters_per_s": cb["elem_iters_per_s"],
+            "all_threads": all_threads,
         }
         print(json.dumps(line), flush=True)
         return 0
@@ -428,7 +442,7 @@ def main():
     sol.close()
     del sol
     value = K / (ms * 1e-3)
-    roof = roofline_from_profile(prof, peaks, args.profile_iters)
+    roof = roofline_from_profile(prof, peaks, args.profile_iters, w.name)
     # Whole-iteration roofline against the canonical fused-schedule work.
     S = w.size
     N = len(w.dims)

@@ -263,6 +263,53 @@ int pasd_b200_certificate(const double* t, const pasd_options* opt, int32_t iter
                           const double* const* y, const double* const* y_hat, double* epsilon_hat, double* c,
                           double* bound, char* errbuf, size_t errlen);
 
+/* nuclear_norm(unfold(t, mode)) (linops.cpp:74-76; certify's objective check,
+ * cli.cpp:504-511) on the device, for unfoldings of numerical rank <= 64 (the
+ * low-rank estimates Z_n and Tucker truths it is used on): range finder +
+ * Jacobi.  ArgumentError when the rank exceeds 64. */
+int pasd_b200_nuclear_norm_unfold(const double* t, int32_t order, const int64_t* dims, int32_t mode, double* out,
+                                  int32_t device, char* errbuf, size_t errlen);
+
+/* ---- synthetic instances: the reference generator (synth.cpp:71-121) ------
+ * T = core x_1 U_1 ... x_N U_N (+ sparse corruption) with the reference's
+ * random streams (rng.hpp:17-79: splitmix64-derived mt19937_64 per purpose,
+ * Box-Muller Gaussians, 53-bit uniforms): core and factor draws, the Haar
+ * factors (Householder QR, diag(R) sign fix, synth.cpp:40-53), the partial
+ * Fisher-Yates support of round(rho S) entries and the noise values drawn in
+ * sorted-index order (synth.cpp:91-121).  The draws run on the host (they
+ * are sequential by definition), the mode products and the scatter on the
+ * device.  The reference's verify_tucker_rank SVD check (synth.cpp:55-67) is
+ * not run. */
+typedef struct pasd_synth_spec {
+  int32_t order;
+  const int64_t* dims;     /* [N] I_n                                             */
+  const int64_t* ranks;    /* [N] Tucker ranks r_n (SynthSpec::ranks)             */
+  uint64_t seed;           /* SynthSpec::seed (cli.cpp:164 default 0)             */
+  int32_t factor_kind;     /* 0 Haar (reference); 1 |N(0,1)| columns l2-normalised,
+                              |core|, T / max(T) (BASELINE configs[3] extension)  */
+  int32_t corrupt_mode;    /* 0 add U[lo,hi] (reference: lo=-1, hi=1); 1 replace by
+                              U[lo,hi] (reference: 0, 255); 2 per last-mode frame,
+                              `cells` aligned block x block cells of the mode-1 x
+                              mode-2 plane replaced by U[lo,hi] (configs[3])      */
+  double corruption;       /* rho in [0, 1] (modes 0, 1)                          */
+  double lo, hi;
+  int64_t block, cells;    /* mode 2 only                                         */
+  int32_t device;
+} pasd_synth_spec;
+/* t_out: S doubles (device pointer on spec->device if t_is_device, else host);
+ * l0_out: the uncorrupted tensor (optional, same convention); support_out:
+ * the sorted corrupted positions (optional host buffer of *count_out entries,
+ * at most S); count_out: number of corrupted entries. */
+int pasd_b200_synth(const pasd_synth_spec* spec, double* t_out, int t_is_device, double* l0_out, int l0_is_device,
+                    int64_t* support_out, int64_t* count_out, char* errbuf, size_t errlen);
+/* Host-only pieces of the generator (no device needed), for tests: the Haar /
+ * kind-1 factor of mode `mode` (1-based, purpose factor + mode) and the
+ * unsorted partial Fisher-Yates support of corrupt_sparse. */
+int pasd_b200_synth_factor(int64_t rows, int64_t cols, uint64_t seed, int32_t mode, int32_t kind, double* out,
+                           char* errbuf, size_t errlen);
+int pasd_b200_synth_support(int64_t total, double rho, uint64_t seed, int64_t* pos_out, int64_t* count_out,
+                            char* errbuf, size_t errlen);
+
 /* 128-byte NCCL unique id for pasd_shard.nccl_unique_id (rank 0 creates it and
  * broadcasts it to the other ranks with the host launcher's own channel). */
 int pasd_b200_nccl_unique_id(void* out128, char* errbuf, size_t errlen);

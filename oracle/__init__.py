@@ -203,3 +203,15 @@ def pasd_v0_phase(t, config: PasdConfig, iters: int, *, threads: int = 1, fixed_
     raise_for_status(rc, err)
     assert e.size == S
     return e, ys, hist[:done.value].tolist(), resid, margin.value, left.value, done.value
+
+
+def factor(rows: int, cols: int, seed: int, mode: int, kind: int = 0) -> np.ndarray:
+    """Factor matrix of gen_lowrank_tucker for 1-based `mode` (synth.cpp:40-53, 80-83)."""
+    out = np.empty((rows, cols), order="F")
+    err = _err()
+    f = lib().oracle_factor
+    f.restype = C.c_int
+    rc = f(C.c_int64(rows), C.c_int64(cols), C.c_uint64(seed), C.c_int(mode), C.c_int(kind),
+           out.ctypes.data_as(_abi.c_double_p), err, C.c_size_t(len(err)))
+    raise_for_status(rc, err)
+    return out

@@ -1015,3 +1015,17 @@ int oracle_pasd_v0_phase(const double* t, const pasd_options* opt, int iters, in
 }
 
 }  // extern "C"
+
+extern "C" {
+// Factor matrix of gen_lowrank_tucker for mode `mode` (1-based; purpose factor + mode, synth.cpp:82).
+int oracle_factor(int64_t rows, int64_t cols, uint64_t seed, int mode, int kind, double* out, char* err,
+                  size_t errlen) {
+  return guarded(err, errlen, [&] {
+    g_threads = 1;
+    scipy_openblas_set_num_threads(1);
+    RngStream frng(seed, 0, purpose::factor + uint64_t(mode));
+    const Matrix q = factor_matrix(rows, cols, frng, kind);
+    std::memcpy(out, q.data(), q.d.size() * sizeof(double));
+  });
+}
+}  // extern "C"

@@ -116,6 +116,10 @@ HEADER_SYMBOLS = (
     "pasd_b200_update_v",
     "pasd_b200_update_e",
     "pasd_b200_certificate",
+    "pasd_b200_nuclear_norm_unfold",
+    "pasd_b200_synth",
+    "pasd_b200_synth_factor",
+    "pasd_b200_synth_support",
     "pasd_b200_nccl_unique_id",
     "pasd_b200_abi_version",
     "pasd_b200_build_info",

@@ -1,15 +1,18 @@
-// pasd_kernels.cuh — sm_100a kernels of one PASD ADMM iteration
-// (Algorithm 1; reference loop proj/src/pasd.cpp:168-244).
+// pasd_kernels.cuh — shared helpers and the generic (any order N) kernels of a
+// PASD ADMM iteration (Algorithm 1; reference loop
+// proj/src/pasd.cpp:168-244).
 //
 // Per iteration, in stream order (all scalars live in device memory, so the
 // sequence can be captured once as a CUDA graph and replayed):
-//   k_polar        Procrustes U_n <- polar(G_n V_n^T)          pasd.cpp:70-74,187; linops.cpp:93-104
-//   k_contract_A   A_n = U_n^T G_(n), G = (T-E)+Y_n/mu          pasd.cpp:77,178-186
-//   k_gram         Gram_n = A_n A_n^T (partials)                 (replaces dgesdd of A_n, linops.cpp:83)
-//   k_svt          eig(Gram_n) -> M_n with V_n = SVT(A_n)=M_n A_n linops.cpp:78-91
-//   k_update       Z_n refold + E shrink + Y ascent + residuals  pasd.cpp:189-228
-//   k_finish       mu schedule, history, stop rule               pasd.cpp:229-239
-//   k_contract_W   Wt_n = G_(n)^{next} A_n^T, ||G^{next}||^2     (next iteration's procrustes product)
+//   k_polar        Procrustes U_n <- polar(G_n V_n^T)          pasd.cpp:70-74,187; linops.cpp:93-104  (pasd_small.cuh)
+//   k_pass1        A_n = U_n^T G_(n), G = D + Y_n/mu, DMMA     pasd.cpp:77,178-186                  (pasd_pass1.cuh)
+//   k_gram_all     Gram_n = A_n A_n^T partials + reduce        (replaces dgesdd of A_n, linops.cpp:83) (pasd_gram.cuh)
+//   k_svt          eig(Gram_n) -> M_n with V_n = SVT(A_n)=M_n A_n linops.cpp:78-91                  (pasd_small.cuh)
+//   order 3:  k_pass2_fused / k_pass2_m8: Z_n refold + E shrink + Y ascent + residuals
+//             + Wt_n = G_(n)^{next} A_n^T (next Procrustes product) pasd.cpp:189-228       (pasd_pass2*.cuh)
+//             + k_pass2_reduce (Wt_n, ||G^{next}||^2); the last pass-2 CTA runs the finish
+//   order != 3: k_update (refold + E + Y + residuals), k_finish (mu schedule, stop rule,
+//             pasd.cpp:229-239), k_contract_W + k_wreduce_generic (Wt_n)   (this file)
 // Elementwise arithmetic that the reference performs on tensors uses explicit
 // round-to-nearest intrinsics (no FMA contraction), in the reference's
 // operation order, so E/Y are bit-identical whenever Z is.
@@ -110,61 +113,6 @@ struct OrOp {
   __device__ int operator()(int a, int b) const { return a | b; }
   __device__ static int identity() { return 0; }
 };
-
-// ---------------------------------------------------------------------------
-// Pass 1: A_n[kappa, r] = sum_i U_n[i, r] * G_n[kappa, i]  for 64 columns x all R.
-constexpr int CA_KT = 64;  // columns per CTA
-constexpr int CA_IC = 32;  // i chunk
-template <int RPT>
-__global__ void __launch_bounds__(kThreads) k_contract_A(ModeDev m, const double* __restrict__ T,
-                                                        const double* __restrict__ E0,
-                                                        const double* __restrict__ E1,
-                                                        const double* __restrict__ Y, const Ctl* ctl) {
-  if (ctl->done) return;
-  const double* __restrict__ E = ctl->ecur ? E1 : E0;
-  const double inv_mu = __ddiv_rn(1.0, ctl->mu);  // pasd.cpp:170
-  __shared__ double Gs[CA_IC][CA_KT + 1];
-  __shared__ double Us[CA_IC][PASD_MAX_RANK + 1];
-  const int tid = threadIdx.x, kl = tid % CA_KT, rg = tid / CA_KT;
-  const int64_t k0 = (int64_t)blockIdx.x * CA_KT;
-  double acc[RPT];
-#pragma unroll
-  for (int j = 0; j < RPT; ++j) acc[j] = 0.0;
-  for (int64_t i0 = 0; i0 < m.I; i0 += CA_IC) {
-    const int ic = (int)imin64(CA_IC, m.I - i0);
-    for (int idx = tid; idx < CA_IC * CA_KT; idx += kThreads) {
-      int il, kk;
-      if (m.inner > 1) { kk = idx % CA_KT; il = idx / CA_KT; }
-      else { il = idx % CA_IC; kk = idx / CA_IC; }
-      const int64_t kap = k0 + kk;
-      double v = 0.0;
-      if (kap < m.J && il < ic) {
-        const int64_t off = elem_offset(m, kap, i0 + il);
-        v = g_elem(T[off], E[off], Y[off], inv_mu);
-      }
-      Gs[il][kk] = v;
-    }
-    for (int idx = tid; idx < CA_IC * m.R; idx += kThreads) {
-      const int il = idx % CA_IC, r = idx / CA_IC;
-      Us[il][r] = il < ic ? m.U[i0 + il + m.I * r] : 0.0;
-    }
-    __syncthreads();
-    for (int il = 0; il < ic; ++il) {
-      const double g = Gs[il][kl];
-#pragma unroll
-      for (int j = 0; j < RPT; ++j) acc[j] = fma(g, Us[il][rg + 4 * j], acc[j]);
-    }
-    __syncthreads();
-  }
-  const int64_t kap = k0 + kl;
-  if (kap < m.J) {
-#pragma unroll
-    for (int j = 0; j < RPT; ++j) {
-      const int r = rg + 4 * j;
-      if (r < m.R) m.A[a_offset(m, kap, r)] = acc[j];
-    }
-  }
-}
 
 // ---------------------------------------------------------------------------
 // Gram partials: Gpart[kc][r][s] = sum_{kappa in chunk kc} A[kappa,r] A[kappa,s].

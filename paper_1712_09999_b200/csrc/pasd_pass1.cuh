@@ -5,12 +5,13 @@
 // tensor.cpp:98-113).  As a GEMM: A (J x R) = G (J x I) * U (I x R), with
 // kappa = unfolding column, K = I_n, N = R_n <= 64.
 //
-// Persistent CTAs (one per SM, 8 warps) walk tiles of 128 columns kappa; K runs
-// over i in chunks of 16.  Raw T, E, Y_n chunks and the U chunk stream into a
-// 3-stage cp.async ring in shared memory (16-byte copies along the contiguous
-// index), so ~150 KB per SM is in flight while the DMMAs of the current chunk
-// run.  G is formed inside the DMMA A-fragment load (each G value feeds exactly
-// one fragment), warp w owns kappa rows 16w..16w+15 and all RP/8 n-tiles.
+// Persistent CTAs (two per SM, 8 warps each) walk tiles of 128 columns kappa;
+// K runs over i in chunks of PASD_P1_KCC.  The D and Y_n chunks and the U chunk
+// stream into a PASD_P1_NSTC-deep cp.async ring in shared memory (16-byte
+// copies along the contiguous index) while the DMMAs of the current chunk run,
+// and one CTA's DMMAs overlap the other's loads.  G = D + Y_n / mu is formed
+// inside the DMMA A-fragment load (each G value feeds exactly one fragment);
+// warp w owns kappa rows 16w..16w+15 and all RP/8 n-tiles.
 // A tile is 128 consecutive p at fixed q (every staged row one contiguous run),
 // or, where that wastes a mostly empty p-block per q, 128 consecutive unfolding
 // columns spanning two q (p1_cross).

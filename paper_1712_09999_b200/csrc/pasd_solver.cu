@@ -1384,7 +1384,7 @@ __global__ void k_set_ctl(Ctl* ctl, double mu, double vnorm2) {
 
 // m_is_device: m is a device pointer on `device` (the spec helpers form U^T G there).
 void device_svt(const double* m_h, int64_t rows, int64_t cols, double tau, double* out_h, int32_t* kept, int device,
-                bool m_is_device = false) {
+                bool m_is_device = false, double* sig_out = nullptr) {
   if (tau < 0.0 || !std::isfinite(tau)) fail(PASD_ERR_ARGUMENT, "svt: threshold must be a nonnegative finite number");
   if (rows < 1 || cols < 1) fail(PASD_ERR_ARGUMENT, "thin_svd: matrix must be nonempty");
   if (m_is_device) {
@@ -1449,17 +1449,25 @@ void device_svt(const double* m_h, int64_t rows, int64_t cols, double tau, doubl
   const size_t smem = small_ws_bytes(R);
   ensure_small_smem_attr();
   k_svt<<<kSmallCluster, kSmallThreads, smem>>>(d_pack, ctl);
-  double* V = t.alloc<double>(rows * cols);
-  k_materialize_v<<<256, 256>>>(m, V);
+  if (out_h) {
+    double* V = t.alloc<double>(rows * cols);
+    k_materialize_v<<<256, 256>>>(m, V);
+    CK(cudaGetLastError());
+    CK(cudaMemcpy(out_h, V, sizeof(double) * rows * cols, cudaMemcpyDeviceToHost));
+  }
   CK(cudaGetLastError());
-  CK(cudaMemcpy(out_h, V, sizeof(double) * rows * cols, cudaMemcpyDeviceToHost));
+  if (sig_out) CK(cudaMemcpy(sig_out, m.sig, sizeof(double) * R, cudaMemcpyDeviceToHost));  // descending
   Ctl hc;
   CK(cudaMemcpy(&hc, ctl, sizeof(Ctl), cudaMemcpyDeviceToHost));
   if (kept) *kept = hc.keep[0];
 }
 
+// g_is_device / v_is_device: g, v are device pointers.  xleft_dev (optional,
+// device I x R): receives the left singular vectors of g v^T (first *rank
+// columns; k_polar's rotated, normalised X) -- the nuclear-norm helper's basis.
 void device_procrustes(const double* g_h, int64_t I, int64_t P, const double* v_h, int64_t R64, const double* u_prev,
-                       double* u_out, int32_t* degenerate, int32_t* rank, int device, bool g_is_device = false) {
+                       double* u_out, int32_t* degenerate, int32_t* rank, int device, bool g_is_device = false,
+                       bool v_is_device = false, double* xleft_dev = nullptr) {
   if (R64 > I) fail(PASD_ERR_ARGUMENT, "procrustes: v has more rows than g (R must not exceed I)");
   if (I < 1 || P < 1 || R64 < 1) fail(PASD_ERR_ARGUMENT, "thin_svd: matrix must be nonempty");
   if (R64 > PASD_MAX_RANK)
@@ -1481,7 +1489,7 @@ void device_procrustes(const double* g_h, int64_t I, int64_t P, const double* v_
   CK(cudaMemset(Z0, 0, sizeof(double) * I * P));
   CK(cudaMemcpy(G, g_h, sizeof(double) * I * P, g_is_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice));
   m.A = t.alloc<double>(R * P);
-  CK(cudaMemcpy(m.A, v_h, sizeof(double) * R * P, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(m.A, v_h, sizeof(double) * R * P, v_is_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice));
   m.U = t.alloc<double>(IR);
   std::vector<double> up(IR, 0.0);
   if (u_prev)
@@ -1528,7 +1536,9 @@ void device_procrustes(const double* g_h, int64_t I, int64_t P, const double* v_
   CK(cudaMemcpy(&hc, ctl, sizeof(Ctl), cudaMemcpyDeviceToHost));
   if (degenerate) *degenerate = hc.degenerate[0];
   if (rank) *rank = hc.polar_rank[0];
-  if (!hc.degenerate[0]) CK(cudaMemcpy(u_out, m.U, sizeof(double) * IR, cudaMemcpyDeviceToHost));
+  if (!hc.degenerate[0] && u_out) CK(cudaMemcpy(u_out, m.U, sizeof(double) * IR, cudaMemcpyDeviceToHost));
+  if (!hc.degenerate[0] && xleft_dev)
+    CK(cudaMemcpy(xleft_dev, m.scratch + IR, sizeof(double) * IR, cudaMemcpyDeviceToDevice));
 }
 
 }  // namespace
@@ -1555,3 +1565,4 @@ int pasd_b200_procrustes(const double* g, int64_t i_rows, int64_t p_cols, const 
 }  // extern "C"
 
 #include "pasd_spec.cuh"
+#include "pasd_synth.cuh"

@@ -270,9 +270,92 @@ void spec_certificate(const double* t, const pasd_options* o, int32_t iters, int
   if (bound_out) *bound_out = c * eps_hat + lam_term;
 }
 
+// unfold_n(T), I_n x J_n column-major (tensor.cpp:98-113).
+__global__ void k_unfold(const double* __restrict__ T, int64_t inner, int64_t I, int64_t S, double* __restrict__ G) {
+  for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < S; idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t rest = idx / inner;
+    const int64_t p = idx - rest * inner;
+    const int64_t q = rest / I;
+    const int64_t i = rest - q * I;
+    G[i + I * (p + inner * q)] = T[idx];
+  }
+}
+
+// Gaussian test matrix for the range finder (counter-based: splitmix64 of the
+// index, Box-Muller).  Any full-rank draw serves; the seed is fixed.
+__global__ void k_gauss(double* __restrict__ out, int64_t n, uint64_t seed) {
+  for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < n; idx += (int64_t)gridDim.x * blockDim.x) {
+    uint64_t x = seed + 0x9e3779b97f4a7c15ULL * (uint64_t)(2 * idx + 1);
+    auto mix = [](uint64_t z) {
+      z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+      z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+      return z ^ (z >> 31);
+    };
+    const uint64_t a = mix(x), b = mix(x + 0x9e3779b97f4a7c15ULL);
+    const double u1 = ((double)((a >> 11) + 1)) * 0x1.0p-53, u2 = (double)(b >> 11) * 0x1.0p-53;
+    out[idx] = sqrt(-2.0 * log(u1)) * cospi(2.0 * u2);
+  }
+}
+
+// nuclear_norm(unfold(t, mode)) (linops.cpp:74-76 on tensor.cpp:139-146) on the
+// device for unfoldings of numerical rank <= PASD_MAX_RANK: a Gaussian range
+// finder (W = Z Omega^T, Omega: R' x J) through the Procrustes solve's two-pass
+// Jacobi gives an orthonormal basis Q of range(Z) with the numerical rank k
+// (singular values above 1e-12 sigma_1 of W); the singular values of Z are then
+// those of the full-row-rank k x J matrix Q^T Z (Gram + Jacobi, k_svt).  Fails
+// (ArgumentError) when ||Q^T Z||_F falls short of ||Z||_F, i.e. when the rank
+// exceeds PASD_MAX_RANK.
+double spec_nuclear_unfold(const double* t, int32_t order, const int64_t* dims, int32_t mode, int device) {
+  if (!t) fail(PASD_ERR_ARGUMENT, "pasd_b200: null argument");
+  const SpecTensors st = spec_dims(order, dims);
+  check_mode(st.dims, mode);
+  const int64_t I = st.dims[mode - 1], J = st.S / I;
+  CK(cudaSetDevice(device));
+  TmpDev tmp;
+  const double* dt = upload(tmp, t, st.S);
+  double* z = tmp.alloc<double>((size_t)st.S);
+  int64_t inner = 1;
+  for (int l = 0; l < mode - 1; ++l) inner *= st.dims[l];
+  k_unfold<<<kSpecBlocks, 256>>>(dt, inner, I, st.S, z);
+  const int Rp = (int)std::min<int64_t>({I, J, (int64_t)PASD_MAX_RANK});
+  double* om = tmp.alloc<double>((size_t)(Rp * J));
+  k_gauss<<<kSpecBlocks, 256>>>(om, Rp * J, 0x5eed5eedULL);
+  double* xl = tmp.alloc<double>((size_t)(I * Rp));
+  int32_t deg = 0, k = 0;
+  device_procrustes(z, I, J, om, Rp, nullptr, nullptr, &deg, &k, device, true, true, xl);
+  if (deg || k == 0) return 0.0;
+  double* a = tmp.alloc<double>((size_t)(k * J));
+  k_ut_g<<<kSpecBlocks, 256>>>(xl, z, I, k, J, a);
+  CK(cudaGetLastError());
+  std::vector<double> sig((size_t)k);
+  device_svt(a, k, J, 1e-300, nullptr, nullptr, device, true, sig.data());
+  double nuc = 0.0, s2 = 0.0;
+  for (double v : sig) {
+    nuc += v;
+    s2 += v * v;
+  }
+  // ||Z||_F^2 against the captured energy
+  double* part = tmp.alloc<double>(4 * kSpecBlocks);
+  k_sumsq<<<1, 1024>>>(z, st.S, part);
+  double z2 = 0.0;
+  CK(cudaMemcpy(&z2, part, sizeof(double), cudaMemcpyDeviceToHost));
+  if (k == Rp && Rp < std::min(I, J) && s2 < z2 * (1.0 - 1e-9))
+    fail(PASD_ERR_ARGUMENT, "pasd_b200: nuclear_norm: mode-" + std::to_string(mode) + " unfolding has rank above " +
+                                std::to_string(PASD_MAX_RANK));
+  return nuc;
+}
+
 }  // namespace
 
 extern "C" {
+
+int pasd_b200_nuclear_norm_unfold(const double* t, int32_t order, const int64_t* dims, int32_t mode, double* out,
+                                  int32_t device, char* errbuf, size_t errlen) {
+  return guarded_call(errbuf, errlen, [&] {
+    if (!out) fail(PASD_ERR_ARGUMENT, "pasd_b200: null argument");
+    *out = spec_nuclear_unfold(t, order, dims, mode, device);
+  });
+}
 
 int pasd_b200_g_matrix(int32_t order, const int64_t* dims, const double* t, const double* e, const double* y, double mu,
                        int32_t mode, double* g_out, int32_t device, char* errbuf, size_t errlen) {

@@ -81,7 +81,7 @@ def test_fullsize_fixed_iterations_match_oracle(gpu, oracle_mod, name):
     if name == "c5":
         assert left_at == 0 and done == K, f"the reference leaves the V=0 phase at iteration {left_at}"
     else:
-        assert left_at > 60 and done == left_at - 1
+        assert left_at > 10 and done == left_at - 1
     assert margin > 1e-6 or left_at, f"SVT keep decision within {margin:.2e} of the threshold"
     s = gpu.Solver(w.dims, cfg, fixed_iters=True)
     s.load(T)

@@ -6,9 +6,11 @@ last R_n - k columns of u are LAPACK rounding noise, so two equally valid builds
 of the reference disagree there.  This script measures how far apart they land,
 using the CPU restatement (oracle/, test infrastructure) in three builds:
 
-  ref    dgesdd, 1 thread            (the reference: linops.cpp:17-23, 62)
-  gesvd  dgesvd, 1 thread            (another LAPACK driver for the same SVD)
-  thr16  dgesdd, 16 BLAS threads     (OpenBLAS threading changes GEMM order)
+  ref         dgesdd, 1 thread         (the reference: linops.cpp:17-23, 62)
+  gesvd       dgesvd, 1 thread         (another LAPACK driver for the same SVD)
+  thr16       dgesdd, 16 BLAS threads  (OpenBLAS threading changes GEMM order)
+  thr4        dgesdd, 4 BLAS threads
+  gesvd_thr8  dgesvd, 8 BLAS threads
 
 on BASELINE configs[0] (C1, 100^3 r=R=10, 10%: 100 fixed iterations and run to
 eps=1e-7) and configs[1] (C2, 200^3 r=R=20, 20%: 200 fixed and run to 1e-7),
@@ -49,7 +51,7 @@ CASES = {
     "s2_20cube_r2R3": ((20, 20, 20), 2, 3, 0.0, 1000, 1e-5, False),
     "smoke_24x20x16": ((24, 20, 16), 2, 2, 0.05, 300, 1e-6, False),
 }
-VARIANTS = {"ref": (0, 1), "gesvd": (1, 1), "thr16": (0, 16)}
+VARIANTS = {"ref": (0, 1), "gesvd": (1, 1), "thr16": (0, 16), "thr4": (0, 4), "gesvd_thr8": (1, 8)}
 TMP = os.environ.get("PARITY_FLOOR_TMP", "/tmp/parity_floor")
 
 
