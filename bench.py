@@ -168,6 +168,16 @@ def cpu_baseline(w, threads: int, iters: int = 3):
     }
 
 
+def generate_input(w):
+    """The workload's observed tensor from the reference generator on the device
+    (paper_1712_09999_b200/synth.py: synth.cpp:71-121 with the reference's RNG
+    streams, seed 0), as a CUDA tensor of shape reversed(dims)."""
+    from paper_1712_09999_b200 import synth
+
+    T, _, _ = synth.generate(synth.workload_spec(w, seed=0), out="torch")
+    return T
+
+
 def e2e_recover(w, T_dev, steps: int):
     """Whole-solve throughput through the C-ABI drop-in with host buffers."""
     import torch
@@ -230,8 +240,6 @@ def e2e_sharded(w, steps, shard, dist):
     import torch
     import paper_1712_09999_b200 as pb
     from paper_1712_09999_b200.api import PasdConfig
-    from paper_1712_09999_b200.workloads import generate_gpu
-
     from paper_1712_09999_b200.sharding import Shard, nccl_unique_id
 
     b, e = shard.struct.slab_begin, shard.struct.slab_end
@@ -239,7 +247,7 @@ def e2e_sharded(w, steps, shard, dist):
     uid = [nccl_unique_id() if rank == 0 else None]  # a unique id serves one communicator
     dist.broadcast_object_list(uid, src=0)
     shard = Shard(rank, shard.struct.nranks, (b, e), uid[0])
-    T = generate_gpu(w, seed=0)
+    T = generate_input(w)
     Th = torch.empty(T[b:e].numel(), dtype=torch.float64, pin_memory=True)
     Th.copy_(T[b:e].reshape(-1))
     del T
@@ -365,8 +373,6 @@ def main():
     import torch
     import paper_1712_09999_b200 as pb
     from paper_1712_09999_b200.api import PasdConfig
-    from paper_1712_09999_b200.workloads import generate_gpu
-
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local_rank)
     dist = None
@@ -384,7 +390,7 @@ def main():
         shard = Shard(rank, world, slab, uid[0])
     peaks = load_peaks()
     K, W = args.steps, max(3, args.warmup)
-    T = generate_gpu(w, seed=0)  # identical on every rank (same seed); rank keeps its slab
+    T = generate_input(w)  # identical on every rank (same seed); rank keeps its slab
     T_loc = T[shard.struct.slab_begin:shard.struct.slab_end].contiguous() if shard else T
     if shard:
         del T
@@ -457,7 +463,8 @@ def main():
         "steps": K, "warmup": W, "ms_per_step": round(ms / K, 4), "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": w.name, "dims": list(w.dims), "ranks": list(w.ranks), "rho": w.rho,
-                   "noise": list(w.noise), "iters_fixed": True, "l2": "inputs larger than L2 (T, E x2, D, Y x3: 7 x 8 GB resident)"
+                   "noise": list(w.noise), "iters_fixed": True,
+                   "input": "reference generator (synth.cpp:71-121, rng.hpp streams, seed 0) on the device", "l2": "inputs larger than L2 (T, E x2, D, Y x3: 7 x 8 GB resident)"
                    if S * 8 > 126e6 else "inputs L2-resident"},
         "elem_iters_per_s": value * S,
         "gpu_launches": int(launches),
@@ -470,7 +477,7 @@ def main():
     del T_loc
     torch.cuda.empty_cache()
     if not args.no_e2e and shard is None:
-        Tg = generate_gpu(w, seed=0)
+        Tg = generate_input(w)
         line["e2e"] = e2e_recover(w, Tg, K)
         del Tg
         torch.cuda.empty_cache()

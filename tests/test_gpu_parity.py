@@ -1,9 +1,10 @@
 """GPU parity: the CUDA path (through the C-ABI) against the oracle on the
-same seeded inputs.  Tolerances are stated per test; see DESIGN.md "Parity"
-for the measured intrinsic floor of the reference itself (dgesdd vs dgesvd
-disagree by 8e-9 on C1 at convergence and completely in the rank-deficient
-transition, because the reference's Procrustes completion is LAPACK rounding
-noise)."""
+same seeded inputs.  Where a run crosses PASD's rank-deficient transition the
+tolerance is the reference's own floor (profiles/r02_parity_floor.json, made by
+tools/parity_floor.py): the reference's Procrustes completion is LAPACK
+rounding noise there, and its equally valid builds disagree (C1 at 100
+iterations: x 0.85 apart; at convergence 8.5e-9).  Full-size configs C3-C5:
+tests/test_gpu_fullsize.py."""
 import json
 import os
 import threading
@@ -42,20 +43,78 @@ def test_trivial_phase_bit_exact(gpu, oracle_mod):
     assert rg.residual_history == ro.residual_history
 
 
+FLOOR = os.path.join(os.path.dirname(GOLD), "..", "profiles", "r02_parity_floor.json")
+
+
+def floor(case):
+    """The reference's own spread on a case (tools/parity_floor.py: max over the
+    10 pairs of 5 equally valid builds -- dgesdd / dgesvd x 1/4/8/16 BLAS
+    threads -- of the CPU restatement).  The GPU is held to it with a 1.5x
+    margin: it is one more build, and a maximum over 10 pairs is an estimate."""
+    with open(FLOOR) as f:
+        return json.load(f)["cases"][case]["floor"]
+
+
+def floor_case(gpu, oracle_mod, case, dims, r, rho, eps, maxiter, fixed, support="exact"):
+    L0, T = instance(oracle_mod, dims, r, rho)
+    cfg = PasdConfig(lambdas=oracle_mod.default_lambdas(T.shape), ranks=[r] * 3, eps=eps, maxiter=maxiter)
+    ro = oracle_mod.pasd_recover(T, cfg, fixed_iters=fixed, threads=16)
+    rg = gpu.pasd_recover(T, cfg, fixed_iters=fixed)
+    f = floor(case)
+    assert rg.converged == ro.converged
+    assert abs(rg.iters - ro.iters) <= max(1, f["d_iters"])
+    assert rel(rg.x, ro.x) <= max(1e-9, 1.5 * f["x_rel"])
+    assert rel(rg.e, ro.e) <= max(1e-9, 1.5 * f["e_rel"])
+    eg, eo = np.ravel(rg.e, order="F"), np.ravel(ro.e, order="F")
+    flips = np.flatnonzero((eg != 0) != (eo != 0))
+    if support == "exact":
+        assert flips.size <= f["support_flips"]
+    elif support == "floor":
+        assert flips.size <= max(1, 1.5 * f["support_flips"])
+    else:
+        # entries where the two E supports differ must sit at the shrink threshold:
+        # |x| - tau_E (the nonzero side's |E|) below 1e-3 tau_E (pasd.cpp:205-208)
+        tau = 1.0 / (cfg.mu0 * cfg.rho ** (rg.iters - 1) * 3)
+        mag = np.maximum(np.abs(eg[flips]), np.abs(eo[flips]))
+        assert flips.size <= max(f["support_flips"], 2e-4 * np.count_nonzero(eo))
+        assert flips.size == 0 or mag.max() <= 1e-3 * tau, (flips.size, mag.max() / tau)
+    return L0, cfg, ro, rg
+
+
 def test_c1_convergence_parity(gpu, oracle_mod):
-    """C1 run-to-tolerance 1e-7 (BASELINE configs[0])."""
-    L0, T = instance(oracle_mod, (100, 100, 100), 10, 0.10)
-    cfg = PasdConfig(lambdas=oracle_mod.default_lambdas(T.shape), ranks=[10, 10, 10], eps=1e-7)
-    ro = oracle_mod.pasd_recover(T, cfg, threads=16)
-    rg = gpu.pasd_recover(T, cfg)
+    """C1 run to tolerance 1e-7 (BASELINE configs[0]): iteration count, L and E
+    within the reference's floor, identical E support."""
+    L0, cfg, ro, rg = floor_case(gpu, oracle_mod, "c1_conv", (100, 100, 100), 10, 0.10, 1e-7, 1000, False)
     assert ro.converged and rg.converged
-    # measured reference floor: dgesdd 191 vs dgesvd 193 iterations
-    assert abs(rg.iters - ro.iters) <= 2
-    assert rel(rg.x, ro.x) <= 2e-8          # floor dgesdd vs dgesvd: 8.2e-9
-    assert rel(rg.e, ro.e) <= 2e-9          # floor: 7.7e-10
-    assert np.array_equal(rg.e != 0, ro.e != 0)  # identical support of E
     assert rel(rg.x, L0) <= 1e-8
     assert rg.certificate is not None and rg.certificate.epsilon_hat <= 1 + sum(cfg.lambdas)
+
+
+def test_c1_fixed100_within_floor(gpu, oracle_mod):
+    """C1 at its own fixed count (100, BASELINE configs[0]): inside the
+    rank-deficient transition (iterations ~95-130), where the reference's
+    Procrustes completion is LAPACK rounding noise and its own builds land
+    0.85 apart in x (profiles/r02_parity_floor.json)."""
+    floor_case(gpu, oracle_mod, "c1_fixed100", (100, 100, 100), 10, 0.10, 1e-7, 100, True, support="floor")
+
+
+@pytest.mark.parametrize("case,fixed,maxiter", [("c2_fixed200", True, 200), ("c2_conv", False, 1000)])
+def test_c2_parity(gpu, oracle_mod, case, fixed, maxiter):
+    """C2 (200^3, r = R = 20, 20% corruption; BASELINE configs[1]) at 200 fixed
+    iterations and run to 1e-7.  L, E and the iteration count within the
+    reference's floor; the E supports agree except for entries at the shrink
+    threshold (the GPU's transition trajectory differs from every LAPACK build's,
+    tools/flip_probe.py: 153 such entries of 1.6e6 at 200 iterations, all with
+    |E| <= 7e-4 tau_E)."""
+    floor_case(gpu, oracle_mod, case, (200, 200, 200), 20, 0.20, 1e-7, maxiter, fixed, support="threshold")
+
+
+def test_pinned_small_case_20x22x24(gpu, oracle_mod):
+    """[20, 22, 24], r = R = 2, 5%: the case on which an earlier Procrustes
+    completion stalled (RSE 0.385, 200 vs 183 iterations)."""
+    L0, cfg, ro, rg = floor_case(gpu, oracle_mod, "s1_20x22x24_r2R2", (20, 22, 24), 2, 0.05, 1e-5, 1000, False,
+                                 support="floor")
+    assert rel(rg.x, L0) <= 2 * rel(ro.x, L0)
 
 
 @pytest.mark.parametrize("name", sorted(d for d in os.listdir(GOLD) if os.path.isdir(os.path.join(GOLD, d))))
@@ -268,53 +327,6 @@ def test_single_step_parity_dmma_pass2(gpu, oracle_mod, monkeypatch, dims, ranks
         assert rel(r.z[n], b.z[n]) <= 1e-11
         assert rel(r.y[n], b.y[n]) <= 1e-9
     np.testing.assert_allclose(r.final_residuals, b.residual_inf, rtol=1e-6, atol=1e-12 * np.abs(T).max())
-
-
-@pytest.mark.parametrize("config", ["c3", "c4"])
-def test_full_size_trivial_phase_bit_exact(gpu, config):
-    """BASELINE full sizes (C3 400^3 R=40, C4 256x256x1024 R=(30,30,15)) through a
-    size-independent property: in the V = 0 phase (Z_n = 0) every entry of E
-    and Y_n follows the reference's elementwise recurrence (pasd.cpp:170-229,
-    SURVEY Appendix A), so a 2^20-entry sample recomputed in numpy (IEEE, no
-    FMA) must match the GPU bit for bit after 30 iterations."""
-    import torch
-
-    from paper_1712_09999_b200.workloads import WORKLOADS, generate_gpu
-
-    w = WORKLOADS[config]
-    K = 30
-    T = generate_gpu(w, seed=0)
-    cfg = PasdConfig(lambdas=w.lambdas(), ranks=list(w.ranks), maxiter=K)
-    s = gpu.Solver(w.dims, cfg, fixed_iters=True)
-    s.load(T.data_ptr(), t_is_device=True)
-    s.run(K)
-    r = s.finalize(want_x=False, want_e=True, want_y=True)
-    s.close()
-    assert r.iters == K
-    flat = T.reshape(-1)  # torch (i1 fastest, like the solver) -- same flat order as r.e
-    idx = np.random.default_rng(1).choice(flat.numel(), 1 << 20, replace=False)
-    t = flat[torch.from_numpy(idx).to(flat.device)].cpu().numpy().astype(np.float64)
-    del T, flat
-    torch.cuda.empty_cache()
-    N = 3
-    y = [np.zeros_like(t) for _ in range(N)]
-    e = np.zeros_like(t)
-    mu = cfg.mu0
-    for _ in range(K):
-        inv_mu = 1.0 / mu
-        h = np.zeros_like(t)
-        for n in range(N):
-            h = h + ((t - 0.0) + y[n] * inv_mu)
-        x = h * (1.0 / N)
-        tau = 1.0 / (mu * N)
-        e = np.where(x > tau, x - tau, np.where(x < -tau, x + tau, 0.0))
-        for n in range(N):
-            y[n] = y[n] + mu * ((t - 0.0) - e)
-        mu = min(cfg.rho * mu, cfg.mu_max)
-    np.testing.assert_array_equal(r.e.reshape(-1, order="F")[idx], e)  # solver order: i1 fastest
-    for n in range(N):
-        np.testing.assert_array_equal(r.y[n].reshape(-1, order="F")[idx], y[n])
-    assert r.objective == pytest.approx(np.abs(r.e).sum(), rel=1e-12)  # V_n = 0: objective = ||E||_1
 
 
 def test_solver_ranks_report_the_phase(gpu, oracle_mod):
