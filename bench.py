@@ -130,7 +130,7 @@ def cpu_sample_dims(w):
         (w.ranks[0], w.ranks[1], min(w.ranks[2], d3))
 
 
-def cpu_baseline(w, threads: int, iters: int = 3):
+def cpu_baseline(w, threads: int, iters: int = 3, sample=None):
     """Time the oracle (reference restatement) per iteration on a bounded sample.
 
     Per-iteration time = median gap between observer callbacks after the first
@@ -139,7 +139,7 @@ def cpu_baseline(w, threads: int, iters: int = 3):
     from paper_1712_09999_b200 import _abi
     from paper_1712_09999_b200.api import PasdConfig
 
-    dims, tucker, ranks = cpu_sample_dims(w)
+    dims, tucker, ranks = sample if sample is not None else cpu_sample_dims(w)
     L0 = oracle.gen_tucker(dims, tucker, seed=0, kind=1 if w.kind == "nonneg" else 0)
     T = oracle.corrupt_sparse(L0, w.rho, seed=0, mode=0 if w.mode == "add" else 1, lo=w.noise[0], hi=w.noise[1])
     total = int(np.prod(dims))

@@ -32,7 +32,7 @@
 extern "C" {
 #endif
 
-#define PASD_B200_ABI_VERSION 1
+#define PASD_B200_ABI_VERSION 2
 
 /* Status codes.  The numeric values follow the reference CLI's exit-code
  * taxonomy (proj/tools/cli.hpp:9-14): argument 1, I/O 2, numerical 3.  State
@@ -62,7 +62,11 @@ enum {
    * A_n (R_n J_n doubles each): ~64 GB at 1000^3, R = 50 -- until
    * pasd_b200_release_cache() or exit; a call with different options frees it
    * before allocating its own. */
-  PASD_FLAG_REUSE_SOLVER = 1u << 2
+  PASD_FLAG_REUSE_SOLVER = 1u << 2,
+  /* Sharded solvers: after every pasd_b200_solver_run, all-reduce a 64-bit
+   * hash of the replicated U_n and M_n and fail (PASD_ERR_NUMERICAL) if any
+   * rank differs (SURVEY 8(e) debug check; also env PASD_CHECK_REPLICAS). */
+  PASD_FLAG_CHECK_REPLICAS = 1u << 3
 };
 
 /* Mirror of tenrec::PasdConfig (pasd.hpp:8-27) plus placement. */
@@ -85,14 +89,29 @@ typedef struct pasd_options {
 } pasd_options;
 
 /* Multi-GPU slab sharding along the LAST mode (one process per GPU).  A NULL
- * shard means the whole tensor on one device. */
+ * shard means the whole tensor on one device.  With `loopback` set (a group
+ * from pasd_b200_loopback_create) the ranks instead share ONE device inside
+ * one process, one host thread per rank: the same sharded code path, with the
+ * all-reduces done by host rendezvous + a reduce kernel (no NCCL, iterations
+ * launched eagerly).  That is a test vehicle for nranks > 1, not a speed-up. */
 typedef struct pasd_shard {
   int32_t rank;                  /* this process's rank                            */
   int32_t nranks;                /* world size                                     */
   const void* nccl_unique_id;    /* 128-byte ncclUniqueId from rank 0 (NULL if nranks==1) */
   int64_t slab_begin;            /* first last-mode index owned by this rank       */
   int64_t slab_end;              /* one past the last                              */
+  void* loopback;                /* loopback group, or NULL for NCCL               */
 } pasd_shard;
+
+/* Loopback group of nranks (1..8) solvers sharing one device.  Destroy it after
+ * every solver that uses it. */
+int pasd_b200_loopback_create(int32_t nranks, void** group_out, char* errbuf, size_t errlen);
+void pasd_b200_loopback_destroy(void* group);
+
+/* Debug: with env PASD_B200_GUARD=1 every device buffer gets 64 KB canary
+ * bands checked when it is freed.  Returns the number of overwritten bands;
+ * `checked` = buffers verified so far, `live` = buffers not yet freed. */
+int64_t pasd_b200_guard_report(int64_t* checked, int64_t* live);
 
 /* Snapshot handed to the observer after each completed iteration
  * (tenrec::IterationView, recovery.hpp:38-48).  Pointers are host copies valid
@@ -142,6 +161,19 @@ int pasd_b200_recover(const double* t, const pasd_options* opt, pasd_outputs* ou
 /* Free the solver kept by pasd_b200_recover under PASD_FLAG_REUSE_SOLVER
  * (device memory returns to the allocator).  Safe to call at any time. */
 void pasd_b200_release_cache(void);
+
+/* SNN / HoRPCA full-SVT ADMM baseline (tenrec::snn_recover,
+ * proj/src/baselines.cpp:37-143) on the device.  Options: order, dims,
+ * lambdas, output_weights, mu0, mu_max, rho, eps, maxiter, device, flags
+ * (PASD_FLAG_FIXED_ITERS honoured); ranks are ignored (SnnConfig has none).
+ * Validation and error messages follow SnnConfig::validate
+ * (baselines.cpp:12-29).  Outputs: x, e, z[N], y[N], iters, converged,
+ * residual_history, final_residuals, objective; y_hat and the certificate are
+ * not produced (snn_recover leaves them empty).  Observer views carry u = v =
+ * NULL.  Limit of this build: every I_n <= 112 and <= prod of the others. */
+int pasd_b200_snn_recover(const double* t, const pasd_options* opt, pasd_outputs* out,
+                          pasd_observer_fn observer, void* user, char* errbuf, size_t errlen);
+
 
 /* ---- device-resident solver handle (benchmarks, multi-GPU) -------------- */
 

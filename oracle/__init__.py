@@ -37,6 +37,8 @@ def lib():
         L.oracle_pasd_recover.argtypes = [
             _abi.c_double_p, C.POINTER(_abi.PasdOptions), C.POINTER(_abi.PasdOutputs), _abi.PasdObserverFn,
             C.c_void_p, C.c_int, C.c_int, C.c_char_p, C.c_size_t]
+        L.oracle_snn_recover.restype = C.c_int
+        L.oracle_snn_recover.argtypes = L.oracle_pasd_recover.argtypes
         _LIB = L
     return _LIB
 
@@ -50,6 +52,14 @@ def pasd_recover(t, config: PasdConfig, observer=None, *, svd_variant: int = 0, 
     """Reference-restated pasd_recover (pasd.cpp:132-275)."""
     flags = _abi.PASD_FLAG_FIXED_ITERS if fixed_iters else 0
     return run_recover(lib().oracle_pasd_recover, t, config, observer, flags=flags, want_z=want_z,
+                       want_y=want_y, extra_args=(C.c_int(svd_variant), C.c_int(threads)))
+
+
+def snn_recover(t, config, observer=None, *, svd_variant: int = 0, threads: int = 1, fixed_iters: bool = False,
+                want_z: bool = True, want_y: bool = True):
+    """Reference-restated snn_recover (baselines.cpp:37-143); config: api.SnnConfig."""
+    flags = _abi.PASD_FLAG_FIXED_ITERS if fixed_iters else 0
+    return run_recover(lib().oracle_snn_recover, t, config, observer, flags=flags, want_z=want_z,
                        want_y=want_y, extra_args=(C.c_int(svd_variant), C.c_int(threads)))
 
 

@@ -16,6 +16,7 @@
 //   * weighted_mean                                                  recovery.cpp:7-25
 //   * splitmix64 / derive_seed / RngStream                           rng.hpp:17-79
 //   * gen_lowrank_tucker (Haar factors), corrupt_sparse              synth.cpp:40-121
+//   * snn_recover + SnnConfig::validate (SNN baseline)              baselines.cpp:12-29, 37-143
 //
 // Third-party arithmetic: the reference uses Eigen3 (>=3.3, unpinned;
 // proj/CMakeLists.txt:12) for GEMM/transposes/norms and LAPACKE dgesdd
@@ -526,6 +527,134 @@ static Result pasd_recover(const double* td, const std::vector<Index>& dims, con
   return res;
 }
 
+// --------------------------------------------------------------- baselines.cpp
+// snn_recover (baselines.cpp:37-143): full-SVT ADMM on the sum of nuclear
+// norms; SnnConfig::validate (baselines.cpp:12-29) with its messages.
+static void snn_validate(const Config& c, const std::vector<Index>& dims) {
+  const size_t n_modes = dims.size();
+  dims_product(dims);
+  if (c.lambdas.size() != n_modes)
+    throw ArgumentError("config: expected " + std::to_string(n_modes) + " lambdas, got " +
+                        std::to_string(c.lambdas.size()));
+  for (size_t n = 0; n < n_modes; ++n)
+    if (!(c.lambdas[n] > 0.0) || !std::isfinite(c.lambdas[n]))
+      throw ArgumentError("config: lambda of mode " + std::to_string(n + 1) + " must be positive");
+  if (!(c.mu0 > 0.0) || !(c.mu_max >= c.mu0) || !(c.rho > 1.0) || !(c.eps > 0.0) || c.maxiter < 1)
+    throw ArgumentError("config: invalid penalty schedule or stopping parameters");
+  if (!c.output_weights.empty()) {
+    if (c.output_weights.size() != n_modes)
+      throw ArgumentError("config: expected " + std::to_string(n_modes) + " output weights");
+    for (double w : c.output_weights)
+      if (!(w > 0.0)) throw ArgumentError("config: output weights must be positive");
+  }
+}
+
+static Result snn_recover(const double* td, const std::vector<Index>& dims, const Config& cfg,
+                          const Observer& observer) {
+  snn_validate(cfg, dims);
+  const Index total = dims_product(dims);
+  for (Index i = 0; i < total; ++i)
+    if (!std::isfinite(td[i])) throw ArgumentError("snn: input tensor contains non-finite entries");
+  const Index n_modes = Index(dims.size());
+  std::vector<double> e(static_cast<size_t>(total), 0.0);
+  std::vector<std::vector<double>> y(size_t(n_modes), std::vector<double>(size_t(total), 0.0));
+  std::vector<std::vector<double>> z(size_t(n_modes), std::vector<double>(size_t(total), 0.0));
+  std::vector<double> scratch(size_t(total), 0.0);
+  double mu = cfg.mu0;
+  std::vector<double> resid(size_t(n_modes), std::numeric_limits<double>::infinity());
+  Result res;
+  bool converged = false;
+  int iter = 0;
+  while (iter < cfg.maxiter && !converged) {  // baselines.cpp:61
+    const double mu_used = mu;
+    const double inv_mu = 1.0 / mu;
+    for (Index n = 0; n < n_modes; ++n) {  // baselines.cpp:66-75
+      const size_t ni = size_t(n);
+      const double* ed = e.data();
+      const double* yd = y[ni].data();
+      double* sd = scratch.data();
+      for (Index i = 0; i < total; ++i) sd[i] = td[i] - ed[i] + yd[i] * inv_mu;
+      const Index rows = dims[ni];
+      Matrix m(rows, total / rows);
+      unfold_into(scratch.data(), dims, n + 1, m.data());
+      const Matrix zmat = svt(m, cfg.lambdas[ni] * inv_mu);
+      fold_into(zmat.data(), dims, n + 1, z[ni].data());
+    }
+    {  // baselines.cpp:77-91
+      double* sd = scratch.data();
+      std::fill(sd, sd + total, 0.0);
+      for (Index n = 0; n < n_modes; ++n) {
+        const double* zd = z[size_t(n)].data();
+        const double* yd = y[size_t(n)].data();
+        for (Index i = 0; i < total; ++i) sd[i] += td[i] - zd[i] + yd[i] * inv_mu;
+      }
+      const double inv_n = 1.0 / double(n_modes);
+      const double tau = 1.0 / (mu * double(n_modes));
+      double* ed = e.data();
+      for (Index i = 0; i < total; ++i) ed[i] = soft_threshold(sd[i] * inv_n, tau);
+    }
+    bool bad = false;  // baselines.cpp:93-112
+    for (Index n = 0; n < n_modes; ++n) {
+      const size_t ni = size_t(n);
+      const double* zd = z[ni].data();
+      const double* ed = e.data();
+      double* yd = y[ni].data();
+      double worst = 0.0;
+      for (Index i = 0; i < total; ++i) {
+        const double r = td[i] - zd[i] - ed[i];
+        yd[i] += mu * r;
+        const double a = std::fabs(r);
+        if (a > worst) worst = a;
+        bad |= !std::isfinite(r);
+      }
+      resid[ni] = worst;
+    }
+    const double mu_next = std::min(cfg.rho * mu, cfg.mu_max);
+    ++iter;
+    if (bad) throw NumericalError("snn: non-finite iterate at iteration " + std::to_string(iter));
+    res.residual_history.push_back(*std::max_element(resid.begin(), resid.end()));
+    converged = true;
+    for (double r : resid) converged = converged && (r < cfg.eps);
+    if (cfg.fixed_iters) converged = false;
+    mu = mu_next;
+    if (observer.fn) {
+      std::vector<const double*> zp, yp;
+      for (Index n = 0; n < n_modes; ++n) {
+        zp.push_back(z[size_t(n)].data());
+        yp.push_back(y[size_t(n)].data());
+      }
+      pasd_iteration_view view{iter, mu_used, mu_next, resid.data(), e.data(), zp.data(), yp.data(), nullptr,
+                               nullptr};
+      observer.fn(&view, observer.user);
+    }
+  }
+  res.converged = converged;  // baselines.cpp:128-141
+  res.iters = iter;
+  res.final_residuals = resid;
+  double l1 = 0.0;
+  for (double x : e) l1 += std::fabs(x);
+  res.objective = l1;
+  for (Index n = 0; n < n_modes; ++n) {
+    const Index rows = dims[size_t(n)];
+    Matrix m(rows, total / rows);
+    unfold_into(z[size_t(n)].data(), dims, n + 1, m.data());
+    res.objective += cfg.lambdas[size_t(n)] * nuclear_norm(m);
+  }
+  const std::vector<double>& w = cfg.alphas();
+  double wsum = 0.0;
+  for (double x : w) wsum += x;
+  res.x.assign(static_cast<size_t>(total), 0.0);
+  for (Index n = 0; n < n_modes; ++n) {
+    const double c = w[size_t(n)] / wsum;
+    const double* zd = z[size_t(n)].data();
+    for (Index i = 0; i < total; ++i) res.x[size_t(i)] = res.x[size_t(i)] + c * zd[i];
+  }
+  res.e = std::move(e);
+  res.z = std::move(z);
+  res.y = std::move(y);
+  return res;
+}
+
 // --------------------------------------------------- pasd.cpp, V = 0 phase
 // The same iteration as pasd_recover above, restricted to the phase in which
 // every V_n is still zero, for the full-size configs whose
@@ -787,9 +916,9 @@ extern "C" {
 
 // Full reference-restated solve.  svd_variant: 0 = dgesdd (reference), 1 = dgesvd.
 // threads: OpenBLAS + elementwise-loop threads (1 = the reference's setting).
-int oracle_pasd_recover(const double* t, const pasd_options* opt, pasd_outputs* out,
-                        pasd_observer_fn obs, void* user, int svd_variant, int threads, char* err,
-                        size_t errlen) {
+static int run_oracle(bool snn, const double* t, const pasd_options* opt, pasd_outputs* out,
+                      pasd_observer_fn obs, void* user, int svd_variant, int threads, char* err,
+                      size_t errlen) {
   return guarded(err, errlen, [&] {
     if (!opt || opt->order < 1) throw ArgumentError("tensor order must be at least 1");
     g_svd_variant = svd_variant;
@@ -799,7 +928,7 @@ int oracle_pasd_recover(const double* t, const pasd_options* opt, pasd_outputs* 
     Config cfg;
     for (int n = 0; n < opt->order; ++n) {
       cfg.lambdas.push_back(opt->lambdas[n]);
-      cfg.ranks.push_back(opt->ranks[n]);
+      if (!snn) cfg.ranks.push_back(opt->ranks[n]);
       if (opt->output_weights) cfg.output_weights.push_back(opt->output_weights[n]);
     }
     cfg.mu0 = opt->mu0;
@@ -809,7 +938,7 @@ int oracle_pasd_recover(const double* t, const pasd_options* opt, pasd_outputs* 
     cfg.maxiter = opt->maxiter;
     cfg.fixed_iters = (opt->flags & PASD_FLAG_FIXED_ITERS) != 0;
     Observer o{obs, user};
-    Result r = pasd_recover(t, dims, cfg, o);
+    Result r = snn ? snn_recover(t, dims, cfg, o) : pasd_recover(t, dims, cfg, o);
     const size_t total = r.e.size();
     auto put = [&](double* dst, const std::vector<double>& src) {
       if (dst) std::memcpy(dst, src.data(), total * sizeof(double));
@@ -819,7 +948,7 @@ int oracle_pasd_recover(const double* t, const pasd_options* opt, pasd_outputs* 
     for (int n = 0; n < opt->order; ++n) {
       if (out->z) put(out->z[n], r.z[size_t(n)]);
       if (out->y) put(out->y[n], r.y[size_t(n)]);
-      if (out->y_hat) put(out->y_hat[n], r.y_hat[size_t(n)]);
+      if (out->y_hat && !snn) put(out->y_hat[n], r.y_hat[size_t(n)]);
       if (out->final_residuals) out->final_residuals[n] = r.final_residuals[size_t(n)];
     }
     if (out->residual_history)
@@ -832,6 +961,17 @@ int oracle_pasd_recover(const double* t, const pasd_options* opt, pasd_outputs* 
     out->cert_c = r.c;
     out->cert_bound = r.bound;
   });
+}
+
+int oracle_pasd_recover(const double* t, const pasd_options* opt, pasd_outputs* out, pasd_observer_fn obs,
+                        void* user, int svd_variant, int threads, char* err, size_t errlen) {
+  return run_oracle(false, t, opt, out, obs, user, svd_variant, threads, err, errlen);
+}
+
+// snn_recover (baselines.cpp:37-143); y_hat and the certificate stay empty.
+int oracle_snn_recover(const double* t, const pasd_options* opt, pasd_outputs* out, pasd_observer_fn obs,
+                       void* user, int svd_variant, int threads, char* err, size_t errlen) {
+  return run_oracle(true, t, opt, out, obs, user, svd_variant, threads, err, errlen);
 }
 
 // Reference generator gen_lowrank_tucker (synth.cpp:71-89) without the rank

@@ -19,6 +19,7 @@ PASD_FLAG_NONE = 0
 PASD_FLAG_NO_CERTIFICATE = 1 << 0
 PASD_FLAG_FIXED_ITERS = 1 << 1
 PASD_FLAG_REUSE_SOLVER = 1 << 2
+PASD_FLAG_CHECK_REPLICAS = 1 << 3
 
 PASD_KERNEL_CLASSES = ("polar", "contract_A", "gram", "svt", "update", "finish", "contract_W")
 
@@ -51,6 +52,7 @@ class PasdShard(C.Structure):
         ("nccl_unique_id", C.c_void_p),
         ("slab_begin", C.c_int64),
         ("slab_end", C.c_int64),
+        ("loopback", C.c_void_p),
     ]
 
 
@@ -121,6 +123,10 @@ HEADER_SYMBOLS = (
     "pasd_b200_synth_factor",
     "pasd_b200_synth_support",
     "pasd_b200_nccl_unique_id",
+    "pasd_b200_loopback_create",
+    "pasd_b200_snn_recover",
+    "pasd_b200_guard_report",
+    "pasd_b200_loopback_destroy",
     "pasd_b200_abi_version",
     "pasd_b200_build_info",
 )

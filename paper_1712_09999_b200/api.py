@@ -101,6 +101,27 @@ class PasdConfig:
 
 
 @dataclass
+class SnnConfig:
+    """Hyperparameters of the full-SVT ADMM baseline (tenrec::SnnConfig,
+    baselines.hpp:9-20): one nuclear-norm term per unfolding, no ranks."""
+
+    lambdas: List[float]
+    mu0: float = 1e-4
+    mu_max: float = 1e10
+    rho: float = 1.1
+    eps: float = 1e-5
+    maxiter: int = 1000
+    output_weights: List[float] = field(default_factory=list)
+
+    @property
+    def ranks(self) -> List[int]:  # the C-ABI options struct carries ranks; SNN ignores them
+        return [1] * len(self.lambdas)
+
+    def alphas(self) -> List[float]:
+        return list(self.output_weights) if self.output_weights else list(self.lambdas)
+
+
+@dataclass
 class Certificate:
     epsilon_hat: float = 0.0
     c: float = 0.0
@@ -199,6 +220,10 @@ def count_checks(dims: Sequence[int], config: PasdConfig) -> None:
     n = len(dims)
     if len(config.lambdas) != n:
         raise ArgumentError(f"config: expected {n} lambdas, got {len(config.lambdas)}")
+    if isinstance(config, SnnConfig):  # SnnConfig::validate (baselines.cpp:12-29)
+        if config.output_weights and len(config.output_weights) != n:
+            raise ArgumentError(f"config: expected {n} output weights")
+        return
     if len(config.ranks) != n:
         raise ArgumentError(f"config: expected {n} ranks, got {len(config.ranks)}")
     if config.output_weights and len(config.output_weights) != n:
@@ -209,6 +234,7 @@ def make_observer(dims: Sequence[int], ranks: Sequence[int], user_fn: Optional[I
     """Wrap a Python observer as a pasd_observer_fn (copies the host view)."""
     if user_fn is None:
         return _abi.PasdObserverFn()
+    snn_view = ranks is None  # SNN views carry no u / v (baselines.cpp:124-125)
     if isinstance(user_fn, _abi.PasdObserverFn):  # raw C callback, passed through
         return user_fn
     dims = [int(x) for x in dims]
@@ -228,8 +254,9 @@ def make_observer(dims: Sequence[int], ranks: Sequence[int], user_fn: Optional[I
             e=arr(v.e, total, dims),
             z=[arr(v.z[i], total, dims) for i in range(n)],
             y=[arr(v.y[i], total, dims) for i in range(n)],
-            u=[arr(v.u[i], dims[i] * ranks[i], (dims[i], ranks[i])) for i in range(n)],
-            v=[arr(v.v[i], ranks[i] * (total // dims[i]), (ranks[i], total // dims[i])) for i in range(n)],
+            u=[] if snn_view else [arr(v.u[i], dims[i] * ranks[i], (dims[i], ranks[i])) for i in range(n)],
+            v=[] if snn_view else [arr(v.v[i], ranks[i] * (total // dims[i]), (ranks[i], total // dims[i]))
+                                   for i in range(n)],
         )
         user_fn(view)
 
@@ -250,7 +277,7 @@ def run_recover(fn, t, config: PasdConfig, observer=None, *, flags=0, want_z=Tru
     e = np.empty(total)
     z = [np.empty(total) for _ in range(n)] if want_z else None
     y = [np.empty(total) for _ in range(n)] if want_y else None
-    yh = [np.empty(total) for _ in range(n)] if want_y else None
+    yh = [np.empty(total) for _ in range(n)] if want_y and not isinstance(config, SnnConfig) else None
     hist = np.zeros(max(1, int(config.maxiter)))
     fres = np.zeros(n)
     out = _abi.PasdOutputs()
@@ -260,7 +287,7 @@ def run_recover(fn, t, config: PasdConfig, observer=None, *, flags=0, want_z=Tru
     out.z, out.y, out.y_hat = zp, yp, yhp
     out.residual_history = _abi.dptr(hist)
     out.final_residuals = _abi.dptr(fres)
-    obs = make_observer(dims, config.ranks, observer)
+    obs = make_observer(dims, None if isinstance(config, SnnConfig) else config.ranks, observer)
     err = C.create_string_buffer(1024)
     rc = fn(flat_t.ctypes.data_as(_abi.c_double_p), C.byref(opt), C.byref(out), obs, None, *extra_args,
             err, C.c_size_t(len(err)))

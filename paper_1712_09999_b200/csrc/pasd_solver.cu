@@ -38,6 +38,7 @@
 #include "pasd_pass1.cuh"
 #include "pasd_gram.cuh"
 #include "pasd_pass2m8.cuh"
+#include "pasd_comm.cuh"
 
 using namespace pasd;
 
@@ -62,6 +63,81 @@ void nk(ncclResult_t r, const char* what) {
 #define NK(x) nk((x), #x)
 
 int guarded_call(char* err, size_t errlen, const std::function<void()>& f);
+
+// NCCL backend of the sharded iteration's collectives (pasd_comm.cuh).
+class NcclComm final : public Comm {
+ public:
+  NcclComm(int nranks, int rank, const ncclUniqueId& id) { NK(ncclCommInitRank(&c_, nranks, id, rank)); }
+  ~NcclComm() override {
+    if (c_) ncclCommDestroy(c_);
+  }
+  void group_start() override { NK(ncclGroupStart()); }
+  void group_end() override { NK(ncclGroupEnd()); }
+  void allreduce(const double* send, double* recv, size_t count, RedOp op, cudaStream_t st) override {
+    NK(ncclAllReduce(send, recv, count, ncclDouble, op == RedOp::Sum ? ncclSum : ncclMax, c_, st));
+  }
+  bool capturable() const override { return true; }
+  const char* kind() const override { return "nccl"; }
+
+ private:
+  ncclComm_t c_ = nullptr;
+};
+
+// Loopback backend: all ranks of a group in this process on one device, one
+// host thread per rank (pasd_comm.cuh).  Grouped calls are queued and run as
+// one rendezvous at group_end.
+class LoopbackComm final : public Comm {
+ public:
+  LoopbackComm(LoopbackGroup* g, int rank) : g_(g), rank_(rank) {}
+  void group_start() override { in_group_ = true; }
+  void group_end() override {
+    in_group_ = false;
+    flush();
+  }
+  void allreduce(const double* send, double* recv, size_t count, RedOp op, cudaStream_t st) override {
+    ops_.push_back({send, recv, count, op, st});
+    if (!in_group_) flush();
+  }
+  bool capturable() const override { return false; }
+  const char* kind() const override { return "loopback"; }
+
+ private:
+  void flush() {
+    std::vector<LoopbackGroup::Op> ops;
+    ops.swap(ops_);
+    for (const auto& o : ops) CK(cudaStreamSynchronize(o.st));  // this rank's partials are complete
+    {
+      std::lock_guard<std::mutex> lk(g_->mu);
+      g_->posted[rank_] = ops;
+    }
+    if (!g_->barrier()) fail(PASD_ERR_CUDA, "pasd_b200: loopback group broken (another rank failed or timed out)");
+    for (int q = 0; q < g_->nranks; ++q) {
+      const auto& oq = g_->posted[q];
+      bool same = oq.size() == ops.size();
+      for (size_t k = 0; same && k < ops.size(); ++k) same = oq[k].count == ops[k].count && oq[k].op == ops[k].op;
+      if (!same) {
+        g_->abort();
+        fail(PASD_ERR_CUDA, "pasd_b200: loopback ranks issued mismatched collectives");
+      }
+    }
+    for (size_t k = 0; k < ops.size(); ++k) {
+      LoopbackSrc src{};
+      for (int q = 0; q < g_->nranks; ++q) src.p[q] = g_->posted[q][k].send;
+      const int64_t cnt = (int64_t)ops[k].count;
+      const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((cnt + 255) / 256, 1184));
+      k_loopback_reduce<<<blocks, 256, 0, ops[k].st>>>(src, g_->nranks, ops[k].recv, cnt,
+                                                       ops[k].op == RedOp::Max ? 1 : 0);
+      CK(cudaGetLastError());
+    }
+    for (const auto& o : ops) CK(cudaStreamSynchronize(o.st));
+    // every rank has read every send buffer before any rank overwrites one
+    if (!g_->barrier()) fail(PASD_ERR_CUDA, "pasd_b200: loopback group broken (another rank failed or timed out)");
+  }
+  LoopbackGroup* g_;
+  int rank_;
+  bool in_group_ = false;
+  std::vector<LoopbackGroup::Op> ops_;
+};
 
 void set_err(char* err, size_t len, const std::string& m) {
   if (err && len) std::snprintf(err, len, "%s", m.c_str());
@@ -125,12 +201,87 @@ void validate_options(const pasd_options* o) {
                                   " exceeds the supported maximum " + std::to_string(PASD_MAX_RANK));
 }
 
+// Guard-band allocations (env PASD_B200_GUARD=1).  compute-sanitizer is closed
+// on this GPU pool, so out-of-bounds global writes are caught by 64 KB canary
+// bands (0xFF bytes, i.e. NaN doubles, so a stray READ of a band poisons the
+// result the parity checks compare) on both sides of every device buffer,
+// verified when the buffer is freed; pasd_b200_guard_report() returns the
+// counts.  Off by default (no cost).
+constexpr size_t kGuardBytes = 1 << 16;
+struct GuardState {
+  std::mutex mu;
+  std::vector<std::pair<char*, size_t>> live;  // (user pointer, bytes)
+  long long checked = 0, violations = 0;
+};
+GuardState& guard_state() {
+  static GuardState g;
+  return g;
+}
+bool guard_on() {
+  static const bool on = [] {
+    const char* e = std::getenv("PASD_B200_GUARD");
+    return e && e[0] == '1';
+  }();
+  return on;
+}
+
 template <class T>
 T* dalloc(size_t count) {
   void* p = nullptr;
   if (count == 0) count = 1;
-  CK(cudaMalloc(&p, count * sizeof(T)));
-  return static_cast<T*>(p);
+  const size_t bytes = count * sizeof(T);
+  if (!guard_on()) {
+    CK(cudaMalloc(&p, bytes));
+    return static_cast<T*>(p);
+  }
+  CK(cudaMalloc(&p, bytes + 2 * kGuardBytes));
+  char* raw = static_cast<char*>(p);
+  CK(cudaMemset(raw, 0xFF, kGuardBytes));
+  CK(cudaMemset(raw + kGuardBytes + bytes, 0xFF, kGuardBytes));
+  CK(cudaDeviceSynchronize());
+  GuardState& g = guard_state();
+  std::lock_guard<std::mutex> lk(g.mu);
+  g.live.emplace_back(raw + kGuardBytes, bytes);
+  return reinterpret_cast<T*>(raw + kGuardBytes);
+}
+
+// cudaFree for dalloc'd buffers; in guard mode verifies both bands first.
+void dfree(void* p) {
+  if (!p) return;
+  if (!guard_on()) {
+    cudaFree(p);
+    return;
+  }
+  GuardState& g = guard_state();
+  size_t bytes = 0;
+  {
+    std::lock_guard<std::mutex> lk(g.mu);
+    for (size_t k = 0; k < g.live.size(); ++k)
+      if (g.live[k].first == p) {
+        bytes = g.live[k].second;
+        g.live.erase(g.live.begin() + (long)k);
+        break;
+      }
+  }
+  char* raw = static_cast<char*>(p) - kGuardBytes;
+  std::vector<unsigned char> band(kGuardBytes);
+  cudaDeviceSynchronize();
+  int bad = 0;
+  for (int side = 0; side < 2; ++side) {
+    cudaMemcpy(band.data(), side ? raw + kGuardBytes + bytes : raw, kGuardBytes, cudaMemcpyDeviceToHost);
+    for (unsigned char c : band)
+      if (c != 0xFF) {
+        bad = 1;
+        break;
+      }
+  }
+  {
+    std::lock_guard<std::mutex> lk(g.mu);
+    ++g.checked;
+    g.violations += bad;
+  }
+  if (bad) std::fprintf(stderr, "pasd_b200: guard band overwritten around a %zu-byte buffer\n", bytes);
+  cudaFree(raw);
 }
 
 int rpt_for(int R) { return R <= 8 ? 2 : R <= 16 ? 4 : R <= 32 ? 8 : 16; }
@@ -213,7 +364,9 @@ struct pasd_solver {
   int rank = 0, nranks = 1;
   int64_t slab_b = 0, slab_e = 0;
   std::vector<int64_t> gdims;  // global dims (dims = local slab dims)
-  ncclComm_t comm = nullptr;
+  std::unique_ptr<Comm> comm;     // NCCL (one GPU per rank) or loopback (ranks share one GPU)
+  LoopbackGroup* loop_group = nullptr;
+  bool check_replicas = false;    // PASD_FLAG_CHECK_REPLICAS: cross-rank hash of U_n / M_n per run
   cudaStream_t side = nullptr;  // A_3 all-reduce, overlapped with pass 1 of modes 1 and 2
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   // finalisation: D2H of E on its own stream, overlapping the X materialisation
@@ -230,7 +383,7 @@ struct pasd_solver {
   double* red = nullptr;
 
   ~pasd_solver() {
-    if (comm) ncclCommDestroy(comm);
+    comm.reset();
     if (ev_fork) cudaEventDestroy(ev_fork);
     if (ev_join) cudaEventDestroy(ev_join);
     if (side) cudaStreamDestroy(side);
@@ -244,7 +397,7 @@ struct pasd_solver {
     }
     if (graph_exec) cudaGraphExecDestroy(graph_exec);
     if (graph) cudaGraphDestroy(graph);
-    for (void* p : owned) cudaFree(p);
+    for (void* p : owned) dfree(p);
     if (h_ctl) cudaFreeHost(h_ctl);
     if (stream) cudaStreamDestroy(stream);
   }
@@ -314,7 +467,7 @@ void launch_iteration_marked(pasd_solver* s, cudaStream_t st, Mark&& mark, bool 
       ++launches;
       CK(cudaEventRecord(s->ev_fork, st));
       CK(cudaStreamWaitEvent(s->side, s->ev_fork, 0));
-      NK(ncclAllReduce(s->A3_partial, s->modes[N - 1].A, (size_t)m3.J * m3.R, ncclDouble, ncclSum, s->comm, s->side));
+      s->comm->allreduce(s->A3_partial, s->modes[N - 1].A, (size_t)m3.J * m3.R, RedOp::Sum, s->side);
       CK(cudaEventRecord(s->ev_join, s->side));
       const int sms_p1 = std::max(1, s->sms - kNcclSms);
       for (int n = 0; n < N - 1; ++n) {
@@ -345,12 +498,12 @@ void launch_iteration_marked(pasd_solver* s, cudaStream_t st, Mark&& mark, bool 
         mark(PASD_K_GRAM, false);
         launches += 2;
       }
-      NK(ncclGroupStart());
+      s->comm->group_start();
       for (int n = 0; n < N - 1; ++n) {
         const ModeDev& m = s->modes[n];
-        NK(ncclAllReduce(s->gram_partial[n], m.Gram, (size_t)m.R * m.R, ncclDouble, ncclSum, s->comm, st));
+        s->comm->allreduce(s->gram_partial[n], m.Gram, (size_t)m.R * m.R, RedOp::Sum, st);
       }
-      NK(ncclGroupEnd());
+      s->comm->group_end();
       mark(PASD_K_SVT, true);
       k_svt<<<N * kSmallCluster, kSmallThreads, s->small_smem, st>>>(s->d_pack, s->d_ctl);
       mark(PASD_K_SVT, false);
@@ -375,14 +528,14 @@ void launch_iteration_marked(pasd_solver* s, cudaStream_t st, Mark&& mark, bool 
     if (s->sharded) {
       k_resid_local<<<1, kThreads, 0, st>>>(s->d_ctl, s->p2_resid, s->p2_bad, s->p2_grid, s->red_local);
       ++launches;
-      NK(ncclGroupStart());
+      s->comm->group_start();
       for (int n = 0; n < N; ++n) {
         const ModeDev& m = s->modes[n];
-        NK(ncclAllReduce(s->wt_partial[n], m.Wt, (size_t)m.Ifull * m.R, ncclDouble, ncclSum, s->comm, st));
+        s->comm->allreduce(s->wt_partial[n], m.Wt, (size_t)m.Ifull * m.R, RedOp::Sum, st);
       }
-      NK(ncclAllReduce(s->g2_partial, ctl_gnorm2(s), (size_t)N, ncclDouble, ncclSum, s->comm, st));
-      NK(ncclAllReduce(s->red_local, s->red, (size_t)N + 1, ncclDouble, ncclMax, s->comm, st));
-      NK(ncclGroupEnd());
+      s->comm->allreduce(s->g2_partial, ctl_gnorm2(s), (size_t)N, RedOp::Sum, st);
+      s->comm->allreduce(s->red_local, s->red, (size_t)N + 1, RedOp::Max, st);
+      s->comm->group_end();
     }
     if (s->sharded) {
       mark(PASD_K_FINISH, true);
@@ -649,14 +802,24 @@ pasd_solver* create_solver(const pasd_options* o, const pasd_shard* shard) {
     s->g2_partial = s->alloc<double>(PASD_MAX_ORDER);
     s->red_local = s->alloc<double>(PASD_MAX_ORDER + 1);
     s->red = s->alloc<double>(PASD_MAX_ORDER + 1);
-    ncclUniqueId id;
-    if (shard->nccl_unique_id)
-      std::memcpy(&id, shard->nccl_unique_id, sizeof(id));
-    else if (s->nranks == 1)
-      NK(ncclGetUniqueId(&id));
-    else
-      fail(PASD_ERR_ARGUMENT, "pasd_b200: nccl_unique_id is required for nranks > 1");
-    NK(ncclCommInitRank(&s->comm, s->nranks, id, s->rank));
+    if (shard->loopback) {  // ranks of one group share this device (pasd_comm.cuh)
+      auto* g = reinterpret_cast<LoopbackGroup*>(shard->loopback);
+      if (g->nranks != s->nranks)
+        fail(PASD_ERR_ARGUMENT, "pasd_b200: loopback group of " + std::to_string(g->nranks) + " ranks, shard says " +
+                                    std::to_string(s->nranks));
+      s->comm = std::make_unique<LoopbackComm>(g, s->rank);
+      s->loop_group = g;
+    } else {
+      ncclUniqueId id;
+      if (shard->nccl_unique_id)
+        std::memcpy(&id, shard->nccl_unique_id, sizeof(id));
+      else if (s->nranks == 1)
+        NK(ncclGetUniqueId(&id));
+      else
+        fail(PASD_ERR_ARGUMENT, "pasd_b200: nccl_unique_id is required for nranks > 1");
+      s->comm = std::make_unique<NcclComm>(s->nranks, s->rank, id);
+    }
+    s->check_replicas = (o->flags & PASD_FLAG_CHECK_REPLICAS) != 0 || std::getenv("PASD_CHECK_REPLICAS") != nullptr;
     CK(cudaStreamCreateWithFlags(&s->side, cudaStreamNonBlocking));
     CK(cudaEventCreateWithFlags(&s->ev_fork, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&s->ev_join, cudaEventDisableTiming));
@@ -693,7 +856,7 @@ pasd_solver* create_solver(const pasd_options* o, const pasd_shard* shard) {
     Pass2Args& a = s->p2;
     for (int n = 0; n < 3; ++n) {
       a.m[n] = s->modes[n];
-      if (s->sharded) a.m[n].Wt = s->wt_partial[n];  // reduced across ranks by NCCL
+      if (s->sharded) a.m[n].Wt = s->wt_partial[n];  // reduced across ranks by the comm
       a.Y[n] = s->Y[n];
     }
     a.T = s->T;
@@ -926,20 +1089,68 @@ void ensure_scratch(pasd_solver* s) {
   }
 }
 
+// Order-independent 64-bit hash of the replicated small state (U_n, M_n of
+// every mode): sum over entries of bits * (2 idx + 1) mod 2^64.  Written as
+// [hi, lo, -hi, -lo] (exact doubles) so one MAX all-reduce gives max and min.
+__global__ void k_replica_hash(const ModePack* mp, double* out) {
+  __shared__ unsigned long long acc;
+  if (threadIdx.x == 0) acc = 0ull;
+  __syncthreads();
+  unsigned long long h = 0ull, base = 0ull;
+  for (int n = 0; n < mp->order; ++n) {
+    const ModeDev& m = mp->m[n];
+    const int64_t nu = m.Ifull * m.R, nm = (int64_t)m.R * m.R;
+    for (int64_t i = threadIdx.x; i < nu; i += blockDim.x)
+      h += (unsigned long long)__double_as_longlong(m.U[i]) * (2ull * (base + i) + 1ull);
+    base += nu;
+    for (int64_t i = threadIdx.x; i < nm; i += blockDim.x)
+      h += (unsigned long long)__double_as_longlong(m.M[i]) * (2ull * (base + i) + 1ull);
+    base += nm;
+  }
+  atomicAdd(&acc, h);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const double hi = (double)(acc >> 32), lo = (double)(acc & 0xffffffffull);
+    out[0] = hi;
+    out[1] = lo;
+    out[2] = -hi;
+    out[3] = -lo;
+  }
+}
+
+// Debug check of SURVEY 8(e): every rank holds bit-identical U_n and M_n.
+void check_replicas(pasd_solver* s) {
+  cudaStream_t st = s->stream;
+  k_replica_hash<<<1, 256, 0, st>>>(s->d_pack, s->d_stats);
+  s->comm->allreduce(s->d_stats, s->d_stats + 4, 4, RedOp::Max, st);
+  double h[4];
+  CK(cudaMemcpyAsync(h, s->d_stats + 4, sizeof(h), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  if (h[0] != -h[2] || h[1] != -h[3])
+    fail(PASD_ERR_NUMERICAL, "pasd_b200: replicated U_n / M_n differ across ranks at iteration " +
+                                 std::to_string(s->h_ctl->iter));
+}
+
 // Runs until stop or `iters` more iterations.
 void run_solver(pasd_solver* s, int iters, pasd_observer_fn obs, void* user) {
   if (!s->loaded) fail(PASD_ERR_STATE, "pasd_b200: no tensor loaded");
   if (obs && s->sharded) fail(PASD_ERR_STATE, "pasd_b200: observers are not available on a sharded solver");
   sync_ctl(s);
   if (s->h_ctl->done) return;
-  build_graph(s);
+  const bool eager = s->comm && !s->comm->capturable();  // loopback ranks: host-sequenced launches
+  if (!eager) build_graph(s);
   HostView hv;
   if (obs) ensure_scratch(s);
   int launched = 0;
   s->launches_last_run = 0;
   while (launched < iters) {
     const int chunk = obs ? 1 : std::min(s->poll_every, iters - launched);
-    for (int k = 0; k < chunk; ++k) CK(cudaGraphLaunch(s->graph_exec, s->stream));
+    for (int k = 0; k < chunk; ++k) {
+      if (eager)
+        launch_iteration_marked(s, s->stream, [](int, bool) {});
+      else
+        CK(cudaGraphLaunch(s->graph_exec, s->stream));
+    }
     launched += chunk;
     s->launches_last_run += (int64_t)chunk * s->launches_per_iter;
     sync_ctl(s);
@@ -949,6 +1160,7 @@ void run_solver(pasd_solver* s, int iters, pasd_observer_fn obs, void* user) {
     if (obs) deliver_observer(s, obs, user, hv);
     if (c.done) break;
   }
+  if (s->sharded && s->check_replicas) check_replicas(s);
 }
 
 void profile_solver(pasd_solver* s, int iters, double* ms, int64_t* cnt, double* bytes, double* flops) {
@@ -1040,16 +1252,16 @@ void finalize_solver(pasd_solver* s, pasd_outputs* out) {
   CK(cudaStreamSynchronize(st));
   double l1 = 0.0;
   abs_stats(e, &l1, nullptr);
-  auto allreduce_scalar = [&](double v, ncclRedOp_t op) {
+  auto allreduce_scalar = [&](double v, RedOp op) {
     if (!s->sharded) return v;
     CK(cudaMemcpyAsync(s->d_stats, &v, sizeof(double), cudaMemcpyHostToDevice, st));
-    NK(ncclAllReduce(s->d_stats, s->d_stats + 1, 1, ncclDouble, op, s->comm, st));
+    s->comm->allreduce(s->d_stats, s->d_stats + 1, 1, op, st);
     double r = 0.0;
     CK(cudaMemcpyAsync(&r, s->d_stats + 1, sizeof(double), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
     return r;
   };
-  l1 = allreduce_scalar(l1, ncclSum);  // ||E||_1 over all slabs
+  l1 = allreduce_scalar(l1, RedOp::Sum);  // ||E||_1 over all slabs
   double obj = l1;
   for (int n = 0; n < N; ++n) obj += s->lambdas[n] * c.nuclear[n];
   out->objective = obj;
@@ -1069,8 +1281,8 @@ void finalize_solver(pasd_solver* s, pasd_outputs* out) {
     double eps_hat = 0.0, tl1 = 0.0;
     abs_stats(s->xbuf, nullptr, &eps_hat);
     abs_stats(s->T, &tl1, nullptr);
-    eps_hat = allreduce_scalar(eps_hat, ncclMax);
-    tl1 = allreduce_scalar(tl1, ncclSum);
+    eps_hat = allreduce_scalar(eps_hat, RedOp::Max);
+    tl1 = allreduce_scalar(tl1, RedOp::Sum);
     const int k_star = c.iter - 1;
     const double geom = s->rho * (1.0 + s->rho) / (s->rho - 1.0) + 0.5 / std::pow(s->rho, k_star);
     double dim_sum = 0.0, lam_term = 0.0;
@@ -1124,7 +1336,26 @@ int pasd_b200_nccl_unique_id(void* out128, char* errbuf, size_t errlen) {
 }
 
 const char* pasd_b200_build_info(void) {
-  return "pasd_b200 sm_100a fp64; kernels: polar,contract_A,gram,svt,update,finish,contract_W";
+  return "pasd_b200 sm_100a fp64; kernels: polar,pass1,gram,svt,pass2,finish,pass2_reduce; comm: nccl,loopback";
+}
+
+int pasd_b200_loopback_create(int32_t nranks, void** out, char* errbuf, size_t errlen) {
+  return guarded_call(errbuf, errlen, [&] {
+    if (!out) fail(PASD_ERR_ARGUMENT, "pasd_b200: null output handle");
+    if (nranks < 1 || nranks > kLoopbackMaxRanks)
+      fail(PASD_ERR_ARGUMENT, "pasd_b200: loopback groups hold 1.." + std::to_string(kLoopbackMaxRanks) + " ranks");
+    *out = new LoopbackGroup(nranks);
+  });
+}
+
+void pasd_b200_loopback_destroy(void* group) { delete reinterpret_cast<LoopbackGroup*>(group); }
+
+int64_t pasd_b200_guard_report(int64_t* checked, int64_t* live) {
+  GuardState& g = guard_state();
+  std::lock_guard<std::mutex> lk(g.mu);
+  if (checked) *checked = g.checked;
+  if (live) *live = (int64_t)g.live.size();
+  return g.violations;
 }
 
 int pasd_b200_validate(const pasd_options* opt, char* errbuf, size_t errlen) {
@@ -1181,7 +1412,12 @@ int pasd_b200_solver_run(pasd_solver* s, int32_t iters, int32_t* iters_done, int
   return guarded_call(errbuf, errlen, [&] {
     if (!s) fail(PASD_ERR_ARGUMENT, "pasd_b200: null solver");
     CK(cudaSetDevice(s->device));
-    run_solver(s, iters, nullptr, nullptr);
+    try {
+      run_solver(s, iters, nullptr, nullptr);
+    } catch (...) {
+      if (s->loop_group) s->loop_group->abort();  // release the other ranks' barriers
+      throw;
+    }
     if (iters_done) *iters_done = s->h_ctl->iter;
     if (converged) *converged = s->h_ctl->converged;
   });
@@ -1191,7 +1427,12 @@ int pasd_b200_solver_finalize(pasd_solver* s, pasd_outputs* out, char* errbuf, s
   return guarded_call(errbuf, errlen, [&] {
     if (!s || !out) fail(PASD_ERR_ARGUMENT, "pasd_b200: null argument");
     CK(cudaSetDevice(s->device));
-    finalize_solver(s, out);
+    try {
+      finalize_solver(s, out);
+    } catch (...) {
+      if (s->loop_group) s->loop_group->abort();
+      throw;
+    }
   });
 }
 
@@ -1363,7 +1604,7 @@ namespace {
 struct TmpDev {
   std::vector<void*> ptrs;
   ~TmpDev() {
-    for (void* p : ptrs) cudaFree(p);
+    for (void* p : ptrs) dfree(p);
   }
   template <class T>
   T* alloc(size_t n) {
@@ -1566,3 +1807,4 @@ int pasd_b200_procrustes(const double* g, int64_t i_rows, int64_t p_cols, const 
 
 #include "pasd_spec.cuh"
 #include "pasd_synth.cuh"
+#include "pasd_snn.cuh"

@@ -114,13 +114,26 @@ def pasd_recover(t, config: PasdConfig, observer=None, *, device: int = 0, fixed
                        device=device, poll_every=poll_every)
 
 
+def snn_recover(t, config, observer=None, *, device: int = 0, fixed_iters: bool = False, want_z: bool = True,
+                want_y: bool = True, poll_every: int = 0) -> RecoveryResult:
+    """Drop-in for tenrec::snn_recover (baselines.hpp:39-40, baselines.cpp:37-143),
+    the full-SVT ADMM baseline, on a B200 (pasd_b200_snn_recover).  `config`
+    is an api.SnnConfig; y_hat and the certificate stay empty as in the
+    reference."""
+    L = lib()
+    L.pasd_b200_snn_recover.restype = C.c_int
+    flags = _abi.PASD_FLAG_FIXED_ITERS if fixed_iters else 0
+    return run_recover(L.pasd_b200_snn_recover, t, config, observer, flags=flags, want_z=want_z, want_y=want_y,
+                       device=device, poll_every=poll_every)
+
+
 class Solver:
     """Device-resident solver handle (``pasd_b200_solver_*``) for benchmarks
     and sharded runs.  ``t`` may be a host numpy array or, with
     ``t_is_device``, an integer device pointer (e.g. ``torch_tensor.data_ptr()``)."""
 
     def __init__(self, dims: Sequence[int], config: PasdConfig, *, device: int = 0, fixed_iters: bool = False,
-                 poll_every: int = 0, shard: Optional[_abi.PasdShard] = None):
+                 poll_every: int = 0, shard: Optional[_abi.PasdShard] = None, flags: int = 0):
         self.dims = [int(d) for d in dims]
         self.local_dims = list(self.dims)
         sh = getattr(shard, "struct", shard)
@@ -128,7 +141,7 @@ class Solver:
             self.local_dims[-1] = int(sh.slab_end - sh.slab_begin)
         self.config = config
         count_checks(self.dims, config)
-        flags = _abi.PASD_FLAG_FIXED_ITERS if fixed_iters else 0
+        flags = int(flags) | (_abi.PASD_FLAG_FIXED_ITERS if fixed_iters else 0)
         self._opt, self._keep = build_options(self.dims, config, device=device, flags=flags, poll_every=poll_every)
         self._h = C.c_void_p()
         err = _err()

@@ -27,7 +27,7 @@ def test_header_symbols_exported():
     assert set(names) == set(_abi.HEADER_SYMBOLS)
     for name in names:
         assert hasattr(lib, name), name  # dlsym succeeds
-    assert lib.pasd_b200_abi_version() == 1
+    assert lib.pasd_b200_abi_version() == 2
 
 
 def test_header_compiles_as_c():
@@ -89,3 +89,48 @@ def test_no_cpu_fallback_without_gpu():
     cfg = PasdConfig(lambdas=[1.0, 1.0, 1.0], ranks=[1, 1, 1])
     with pytest.raises(DeviceError, match="cuda"):
         pb.pasd_recover(np.ones((3, 3, 3)), cfg)
+
+
+def test_snn_validate_matches_oracle_messages(oracle_mod):
+    """pasd_b200_snn_recover validates like SnnConfig::validate (baselines.cpp:12-29)
+    before touching the device: same messages as the oracle's snn_recover."""
+    from paper_1712_09999_b200.api import SnnConfig
+
+    dims = (4, 3, 2)
+    lam = [1.0, 1.0, 1.0]
+    bad = [
+        SnnConfig(lambdas=[1.0, 0.0, 1.0]),
+        SnnConfig(lambdas=lam, mu0=-1.0),
+        SnnConfig(lambdas=lam, mu_max=1e-6),
+        SnnConfig(lambdas=lam, rho=1.0),
+        SnnConfig(lambdas=lam, eps=0.0),
+        SnnConfig(lambdas=lam, maxiter=0),
+        SnnConfig(lambdas=lam, output_weights=[1.0, 0.0, 1.0]),
+        SnnConfig(lambdas=[1.0, 1.0]),
+    ]
+    for cfg in bad:
+        with pytest.raises(ArgumentError) as ours:
+            pb.snn_recover(np.zeros(dims), cfg)
+        with pytest.raises(ArgumentError) as ref:
+            oracle_mod.snn_recover(np.zeros(dims), cfg)
+        assert str(ours.value) == str(ref.value)
+    t = np.zeros(dims)
+    t[1, 1, 1] = np.inf
+    for f in (pb.snn_recover, oracle_mod.snn_recover):
+        with pytest.raises(ArgumentError, match="snn: input tensor contains non-finite entries"):
+            f(t, SnnConfig(lambdas=lam))
+    with pytest.raises(ArgumentError, match="snn supports unfoldings"):
+        pb.snn_recover(np.zeros((120, 120, 2)), SnnConfig(lambdas=lam))
+
+
+def test_oracle_snn_recovers_desk_case(oracle_mod):
+    """SPEC.md desk case (30^3, r = 3, 5% corruption): the restated SNN baseline
+    recovers L0 (RSE <= 1e-4) and leaves y_hat / the certificate empty."""
+    from paper_1712_09999_b200.api import SnnConfig
+
+    dims = (30, 30, 30)
+    L0 = oracle_mod.gen_tucker(dims, [3, 3, 3], seed=0)
+    T = oracle_mod.corrupt_sparse(L0, 0.05, seed=0)
+    r = oracle_mod.snn_recover(T, SnnConfig(lambdas=oracle_mod.default_lambdas(dims)))
+    assert r.converged and r.certificate is None and r.y_hat is None
+    assert np.linalg.norm(r.x - L0) / np.linalg.norm(L0) <= 1e-4

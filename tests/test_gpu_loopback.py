@@ -1,0 +1,93 @@
+"""The library's own slab-sharded path with nranks = 2 and 3 on ONE device
+(pasd_shard.loopback, pasd_comm.cuh): the same partial buffers, the same
+sequence of all-reduces (A_3, Gram_1/2, Wt_n, ||G_n||^2, residual maxima and
+NaN flag, finalisation scalars) and replicated small solves as the NCCL path,
+with ragged mode-3 slabs that cut through the 8-wide pass-2 bricks.  Every
+run also checks that the replicated U_n / M_n are bit-identical on all ranks
+(PASD_FLAG_CHECK_REPLICAS).  Compared with the unsharded solver and the oracle
+("parity for 2/4/8 GPUs is checked against the oracle and
+against 1 GPU")."""
+import numpy as np
+import pytest
+
+from paper_1712_09999_b200.api import PasdConfig
+
+pytestmark = pytest.mark.gpu
+
+
+def rel(a, b):
+    n = np.linalg.norm(b)
+    return np.linalg.norm(a - b) / n if n > 0 else np.linalg.norm(a - b)
+
+
+def instance(oracle_mod, dims, r, rho, seed=0):
+    L0 = oracle_mod.gen_tucker(dims, [r] * len(dims), seed=seed)
+    return L0, oracle_mod.corrupt_sparse(L0, rho, seed=seed)
+
+
+def gather(parts, slabs, shape, key):
+    out = np.empty(shape)
+    for res, (b, e) in zip(parts, slabs):
+        out[:, :, b:e] = getattr(res, key)
+    return out
+
+
+@pytest.mark.parametrize("nranks", [2, 3])
+@pytest.mark.parametrize("variant", ["m8", "m16"])
+def test_loopback_trivial_phase_bit_exact(gpu, oracle_mod, monkeypatch, nranks, variant):
+    """V_n = 0 phase (first 25 iterations): Z = 0, so every rank's E slab and the
+    residual history equal the unsharded solver's bit for bit."""
+    from paper_1712_09999_b200.sharding import run_loopback
+
+    monkeypatch.setenv("PASD_PASS2_M16" if variant == "m16" else "PASD_PASS2_M8", "1")
+    L0, T = instance(oracle_mod, (40, 36, 31), 3, 0.10, seed=3)
+    cfg = PasdConfig(lambdas=oracle_mod.default_lambdas(T.shape), ranks=[3, 3, 3], maxiter=25)
+    r0 = gpu.pasd_recover(T, cfg, fixed_iters=True)
+    it, conv, parts, slabs = run_loopback(T, cfg, nranks, 25)
+    assert it == 25 and not conv
+    np.testing.assert_array_equal(gather(parts, slabs, T.shape, "e"), r0.e)
+    for p in parts:
+        assert p.residual_history == r0.residual_history
+
+
+@pytest.mark.parametrize("nranks", [2, 3])
+@pytest.mark.parametrize("variant", ["m8", "m16"])
+def test_loopback_convergence_matches_unsharded_and_oracle(gpu, oracle_mod, monkeypatch, nranks, variant):
+    """Run to eps = 1e-7 through the rank-deficient transition into the
+    full-rank phase: the sharded solve (partial sums in another order, so
+    rounding-level differences) agrees with the unsharded one and the oracle."""
+    from paper_1712_09999_b200.sharding import run_loopback
+
+    monkeypatch.setenv("PASD_PASS2_M16" if variant == "m16" else "PASD_PASS2_M8", "1")
+    L0, T = instance(oracle_mod, (30, 28, 27), 2, 0.05, seed=1)
+    cfg = PasdConfig(lambdas=oracle_mod.default_lambdas(T.shape), ranks=[2, 2, 2], eps=1e-7, maxiter=400)
+    r0 = gpu.pasd_recover(T, cfg)
+    ro = oracle_mod.pasd_recover(T, cfg)
+    it, conv, parts, slabs = run_loopback(T, cfg, nranks, cfg.maxiter, fixed_iters=False)
+    assert conv and r0.converged and ro.converged
+    assert abs(it - r0.iters) <= 1 and abs(it - ro.iters) <= 2, (it, r0.iters, ro.iters)
+    x = gather(parts, slabs, T.shape, "x")
+    e = gather(parts, slabs, T.shape, "e")
+    assert rel(x, r0.x) <= 1e-7, rel(x, r0.x)
+    assert rel(e, r0.e) <= 1e-7, rel(e, r0.e)
+    assert np.array_equal(e != 0, r0.e != 0)
+    assert rel(x, L0) <= max(2 * rel(ro.x, L0), 1e-5)
+    # replicated scalars agree on every rank (objective, certificate)
+    objs = {p.objective for p in parts}
+    assert len(objs) == 1
+    assert abs(objs.pop() - r0.objective) <= 1e-7 * abs(r0.objective)
+    assert all(p.certificate is not None for p in parts)
+
+
+def test_loopback_full_rank_steady_state(gpu, oracle_mod):
+    """A fixed 150 iterations (every V_n at full rank, non-degenerate Procrustes
+    and SVT on all-reduced Gram / Wt): 3 ragged slabs vs the unsharded solver."""
+    from paper_1712_09999_b200.sharding import run_loopback
+
+    L0, T = instance(oracle_mod, (26, 24, 29), 3, 0.05, seed=2)
+    cfg = PasdConfig(lambdas=oracle_mod.default_lambdas(T.shape), ranks=[3, 3, 3], maxiter=150)
+    r0 = gpu.pasd_recover(T, cfg, fixed_iters=True)
+    it, conv, parts, slabs = run_loopback(T, cfg, 3, 150, slabs=[(0, 5), (5, 19), (19, 29)])
+    assert it == 150
+    assert rel(gather(parts, slabs, T.shape, "x"), r0.x) <= 1e-8
+    assert rel(gather(parts, slabs, T.shape, "e"), r0.e) <= 1e-8

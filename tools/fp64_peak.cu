@@ -1,6 +1,7 @@
 // Microbenchmark: FP64 FFMA pipe and DMMA (mma.sync f64) throughput on sm_100a,
 // plus a float64 streaming copy. Used to set the FP64 roofline denominator.
 #include <cstdio>
+#include <cstdlib>
 #include <cuda_runtime.h>
 #define CK(x) do{cudaError_t e=(x); if(e!=cudaSuccess){printf("CUDA %s at %d\n",cudaGetErrorString(e),__LINE__);return 1;}}while(0)
 
@@ -35,7 +36,8 @@ __global__ void copy_k(const double2* __restrict__ a, double2* __restrict__ b, s
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) b[i] = a[i];
 }
 
-int main() {
+int main(int argc, char** argv) {
+  const double sustain_s = argc > 1 ? atof(argv[1]) : 0.0;  // > 0: also a sustained DMMA run of this length
   int dev = 0; cudaDeviceProp p; CK(cudaGetDeviceProperties(&p, dev));
   printf("{\"name\":\"%s\",\"sms\":%d,\"l2_bytes\":%d,\"smem_optin\":%zu,\"regs_per_sm\":%d}\n", p.name, p.multiProcessorCount, p.l2CacheSize, p.sharedMemPerBlockOptin, p.regsPerMultiprocessor);
   double* out; CK(cudaMalloc(&out, 148 * 64 * 1024 * sizeof(double)));
@@ -62,6 +64,19 @@ int main() {
     float ms; cudaEventElapsedTime(&ms, e0, e1);
     double flops = 2.0 * 16 * 8 * 4 * 4.0 * iters * (double)grid * (threads / 32);
     printf("{\"kernel\":\"dmma_m16n8k4\",\"blocks_per_sm\":%d,\"ms\":%.3f,\"tflops\":%.2f}\n", blocksPerSm, ms, flops / ms / 1e9);
+  }
+  if (sustain_s > 0) {  // back-to-back launches for sustain_s seconds (the figure for a kernel inside a long step)
+    int threads = 128, iters = 4096, grid = sms * 4;
+    double flops1 = 2.0 * 16 * 8 * 4 * 4.0 * iters * (double)grid * (threads / 32);
+    float ms = 0; long launches = 0;
+    cudaEventRecord(e0);
+    while (ms < sustain_s * 1e3) {
+      for (int k = 0; k < 50; ++k) dmma_loop<<<grid, threads>>>(out, iters);
+      launches += 50;
+      cudaEventRecord(e1); CK(cudaEventSynchronize(e1));
+      cudaEventElapsedTime(&ms, e0, e1);
+    }
+    printf("{\"kernel\":\"dmma_m16n8k4_sustained\",\"seconds\":%.2f,\"launches\":%ld,\"tflops\":%.2f}\n", ms / 1e3, launches, flops1 * launches / ms / 1e9);
   }
   size_t n = (size_t)1 << 28; // 2 GiB per buffer of doubles
   double2 *a, *b; CK(cudaMalloc(&a, n * 8)); CK(cudaMalloc(&b, n * 8));

@@ -1,8 +1,14 @@
-"""Small solves that touch every kernel of the library, for compute-sanitizer
-(memcheck / racecheck / synccheck, one tool per invocation):
+"""Small solves that touch every kernel of the library, for memory checking.
 
-    compute-sanitizer --tool memcheck  python tools/sanitize_run.py
-    compute-sanitizer --tool racecheck python tools/sanitize_run.py
+compute-sanitizer is closed on this GPU pool (runs under it left GPUs needing
+a reset), so the check is the library's own guard-band mode:
+
+    PASD_B200_GUARD=1 python tools/sanitize_run.py
+
+(every device buffer gets 64 KB canary bands of NaN bytes, verified on free;
+the run fails if any band was written, and a stray read of a band poisons the
+result with NaN, which the NaN guard and the parity tests catch).  Under a
+working compute-sanitizer the same script serves memcheck / racecheck.
 
 Covers k_pass2_fused (16x8x8, RP 40 and 56 with ragged bricks), k_pass2_m8
 (8x8x8), k_pass1 (both tile shapes), the Gram kernels, the cluster small
@@ -65,4 +71,26 @@ s.load(T)
 s.run(50)
 s.finalize()
 s.close()
+# SNN baseline kernels and the loopback (nranks = 3) sharded path
+from paper_1712_09999_b200.api import SnnConfig  # noqa: E402
+from paper_1712_09999_b200.sharding import run_loopback  # noqa: E402
+
+Ts = instance((20, 18, 16), 2, 0.05, seed=4)
+pb.snn_recover(Ts, SnnConfig(lambdas=pb.default_lambdas(Ts.shape), maxiter=30), fixed_iters=True)
+Tl = instance((26, 24, 29), 3, 0.05, seed=2)
+run_loopback(Tl, PasdConfig(lambdas=pb.default_lambdas(Tl.shape), ranks=[3, 3, 3], maxiter=60), 3, 60)
+import ctypes as C  # noqa: E402
+
+L = pb.lib()
+L.pasd_b200_guard_report.restype = C.c_int64
+L.pasd_b200_guard_report.argtypes = [C.POINTER(C.c_int64), C.POINTER(C.c_int64)]
+pb.release_cache()
+import gc  # noqa: E402
+
+gc.collect()
+checked, live = C.c_int64(0), C.c_int64(0)
+viol = L.pasd_b200_guard_report(C.byref(checked), C.byref(live))
+print(f"guard bands: mode={'on' if os.environ.get('PASD_B200_GUARD') == '1' else 'off'} buffers checked={checked.value} "
+      f"still live={live.value} violations={viol}", flush=True)
+assert viol == 0, "guard band overwritten"
 print("sanitize_run done", flush=True)
