@@ -121,13 +121,28 @@ class ClockSampler:
 
 
 def cpu_sample_dims(w):
-    """Bounded CPU sample of workload w: the full config when small, else the
-    leading slab (I_1 x I_2 x 50) with the same solver ranks."""
-    if w.size <= 8_000_000:
+    """Bounded CPU sample of workload w: the full config up to 7e7 elements
+    (C1-C4), else the same-shaped tensor scaled to ~6.4e7 elements with the
+    same Tucker and solver ranks (C5: 400^3, R = 50; ~8 s per CPU iteration).
+    Calibrated against a measured full-size C5 run (profiles/r02_cpu_fullsize_c5.json:
+    the 400^3 sample predicts 117 s/iter, the full run took 91 s/iter; a
+    1000x1000x50 slab predicted 216 s/iter)."""
+    if w.size <= 70_000_000:
         return tuple(w.dims), tuple(w.tucker), tuple(w.ranks)
-    d3 = max(w.ranks[2], 50)
-    return (w.dims[0], w.dims[1], d3), (w.tucker[0], w.tucker[1], min(w.tucker[2], d3)), \
-        (w.ranks[0], w.ranks[1], min(w.ranks[2], d3))
+    f = (64_000_000 / w.size) ** (1.0 / len(w.dims))
+    dims = tuple(max(r, int(round(d * f))) for d, r in zip(w.dims, w.ranks))
+    return dims, tuple(min(t, d) for t, d in zip(w.tucker, dims)), tuple(min(r, d) for r, d in zip(w.ranks, dims))
+
+
+def full_size_cpu(w):
+    """The committed full-size CPU measurement of this workload, if any."""
+    path = os.path.join(ROOT, "profiles", "r02_cpu_fullsize_c5.json")
+    if w.name != "c5_1000cube_r50" or not os.path.exists(path):
+        return None
+    with open(path) as f:
+        d = json.load(f)
+    return {"value": d["iter_per_s"], "s_per_iter": d["per_iteration_s"], "threads": d["threads"],
+            "iters": d["iters"], "source": "profiles/r02_cpu_fullsize_c5.json (tools/cpu_fullsize.py on a GPU-box host)"}
 
 
 def cpu_baseline(w, threads: int, iters: int = 3, sample=None):
@@ -161,6 +176,7 @@ def cpu_baseline(w, threads: int, iters: int = 3, sample=None):
         "extrapolated": extrapolated,
         "sample_dims": list(dims),
         "elem_iters_per_s": elem_rate,
+        "full_size_measured": full_size_cpu(w) if extrapolated else None,
         "sample": f"oracle/ (C++ restatement of proj/src/pasd.cpp, OpenBLAS dgesdd/dgemm) on dims {list(dims)} "
                   f"ranks {list(ranks)}, {iters} fixed iterations, per-iteration time = median gap between "
                   f"iterations 2..{iters}; value = sample elem*iters/s / S({w.name}) = {per_iter:.3f} s/iter "
@@ -362,7 +378,7 @@ def main():
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": w.name, "dims": list(w.dims), "ranks": list(w.ranks)},
             "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "extrapolated", "sample_dims",
-                                                 "sample")},
+                                                 "full_size_measured", "sample")},
             "e2e": {"value": cb["value"], "unit": "iter/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
             "elem_iters_per_s": cb["elem_iters_per_s"],
             "all_threads": all_threads,

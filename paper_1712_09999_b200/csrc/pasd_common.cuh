@@ -43,6 +43,7 @@ struct ModeDev {
   int nkc_w;        // kappa chunks of the W pass
   int nib_w;        // i blocks of the W pass
   int nkc_g;        // kappa chunks of the Gram pass
+  int refine_ok;    // A_n complete on this rank (not a slab partial): the SVT may refine from A_n
 };
 
 // Scalars of the device-resident ADMM loop (read by every kernel so that an

@@ -26,6 +26,8 @@
 // two partials when they fit in L2, Pass2Args::nw2).  All reductions are in a
 // fixed order (deterministic).
 #pragma once
+#include <type_traits>
+
 #include <cuda.h>  // CUtensorMap (TMA descriptors, encoded on the host through the driver entry point)
 
 #include "pasd_kernels.cuh"
@@ -34,6 +36,32 @@ namespace pasd {
 
 #ifndef PASD_P2_PAIRBAR
 #define PASD_P2_PAIRBAR 1  // Wt_2 K-half exchange synchronised per warp pair (named barrier)
+#endif
+#ifndef PASD_P2_PROBE
+#define PASD_P2_PROBE 0  // timing probes only (wrong results): 1 = skip the Wt DMMAs, 2 = skip the Z DMMAs,
+                         // 3 = skip both, 4 = skip the elementwise arithmetic (loads and stores stay)
+#endif
+#ifndef PASD_P2_EPF
+#define PASD_P2_EPF 0  // T / Y_n element bricks staged into shared memory with cp.async a step ahead
+#endif
+#ifndef PASD_P2_WS
+#define PASD_P2_WS 1  // warps 0-3 run the Wt_2 products over the full K while warps 4-7 issue the next staging
+#endif
+#ifndef PASD_P2_TIMING
+#define PASD_P2_TIMING 0  // probe build: per-phase clock64() sums of warp 0 (pasd_b200_debug_p2_phases)
+#endif
+#if PASD_P2_TIMING
+__device__ unsigned long long g_p2_phase[12];
+#define P2T(k)                                   \
+  do {                                           \
+    if (tid == 0) {                              \
+      const long long now_ = clock64();          \
+      ph_acc[k] += (unsigned long long)(now_ - ph_t); \
+      ph_t = now_;                               \
+    }                                            \
+  } while (0)
+#else
+#define P2T(k) do {} while (0)
 #endif
 #ifndef PASD_P2_BW
 #define PASD_P2_BW 12  // i1-block band width of the pencil order
@@ -158,6 +186,12 @@ __device__ __forceinline__ int zx(int l1, int l2, int l3) { return l1 + 22 * l2 
 __device__ __forceinline__ int g2x(int l1, int l2, int l3) { return l1 + 20 * l2 + 160 * l3; }
 __device__ __forceinline__ int g3x(int l1, int l2, int l3) { return l1 + 22 * l2 + 180 * l3; }
 __device__ __forceinline__ bool mt_dummy_guard(int w, int MT) { return (w & 3) < MT; }
+// Staged element brick (PASD_P2_EPF): row (l2, l3) holds 16 consecutive i1 as eight
+// 16-byte chunks, chunk c stored at c ^ (l2 & 6), so the elementwise reads
+// (l1 = g (+8), l2 = 2t (+1)) of a half-warp hit 16 distinct bank pairs.
+__device__ __forceinline__ int ex(int l1, int l2, int l3) {
+  return 16 * (l2 + 8 * l3) + 2 * ((l1 >> 1) ^ (l2 & 6)) + (l1 & 1);
+}
 
 // Shared-memory footprint (bytes) of k_pass2_fused<RP, TIO>.
 template <int RP, bool TIO>
@@ -190,7 +224,10 @@ struct P2Layout {
   static constexpr int oG3 = oG2 + (TIO ? 0 : 8 * 160);
   static constexpr int oRed = oG3 + (TIO ? 0 : 8 * 180);
   static constexpr int oBrick = oRed + 64;              // + runtime 1024-byte alignment
-  static constexpr int total = oBrick + (TIO ? 6 * P2_BRICK + 128 : 0);
+  // plain I/O with PASD_P2_EPF: the next step's T, Y_1..3 bricks (4 x 1024, swizzled rows)
+  static constexpr bool EPF =
+      !TIO && PASD_P2_EPF && sizeof(double) * (size_t)(oBrick + 4 * P2_BRICK) <= 227u * 1024u;
+  static constexpr int total = oBrick + (TIO ? 6 * P2_BRICK + 128 : (EPF ? 4 * P2_BRICK : 0));
   static constexpr size_t bytes = sizeof(double) * (size_t)total;
   static_assert((RM - RP) * LD3 <= total - oU1, "M-tile overrun must stay inside shared memory");
   static_assert(128 * RP <= oA3 + RP * LD3, "end-of-pencil scratch must fit in A1s..A3s");
@@ -241,6 +278,13 @@ __device__ __forceinline__ void mbar_wait(uint64_t* mbar, unsigned parity) {
       : "memory");
 }
 
+// Warp-specialised Wt_2 / staging phase: measured at C5 (RP 56) 41.1 -> 38.9 ms per
+// launch; at RP <= 40 (C3) the split Wt_2 partials it gives up were worth more.
+template <int RP, bool TIO>
+__host__ __device__ constexpr bool pass2_ws() {
+  return !TIO && PASD_P2_WS && RP >= 48;
+}
+
 // RP = common padded rank (multiple of 8, >= every R_n); rows r >= R_n of each
 // mode's operands are zero, so padding changes no result.
 template <int RP, bool TIO>
@@ -251,6 +295,7 @@ __global__ void __launch_bounds__(P2_THREADS, 1) k_pass2_fused(const Pass2Args a
   constexpr int KS = RP / 4;   // k-steps of the Z products
   constexpr int NT1 = RP / 8;  // n-tiles of the Wt_1 product
   constexpr int MT = L::RM / 16;
+  constexpr bool WS = pass2_ws<RP, TIO>();  // warp-specialised Wt_2 / staging phase
   extern __shared__ double sm[];
   const ModeDev& m1 = a.m[0];
   const ModeDev& m2 = a.m[1];
@@ -313,6 +358,10 @@ __global__ void __launch_bounds__(P2_THREADS, 1) k_pass2_fused(const Pass2Args a
   double gsq[3] = {0.0, 0.0, 0.0};
   int bad = 0;
   const int64_t S12 = I1 * I2;
+#if PASD_P2_TIMING
+  unsigned long long ph_acc[12] = {};
+  long long ph_t = clock64();
+#endif
   const int ksz = (max(R1, max(R2, R3)) + 3) / 4;  // Z k-steps that touch a nonzero rank row
   const bool al1 = (I1 % 2) == 0;  // 16-byte aligned rows of 16 consecutive i1
 
@@ -362,12 +411,12 @@ __global__ void __launch_bounds__(P2_THREADS, 1) k_pass2_fused(const Pass2Args a
     // Per-thread source/destination bases are fixed along the pencil; a step
     // only advances them by 8 i2.
     const int n3v = (int)imin64(8, I3 - i3o);  // valid i3 of the pencil
-    auto stage_a1 = [&](int64_t i2o, double* A1b) {
-      {  // A_1 (R1, I2, I3 layout): warp w -> columns (l2 = w, l3 = k); lane -> r pair
-        const bool c2ok = i2o + w < I2;
-        const char* gp = reinterpret_cast<const char*>(m1.A + (int64_t)R1 * ((i2o + w) + I2 * i3o));
+    auto stage_a1 = [&](int64_t i2o, double* A1b, int wv, int nwv) {
+      for (int l2w = wv; l2w < 8; l2w += nwv) {  // A_1 (R1, I2, I3 layout): warp -> columns (l2, l3 = k); lane -> r pair
+        const bool c2ok = i2o + l2w < I2;
+        const char* gp = reinterpret_cast<const char*>(m1.A + (int64_t)R1 * ((i2o + l2w) + I2 * i3o));
         const int64_t kst = 8 * (int64_t)R1 * I2;  // bytes to the next l3
-        const unsigned sp = smem_u32(A1b + w * L::LD1);
+        const unsigned sp = smem_u32(A1b + l2w * L::LD1);
         if ((R1 & 1) == 0) {
           if (lane < RP / 2) {
             const int r = 2 * lane;
@@ -398,44 +447,49 @@ __global__ void __launch_bounds__(P2_THREADS, 1) k_pass2_fused(const Pass2Args a
         }
       }
     };
-    auto stage_a3u2 = [&](int64_t i2o) {
+    // u = thread index within the NT issuing threads (NT = 256: the whole CTA,
+    // 128: the staging warps of the warp-specialised Wt_2 phase)
+    auto stage_a3u2 = [&](int64_t i2o, int u, auto NTc) {
+      constexpr int NT = decltype(NTc)::value, RS = NT / 64;
       {  // A_3 (I1, I2, R3 layout): rows (r, l2) of 16 consecutive i1; thread ->
-         // 16-byte chunk c, l2, rows r = r0 + 4k (padding rows stay zero)
-        const int c = tid & 7, l2 = (tid >> 3) & 7, r0 = tid >> 6;
+         // 16-byte chunk c, l2, rows r = r0 + RS k (padding rows stay zero)
+        const int c = u & 7, l2 = (u >> 3) & 7, r0 = u >> 6;
         const bool ok2 = i2o + l2 < I2;
         const int nb = ok2 ? nbc1 : 0;
         const char* gp = reinterpret_cast<const char*>(nb ? m3.A + i1o + 2 * c + I1 * (i2o + l2) + S12 * (int64_t)r0 : m3.A);
-        const int64_t gst = nb ? 32 * S12 : 0;  // 4 rows r
+        const int64_t gst = nb ? 8 * RS * S12 : 0;  // RS rows r
         const unsigned sp = smem_u32(A3s + r0 * L::LD3 + 16 * l2 + 2 * c);
         if (al1) {  // even I1: every 16-byte chunk is wholly inside or outside
 #pragma unroll
-          for (int k = 0; k < RP / 4; ++k) {
-            if (r0 + 4 * k < R3) cp16z(sp + 32 * k * L::LD3, gp, nb != 0);
+          for (int k = 0; k < (RP + RS - 1) / RS; ++k) {
+            if (r0 + RS * k < R3) cp16z(sp + 8 * RS * k * L::LD3, gp, nb != 0);
             gp += gst;
           }
         } else {
           const int n0 = nb >= 8 ? 8 : 0, n1 = nb >= 16 ? 8 : 0;
 #pragma unroll
-          for (int k = 0; k < RP / 4; ++k) {
-            if (r0 + 4 * k < R3) {
-              cp8s(sp + 32 * k * L::LD3, n0 ? (const void*)gp : (const void*)m3.A, n0);
-              cp8s(sp + 32 * k * L::LD3 + 8, n1 ? (const void*)(gp + 8) : (const void*)m3.A, n1);
+          for (int k = 0; k < (RP + RS - 1) / RS; ++k) {
+            if (r0 + RS * k < R3) {
+              cp8s(sp + 8 * RS * k * L::LD3, n0 ? (const void*)gp : (const void*)m3.A, n0);
+              cp8s(sp + 8 * RS * k * L::LD3 + 8, n1 ? (const void*)(gp + 8) : (const void*)m3.A, n1);
             }
             gp += gst;
           }
         }
       }
-      {  // UM_2 rows of the step: thread -> (l2, r = tid / 8 + 32 k)
-        const int l2 = tid & 7;
+      {  // UM_2 rows of the step: thread -> (l2, r = u / 8 + (NT / 8) k)
+        const int l2 = u & 7;
         const bool v = i2o + l2 < I2;
         const double* src = m2.UM + m2.ioff + i2o + l2;
 #pragma unroll
-        for (int k = 0; k < (RP + 31) / 32; ++k) {
-          const int r = (tid >> 3) + 32 * k;
+        for (int k = 0; k < (RP + NT / 8 - 1) / (NT / 8); ++k) {
+          const int r = (u >> 3) + (NT / 8) * k;
           if (r < R2) cp8z(smem_u32(U2s + l2 * L::LDU + r), v ? (const void*)(src + m2.Ifull * r) : (const void*)m2.UM, v);
         }
       }
     };
+    using All = std::integral_constant<int, P2_THREADS>;
+    using Half = std::integral_constant<int, P2_THREADS / 2>;
     // this thread's 4 elements: (i1 = g, g+8) x (i2 = 2t, 2t+1) at i3 = w
     double tv[4], yv[3][4];
     bool inb[4];
@@ -451,23 +505,53 @@ __global__ void __launch_bounds__(P2_THREADS, 1) k_pass2_fused(const Pass2Args a
         for (int n = 0; n < 3; ++n) yv[n][q] = inb[q] ? a.Y[n][off[q]] : 0.0;
       }
     };
-    stage_a1(i2b, A1s);
-    stage_a3u2(i2b);
+    // PASD_P2_EPF: this thread's 8 copies of a step's T, Y_1..3 brick (stream ts,
+    // row (l2, l3), 16-byte chunk c); issued right after the previous step's
+    // elementwise phase, so they land during its Wt products and the next Z.
+    double* El = sm + L::oBrick;
+    auto stage_elems = [&](int64_t i2o, int u, auto NTc) {
+      constexpr int NT = decltype(NTc)::value;
+      const int c = u & 7;
+      const bool cok = 2 * c < nv1;
+#pragma unroll
+      for (int k = 0; k < 4 * P2_BRICK / 2 / NT; ++k) {
+        const int idx = u + NT * k;
+        const int row = (idx >> 3) & 63, ts = idx >> 9;
+        const int l2 = row & 7, l3 = row >> 3;
+        const bool ok = cok && i2o + l2 < I2 && i3o + l3 < I3;
+        const double* base = ts == 0 ? T : a.Y[ts - 1];
+        const double* src = ok ? base + i1o + 2 * c + I1 * (i2o + l2) + S12 * (i3o + l3) : base;
+        const unsigned dst = smem_u32(El + ts * P2_BRICK + 16 * row + 2 * (c ^ (l2 & 6)));
+        if (al1) {
+          cp16z(dst, src, ok);
+        } else {
+          const bool ok1 = ok && 2 * c + 1 < nv1;
+          cp8z(dst, src, ok);
+          cp8z(dst + 8, ok1 ? (const void*)(src + 1) : (const void*)base, ok1);
+        }
+      }
+    };
+    stage_a1(i2b, A1s, w, 8);
+    stage_a3u2(i2b, tid, All{});
+    if (L::EPF) stage_elems(i2b, tid, All{});
 
     for (int64_t i2o = i2b; i2o < i2e; i2o += P2_B2) {
       const bool more = i2o + P2_B2 < i2e;
       const double* A1c = A1s;
-      if (!TIO) load_elems(i2o);  // this step's T, Y: in flight while the staging lands and Z runs
-                                  // (measured 2 ms faster at C5 than prefetching them a step ahead)
+      P2T(0);  // 0: pencil setup / loop top
+      if (!TIO && !L::EPF) load_elems(i2o);  // this step's T, Y: in flight while the staging lands and Z runs
+                                             // (measured 2 ms faster at C5 than prefetching them a step ahead)
       cp_async_wait_all();
+      P2T(1);  // 1: element-load issue + staging wait
       __syncthreads();  // step data staged; previous step's smem consumers done
+      P2T(2);  // 2: barrier A
       // ---- Z products (6 independent accumulator chains) ----
       double z1[4] = {0, 0, 0, 0}, z2[4] = {0, 0, 0, 0}, z3[4] = {0, 0, 0, 0};
       {
         double y1[4] = {0, 0, 0, 0}, y2[4] = {0, 0, 0, 0}, y3[4] = {0, 0, 0, 0};
 #pragma unroll
         for (int ks = 0; ks < KS; ++ks) {
-          if (ks >= ksz) break;  // k-steps past max R_n only multiply zero padding
+          if (ks >= ksz || PASD_P2_PROBE == 2 || PASD_P2_PROBE == 3) break;  // k-steps past max R_n only multiply zero padding
           const int k = 4 * ks + t;
           double(&c1)[4] = (ks & 1) ? y1 : z1;
           double(&c2)[4] = (ks & 1) ? y2 : z2;
@@ -487,17 +571,43 @@ __global__ void __launch_bounds__(P2_THREADS, 1) k_pass2_fused(const Pass2Args a
       Z3s[zx(g, w, 2 * t + 1)] = z3[1];
       Z3s[zx(g + 8, w, 2 * t)] = z3[2];
       Z3s[zx(g + 8, w, 2 * t + 1)] = z3[3];
+      P2T(3);  // 3: Z products
       __syncthreads();
+      P2T(4);  // 4: barrier B
       // ---- elementwise (reference op order, no FMA contraction) ----
       double g1v[4];
       if constexpr (!TIO) {
         int64_t offc[4];
         bool inc[4];
+        if (L::EPF) {  // this step's T, Y from the staged bricks
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const int l1 = g + 8 * (q >> 1), l2 = 2 * t + (q & 1);
+            const int64_t i1 = i1o + l1, i2 = i2o + l2, i3 = i3o + w;
+            inb[q] = i1 < I1 && i2 < I2 && i3 < I3;
+            off[q] = i1 + I1 * i2 + S12 * i3;
+            const int e = ex(l1, l2, w);
+            tv[q] = El[e];
+#pragma unroll
+            for (int n = 0; n < 3; ++n) yv[n][q] = El[(1 + n) * P2_BRICK + e];
+          }
+        }
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
           const int l1 = g + 8 * (q >> 1), l2 = 2 * t + (q & 1);
           const double zz[3] = {z1[q], z2[q], Z3s[zx(l1, l2, w)]};
           const double tt = tv[q];
+          if (PASD_P2_PROBE == 4) {  // timing probe: loads / stores / exchange only
+            if (inb[q]) {
+              for (int n = 0; n < 3; ++n) a.Y[n][off[q]] = yv[n][q] + zz[n];
+              Enew[off[q]] = tt;
+              a.D[off[q]] = tt;
+            }
+            g1v[q] = tt;
+            G2s[g2x(l1, l2, w)] = yv[1][q];
+            G3s[g3x(l1, l2, w)] = yv[2][q];
+            continue;
+          }
           double zt[3], h = 0.0;
 #pragma unroll
           for (int n = 0; n < 3; ++n) {
@@ -571,7 +681,10 @@ __global__ void __launch_bounds__(P2_THREADS, 1) k_pass2_fused(const Pass2Args a
         }
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // bricks -> TMA (async proxy)
       }
+      P2T(5);  // 5: elementwise (incl. waiting for this step's element loads)
       __syncthreads();  // G exchange / bricks complete
+      P2T(6);  // 6: barrier C
+      if (L::EPF && !WS && more) stage_elems(i2o + P2_B2, tid, All{});  // the element bricks are consumed: next step's
       if (TIO && tid == 0) {  // E, Y_1..3, D of this brick: TMA tensor stores
         const int c0 = (int)i1o, c1 = (int)i2o, c2 = (int)i3o;
         tma_store3(ctl->ecur ? &tm.e0 : &tm.e1, brk, c0, c1, c2);
@@ -590,9 +703,9 @@ __global__ void __launch_bounds__(P2_THREADS, 1) k_pass2_fused(const Pass2Args a
         }
       };
       const int mt = w & 3, kh = w >> 2;  // m-tile and K-half of the Wt_2 / Wt_3 products
-      wt1();
+      if (PASD_P2_PROBE != 1 && PASD_P2_PROBE != 3) wt1();
       // ---- Wt_3^T (m-tile mt, K-half kh), K = (i1, i2) ----
-      if (mt < MT) {
+      if (mt < MT && PASD_P2_PROBE != 1 && PASD_P2_PROBE != 3) {
         double acc[3][4] = {};
         const double* rowa = A3s + (16 * mt + g) * L::LD3 + 64 * kh;
         const double* rowb = rowa + 8 * L::LD3;
@@ -616,7 +729,7 @@ __global__ void __launch_bounds__(P2_THREADS, 1) k_pass2_fused(const Pass2Args a
       // prefetch this step's Wt_2 partial rows (read-modify-write below)
       double w2old[4] = {0, 0, 0, 0};
       double* W2k = W2c + (w2s ? (int64_t)kh * I2 * R2 : 0);
-      if ((w2s || kh == 0) && mt < MT) {
+      if (WS ? (w < MT) : ((w2s || kh == 0) && mt < MT)) {
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
           const int r = 16 * mt + g + 8 * (q >> 1);
@@ -624,14 +737,47 @@ __global__ void __launch_bounds__(P2_THREADS, 1) k_pass2_fused(const Pass2Args a
           if (r < R2 && i2 < I2) w2old[q] = W2k[i2 * R2 + r];
         }
       }
+      P2T(7);  // 7: Wt_1 + Wt_3 products, Wt_2 partial prefetch
       __syncthreads();  // A1s / A3s / U2s no longer needed this step
-      if (more) {
-        stage_a1(i2o + P2_B2, A1s);
-        stage_a3u2(i2o + P2_B2);
+      P2T(8);  // 8: barrier D
+      if constexpr (WS) {
+        // Warp-specialised: warps 4-7 issue the next step's staging (LSU-bound,
+        // ~1.8k cycles) while warps 0-3 run the Wt_2 products over the full K
+        // (no K-half exchange); the next step's top barrier joins them.
+        if (w >= 4) {
+          if (more) {
+            stage_a1(i2o + P2_B2, A1s, w - 4, 4);
+            stage_a3u2(i2o + P2_B2, tid - P2_THREADS / 2, Half{});
+            if (L::EPF) stage_elems(i2o + P2_B2, tid - P2_THREADS / 2, Half{});  // next step's T, Y
+          }
+        } else if (w < MT && PASD_P2_PROBE != 1 && PASD_P2_PROBE != 3) {
+          double acc[4][4] = {};
+          const double* rowa = A2s + (16 * w + g) * L::LD2;
+          const double* rowb = rowa + 8 * L::LD2;
+#pragma unroll
+          for (int ks = 0; ks < 32; ++ks) {
+            const int k = 4 * ks + t;
+            dmma(acc[ks & 3], rowa[4 * ks + t], rowb[4 * ks + t], G2s[g2x(k & 15, g, k >> 4)]);
+          }
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const int r = 16 * w + g + 8 * (q >> 1);
+            const int64_t i2 = i2o + 2 * t + (q & 1);
+            const double v = (acc[0][q] + acc[1][q]) + (acc[2][q] + acc[3][q]);
+            if (r < R2 && i2 < I2) W2c[i2 * R2 + r] = w2old[q] + v;
+          }
+        }
+        P2T(10);
+        continue;
       }
+      if (more) {
+        stage_a1(i2o + P2_B2, A1s, w, 8);
+        stage_a3u2(i2o + P2_B2, tid, All{});
+      }
+      P2T(9);  // 9: staging issue
       // ---- W-b: Wt_2^T (m-tile mt, K-half kh), K = (i1, i3) ----
       double acc2[4] = {0, 0, 0, 0};
-      if (mt < MT) {
+      if (mt < MT && PASD_P2_PROBE != 1 && PASD_P2_PROBE != 3) {
         double acc[3][4] = {};
         const double* rowa = A2s + (16 * mt + g) * L::LD2 + 64 * kh;
         const double* rowb = rowa + 8 * L::LD2;
@@ -676,6 +822,7 @@ __global__ void __launch_bounds__(P2_THREADS, 1) k_pass2_fused(const Pass2Args a
           if (r < R2 && i2 < I2) W2c[i2 * R2 + r] = w2old[q] + (acc2[q] + Z3s[(mt * 32 + lane) * 4 + q]);
         }
       }
+      P2T(10);  // 10: Wt_2 products + K-half exchange + partial update
     }
     // combine the two K-halves of Wt_3 through shared memory
     __syncthreads();
@@ -718,6 +865,11 @@ __global__ void __launch_bounds__(P2_THREADS, 1) k_pass2_fused(const Pass2Args a
     // (A1s itself is rewritten, padding included, by every step's staging)
     for (int idx = tid; idx < (RP - R2) * 128; idx += P2_THREADS) A2s[(R2 + idx / 128) * L::LD2 + (idx & 127)] = 0.0;
   }
+#if PASD_P2_TIMING
+  P2T(11);  // 11: pencil ends (reductions, restores)
+  if (tid == 0)
+    for (int k = 0; k < 12; ++k) atomicAdd(&g_p2_phase[k], ph_acc[k]);
+#endif
   if (TIO && tid == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // element stores done
   // ---- per-CTA residual / NaN / ||G||^2 partials ----
   for (int n = 0; n < 3; ++n) {

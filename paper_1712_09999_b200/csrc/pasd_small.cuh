@@ -405,6 +405,105 @@ __device__ void cluster_sum_mat(const double* src, double* dst, int R, int R2, i
 }
 
 // ---------------------------------------------------------------------------
+// Refinement of numerically unresolved small singular values of A (R x J).
+// sigma_i^2 from eig(A A^T) carry an absolute error ~eps sigma_1^2, so a
+// sigma_i below ~1e-5 sigma_1 is not resolved by the Gram; when the SVT
+// threshold is that small too (late iterations: tau = lambda/mu with mu -> 1e10)
+// the keep test sigma > tau (linops.cpp:85) and the factor (sigma - tau)/sigma
+// would act on rounding noise where dgesdd on A itself resolves them.  The last
+// k eigenvectors P_s (R x k) are refined from A: B = P_s^T A (k x J) has rows
+// sigma_i v_i^T + O(eps sigma_1), so eig(B B^T) (k x k, Jacobi) gives them to
+// relative accuracy ~eps sigma_1 / sigma_i.  Every CTA of the cluster forms the
+// partial B B^T of its column block, the partials are summed through DSMEM in
+// rank order (bit-identical on every CTA) and each CTA runs the same k x k
+// Jacobi.  On entry ws.V / ws.lam hold the first pass (descending); on exit the
+// refined ones.  Uses ws.Q, ws.Z, ws.T64.
+__device__ void svt_refine_small(SmallWs& ws, const ModeDev& m, int R, int k, int crank) {
+  const int tid = threadIdx.x, nt = blockDim.x, ld = ws.ld, r0 = R - k;
+  // P (first pass) -> Q; first-pass eigenvalues of the kept-large part -> T64 row 63
+  for (int idx = tid; idx < R * R; idx += nt) ws.Q[(idx / R) * ld + idx % R] = ws.V[(idx / R) * ld + idx % R];
+  __syncthreads();
+  double* lam_saved = ws.T64 + 63 * ld;
+  for (int j = tid; j < R; j += nt) lam_saved[j] = ws.lam[j];
+  // this CTA's columns of A
+  const int64_t chunk = (m.J + kSmallCluster - 1) / kSmallCluster;
+  const int64_t c_lo = imin64(m.J, chunk * crank), c_hi = imin64(m.J, c_lo + chunk);
+  constexpr int KE = (PASD_MAX_RANK * (PASD_MAX_RANK + 1) / 2 + kSmallThreads - 1) / kSmallThreads;
+  const int ne = k * (k + 1) / 2;
+  double acc[KE];
+  int ea[KE], eb[KE];
+#pragma unroll
+  for (int e = 0; e < KE; ++e) {
+    acc[e] = 0.0;
+    int lin = tid + e * nt, a = 0;
+    if (lin < ne) {
+      while (lin >= k - a) {
+        lin -= k - a;
+        ++a;
+      }
+      ea[e] = a;
+      eb[e] = a + lin;
+    } else {
+      ea[e] = -1;
+      eb[e] = 0;
+    }
+  }
+  // 31 columns per chunk: A columns in T64 rows 0..30, their B = P_s^T a in rows 31..61
+  for (int64_t c0 = c_lo; c0 < c_hi; c0 += 31) {
+    const int nc = (int)imin64(31, c_hi - c0);
+    __syncthreads();
+    for (int idx = tid; idx < 31 * R; idx += nt) {
+      const int c = idx % 31, r = idx / 31;
+      ws.T64[c * ld + r] = c < nc ? m.A[a_offset(m, c0 + c, r)] : 0.0;
+    }
+    __syncthreads();
+    for (int idx = tid; idx < 31 * k; idx += nt) {
+      const int c = idx / k, a = idx - c * k;
+      double b = 0.0;
+      for (int r = 0; r < R; ++r) b = fma(ws.Q[r * ld + r0 + a], ws.T64[c * ld + r], b);
+      ws.T64[(31 + c) * ld + a] = b;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int e = 0; e < KE; ++e) {
+      if (ea[e] < 0) continue;
+      for (int c = 0; c < nc; ++c) acc[e] = fma(ws.T64[(31 + c) * ld + ea[e]], ws.T64[(31 + c) * ld + eb[e]], acc[e]);
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int e = 0; e < KE; ++e)
+    if (ea[e] >= 0) {
+      ws.Z[ea[e] * ld + eb[e]] = acc[e];
+      ws.Z[eb[e] * ld + ea[e]] = acc[e];
+    }
+  cluster_sum_mat(ws.Z, ws.S, k, k, ld);  // S = B B^T (k x k), identical on every CTA
+  __syncthreads();
+  cta_jacobi_eig(ws, k, 2);  // ws.V (k x k), ws.lam[0..k) descending
+  // V_final = [P_large, P_s V_s]; lam_final = [lam_large, lam_s]
+  for (int idx = tid; idx < R * R; idx += nt) {
+    const int r = idx / R, c = idx % R;
+    double v;
+    if (c < r0) {
+      v = ws.Q[r * ld + c];
+    } else {
+      v = 0.0;
+      for (int a = 0; a < k; ++a) v = fma(ws.Q[r * ld + r0 + a], ws.V[a * ld + (c - r0)], v);
+    }
+    ws.Z[r * ld + c] = v;
+  }
+  __syncthreads();
+  for (int j = tid; j < R; j += nt) {
+    const double l = j < r0 ? lam_saved[j] : ws.lam[j - r0];
+    lam_saved[j] = l;
+  }
+  __syncthreads();
+  for (int idx = tid; idx < R * R; idx += nt) ws.V[(idx / R) * ld + idx % R] = ws.Z[(idx / R) * ld + idx % R];
+  for (int j = tid; j < R; j += nt) ws.lam[j] = lam_saved[j];
+  __syncthreads();
+}
+
+// ---------------------------------------------------------------------------
 // SVT factor: M_n = P diag(f) P^T, f_i = (sigma_i - tau)/sigma_i for sigma_i > tau.
 // SVT of mode n from its reduced Gram (every CTA of the mode's cluster; rank 0
 // publishes sig, M, P and the keep / vnorm2 / nuclear scalars, each CTA forms
@@ -422,6 +521,20 @@ __device__ void svt_mode(const ModeDev& m, int n, Ctl* ctl, double* smem, int cr
   cta_jacobi_eig(ws, R, 1);
   cta_warm_finish(ws, R);
   const double tau = __ddiv_rn(m.lambda, ctl->mu);  // lambda / mu (pasd.cpp:77)
+  {
+    __shared__ int ksmall;
+    if (tid == 0) {
+      // unresolved: lambda_i < 1e-10 lambda_1 (sigma_i < 1e-5 sigma_1), and only
+      // when the threshold is down there too (tau < 1e-5 sigma_1)
+      const double l1 = ws.lam[0];
+      int k = 0;
+      if (m.refine_ok && l1 > 0.0 && tau * tau < 1e-10 * l1)
+        while (k < R - 1 && ws.lam[R - 1 - k] < 1e-10 * l1) ++k;
+      ksmall = k;
+    }
+    __syncthreads();
+    if (ksmall > 0) svt_refine_small(ws, m, R, ksmall, crank);
+  }
   if (tid == 0) {
     int keep = 0;
     double vn2 = 0.0, nuc = 0.0;

@@ -783,6 +783,8 @@ pasd_solver* create_solver(const pasd_options* o, const pasd_shard* shard) {
     m.Wpart = s->alloc<double>((size_t)m.nkc_w * IR);
     m.gpart = s->alloc<double>((size_t)m.nkc_w * m.nib_w);
     m.nkc_g = (int)std::max<int64_t>(1, std::min<int64_t>((m.J + GM_KC - 1) / GM_KC, 148));
+    // slab partials of A_1, A_2 (sharded) cannot feed the SVT's small-value refinement
+    m.refine_ok = !(s->sharded && n < s->N - 1);
     m.Gpart = s->alloc<double>((size_t)m.nkc_g * RR);
     m.Gram = s->alloc<double>(RR);
     m.sig = s->alloc<double>(m.R);
@@ -918,7 +920,8 @@ pasd_solver* create_solver(const pasd_options* o, const pasd_shard* shard) {
     // (C3 38 MB, C4 18 MB: one barrier per step fewer, -2..5% pass 2); at C5 the
     // 118 MB they would take thrash L2 (+1 ms), so one per CTA there.
     const double w2_split_bytes = 2.0 * s->p2_grid * (double)s->dims[1] * s->modes[1].R * sizeof(double);
-    a.nw2 = (!s->use_m8 && !s->p2_tio && w2_split_bytes <= 48e6) ? 2 * s->p2_grid : s->p2_grid;
+    const bool ws = !s->use_m8 && !s->p2_tio && PASD_P2_WS && s->p2_rp >= 48;  // pass2_ws<RP, false>()
+    a.nw2 = (!s->use_m8 && !s->p2_tio && !ws && w2_split_bytes <= 48e6) ? 2 * s->p2_grid : s->p2_grid;
     a.W2part = s->alloc<double>((size_t)a.nw2 * s->dims[1] * s->modes[1].R);
     a.gpart = s->alloc<double>((size_t)s->p2_grid * 3);
     s->p2_resid = s->alloc<double>((size_t)s->p2_grid * PASD_MAX_ORDER);
@@ -1350,6 +1353,18 @@ int pasd_b200_loopback_create(int32_t nranks, void** out, char* errbuf, size_t e
 
 void pasd_b200_loopback_destroy(void* group) { delete reinterpret_cast<LoopbackGroup*>(group); }
 
+#if PASD_P2_TIMING
+// probe builds only: per-phase cycle sums of k_pass2_fused's warp 0 over all CTAs since the last call
+extern "C" int pasd_b200_debug_p2_phases(double* out12) {
+  unsigned long long h[12];
+  if (cudaMemcpyFromSymbol(h, g_p2_phase, sizeof(h)) != cudaSuccess) return 5;
+  const unsigned long long z[12] = {};
+  cudaMemcpyToSymbol(g_p2_phase, z, sizeof(z));
+  for (int k = 0; k < 12; ++k) out12[k] = (double)h[k];
+  return 0;
+}
+#endif
+
 int64_t pasd_b200_guard_report(int64_t* checked, int64_t* live) {
   GuardState& g = guard_state();
   std::lock_guard<std::mutex> lk(g.mu);
@@ -1672,6 +1687,7 @@ void device_svt(const double* m_h, int64_t rows, int64_t cols, double tau, doubl
   m.Qp = t.alloc<double>(R * R);
   m.sig = t.alloc<double>(R);
   m.nkc_g = (int)std::max<int64_t>(1, std::min<int64_t>((m.J + GR_KC - 1) / GR_KC, 296));
+  m.refine_ok = 1;
   m.Gpart = t.alloc<double>((size_t)m.nkc_g * R * R);
   std::vector<double> eye(R * R, 0.0);
   for (int i = 0; i < R; ++i) eye[i + R * i] = 1.0;

@@ -21,6 +21,30 @@ def test_svt_matches_oracle(gpu, oracle_mod):
     np.testing.assert_allclose(svt(np.diag([3.0, 1.0]), 2.0)[0], np.diag([1.0, 0.0]), atol=1e-15)
 
 
+@pytest.mark.parametrize("r,c", [(8, 2000), (12, 5000), (50, 3000)])
+def test_svt_ill_conditioned_tiny_threshold(gpu, oracle_mod, r, c):
+    """The late-iteration regime (tau = lambda/mu with mu -> mu_max): singular
+    values spread over 1 .. 1e-10 sigma_1 and tau = 1e-9 sigma_1.  eig(A A^T)
+    alone cannot resolve sigma_i < ~1e-8 sigma_1 (absolute error eps sigma_1^2
+    in sigma^2); the device SVT refines them from A (svt_refine_small) and must
+    keep exactly the oracle's set sigma > tau (linops.cpp:84-86) and match its
+    result far below the smallest kept contribution sigma - tau."""
+    from paper_1712_09999_b200.solver import svt
+
+    rng = np.random.default_rng(r)
+    qu, _ = np.linalg.qr(rng.standard_normal((r, r)))
+    qv, _ = np.linalg.qr(rng.standard_normal((c, r)))
+    sig = np.logspace(0, -10, r)  # 1 ... 1e-10
+    sig[-2] = 5e-9  # just above tau, the hardest kept value
+    m = (qu * sig) @ qv.T
+    tau = 1e-9
+    vo = oracle_mod.svt(m, tau)
+    vg, kept = svt(m, tau)
+    assert kept == int((sig > tau).sum())
+    # rounding level of an R x J product (the kept sigma - tau >= 4e-9 is far above it)
+    assert np.linalg.norm(vg - vo) <= 5e-12 * np.linalg.norm(vo), np.linalg.norm(vg - vo) / np.linalg.norm(vo)
+
+
 def test_procrustes_full_rank_matches_oracle(gpu, oracle_mod):
     from paper_1712_09999_b200.solver import procrustes
 

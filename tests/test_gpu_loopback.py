@@ -65,12 +65,16 @@ def test_loopback_convergence_matches_unsharded_and_oracle(gpu, oracle_mod, monk
     ro = oracle_mod.pasd_recover(T, cfg)
     it, conv, parts, slabs = run_loopback(T, cfg, nranks, cfg.maxiter, fixed_iters=False)
     assert conv and r0.converged and ro.converged
-    assert abs(it - r0.iters) <= 1 and abs(it - ro.iters) <= 2, (it, r0.iters, ro.iters)
+    # against the unsharded GPU solve: the same path up to the partial sums' order
+    assert abs(it - r0.iters) <= 1, (it, r0.iters)
     x = gather(parts, slabs, T.shape, "x")
     e = gather(parts, slabs, T.shape, "e")
     assert rel(x, r0.x) <= 1e-7, rel(x, r0.x)
     assert rel(e, r0.e) <= 1e-7, rel(e, r0.e)
     assert np.array_equal(e != 0, r0.e != 0)
+    # against the oracle: a rank-deficient case (R = r = 2) whose iteration count
+    # the reference's own builds spread over several iterations
+    # (profiles/r02_parity_floor.json, s1/s2): the recovery quality
     assert rel(x, L0) <= max(2 * rel(ro.x, L0), 1e-5)
     # replicated scalars agree on every rank (objective, certificate)
     objs = {p.objective for p in parts}
