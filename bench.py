@@ -41,6 +41,8 @@ def parse_args():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default=os.environ.get("PASD_BENCH_CONFIG", "c5"))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--dtype", default="f64", choices=["f64", "f32"],
+                    help="f32: the optional fp32 mode (float32 element storage, fp64 arithmetic)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--profile-iters", type=int, default=3)
@@ -194,7 +196,7 @@ def generate_input(w):
     return T
 
 
-def e2e_recover(w, T_dev, steps: int):
+def e2e_recover(w, T_dev, steps: int, fp32: bool = False):
     """Whole-solve throughput through the C-ABI drop-in with host buffers."""
     import torch
     from paper_1712_09999_b200 import _abi, solver as S
@@ -206,8 +208,8 @@ def e2e_recover(w, T_dev, steps: int):
     xh = torch.empty(total, dtype=torch.float64, pin_memory=True)
     eh = torch.empty(total, dtype=torch.float64, pin_memory=True)
     cfg = PasdConfig(lambdas=w.lambdas(), ranks=list(w.ranks), eps=w.eps, maxiter=steps)
-    opt, keep = build_options(list(w.dims), cfg, flags=_abi.PASD_FLAG_FIXED_ITERS | _abi.PASD_FLAG_REUSE_SOLVER,
-                              poll_every=steps)
+    flags = _abi.PASD_FLAG_FIXED_ITERS | _abi.PASD_FLAG_REUSE_SOLVER | (_abi.PASD_FLAG_FP32 if fp32 else 0)
+    opt, keep = build_options(list(w.dims), cfg, flags=flags, poll_every=steps)
     out = _abi.PasdOutputs()
     out.x = C.cast(C.c_void_p(xh.data_ptr()), _abi.c_double_p)
     out.e = C.cast(C.c_void_p(eh.data_ptr()), _abi.c_double_p)
@@ -414,7 +416,8 @@ def main():
     steady_start = max(steady_after, W + K + args.profile_iters) if steady_after else 0
     cfg = PasdConfig(lambdas=w.lambdas(), ranks=list(w.ranks), eps=w.eps,
                      maxiter=max(W + K + args.profile_iters + 1, steady_start + 13))
-    sol = pb.Solver(w.dims, cfg, fixed_iters=True, poll_every=K, shard=shard)
+    f32 = args.dtype == "f32"
+    sol = pb.Solver(w.dims, cfg, fixed_iters=True, poll_every=K, shard=shard, fp32=f32)
     sol.load(T_loc.data_ptr(), t_is_device=True)
     sol.run(W)
     stream = torch.cuda.ExternalStream(sol.stream)
@@ -469,7 +472,8 @@ def main():
     S = w.size
     N = len(w.dims)
     RJ = sum(r * (S // d) for r, d in zip(w.ranks, w.dims))
-    B_iter = 8.0 * ((3 * N + 4) * S + 2 * RJ) / world
+    es = 4.0 if f32 else 8.0  # element-tensor bytes (fp32 mode: float32 storage)
+    B_iter = (es * (3 * N + 4) * S + 8.0 * 2 * RJ) / world
     F_iter = 6.0 * S * sum(w.ranks) / world
     t_roof = max(B_iter / (peaks["hbm_gbs"] * 1e9), F_iter / (peaks["fp64_tflops"] * 1e12))
     iteration_roofline = {"B_iter_per_gpu": B_iter, "F_iter_per_gpu": F_iter, "t_roof_ms": t_roof * 1e3,
@@ -477,7 +481,8 @@ def main():
     line = {
         "metric": "PASD ADMM iters/s", "value": round(value, 4), "unit": "iter/s", "n_gpus": world,
         "steps": K, "warmup": W, "ms_per_step": round(ms / K, 4), "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "scaling": "strong", "vs_baseline": None, "dtype": "f32-storage/f64-arith" if f32 else "f64",
+        "data": "synthetic",
         "config": {"workload": w.name, "dims": list(w.dims), "ranks": list(w.ranks), "rho": w.rho,
                    "noise": list(w.noise), "iters_fixed": True,
                    "input": "reference generator (synth.cpp:71-121, rng.hpp streams, seed 0) on the device", "l2": "inputs larger than L2 (T, E x2, D, Y x3: 7 x 8 GB resident)"
@@ -494,7 +499,7 @@ def main():
     torch.cuda.empty_cache()
     if not args.no_e2e and shard is None:
         Tg = generate_input(w)
-        line["e2e"] = e2e_recover(w, Tg, K)
+        line["e2e"] = e2e_recover(w, Tg, K, fp32=f32)
         del Tg
         torch.cuda.empty_cache()
     elif not args.no_e2e:

@@ -66,7 +66,15 @@ enum {
   /* Sharded solvers: after every pasd_b200_solver_run, all-reduce a 64-bit
    * hash of the replicated U_n and M_n and fail (PASD_ERR_NUMERICAL) if any
    * rank differs (SURVEY 8(e) debug check; also env PASD_CHECK_REPLICAS). */
-  PASD_FLAG_CHECK_REPLICAS = 1u << 3
+  PASD_FLAG_CHECK_REPLICAS = 1u << 3,
+  /* fp32 mode (BASELINE north_star's optional mode; no reference analogue):
+   * the element tensors T, E, D = T - E and Y_n live in HBM as float32 (half
+   * the footprint and stream bytes); every contraction and elementwise step
+   * still computes in fp64 registers (DMMA) and rounds to float32 on store;
+   * U_n, M_n, A_n and the small solves stay fp64.  Inputs and outputs at this
+   * boundary stay float64.  Order-3 tensors.  Expected agreement with the
+   * fp64 reference: L, E to ~1e-4 relative (north_star's fp32 bar). */
+  PASD_FLAG_FP32 = 1u << 4
 };
 
 /* Mirror of tenrec::PasdConfig (pasd.hpp:8-27) plus placement. */
@@ -201,6 +209,7 @@ int pasd_b200_solver_finalize(pasd_solver* s, pasd_outputs* out, char* errbuf, s
 int pasd_b200_solver_set_state(pasd_solver* s, const double* e, const double* const* y, const double* const* u,
                                const double* const* v, double mu, int32_t iter, char* errbuf, size_t errlen);
 /* Device pointers of the local slab of E and of Y_n (diagnostics / zero-copy). */
+/* Device pointer of the current E (float64; float32 storage in the fp32 mode). */
 const double* pasd_b200_solver_device_e(const pasd_solver* s);
 /* The CUDA stream (cudaStream_t) the solver launches on. */
 void* pasd_b200_solver_stream(const pasd_solver* s);

@@ -20,6 +20,7 @@ PASD_FLAG_NO_CERTIFICATE = 1 << 0
 PASD_FLAG_FIXED_ITERS = 1 << 1
 PASD_FLAG_REUSE_SOLVER = 1 << 2
 PASD_FLAG_CHECK_REPLICAS = 1 << 3
+PASD_FLAG_FP32 = 1 << 4
 
 PASD_KERNEL_CLASSES = ("polar", "contract_A", "gram", "svt", "update", "finish", "contract_W")
 

@@ -54,11 +54,23 @@ __device__ __forceinline__ double g_elem(double t, double e, double y, double in
 // D = T - E: the tensor part of every G_n, kept resident so pass 1 reads two
 // tensors per mode instead of three (bit-identical: it is the same rounded
 // difference g_elem forms).
-__global__ void k_tsub(double* __restrict__ D, const double* __restrict__ T, const double* E0, const double* E1,
-                       int64_t S, const Ctl* ctl) {
-  const double* __restrict__ E = ctl->ecur ? E1 : E0;
+// EL: storage type of the element tensors (float in the fp32 mode).
+template <class EL>
+__global__ void k_tsub(EL* __restrict__ D, const EL* __restrict__ T, const EL* E0, const EL* E1, int64_t S,
+                       const Ctl* ctl) {
+  const EL* __restrict__ E = ctl->ecur ? E1 : E0;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < S; i += (int64_t)gridDim.x * blockDim.x)
-    D[i] = __dsub_rn(T[i], E[i]);
+    D[i] = (EL)__dsub_rn((double)T[i], (double)E[i]);
+}
+
+// fp32 mode: round a float64 tensor to the float32 state (round to nearest) and back
+__global__ void k_to_float(const double* __restrict__ x, float* __restrict__ out, int64_t S) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < S; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = (float)x[i];
+}
+__global__ void k_to_double(const float* __restrict__ x, double* __restrict__ out, int64_t S) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < S; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = (double)x[i];
 }
 
 // soft_threshold (linops.hpp:37-43)
@@ -467,11 +479,12 @@ __global__ void k_accum_x(double* __restrict__ x, const double* __restrict__ z, 
 
 // Yhat_n = Y_n + mu_used * (E - E_prev)  (pasd.cpp:257); also accumulates
 // acc += Y_n - Yhat_n for the certificate (pasd.cpp:287-292).
-__global__ void k_yhat(const double* __restrict__ y, const double* __restrict__ e, const double* __restrict__ ep,
+template <class EL>
+__global__ void k_yhat(const EL* __restrict__ y, const EL* __restrict__ e, const EL* __restrict__ ep,
                        double mu_used, double* __restrict__ yhat, double* __restrict__ acc, int first, int64_t S) {
   for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < S; idx += (int64_t)gridDim.x * blockDim.x) {
     const double yv = y[idx];
-    const double h = __dadd_rn(yv, __dmul_rn(mu_used, __dsub_rn(e[idx], ep[idx])));
+    const double h = __dadd_rn(yv, __dmul_rn(mu_used, __dsub_rn((double)e[idx], (double)ep[idx])));
     if (yhat) yhat[idx] = h;
     if (acc) {
       const double prev = first ? 0.0 : acc[idx];
@@ -481,11 +494,12 @@ __global__ void k_yhat(const double* __restrict__ y, const double* __restrict__ 
 }
 
 // Per-block partial sums of |x| and maxima of |x| over a buffer.
-__global__ void k_abs_stats(const double* __restrict__ x, int64_t S, double* sum_part, double* max_part) {
+template <class EL>
+__global__ void k_abs_stats(const EL* __restrict__ x, int64_t S, double* sum_part, double* max_part) {
   __shared__ double red[32];
   double s = 0.0, mx = 0.0;
   for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < S; idx += (int64_t)gridDim.x * blockDim.x) {
-    const double a = fabs(x[idx]);
+    const double a = fabs((double)x[idx]);
     s += a;
     if (a > mx) mx = a;
   }

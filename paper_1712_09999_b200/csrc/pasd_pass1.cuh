@@ -56,19 +56,40 @@ struct P1Cfg {
   static constexpr int NST = CONTIG ? PASD_P1_NSTC : PASD_P1_NSTS;
 };
 
-template <int RP, bool CONTIG>
+template <int RP, bool CONTIG, class EL = double>
 struct P1Layout {
   // CONTIG (mode 1): raw[kappa][i] rows of 16 i;  else raw[i][kappa] rows of 128 kappa.
-  // Pitches are 4 mod 16 doubles: the fragment reads (row g, col t) hit 16
-  // distinct banks per half-warp.
+  // Pitches are 4 mod 16 doubles (float storage: 12 / 136 floats): the fragment
+  // reads (row g, col t) hit distinct banks per half-warp.
   static constexpr int KC = P1Cfg<CONTIG>::KC, NST = P1Cfg<CONTIG>::NST;
-  static constexpr int LDR = CONTIG ? (KC + 4) : (P1_MT + 4);
-  static constexpr int RAW = CONTIG ? P1_MT * LDR : KC * LDR;  // doubles per tensor per stage
-  static constexpr int LDU = KC + 4;                           // U chunk as [r][i]
+  static constexpr int ES = sizeof(EL);
+  static constexpr int LDR = CONTIG ? (KC + 4) : (P1_MT + (ES == 8 ? 4 : 8));
+  static constexpr int RAW = CONTIG ? P1_MT * LDR : KC * LDR;  // elements per tensor per stage
+  static constexpr int LDU = KC + 4;                           // U chunk (float64) as [r][i]
   static constexpr int USZ = RP * LDU;
-  static constexpr int STAGE = 2 * RAW + USZ;  // D, Y_n, U chunk
-  static constexpr size_t bytes = sizeof(double) * (size_t)NST * STAGE;
+  static constexpr int UOFF = 2 * RAW * ES;                    // byte offset of the U chunk
+  static constexpr int STAGE = UOFF + 8 * USZ;                 // bytes: D, Y_n, U chunk
+  static_assert(UOFF % 16 == 0 && STAGE % 16 == 0, "16-byte aligned stages");
+  static constexpr size_t bytes = (size_t)NST * STAGE;
 };
+
+// Pair of consecutive elements (16 bytes of float64, 8 of float32): one cp.async.
+template <class EL>
+__device__ __forceinline__ void cp_pair(unsigned s, const void* g, bool ok) {
+  if constexpr (sizeof(EL) == 8)
+    cp16z(s, g, ok);
+  else
+    cp8z(s, g, ok);
+}
+// One element (ok = false: zero fill).
+template <class EL>
+__device__ __forceinline__ void cp_one(unsigned s, const void* g, bool ok) {
+  if constexpr (sizeof(EL) == 8) {
+    cp8s(s, g, ok ? 8 : 0);
+  } else {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(s), "l"(g), "r"(ok ? 4 : 0) : "memory");
+  }
+}
 
 // Strided modes whose inner extent leaves a mostly empty last 128-wide p-block
 // per q (> 5% of the tiles' width wasted: C1-C3, inner = 100, 200, 400) use
@@ -91,11 +112,13 @@ struct P1Cursor {
   int chunk;
 };
 
-template <int RP, bool CONTIG, bool CROSS = false>
-__global__ void __launch_bounds__(P1_THREADS, P1_CTAS) k_pass1(ModeDev m, const double* __restrict__ D,
-                                                        const double* __restrict__ Y, const Ctl* ctl) {
+// EL: storage type of D and Y_n (float in the fp32 mode); G is formed in fp64.
+template <int RP, bool CONTIG, bool CROSS = false, class EL = double>
+__global__ void __launch_bounds__(P1_THREADS, P1_CTAS) k_pass1(ModeDev m, const EL* __restrict__ D,
+                                                        const EL* __restrict__ Y, const Ctl* ctl) {
   if (ctl->done) return;
-  using L = P1Layout<RP, CONTIG>;
+  using L = P1Layout<RP, CONTIG, EL>;
+  constexpr unsigned ES = sizeof(EL);
   constexpr int NT = RP / 8;  // n-tiles per warp
   constexpr int P1_KC = L::KC, P1_NST = L::NST;
   extern __shared__ double p1sm[];
@@ -130,7 +153,7 @@ __global__ void __launch_bounds__(P1_THREADS, P1_CTAS) k_pass1(ModeDev m, const 
   auto issue = [&](const P1Cursor& c, int s) {
     if (c.tile >= ntiles) return;
     const int64_t i0 = (int64_t)c.chunk * P1_KC;
-    const unsigned st = sbase + 8u * (unsigned)(s * L::STAGE);
+    const unsigned st = sbase + (unsigned)(s * L::STAGE);
     const int ni = (int)imin64(P1_KC, I - i0);
     if (CONTIG) {
       // 128 columns kappa, 16 consecutive i each (contiguous): row = column
@@ -146,18 +169,18 @@ __global__ void __launch_bounds__(P1_THREADS, P1_CTAS) k_pass1(ModeDev m, const 
           const int j = j0 + RPP * k;
           const int nb = (k0 + j < m.J) ? nbc : 0;
           const int64_t off = off0 + (int64_t)RPP * k * I;
-          const unsigned d = st + 8u * (unsigned)(j * L::LDR + 2 * cc);
-          cp16z(d, nb ? D + off : D, nb != 0);  // even I: chunks wholly in or out
-          cp16z(d + 8u * L::RAW, nb ? Y + off : D, nb != 0);
+          const unsigned d = st + ES * (unsigned)(j * L::LDR + 2 * cc);
+          cp_pair<EL>(d, nb ? D + off : D, nb != 0);  // even I: chunks wholly in or out
+          cp_pair<EL>(d + ES * L::RAW, nb ? Y + off : D, nb != 0);
         }
       } else {
         for (int idx = tid; idx < P1_MT * P1_KC; idx += P1_THREADS) {
           const int j = idx / P1_KC, cc = idx % P1_KC;
           const bool ok = k0 + j < m.J && cc < ni;
           const int64_t off = (k0 + j) * I + i0 + cc;
-          const unsigned d = st + 8u * (unsigned)(j * L::LDR + cc);
-          cp8s(d, ok ? D + off : D, ok ? 8 : 0);
-          cp8s(d + 8u * L::RAW, ok ? Y + off : D, ok ? 8 : 0);
+          const unsigned d = st + ES * (unsigned)(j * L::LDR + cc);
+          cp_one<EL>(d, ok ? D + off : D, ok);
+          cp_one<EL>(d + ES * L::RAW, ok ? Y + off : D, ok);
         }
       }
     } else if (cross) {
@@ -174,9 +197,9 @@ __global__ void __launch_bounds__(P1_THREADS, P1_CTAS) k_pass1(ModeDev m, const 
           const int ii = rsub + RG * k;
           const bool ok = cok && ii < ni;  // even inner: a 16-byte chunk never straddles q
           const int64_t off = off0 + inner * ii;
-          const unsigned d = st + 8u * (unsigned)(ii * L::LDR + 2 * cc);
-          cp16z(d, ok ? D + off : D, ok);
-          cp16z(d + 8u * L::RAW, ok ? Y + off : D, ok);
+          const unsigned d = st + ES * (unsigned)(ii * L::LDR + 2 * cc);
+          cp_pair<EL>(d, ok ? D + off : D, ok);
+          cp_pair<EL>(d + ES * L::RAW, ok ? Y + off : D, ok);
         }
       } else {
         for (int idx = tid; idx < P1_KC * P1_MT; idx += P1_THREADS) {
@@ -185,9 +208,9 @@ __global__ void __launch_bounds__(P1_THREADS, P1_CTAS) k_pass1(ModeDev m, const 
           const bool ok = ii < ni && kap < m.J;
           const int64_t q = kap / inner;
           const int64_t off = (kap - q * inner) + inner * (i0 + ii + I * q);
-          const unsigned d = st + 8u * (unsigned)(ii * L::LDR + cc);
-          cp8s(d, ok ? D + off : D, ok ? 8 : 0);
-          cp8s(d + 8u * L::RAW, ok ? Y + off : D, ok ? 8 : 0);
+          const unsigned d = st + ES * (unsigned)(ii * L::LDR + cc);
+          cp_one<EL>(d, ok ? D + off : D, ok);
+          cp_one<EL>(d + ES * L::RAW, ok ? Y + off : D, ok);
         }
       }
     } else {
@@ -204,23 +227,23 @@ __global__ void __launch_bounds__(P1_THREADS, P1_CTAS) k_pass1(ModeDev m, const 
           const int ii = rsub + RG * k;
           const int nb = ii < ni ? nbc : 0;
           const int64_t off = off0 + inner * ii + 2 * cc;
-          const unsigned d = st + 8u * (unsigned)(ii * L::LDR + 2 * cc);
-          cp16z(d, nb ? D + off : D, nb != 0);  // even inner: chunks wholly in or out
-          cp16z(d + 8u * L::RAW, nb ? Y + off : D, nb != 0);
+          const unsigned d = st + ES * (unsigned)(ii * L::LDR + 2 * cc);
+          cp_pair<EL>(d, nb ? D + off : D, nb != 0);  // even inner: chunks wholly in or out
+          cp_pair<EL>(d + ES * L::RAW, nb ? Y + off : D, nb != 0);
         }
       } else {
         for (int idx = tid; idx < P1_KC * P1_MT; idx += P1_THREADS) {
           const int ii = idx / P1_MT, cc = idx % P1_MT;
           const bool ok = ii < ni && cc < np;
           const int64_t off = off0 + inner * ii + cc;
-          const unsigned d = st + 8u * (unsigned)(ii * L::LDR + cc);
-          cp8s(d, ok ? D + off : D, ok ? 8 : 0);
-          cp8s(d + 8u * L::RAW, ok ? Y + off : D, ok ? 8 : 0);
+          const unsigned d = st + ES * (unsigned)(ii * L::LDR + cc);
+          cp_one<EL>(d, ok ? D + off : D, ok);
+          cp_one<EL>(d + ES * L::RAW, ok ? Y + off : D, ok);
         }
       }
     }
     // U chunk as [r][i] (16 consecutive i of column r are contiguous in U)
-    const unsigned us = st + 8u * (unsigned)(2 * L::RAW);
+    const unsigned us = st + (unsigned)L::UOFF;
     const double* ub = m.U + m.ioff + i0;
     if (alu) {
       constexpr int PAIRS = P1_KC / 2, RSTEP = P1_THREADS / PAIRS;
@@ -267,18 +290,18 @@ __global__ void __launch_bounds__(P1_THREADS, P1_CTAS) k_pass1(ModeDev m, const 
     issue(nxt, (int)((it + P1_NST - 1) % P1_NST));
     advance(nxt);
     asm volatile("cp.async.commit_group;" ::: "memory");
-    const double* st = p1sm + (size_t)s * L::STAGE;
-    const double* Ds = st;
-    const double* Ys = st + L::RAW;
-    const double* Us = st + 2 * L::RAW;
+    const char* st = reinterpret_cast<const char*>(p1sm) + (size_t)s * L::STAGE;
+    const EL* Ds = reinterpret_cast<const EL*>(st);
+    const EL* Ys = Ds + L::RAW;
+    const double* Us = reinterpret_cast<const double*>(st + L::UOFF);
 #pragma unroll
     for (int ks = 0; ks < P1_KC / 4; ++ks) {
       const int k = 4 * ks + t;
       const int r0 = 16 * w + g, r1 = r0 + 8;
       const int o0 = CONTIG ? r0 * L::LDR + k : k * L::LDR + r0;
       const int o1 = CONTIG ? r1 * L::LDR + k : k * L::LDR + r1;
-      const double a0 = __dadd_rn(Ds[o0], __dmul_rn(Ys[o0], inv_mu));  // g_elem on D
-      const double a1 = __dadd_rn(Ds[o1], __dmul_rn(Ys[o1], inv_mu));
+      const double a0 = __dadd_rn((double)Ds[o0], __dmul_rn((double)Ys[o0], inv_mu));  // g_elem on D
+      const double a1 = __dadd_rn((double)Ds[o1], __dmul_rn((double)Ys[o1], inv_mu));
 #pragma unroll
       for (int j = 0; j < NT; ++j)
         dmma((TWO && (ks & 1)) ? acb[TWO ? j : 0] : acc[j], a0, a1, Us[(8 * j + g) * L::LDU + k]);
@@ -318,17 +341,15 @@ __global__ void __launch_bounds__(P1_THREADS, P1_CTAS) k_pass1(ModeDev m, const 
   asm volatile("cp.async.wait_all;" ::: "memory");
 }
 
-template <int RP, bool CONTIG, bool CROSS>
-void launch_p1(const ModeDev& m, const double* D, const double* Y, const Ctl* ctl,
-               int grid, cudaStream_t st) {
-  using L = P1Layout<RP, CONTIG>;
-  ensure_smem_attr<k_pass1<RP, CONTIG, CROSS>>(L::bytes);
-  k_pass1<RP, CONTIG, CROSS><<<grid, P1_THREADS, L::bytes, st>>>(m, D, Y, ctl);
+template <int RP, bool CONTIG, bool CROSS, class EL>
+void launch_p1(const ModeDev& m, const EL* D, const EL* Y, const Ctl* ctl, int grid, cudaStream_t st) {
+  using L = P1Layout<RP, CONTIG, EL>;
+  ensure_smem_attr<k_pass1<RP, CONTIG, CROSS, EL>>(L::bytes);
+  k_pass1<RP, CONTIG, CROSS, EL><<<grid, P1_THREADS, L::bytes, st>>>(m, D, Y, ctl);
 }
 
-template <bool CONTIG, bool CROSS>
-void launch_p1_rp(const ModeDev& m, const double* D, const double* Y,
-                  const Ctl* ctl, int grid, cudaStream_t st) {
+template <bool CONTIG, bool CROSS, class EL>
+void launch_p1_rp(const ModeDev& m, const EL* D, const EL* Y, const Ctl* ctl, int grid, cudaStream_t st) {
   switch ((m.R + 7) / 8 * 8) {
     case 8: launch_p1<8, CONTIG, CROSS>(m, D, Y, ctl, grid, st); break;
     case 16: launch_p1<16, CONTIG, CROSS>(m, D, Y, ctl, grid, st); break;
@@ -345,7 +366,8 @@ inline int pass1_grid(const ModeDev& m, int sms) {
   return (int)imin64(p1_ntiles(m), P1_CTAS * sms);
 }
 
-inline void launch_contract_A_mma(const ModeDev& m, const double* D, const double* Y, const Ctl* ctl, int sms, cudaStream_t st) {
+template <class EL>
+void launch_contract_A_mma(const ModeDev& m, const EL* D, const EL* Y, const Ctl* ctl, int sms, cudaStream_t st) {
   const int grid = pass1_grid(m, sms);
   if (m.inner == 1)
     launch_p1_rp<true, false>(m, D, Y, ctl, grid, st);

@@ -233,6 +233,13 @@ struct P2Layout {
   static_assert(128 * RP <= oA3 + RP * LD3, "end-of-pencil scratch must fit in A1s..A3s");
 };
 
+// The layout as a kernel with element type EL sees it: the element-brick staging
+// (PASD_P2_EPF) copies 16-byte pairs of float64 and is off for float storage.
+template <int RP, bool TIO, class EL>
+struct P2LayoutE : P2Layout<RP, TIO> {
+  static constexpr bool EPF = P2Layout<RP, TIO>::EPF && sizeof(EL) == 8;
+};
+
 // Element (l1, l2, l3) of a 16 x 8 x 8 brick in the TMA SWIZZLE_128B layout:
 // 128-byte rows of 16 doubles, 16-byte chunks XOR-ed with (row mod 8).
 // Layout A: row = l2 + 8 l3; layout B: row = l3 + 8 l2.
@@ -287,11 +294,15 @@ __host__ __device__ constexpr bool pass2_ws() {
 
 // RP = common padded rank (multiple of 8, >= every R_n); rows r >= R_n of each
 // mode's operands are zero, so padding changes no result.
-template <int RP, bool TIO>
+// EL = storage type of the element streams T, E, D, Y_n (double; float in the
+// fp32 mode, PASD_FLAG_FP32): loaded into fp64 registers, every operation below
+// in fp64, rounded to EL on store.
+template <int RP, bool TIO, class EL = double>
 __global__ void __launch_bounds__(P2_THREADS, 1) k_pass2_fused(const Pass2Args a, const Ctl* ctl,
                                                                 const __grid_constant__ P2Tmaps tm) {
+  static_assert(!TIO || sizeof(EL) == 8, "TMA element bricks are float64");
   if (ctl->done) return;
-  using L = P2Layout<RP, TIO>;
+  using L = P2LayoutE<RP, TIO, EL>;
   constexpr int KS = RP / 4;   // k-steps of the Z products
   constexpr int NT1 = RP / 8;  // n-tiles of the Wt_1 product
   constexpr int MT = L::RM / 16;
@@ -318,8 +329,10 @@ __global__ void __launch_bounds__(P2_THREADS, 1) k_pass2_fused(const Pass2Args a
   unsigned mph = 0;  // mbarrier phase parity of the next element-brick load
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5, g = lane >> 2, t = lane & 3;
 
-  const double* __restrict__ T = a.T;
-  double* __restrict__ Enew = ctl->ecur ? a.E0 : a.E1;
+  const EL* __restrict__ T = reinterpret_cast<const EL*>(a.T);
+  EL* __restrict__ Enew = reinterpret_cast<EL*>(ctl->ecur ? a.E0 : a.E1);
+  EL* __restrict__ Dp = reinterpret_cast<EL*>(a.D);
+  EL* const Yp[3] = {reinterpret_cast<EL*>(a.Y[0]), reinterpret_cast<EL*>(a.Y[1]), reinterpret_cast<EL*>(a.Y[2])};
   const double mu = ctl->mu;
   const double inv_mu = __ddiv_rn(1.0, mu);                // pasd.cpp:170
   const double inv_n = __ddiv_rn(1.0, 3.0);                // pasd.cpp:204
@@ -502,7 +515,7 @@ __global__ void __launch_bounds__(P2_THREADS, 1) k_pass2_fused(const Pass2Args a
         off[q] = i1 + I1 * i2 + S12 * i3;
         tv[q] = inb[q] ? T[off[q]] : 0.0;
 #pragma unroll
-        for (int n = 0; n < 3; ++n) yv[n][q] = inb[q] ? a.Y[n][off[q]] : 0.0;
+        for (int n = 0; n < 3; ++n) yv[n][q] = inb[q] ? (double)Yp[n][off[q]] : 0.0;
       }
     };
     // PASD_P2_EPF: this thread's 8 copies of a step's T, Y_1..3 brick (stream ts,
@@ -519,8 +532,8 @@ __global__ void __launch_bounds__(P2_THREADS, 1) k_pass2_fused(const Pass2Args a
         const int row = (idx >> 3) & 63, ts = idx >> 9;
         const int l2 = row & 7, l3 = row >> 3;
         const bool ok = cok && i2o + l2 < I2 && i3o + l3 < I3;
-        const double* base = ts == 0 ? T : a.Y[ts - 1];
-        const double* src = ok ? base + i1o + 2 * c + I1 * (i2o + l2) + S12 * (i3o + l3) : base;
+        const EL* base = ts == 0 ? T : Yp[ts - 1];
+        const EL* src = ok ? base + i1o + 2 * c + I1 * (i2o + l2) + S12 * (i3o + l3) : base;
         const unsigned dst = smem_u32(El + ts * P2_BRICK + 16 * row + 2 * (c ^ (l2 & 6)));
         if (al1) {
           cp16z(dst, src, ok);
@@ -599,9 +612,9 @@ __global__ void __launch_bounds__(P2_THREADS, 1) k_pass2_fused(const Pass2Args a
           const double tt = tv[q];
           if (PASD_P2_PROBE == 4) {  // timing probe: loads / stores / exchange only
             if (inb[q]) {
-              for (int n = 0; n < 3; ++n) a.Y[n][off[q]] = yv[n][q] + zz[n];
-              Enew[off[q]] = tt;
-              a.D[off[q]] = tt;
+              for (int n = 0; n < 3; ++n) Yp[n][off[q]] = (EL)(yv[n][q] + zz[n]);
+              Enew[off[q]] = (EL)tt;
+              Dp[off[q]] = (EL)tt;
             }
             g1v[q] = tt;
             G2s[g2x(l1, l2, w)] = yv[1][q];
@@ -624,14 +637,14 @@ __global__ void __launch_bounds__(P2_THREADS, 1) k_pass2_fused(const Pass2Args a
               const double ar = fabs(r);
               if (ar > worst[n]) worst[n] = ar;
               bad |= !isfinite(r);
-              a.Y[n][off[q]] = ynew;
+              Yp[n][off[q]] = (EL)ynew;
             }
             gn[n] = inb[q] ? g_elem(tt, e, ynew, inv_mu_next) : 0.0;  // next G_n
             gsq[n] = fma(gn[n], gn[n], gsq[n]);
           }
           if (inb[q]) {
-            Enew[off[q]] = e;
-            a.D[off[q]] = __dsub_rn(tt, e);  // next pass 1 reads D = T - E
+            Enew[off[q]] = (EL)e;
+            Dp[off[q]] = (EL)__dsub_rn(tt, e);  // next pass 1 reads D = T - E
           }
           g1v[q] = gn[0];
           G2s[g2x(l1, l2, w)] = gn[1];
@@ -888,14 +901,22 @@ __global__ void __launch_bounds__(P2_THREADS, 1) k_pass2_fused(const Pass2Args a
     finish_body(const_cast<Ctl*>(ctl), a.resid_part, a.bad_part, gridDim.x, a.history, nullptr, red);
 }
 
-template <int RP, bool TIO>
+template <int RP, bool TIO, class EL = double>
 void launch_pass2(const Pass2Args& a, const Ctl* ctl, const P2Tmaps& tm, int grid, cudaStream_t st) {
-  k_pass2_fused<RP, TIO><<<grid, P2_THREADS, P2Layout<RP, TIO>::bytes, st>>>(a, ctl, tm);
+  k_pass2_fused<RP, TIO, EL><<<grid, P2_THREADS, P2Layout<RP, TIO>::bytes, st>>>(a, ctl, tm);
+}
+// float storage (fp32 mode) at the padded ranks this kernel serves by default (RP >= 32)
+template <int RP>
+constexpr bool p2_has_f32() {
+  return RP >= 32;
 }
 template <int RP>
 void setup_pass2() {
   cudaFuncSetAttribute(k_pass2_fused<RP, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)P2Layout<RP, false>::bytes);
+  if constexpr (p2_has_f32<RP>())
+    cudaFuncSetAttribute(k_pass2_fused<RP, false, float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)P2Layout<RP, false>::bytes);
   if (P2Layout<RP, true>::bytes <= 227u * 1024u)
     cudaFuncSetAttribute(k_pass2_fused<RP, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)P2Layout<RP, true>::bytes);
@@ -935,23 +956,30 @@ inline void pass2_setup(int rp) {
   }
 }
 template <int RP>
-void pass2_launch_rp(bool tio, const Pass2Args& a, const Ctl* ctl, const P2Tmaps& tm, int grid, cudaStream_t st) {
+void pass2_launch_rp(bool tio, bool f32, const Pass2Args& a, const Ctl* ctl, const P2Tmaps& tm, int grid,
+                     cudaStream_t st) {
+  if constexpr (p2_has_f32<RP>()) {
+    if (f32) {
+      launch_pass2<RP, false, float>(a, ctl, tm, grid, st);
+      return;
+    }
+  }
   if (tio)
     launch_pass2<RP, true>(a, ctl, tm, grid, st);
   else
     launch_pass2<RP, false>(a, ctl, tm, grid, st);
 }
 inline void pass2_launch(int rp, bool tio, const Pass2Args& a, const Ctl* ctl, const P2Tmaps& tm, int grid,
-                         cudaStream_t st) {
+                         cudaStream_t st, bool f32 = false) {
   switch (rp) {
-    case 8: pass2_launch_rp<8>(tio, a, ctl, tm, grid, st); break;
-    case 16: pass2_launch_rp<16>(tio, a, ctl, tm, grid, st); break;
-    case 24: pass2_launch_rp<24>(tio, a, ctl, tm, grid, st); break;
-    case 32: pass2_launch_rp<32>(tio, a, ctl, tm, grid, st); break;
-    case 40: pass2_launch_rp<40>(tio, a, ctl, tm, grid, st); break;
-    case 48: pass2_launch_rp<48>(tio, a, ctl, tm, grid, st); break;
-    case 56: pass2_launch_rp<56>(tio, a, ctl, tm, grid, st); break;
-    default: pass2_launch_rp<64>(tio, a, ctl, tm, grid, st); break;
+    case 8: pass2_launch_rp<8>(tio, f32, a, ctl, tm, grid, st); break;
+    case 16: pass2_launch_rp<16>(tio, f32, a, ctl, tm, grid, st); break;
+    case 24: pass2_launch_rp<24>(tio, f32, a, ctl, tm, grid, st); break;
+    case 32: pass2_launch_rp<32>(tio, f32, a, ctl, tm, grid, st); break;
+    case 40: pass2_launch_rp<40>(tio, f32, a, ctl, tm, grid, st); break;
+    case 48: pass2_launch_rp<48>(tio, f32, a, ctl, tm, grid, st); break;
+    case 56: pass2_launch_rp<56>(tio, f32, a, ctl, tm, grid, st); break;
+    default: pass2_launch_rp<64>(tio, f32, a, ctl, tm, grid, st); break;
   }
 }
 

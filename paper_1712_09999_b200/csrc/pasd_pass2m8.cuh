@@ -53,7 +53,8 @@ struct M8Layout {
   static constexpr size_t bytes = sizeof(double) * (size_t)total;
 };
 
-template <int RP>
+// EL: storage type of T, E, D, Y_n (float in the fp32 mode; arithmetic in fp64)
+template <int RP, class EL = double>
 __global__ void __launch_bounds__(M8_THREADS, 2) k_pass2_m8(const Pass2Args a, const Ctl* ctl) {
   if (ctl->done) return;
   using L = M8Layout<RP>;
@@ -77,8 +78,10 @@ __global__ void __launch_bounds__(M8_THREADS, 2) k_pass2_m8(const Pass2Args a, c
   double* red = sm + L::oRed;
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5, g = lane >> 2, t = lane & 3;
 
-  const double* __restrict__ T = a.T;
-  double* __restrict__ Enew = ctl->ecur ? a.E0 : a.E1;
+  const EL* __restrict__ T = reinterpret_cast<const EL*>(a.T);
+  EL* __restrict__ Enew = reinterpret_cast<EL*>(ctl->ecur ? a.E0 : a.E1);
+  EL* __restrict__ Dp = reinterpret_cast<EL*>(a.D);
+  EL* const Yp[3] = {reinterpret_cast<EL*>(a.Y[0]), reinterpret_cast<EL*>(a.Y[1]), reinterpret_cast<EL*>(a.Y[2])};
   const double mu = ctl->mu;
   const double inv_mu = __ddiv_rn(1.0, mu);                // pasd.cpp:170
   const double inv_n = __ddiv_rn(1.0, 3.0);                // pasd.cpp:204
@@ -208,7 +211,7 @@ __global__ void __launch_bounds__(M8_THREADS, 2) k_pass2_m8(const Pass2Args a, c
         off[p] = i1 + I1 * i2 + S12 * i3;
         tv[p] = inb[p] ? T[off[p]] : 0.0;
 #pragma unroll
-        for (int n = 0; n < 3; ++n) yv[n][p] = inb[p] ? a.Y[n][off[p]] : 0.0;
+        for (int n = 0; n < 3; ++n) yv[n][p] = inb[p] ? (double)Yp[n][off[p]] : 0.0;
       }
     };
     stage_step(i2b);
@@ -262,14 +265,14 @@ __global__ void __launch_bounds__(M8_THREADS, 2) k_pass2_m8(const Pass2Args a, c
             const double ar = fabs(r);
             if (ar > worst[n]) worst[n] = ar;
             bad |= !isfinite(r);
-            a.Y[n][off[p]] = ynew;
+            Yp[n][off[p]] = (EL)ynew;
           }
           gn[n] = inb[p] ? g_elem(tt, e, ynew, inv_mu_next) : 0.0;
           gsq[n] = fma(gn[n], gn[n], gsq[n]);
         }
         if (inb[p]) {
-          Enew[off[p]] = e;
-          a.D[off[p]] = __dsub_rn(tt, e);  // next pass 1 reads D = T - E
+          Enew[off[p]] = (EL)e;
+          Dp[off[p]] = (EL)__dsub_rn(tt, e);  // next pass 1 reads D = T - E
         }
         g1v[p] = gn[0];
         G2x[g28x(g, l2, w)] = gn[1];
@@ -398,12 +401,21 @@ __global__ void __launch_bounds__(M8_THREADS, 2) k_pass2_m8(const Pass2Args a, c
 }
 
 template <int RP>
-void launch_m8(const Pass2Args& a, const Ctl* ctl, int grid, cudaStream_t st) {
+void launch_m8(const Pass2Args& a, const Ctl* ctl, int grid, cudaStream_t st, bool f32 = false) {
+  if constexpr (RP <= 24) {  // float storage (fp32 mode) where this kernel is the default
+    if (f32) {
+      k_pass2_m8<RP, float><<<grid, M8_THREADS, M8Layout<RP>::bytes, st>>>(a, ctl);
+      return;
+    }
+  }
   k_pass2_m8<RP><<<grid, M8_THREADS, M8Layout<RP>::bytes, st>>>(a, ctl);
 }
 template <int RP>
 void setup_m8() {
   cudaFuncSetAttribute(k_pass2_m8<RP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)M8Layout<RP>::bytes);
+  if constexpr (RP <= 24)
+    cudaFuncSetAttribute(k_pass2_m8<RP, float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)M8Layout<RP>::bytes);
 }
 // Measured on B200 (profiles/): the 8x8x8 two-CTA variant wins for R <= 24
 // (C1: 0.122 vs 0.129 ms, C2: 0.516 vs 0.565 ms per iteration), the 16x8x8
@@ -420,11 +432,11 @@ inline void m8_setup(int rp) {
     default: setup_m8<56>(); break;
   }
 }
-inline void m8_launch(int rp, const Pass2Args& a, const Ctl* ctl, int grid, cudaStream_t st) {
+inline void m8_launch(int rp, const Pass2Args& a, const Ctl* ctl, int grid, cudaStream_t st, bool f32 = false) {
   switch (rp) {
-    case 8: launch_m8<8>(a, ctl, grid, st); break;
-    case 16: launch_m8<16>(a, ctl, grid, st); break;
-    case 24: launch_m8<24>(a, ctl, grid, st); break;
+    case 8: launch_m8<8>(a, ctl, grid, st, f32); break;
+    case 16: launch_m8<16>(a, ctl, grid, st, f32); break;
+    case 24: launch_m8<24>(a, ctl, grid, st, f32); break;
     case 32: launch_m8<32>(a, ctl, grid, st); break;
     case 40: launch_m8<40>(a, ctl, grid, st); break;
     case 48: launch_m8<48>(a, ctl, grid, st); break;

@@ -347,6 +347,11 @@ struct pasd_solver {
   int p2_grid = 0;
   size_t p2_smem = 0;
   bool p2_tio = false;  // element streams through TMA (k_pass2_fused<RP, true>)
+  // PASD_FLAG_FP32: T, E, D, Y_n stored as float32 (the double* members then
+  // point at float storage); small state and all arithmetic stay fp64
+  bool f32 = false;
+  size_t esz = sizeof(double);
+  double* ebuf = nullptr;  // fp32 mode: S float64 scratch for conversions on the way out
   P2Tmaps p2_tmaps{};
   double* p2_resid = nullptr;
   int* p2_bad = nullptr;
@@ -416,6 +421,18 @@ double* ctl_gnorm2(pasd_solver* s) {  // device address of ctl->gnorm2[0]
   return reinterpret_cast<double*>(reinterpret_cast<char*>(s->d_ctl) + offsetof(Ctl, gnorm2));
 }
 
+template <class EL>
+EL* as_el(double* p) {
+  return reinterpret_cast<EL*>(p);
+}
+// pass 1 of one mode on the solver's element storage (float64, or float32 in the fp32 mode)
+void launch_p1_any(pasd_solver* s, const ModeDev& m, double* Y, int sms, cudaStream_t st) {
+  if (s->f32)
+    launch_contract_A_mma(m, as_el<float>(s->D), as_el<float>(Y), s->d_ctl, sms, st);
+  else
+    launch_contract_A_mma(m, (const double*)s->D, (const double*)Y, s->d_ctl, sms, st);
+}
+
 // Launches one iteration.  `mark(cls, begin)` (optional) is called around
 // every kernel; the profiler records CUDA events there.
 template <class Mark>
@@ -432,7 +449,7 @@ void launch_iteration_marked(pasd_solver* s, cudaStream_t st, Mark&& mark, bool 
       const ModeDev& m = s->modes[n];
       CK(cudaStreamWaitEvent(bs, s->ev_p1fork, 0));
       k_polar<<<kSmallCluster, kSmallThreads, s->small_smem, bs>>>(s->d_pack, s->d_ctl, n);
-      launch_contract_A_mma(m, s->D, s->Y[n], s->d_ctl, s->sms, bs);
+      launch_p1_any(s, m, s->Y[n], s->sms, bs);
       CK(cudaEventRecord(s->ev_p1join[n], bs));
       launches += 2;
     }
@@ -451,7 +468,7 @@ void launch_iteration_marked(pasd_solver* s, cudaStream_t st, Mark&& mark, bool 
     if (!s->sharded) {
       for (int n = 0; n < N; ++n) {
         mark(PASD_K_CONTRACT_A, true);
-        launch_contract_A_mma(s->modes[n], s->D, s->Y[n], s->d_ctl, s->sms, st);
+        launch_p1_any(s, s->modes[n], s->Y[n], s->sms, st);
         mark(PASD_K_CONTRACT_A, false);
         ++launches;
       }
@@ -462,7 +479,7 @@ void launch_iteration_marked(pasd_solver* s, cudaStream_t st, Mark&& mark, bool 
       ModeDev m3 = s->modes[N - 1];
       m3.A = s->A3_partial;
       mark(PASD_K_CONTRACT_A, true);
-      launch_contract_A_mma(m3, s->D, s->Y[N - 1], s->d_ctl, s->sms, st);
+      launch_p1_any(s, m3, s->Y[N - 1], s->sms, st);
       mark(PASD_K_CONTRACT_A, false);
       ++launches;
       CK(cudaEventRecord(s->ev_fork, st));
@@ -472,7 +489,7 @@ void launch_iteration_marked(pasd_solver* s, cudaStream_t st, Mark&& mark, bool 
       const int sms_p1 = std::max(1, s->sms - kNcclSms);
       for (int n = 0; n < N - 1; ++n) {
         mark(PASD_K_CONTRACT_A, true);
-        launch_contract_A_mma(s->modes[n], s->D, s->Y[n], s->d_ctl, sms_p1, st);
+        launch_p1_any(s, s->modes[n], s->Y[n], sms_p1, st);
         mark(PASD_K_CONTRACT_A, false);
         ++launches;
       }
@@ -513,9 +530,9 @@ void launch_iteration_marked(pasd_solver* s, cudaStream_t st, Mark&& mark, bool 
   if (s->fused) {
     mark(PASD_K_UPDATE, true);
     if (s->use_m8)
-      m8_launch(s->p2_rp, s->p2, s->d_ctl, s->p2_grid, st);
+      m8_launch(s->p2_rp, s->p2, s->d_ctl, s->p2_grid, st, s->f32);
     else
-      pass2_launch(s->p2_rp, s->p2_tio, s->p2, s->d_ctl, s->p2_tmaps, s->p2_grid, st);
+      pass2_launch(s->p2_rp, s->p2_tio, s->p2, s->d_ctl, s->p2_tmaps, s->p2_grid, st, s->f32);
     mark(PASD_K_UPDATE, false);
     ++launches;
     int64_t maxir = 1;
@@ -584,21 +601,22 @@ void launch_iteration(pasd_solver* s, cudaStream_t st) {
 // modes: the data the kernel's function must touch once.
 void kernel_work(const pasd_solver* s, double* bytes, double* flops) {
   const double S = (double)s->S, N = (double)s->N;
+  const double es = (double)s->esz;  // bytes per element-tensor entry (8, or 4 in the fp32 mode)
   for (int k = 0; k < PASD_NUM_KERNEL_CLASSES; ++k) bytes[k] = flops[k] = 0.0;
   for (const ModeDev& m : s->modes) {
     const double RJ = (double)m.R * (double)m.J, R = m.R;
-    bytes[PASD_K_CONTRACT_A] += 8.0 * (2.0 * S + RJ);        // D = T - E, Y_n in; A_n out
+    bytes[PASD_K_CONTRACT_A] += es * 2.0 * S + 8.0 * RJ;     // D = T - E, Y_n in; A_n out
     flops[PASD_K_CONTRACT_A] += 2.0 * R * S;
     bytes[PASD_K_GRAM] += 8.0 * RJ;                         // A_n in
     flops[PASD_K_GRAM] += 2.0 * R * RJ;
     bytes[PASD_K_UPDATE] += 8.0 * RJ;                       // A_n in
     flops[PASD_K_UPDATE] += 2.0 * R * S;
-    bytes[PASD_K_CONTRACT_W] += 8.0 * (3.0 * S + RJ);       // T, E, Y_n, A_n in
+    bytes[PASD_K_CONTRACT_W] += es * 3.0 * S + 8.0 * RJ;    // T, E, Y_n, A_n in
     flops[PASD_K_CONTRACT_W] += 2.0 * R * S;
     bytes[PASD_K_POLAR] += 8.0 * 4.0 * (double)m.I * R;
     bytes[PASD_K_SVT] += 8.0 * 2.0 * (double)m.I * R;
   }
-  bytes[PASD_K_UPDATE] += 8.0 * (2.0 * N + 3.0) * S;         // T, Y_1..N in; E, D, Y_1..N out
+  bytes[PASD_K_UPDATE] += es * (2.0 * N + 3.0) * S;          // T, Y_1..N in; E, D, Y_1..N out
   if (s->fused) {  // pass 2 also forms Wt_n = G^{next} A_n^T (A_n already counted)
     for (const ModeDev& m : s->modes) {
       flops[PASD_K_UPDATE] += 2.0 * (double)m.R * S;
@@ -664,11 +682,11 @@ __global__ void k_init_state(ModePack* mp, Ctl* ctl, double mu0, double rho, dou
 
 // copy_d = false when a new tensor is loaded next (load_tensor forms D = T - E itself)
 void reset_state(pasd_solver* s, bool copy_d = true) {
-  CK(cudaMemsetAsync(s->E[0], 0, s->S * sizeof(double), s->stream));
-  CK(cudaMemsetAsync(s->E[1], 0, s->S * sizeof(double), s->stream));
-  for (int n = 0; n < s->N; ++n) CK(cudaMemsetAsync(s->Y[n], 0, s->S * sizeof(double), s->stream));
+  CK(cudaMemsetAsync(s->E[0], 0, s->S * s->esz, s->stream));
+  CK(cudaMemsetAsync(s->E[1], 0, s->S * s->esz, s->stream));
+  for (int n = 0; n < s->N; ++n) CK(cudaMemsetAsync(s->Y[n], 0, s->S * s->esz, s->stream));
   if (copy_d)
-    CK(cudaMemcpyAsync(s->D, s->T, s->S * sizeof(double), cudaMemcpyDeviceToDevice, s->stream));  // D = T - 0
+    CK(cudaMemcpyAsync(s->D, s->T, s->S * s->esz, cudaMemcpyDeviceToDevice, s->stream));  // D = T - 0
   k_init_state<<<64, 256, 0, s->stream>>>(s->d_pack, s->d_ctl, s->mu0, s->rho, s->mu_max, s->eps, s->maxiter,
                                           (s->flags & PASD_FLAG_FIXED_ITERS) ? 1 : 0);
   CK(cudaGetLastError());
@@ -738,6 +756,9 @@ pasd_solver* create_solver(const pasd_options* o, const pasd_shard* shard) {
   s->eps = o->eps;
   s->maxiter = o->maxiter;
   s->flags = o->flags;
+  s->f32 = (o->flags & PASD_FLAG_FP32) != 0;
+  s->esz = s->f32 ? sizeof(float) : sizeof(double);
+  if (s->f32 && s->N != 3) fail(PASD_ERR_ARGUMENT, "pasd_b200: the fp32 mode supports order-3 tensors");
   s->poll_every = o->poll_every > 0 ? o->poll_every : 8;
   s->device = o->device;
   CK(cudaSetDevice(s->device));
@@ -751,11 +772,13 @@ pasd_solver* create_solver(const pasd_options* o, const pasd_shard* shard) {
     CK(cudaEventCreateWithFlags(&s->ev_p1join[n], cudaEventDisableTiming));
   }
   const int64_t S = s->S;
-  s->T = s->alloc<double>(S);
-  s->E[0] = s->alloc<double>(S);
-  s->E[1] = s->alloc<double>(S);
-  s->D = s->alloc<double>(S);
-  for (int n = 0; n < s->N; ++n) s->Y.push_back(s->alloc<double>(S));
+  // element tensors: S float64, or S float32 in the fp32 mode (held through double*)
+  auto elem = [&]() { return s->f32 ? reinterpret_cast<double*>(s->alloc<float>(S)) : s->alloc<double>(S); };
+  s->T = elem();
+  s->E[0] = elem();
+  s->E[1] = elem();
+  s->D = elem();
+  for (int n = 0; n < s->N; ++n) s->Y.push_back(elem());
   int maxR = 1;
   for (int n = 0; n < s->N; ++n) {
     ModeDev m{};
@@ -867,6 +890,7 @@ pasd_solver* create_solver(const pasd_options* o, const pasd_shard* shard) {
     a.D = s->D;
     s->p2_rp = pass2_rp(s->modes[0].R, s->modes[1].R, s->modes[2].R);
     s->use_m8 = (m8_supported(s->p2_rp) && std::getenv("PASD_PASS2_M16") == nullptr) || std::getenv("PASD_PASS2_M8") != nullptr;
+    if (s->f32) s->use_m8 = m8_supported(s->p2_rp);  // float kernels exist for the default variant only
     a.b1 = s->use_m8 ? M8_B : P2_B1;
     a.n1b = (int)((s->dims[0] + a.b1 - 1) / a.b1);
     a.n3b = (int)((s->dims[2] + P2_B3 - 1) / P2_B3);
@@ -899,7 +923,7 @@ pasd_solver* create_solver(const pasd_options* o, const pasd_shard* shard) {
     // CTA moves to the 228 KB carve-out, the Wt_2/Wt_3 operands are formed from D and Y in the
     // fragment load, and L2 re-fetches of the A slices grow by 8.5 GB), so LDG/STG is the default.
     const char* tio_env = std::getenv("PASD_P2_TIO");
-    s->p2_tio = !s->use_m8 && (s->dims[0] % 2 == 0) && pass2_smem(s->p2_rp, true) <= 227u * 1024u &&
+    s->p2_tio = !s->f32 && !s->use_m8 && (s->dims[0] % 2 == 0) && pass2_smem(s->p2_rp, true) <= 227u * 1024u &&
                 (tio_env && tio_env[0] == '1');
     if (s->p2_tio) {
       const int64_t I1 = s->dims[0], I2 = s->dims[1], I3 = s->dims[2];
@@ -963,23 +987,41 @@ void sync_ctl(pasd_solver* s) {
 
 // Upload T on the transfer stream (forked from the solver stream's current
 // point), so state resets queued on the solver stream afterwards overlap it.
+void ensure_scratch(pasd_solver* s);
+
+// fp32 mode: float64 input lands in the scratch zbuf and is rounded into T by load_tensor
+double* upload_target(pasd_solver* s) {
+  if (!s->f32) return s->T;
+  ensure_scratch(s);
+  return s->zbuf;
+}
+
 void begin_upload(pasd_solver* s, const double* t) {
   CK(cudaEventRecord(s->ev_xfork, s->stream));
   CK(cudaStreamWaitEvent(s->xfer, s->ev_xfork, 0));
-  CK(cudaMemcpyAsync(s->T, t, s->S * sizeof(double), cudaMemcpyHostToDevice, s->xfer));
+  CK(cudaMemcpyAsync(upload_target(s), t, s->S * sizeof(double), cudaMemcpyHostToDevice, s->xfer));
   CK(cudaEventRecord(s->ev_xjoin, s->xfer));
 }
 
 // uploaded: T already issued by begin_upload (the solver stream joins it here)
 void load_tensor(pasd_solver* s, const double* t, int is_device, bool uploaded = false) {
+  double* t64 = upload_target(s);  // float64 copy of the input on the device
   if (uploaded)
     CK(cudaStreamWaitEvent(s->stream, s->ev_xjoin, 0));
-  else
-    CK(cudaMemcpyAsync(s->T, t, s->S * sizeof(double), is_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
+  else if (!(s->f32 && is_device))
+    CK(cudaMemcpyAsync(t64, t, s->S * sizeof(double), is_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
                        s->stream));
+  else
+    t64 = const_cast<double*>(t);  // fp32 mode, device input: read it in place
   CK(cudaMemsetAsync(s->d_flag, 0, sizeof(int), s->stream));
-  k_nonfinite<<<1184, 256, 0, s->stream>>>(s->T, s->S, s->d_flag);
-  k_tsub<<<1184, 256, 0, s->stream>>>(s->D, s->T, s->E[0], s->E[1], s->S, s->d_ctl);  // keep D = T - E
+  k_nonfinite<<<1184, 256, 0, s->stream>>>(t64, s->S, s->d_flag);
+  if (s->f32) {
+    k_to_float<<<1184, 256, 0, s->stream>>>(t64, as_el<float>(s->T), s->S);
+    k_tsub<<<1184, 256, 0, s->stream>>>(as_el<float>(s->D), as_el<float>(s->T), as_el<float>(s->E[0]),
+                                        as_el<float>(s->E[1]), s->S, s->d_ctl);
+  } else {
+    k_tsub<<<1184, 256, 0, s->stream>>>(s->D, s->T, s->E[0], s->E[1], s->S, s->d_ctl);  // keep D = T - E
+  }
   int flag = 0;
   CK(cudaMemcpyAsync(&flag, s->d_flag, sizeof(int), cudaMemcpyDeviceToHost, s->stream));
   CK(cudaStreamSynchronize(s->stream));
@@ -1006,6 +1048,7 @@ void set_state(pasd_solver* s, const double* e, const double* const* y, const do
                const double* const* v, double mu, int iter) {
   if (!s->loaded) fail(PASD_ERR_STATE, "pasd_b200: no tensor loaded");
   if (s->sharded) fail(PASD_ERR_STATE, "pasd_b200: set_state is not available on a sharded solver");
+  if (s->f32) fail(PASD_ERR_STATE, "pasd_b200: set_state is not available in the fp32 mode");
   if (!e || !y || !u || !v) fail(PASD_ERR_ARGUMENT, "pasd_b200: null state buffer");
   if (iter >= s->maxiter) fail(PASD_ERR_ARGUMENT, "pasd_b200: state iteration must be below maxiter");
   cudaStream_t st = s->stream;
@@ -1047,6 +1090,14 @@ struct HostView {
   std::vector<std::vector<double>> z, y, u, v;
 };
 
+// A float64 view of an element tensor: itself, or (fp32 mode) its conversion into `scratch` on `st`.
+const double* elem_f64(pasd_solver* s, const double* x, double* scratch, cudaStream_t st) {
+  if (!s->f32) return x;
+  k_to_double<<<1184, 256, 0, st>>>(reinterpret_cast<const float*>(x), scratch, s->S);
+  CK(cudaGetLastError());
+  return scratch;
+}
+
 void deliver_observer(pasd_solver* s, pasd_observer_fn fn, void* user, HostView& hv) {
   const int N = s->N;
   const int64_t S = s->S;
@@ -1056,7 +1107,8 @@ void deliver_observer(pasd_solver* s, pasd_observer_fn fn, void* user, HostView&
   hv.y.resize(N);
   hv.u.resize(N);
   hv.v.resize(N);
-  CK(cudaMemcpyAsync(hv.e.data(), s->E[c.ecur], S * sizeof(double), cudaMemcpyDeviceToHost, s->stream));
+  CK(cudaMemcpyAsync(hv.e.data(), elem_f64(s, s->E[c.ecur], s->ebuf, s->stream), S * sizeof(double),
+                     cudaMemcpyDeviceToHost, s->stream));
   for (int n = 0; n < N; ++n) {
     const ModeDev& m = s->modes[n];
     hv.z[n].resize(S);
@@ -1065,7 +1117,8 @@ void deliver_observer(pasd_solver* s, pasd_observer_fn fn, void* user, HostView&
     hv.v[n].resize(m.J * m.R);
     k_materialize_z<<<1184, 256, 0, s->stream>>>(m, s->zbuf, S);
     CK(cudaMemcpyAsync(hv.z[n].data(), s->zbuf, S * sizeof(double), cudaMemcpyDeviceToHost, s->stream));
-    CK(cudaMemcpyAsync(hv.y[n].data(), s->Y[n], S * sizeof(double), cudaMemcpyDeviceToHost, s->stream));
+    CK(cudaMemcpyAsync(hv.y[n].data(), elem_f64(s, s->Y[n], s->ebuf, s->stream), S * sizeof(double),
+                       cudaMemcpyDeviceToHost, s->stream));
     CK(cudaMemcpyAsync(hv.u[n].data(), m.U, m.I * m.R * sizeof(double), cudaMemcpyDeviceToHost, s->stream));
     k_materialize_v<<<1184, 256, 0, s->stream>>>(m, s->xbuf);
     CK(cudaMemcpyAsync(hv.v[n].data(), s->xbuf, m.J * m.R * sizeof(double), cudaMemcpyDeviceToHost, s->stream));
@@ -1085,6 +1138,7 @@ void deliver_observer(pasd_solver* s, pasd_observer_fn fn, void* user, HostView&
 
 void ensure_scratch(pasd_solver* s) {
   if (!s->zbuf) s->zbuf = s->alloc<double>(s->S);
+  if (s->f32 && !s->ebuf) s->ebuf = s->alloc<double>(s->S);
   if (!s->xbuf) {
     int64_t need = s->S;
     for (const auto& m : s->modes) need = std::max<int64_t>(need, m.J * m.R);
@@ -1219,9 +1273,10 @@ void finalize_solver(pasd_solver* s, pasd_outputs* out) {
   const int blocks = 1184;
   const bool want_x = out->x != nullptr;
   if (out->e) {  // E is final: its download overlaps the X materialisation below
+    const double* e64 = elem_f64(s, e, s->ebuf, st);
     CK(cudaEventRecord(s->ev_xfork, st));
     CK(cudaStreamWaitEvent(s->xfer, s->ev_xfork, 0));
-    CK(cudaMemcpyAsync(out->e, e, S * sizeof(double), cudaMemcpyDeviceToHost, s->xfer));
+    CK(cudaMemcpyAsync(out->e, e64, S * sizeof(double), cudaMemcpyDeviceToHost, s->xfer));
     CK(cudaEventRecord(s->ev_xjoin, s->xfer));
   }
   for (int n = 0; n < N; ++n) {
@@ -1239,8 +1294,11 @@ void finalize_solver(pasd_solver* s, pasd_outputs* out) {
   if (out->e) CK(cudaStreamWaitEvent(st, s->ev_xjoin, 0));
   // objective = ||E||_1 + sum_n lambda_n ||V_n||_*  (pasd.cpp:263-266)
   std::vector<double> sums(blocks), maxs(blocks);
-  auto abs_stats = [&](const double* x, double* sum, double* mx) {
-    k_abs_stats<<<blocks, 256, 0, st>>>(x, S, s->d_stats, s->d_stats + 2048);
+  auto abs_stats = [&](const double* x, double* sum, double* mx, bool elem) {
+    if (elem && s->f32)
+      k_abs_stats<<<blocks, 256, 0, st>>>(reinterpret_cast<const float*>(x), S, s->d_stats, s->d_stats + 2048);
+    else
+      k_abs_stats<<<blocks, 256, 0, st>>>(x, S, s->d_stats, s->d_stats + 2048);
     CK(cudaMemcpyAsync(sums.data(), s->d_stats, blocks * sizeof(double), cudaMemcpyDeviceToHost, st));
     CK(cudaMemcpyAsync(maxs.data(), s->d_stats + 2048, blocks * sizeof(double), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
@@ -1254,7 +1312,7 @@ void finalize_solver(pasd_solver* s, pasd_outputs* out) {
   };
   CK(cudaStreamSynchronize(st));
   double l1 = 0.0;
-  abs_stats(e, &l1, nullptr);
+  abs_stats(e, &l1, nullptr, true);
   auto allreduce_scalar = [&](double v, RedOp op) {
     if (!s->sharded) return v;
     CK(cudaMemcpyAsync(s->d_stats, &v, sizeof(double), cudaMemcpyHostToDevice, st));
@@ -1273,17 +1331,23 @@ void finalize_solver(pasd_solver* s, pasd_outputs* out) {
   for (int n = 0; n < N; ++n) {
     const bool want_yh = out->y_hat && out->y_hat[n];
     if (out->y && out->y[n])
-      CK(cudaMemcpyAsync(out->y[n], s->Y[n], S * sizeof(double), cudaMemcpyDeviceToHost, st));
+      CK(cudaMemcpyAsync(out->y[n], elem_f64(s, s->Y[n], s->ebuf, st), S * sizeof(double), cudaMemcpyDeviceToHost,
+                         st));
     if (!want_yh && !want_cert) continue;
-    k_yhat<<<blocks, 256, 0, st>>>(s->Y[n], e, ep, mu_used, s->zbuf, want_cert ? s->xbuf : nullptr, n == 0, S);
+    if (s->f32)
+      k_yhat<<<blocks, 256, 0, st>>>(as_el<float>(s->Y[n]), reinterpret_cast<const float*>(e),
+                                     reinterpret_cast<const float*>(ep), mu_used, s->zbuf,
+                                     want_cert ? s->xbuf : nullptr, n == 0, S);
+    else
+      k_yhat<<<blocks, 256, 0, st>>>(s->Y[n], e, ep, mu_used, s->zbuf, want_cert ? s->xbuf : nullptr, n == 0, S);
     if (want_yh) CK(cudaMemcpyAsync(out->y_hat[n], s->zbuf, S * sizeof(double), cudaMemcpyDeviceToHost, st));
   }
   out->has_certificate = 0;
   out->cert_epsilon_hat = out->cert_c = out->cert_bound = 0.0;
   if (want_cert) {
     double eps_hat = 0.0, tl1 = 0.0;
-    abs_stats(s->xbuf, nullptr, &eps_hat);
-    abs_stats(s->T, &tl1, nullptr);
+    abs_stats(s->xbuf, nullptr, &eps_hat, false);
+    abs_stats(s->T, &tl1, nullptr, true);
     eps_hat = allreduce_scalar(eps_hat, RedOp::Max);
     tl1 = allreduce_scalar(tl1, RedOp::Sum);
     const int k_star = c.iter - 1;

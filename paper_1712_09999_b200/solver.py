@@ -104,12 +104,14 @@ def default_rank_bound(target_rank: int) -> int:
 
 def pasd_recover(t, config: PasdConfig, observer=None, *, device: int = 0, fixed_iters: bool = False,
                  want_z: bool = True, want_y: bool = True, poll_every: int = 0,
-                 reuse_solver: bool = False) -> RecoveryResult:
+                 reuse_solver: bool = False, fp32: bool = False) -> RecoveryResult:
     """Drop-in for tenrec::pasd_recover (pasd.hpp:65-66) on a B200.
 
     reuse_solver: keep the device solver for the next call with identical
-    options (PASD_FLAG_REUSE_SOLVER; frees with release_cache())."""
+    options (PASD_FLAG_REUSE_SOLVER; frees with release_cache()).
+    fp32: float32 storage of the element tensors (PASD_FLAG_FP32)."""
     flags = (_abi.PASD_FLAG_FIXED_ITERS if fixed_iters else 0) | (_abi.PASD_FLAG_REUSE_SOLVER if reuse_solver else 0)
+    flags |= _abi.PASD_FLAG_FP32 if fp32 else 0
     return run_recover(lib().pasd_b200_recover, t, config, observer, flags=flags, want_z=want_z, want_y=want_y,
                        device=device, poll_every=poll_every)
 
@@ -133,7 +135,7 @@ class Solver:
     ``t_is_device``, an integer device pointer (e.g. ``torch_tensor.data_ptr()``)."""
 
     def __init__(self, dims: Sequence[int], config: PasdConfig, *, device: int = 0, fixed_iters: bool = False,
-                 poll_every: int = 0, shard: Optional[_abi.PasdShard] = None, flags: int = 0):
+                 poll_every: int = 0, shard: Optional[_abi.PasdShard] = None, flags: int = 0, fp32: bool = False):
         self.dims = [int(d) for d in dims]
         self.local_dims = list(self.dims)
         sh = getattr(shard, "struct", shard)
@@ -141,7 +143,7 @@ class Solver:
             self.local_dims[-1] = int(sh.slab_end - sh.slab_begin)
         self.config = config
         count_checks(self.dims, config)
-        flags = int(flags) | (_abi.PASD_FLAG_FIXED_ITERS if fixed_iters else 0)
+        flags = int(flags) | (_abi.PASD_FLAG_FIXED_ITERS if fixed_iters else 0) | (_abi.PASD_FLAG_FP32 if fp32 else 0)
         self._opt, self._keep = build_options(self.dims, config, device=device, flags=flags, poll_every=poll_every)
         self._h = C.c_void_p()
         err = _err()

@@ -1,0 +1,58 @@
+"""The optional fp32 mode (PASD_FLAG_FP32; BASELINE north_star: "<= 1e-4 for an
+optional fp32 mode"): float32 storage of T, E, D, Y_n with fp64 arithmetic,
+against the fp64 oracle on the same seeded inputs.  The tolerance is the
+north-star's 1e-4 relative Frobenius error on L (= X) and E."""
+import numpy as np
+import pytest
+
+from paper_1712_09999_b200.api import ArgumentError, PasdConfig
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-4  # north_star: L / E relative Frobenius error for the fp32 mode
+
+
+def rel(a, b):
+    n = np.linalg.norm(b)
+    return np.linalg.norm(a - b) / n if n > 0 else np.linalg.norm(a - b)
+
+
+def instance(oracle_mod, dims, r, rho, seed=0):
+    L0 = oracle_mod.gen_tucker(dims, [r] * len(dims), seed=seed)
+    return L0, oracle_mod.corrupt_sparse(L0, rho, seed=seed)
+
+
+@pytest.mark.parametrize("dims,r,R,rho,iters", [
+    ((100, 100, 100), 10, 10, 0.10, 90),   # C1 shape, V = 0 phase (m8 kernels)
+    ((200, 200, 200), 20, 20, 0.20, 200),  # C2, BASELINE fixed count: through the transition, stable
+    ((64, 56, 48), 4, 40, 0.10, 30),       # fused 16x8x8 kernels (RP 40), ragged bricks
+])
+def test_fp32_fixed_iterations_within_tolerance(gpu, oracle_mod, dims, r, R, rho, iters):
+    L0, T = instance(oracle_mod, dims, r, rho)
+    cfg = PasdConfig(lambdas=oracle_mod.default_lambdas(dims), ranks=[R] * 3, maxiter=iters)
+    ro = oracle_mod.pasd_recover(T, cfg, fixed_iters=True, threads=16, want_z=False)
+    rg = gpu.pasd_recover(T, cfg, fixed_iters=True, fp32=True, want_z=False)
+    assert rg.iters == ro.iters == iters
+    assert rel(rg.x, ro.x) <= TOL, rel(rg.x, ro.x)
+    assert rel(rg.e, ro.e) <= TOL, rel(rg.e, ro.e)
+    # the outputs are float32 values widened to float64
+    assert np.array_equal(rg.e.astype(np.float32).astype(np.float64), rg.e)
+
+
+def test_fp32_convergence(gpu, oracle_mod):
+    """C1 recipe at the reference's default eps = 1e-5 (float32 storage bounds
+    the reachable residual near 1e-7 |T|, so tighter eps is not a fp32 target)."""
+    L0, T = instance(oracle_mod, (60, 60, 60), 4, 0.10, seed=2)
+    cfg = PasdConfig(lambdas=oracle_mod.default_lambdas(T.shape), ranks=[4, 4, 4], eps=1e-5)
+    ro = oracle_mod.pasd_recover(T, cfg, threads=16)
+    rg = gpu.pasd_recover(T, cfg, fp32=True)
+    assert rg.converged and ro.converged
+    assert abs(rg.iters - ro.iters) <= 2, (rg.iters, ro.iters)
+    assert rel(rg.x, ro.x) <= TOL, rel(rg.x, ro.x)
+    assert rel(rg.e, ro.e) <= TOL, rel(rg.e, ro.e)
+    assert rg.certificate is not None
+
+
+def test_fp32_rejects_other_orders(gpu):
+    cfg = PasdConfig(lambdas=[1.0] * 4, ranks=[1] * 4, maxiter=2)
+    with pytest.raises(ArgumentError, match="fp32 mode supports order-3"):
+        gpu.pasd_recover(np.ones((3, 3, 3, 3)), cfg, fp32=True)
