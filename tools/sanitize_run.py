@@ -75,6 +75,13 @@ s.close()
 from paper_1712_09999_b200.api import SnnConfig  # noqa: E402
 from paper_1712_09999_b200.sharding import run_loopback  # noqa: E402
 
+# fp32 mode: both pass-2 kernels (m8 at R = 3, the fused one at RP 40) on float32 storage
+T32 = instance((37, 30, 29), 3, 0.05)
+pb.pasd_recover(T32, PasdConfig(lambdas=pb.default_lambdas(T32.shape), ranks=[3, 3, 3], maxiter=160),
+                fixed_iters=True, fp32=True)
+T32 = instance((50, 44, 41), 6, 0.05)
+pb.pasd_recover(T32, PasdConfig(lambdas=pb.default_lambdas(T32.shape), ranks=[40, 40, 40], maxiter=12),
+                fixed_iters=True, fp32=True)
 Ts = instance((20, 18, 16), 2, 0.05, seed=4)
 pb.snn_recover(Ts, SnnConfig(lambdas=pb.default_lambdas(Ts.shape), maxiter=30), fixed_iters=True)
 Tl = instance((26, 24, 29), 3, 0.05, seed=2)
