@@ -17,6 +17,10 @@
 namespace pasd {
 
 constexpr int M8_THREADS = 256;
+#ifndef PASD_M8_CTAS
+#define PASD_M8_CTAS 2  // resident CTAs per SM (register budget 65536 / (256 x CTAS))
+#endif
+constexpr int M8_CTAS = PASD_M8_CTAS;
 constexpr int M8_B = 8;  // brick edge
 
 __device__ __forceinline__ void dmma8(double (&c)[2], double a0, double b0) {
@@ -55,7 +59,7 @@ struct M8Layout {
 
 // EL: storage type of T, E, D, Y_n (float in the fp32 mode; arithmetic in fp64)
 template <int RP, class EL = double>
-__global__ void __launch_bounds__(M8_THREADS, 2) k_pass2_m8(const Pass2Args a, const Ctl* ctl) {
+__global__ void __launch_bounds__(M8_THREADS, M8_CTAS) k_pass2_m8(const Pass2Args a, const Ctl* ctl) {
   if (ctl->done) return;
   using L = M8Layout<RP>;
   constexpr int KS = RP / 4;   // k-steps of the Z products

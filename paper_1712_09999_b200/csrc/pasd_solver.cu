@@ -901,7 +901,7 @@ pasd_solver* create_solver(const pasd_options* o, const pasd_shard* shard) {
     // Segments keep >= 4 steps each so the pencil-resident A_2 slice is reused.
     a.nseg = 1;
     {
-      const int slots = (s->use_m8 ? 2 : 1) * sms;
+      const int slots = (s->use_m8 ? M8_CTAS : 1) * sms;
       const int64_t steps = (s->dims[1] + (s->use_m8 ? M8_B : P2_B2) - 1) / (s->use_m8 ? M8_B : P2_B2);
       // modelled time ~ waves x (steps per item + per-item overhead), the
       // overhead (pencil-resident staging, Wt_1 / Wt_3 partial reductions)
@@ -917,7 +917,7 @@ pasd_solver* create_solver(const pasd_options* o, const pasd_shard* shard) {
         }
       }
     }
-    s->p2_grid = std::max(1, (int)std::min<int64_t>((int64_t)a.npencils * a.nseg, (s->use_m8 ? 2 : 1) * sms));
+    s->p2_grid = std::max(1, (int)std::min<int64_t>((int64_t)a.npencils * a.nseg, (s->use_m8 ? M8_CTAS : 1) * sms));
     // TMA element streams (PASD_P2_TIO=1; needs 16-byte global strides, i.e. I1 even, and the
     // bricks within 227 KB).  Parity-green but slower at C5 (45.7 vs 42.3 ms per launch: the
     // CTA moves to the 228 KB carve-out, the Wt_2/Wt_3 operands are formed from D and Y in the

@@ -20,13 +20,19 @@ T = oracle.corrupt_sparse(L0, 0.10, seed=0)
 cfg = PasdConfig(lambdas=oracle.default_lambdas(dims), ranks=[10, 10, 10], eps=1e-7)
 rse = lambda x: float(np.linalg.norm(x - L0) / np.linalg.norm(L0))  # noqa: E731
 out = {"workload": "c1_100cube_r10 solve to eps 1e-7 (BASELINE configs[0])"}
-pb.pasd_recover(T, cfg)  # warm-up (module load, solver cache)
-ts = []
-for _ in range(5):
-    t0 = time.perf_counter()
-    rg = pb.pasd_recover(T, cfg)
-    ts.append(time.perf_counter() - t0)
-out["gpu"] = {"seconds": float(np.median(ts)), "iters": rg.iters, "converged": rg.converged, "rse": rse(rg.x)}
+pb.pasd_recover(T, cfg)  # warm-up (module load)
+for key, reuse in (("gpu", False), ("gpu_reuse", True)):
+    # gpu: every call builds its solver (allocation, graph capture, teardown);
+    # gpu_reuse: PASD_FLAG_REUSE_SOLVER, the repeated-solve setting (first call excluded)
+    if reuse:
+        pb.pasd_recover(T, cfg, reuse_solver=True)
+    ts = []
+    for _ in range(5):
+        t0 = time.perf_counter()
+        rg = pb.pasd_recover(T, cfg, reuse_solver=reuse)
+        ts.append(time.perf_counter() - t0)
+    out[key] = {"seconds": float(np.median(ts)), "iters": rg.iters, "converged": rg.converged, "rse": rse(rg.x)}
+pb.release_cache()
 for threads in (1, os.cpu_count() or 1):
     t0 = time.perf_counter()
     ro = oracle.pasd_recover(T, cfg, threads=threads)
