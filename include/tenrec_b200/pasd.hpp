@@ -140,6 +140,7 @@ struct PasdConfig {
   int maxiter = 1000;
   std::vector<double> output_weights;
   int device = 0;  // placement (no reference analogue)
+  bool fp32 = false;  // PASD_FLAG_FP32: float32 element storage, fp64 arithmetic (no reference analogue)
 
   const std::vector<double>& alphas() const { return output_weights.empty() ? lambdas : output_weights; }
 
@@ -156,7 +157,7 @@ struct PasdConfig {
     o.eps = eps;
     o.maxiter = maxiter;
     o.device = device;
-    o.flags = PASD_FLAG_NONE;
+    o.flags = fp32 ? PASD_FLAG_FP32 : PASD_FLAG_NONE;
     o.poll_every = 0;
     return o;
   }
@@ -378,6 +379,95 @@ inline Certificate suboptimality_certificate(const RecoveryResult& result, const
                                       &c.bound, err, sizeof(err)),
                 err);
   return c;
+}
+
+// baselines.hpp:9-20 -- the SNN / HoRPCA full-SVT baseline's settings.
+struct SnnConfig {
+  std::vector<double> lambdas;
+  double mu0 = 1e-4;
+  double mu_max = 1e10;
+  double rho = 1.1;
+  double eps = 1e-5;
+  int maxiter = 1000;
+  std::vector<double> output_weights;  // empty = lambdas
+  int device = 0;
+
+  const std::vector<double>& alphas() const { return output_weights.empty() ? lambdas : output_weights; }
+};
+
+// Drop-in for tenrec::snn_recover (baselines.hpp:39-40, baselines.cpp:37-143) on the device.
+// Observer views carry u = v = nullptr, as the reference's; no y_hat, no certificate.
+inline RecoveryResult snn_recover(const DenseTensor& t, const SnnConfig& config,
+                                  const IterationObserver& observer = {}) {
+  const std::vector<Index>& dims = t.dims();
+  const std::size_t n = dims.size();
+  if (config.lambdas.size() != n)  // baselines.cpp:15-17
+    throw ArgumentError("config: expected " + std::to_string(n) + " lambdas, got " +
+                        std::to_string(config.lambdas.size()));
+  if (!config.output_weights.empty() && config.output_weights.size() != n)
+    throw ArgumentError("config: expected " + std::to_string(n) + " output weights");
+  pasd_options o{};
+  o.order = static_cast<int32_t>(n);
+  o.dims = dims.data();
+  o.ranks = nullptr;
+  o.lambdas = config.lambdas.data();
+  o.output_weights = config.output_weights.empty() ? nullptr : config.output_weights.data();
+  o.mu0 = config.mu0;
+  o.mu_max = config.mu_max;
+  o.rho = config.rho;
+  o.eps = config.eps;
+  o.maxiter = config.maxiter;
+  o.device = config.device;
+  RecoveryResult res;
+  res.x = DenseTensor::zeros(dims);
+  res.e = DenseTensor::zeros(dims);
+  res.z.assign(n, DenseTensor::zeros(dims));
+  res.y.assign(n, DenseTensor::zeros(dims));
+  std::vector<double*> zp(n), yp(n);
+  for (std::size_t k = 0; k < n; ++k) {
+    zp[k] = res.z[k].data();
+    yp[k] = res.y[k].data();
+  }
+  res.residual_history.assign(static_cast<std::size_t>(config.maxiter > 0 ? config.maxiter : 1), 0.0);
+  res.final_residuals.assign(n, 0.0);
+  pasd_outputs out{};
+  out.x = res.x.data();
+  out.e = res.e.data();
+  out.z = zp.data();
+  out.y = yp.data();
+  out.residual_history = res.residual_history.data();
+  out.final_residuals = res.final_residuals.data();
+  struct Ctx {
+    const IterationObserver* obs;
+    const std::vector<Index>* dims;
+  } ctx{&observer, &dims};
+  pasd_observer_fn fn = nullptr;
+  if (observer) {
+    fn = [](const pasd_iteration_view* v, void* user) {
+      auto* c = static_cast<Ctx*>(user);
+      const std::vector<Index>& d = *c->dims;
+      const std::size_t N = d.size();
+      Index S = 1;
+      for (Index x : d) S *= x;
+      auto tensor = [&](const double* p) { return DenseTensor::from_data(d, std::vector<double>(p, p + S)); };
+      std::vector<double> resid(v->residual_inf, v->residual_inf + N);
+      const DenseTensor e = tensor(v->e);
+      std::vector<DenseTensor> z, y;
+      for (std::size_t k = 0; k < N; ++k) {
+        z.push_back(tensor(v->z[k]));
+        y.push_back(tensor(v->y[k]));
+      }
+      const IterationView view{v->iter, v->mu_used, v->mu_next, resid, e, z, y, nullptr, nullptr};
+      (*c->obs)(view);
+    };
+  }
+  char err[1024] = {0};
+  detail::check(pasd_b200_snn_recover(t.data(), &o, &out, fn, &ctx, err, sizeof(err)), err);
+  res.iters = out.iters;
+  res.converged = out.converged != 0;
+  res.residual_history.resize(static_cast<std::size_t>(out.iters));
+  res.objective = out.objective;
+  return res;
 }
 
 }  // namespace tenrec_b200

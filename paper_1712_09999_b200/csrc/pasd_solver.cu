@@ -720,7 +720,16 @@ void encode_brick_map(CUtensorMap* map, double* base, const std::vector<int64_t>
     fail(PASD_ERR_CUDA, "pasd_b200: cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
 }
 
+bool trace_on() {
+  static const bool on = std::getenv("PASD_B200_TRACE") != nullptr;
+  return on;
+}
+double trace_ms() {
+  return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
 pasd_solver* create_solver(const pasd_options* o, const pasd_shard* shard) {
+  const double tc0 = trace_on() ? trace_ms() : 0.0;
   validate_options(o);
   auto s = std::make_unique<pasd_solver>();
   s->N = o->order;
@@ -965,8 +974,11 @@ pasd_solver* create_solver(const pasd_options* o, const pasd_shard* shard) {
   }
   s->d_stats = s->alloc<double>(2 * 2048);
   s->d_flag = s->alloc<int>(1);
+  const double tc1 = trace_on() ? trace_ms() : 0.0;
   reset_state(s.get());
   CK(cudaStreamSynchronize(s->stream));
+  if (trace_on())
+    std::fprintf(stderr, "create_solver: buffers/streams %.2f ms, reset %.2f ms\n", tc1 - tc0, trace_ms() - tc1);
   return s.release();
 }
 
@@ -974,10 +986,12 @@ void ensure_scratch(pasd_solver* s);
 
 void build_graph(pasd_solver* s) {
   if (s->graph_exec) return;
+  const double t0 = trace_on() ? trace_ms() : 0.0;
   CK(cudaStreamBeginCapture(s->stream, cudaStreamCaptureModeThreadLocal));
   launch_iteration(s, s->stream);
   CK(cudaStreamEndCapture(s->stream, &s->graph));
   CK(cudaGraphInstantiate(&s->graph_exec, s->graph, 0));
+  if (trace_on()) std::fprintf(stderr, "build_graph: %.2f ms\n", trace_ms() - t0);
 }
 
 void sync_ctl(pasd_solver* s) {
@@ -1557,8 +1571,10 @@ int pasd_b200_solver_ranks(pasd_solver* s, int32_t* svt_keep, int32_t* polar_ran
 
 void pasd_b200_solver_destroy(pasd_solver* s) {
   if (s) {
+    const double t0 = trace_on() ? trace_ms() : 0.0;
     cudaSetDevice(s->device);
     delete s;
+    if (trace_on()) std::fprintf(stderr, "solver_destroy: %.2f ms\n", trace_ms() - t0);
   }
 }
 

@@ -115,3 +115,24 @@ def test_strict_non_convergence_exits_4(client, gpu, tmp_path):
     assert p.returncode == 0
     p = run(client, "recover", "--input", src, "--out-prefix", tmp_path / "s", "--ranks", "9,9,9,9")
     assert p.returncode == 1 and "expected 3 ranks" in p.stderr
+
+
+@pytest.mark.gpu
+def test_recover_snn_solver(client, gpu, tmp_path):
+    """`recover --solver snn` (cli.cpp:278-282) runs the device SNN baseline through the
+    C++ drop-in tenrec_b200::snn_recover: same X / E as the Python binding, no
+    certificate in the manifest; rpca stays outside this build."""
+    src = os.path.join(ROOT, "tests", "golden", "g3_24x20x16_r3_R4", "t.tnsr")
+    out = tmp_path / "snn"
+    p = run(client, "recover", "--input", src, "--out-prefix", out, "--solver", "snn", "--maxiter", 60)
+    assert p.returncode == 0, p.stderr
+    man = manifest(str(out) + ".manifest")
+    assert man["solver"] == "snn" and "ranks" not in man and "cert_epsilon_hat" not in man
+    from paper_1712_09999_b200.api import SnnConfig
+    T = read_tensor(src)
+    r = gpu.snn_recover(T, SnnConfig(lambdas=[float(v) for v in man["lambdas"].split(",")], maxiter=60))
+    assert int(man["iters"]) == r.iters
+    np.testing.assert_array_equal(read_tensor(str(out) + "_x.tnsr"), r.x)
+    np.testing.assert_array_equal(read_tensor(str(out) + "_e.tnsr"), r.e)
+    p = run(client, "recover", "--input", src, "--out-prefix", out, "--solver", "rpca")
+    assert p.returncode == 1 and "rpca" in p.stderr

@@ -4,7 +4,7 @@
 //
 //   synth    --dims --rank|--ranks [--corruption --seed --mode additive|replace255] --out-prefix
 //            (cli.cpp:158-208; generator on the device, pasd_b200_synth)
-//   recover  --input | --from-manifest, --out-prefix, [--truth --strict --no-z --solver pasd
+//   recover  --input | --from-manifest, --out-prefix, [--truth --strict --no-z --solver pasd|snn
 //            --lambdas --ranks --target-rank --alphas --mu0 --mu-max --mu-growth --eps --maxiter]
 //            (cli.cpp:95-130, 210-354)
 //   certify  --manifest [--truth]   (cli.cpp:452-553; nuclear norms on the device)
@@ -413,6 +413,18 @@ PasdConfig build_pasd_config(const SolverOptions& o, const std::vector<Index>& d
   return cfg;
 }
 
+SnnConfig build_snn_config(const SolverOptions& o, const std::vector<Index>& dims) {  // cli.cpp:132-143
+  SnnConfig cfg;
+  cfg.lambdas = o.lambdas.empty() ? PasdConfig::default_lambdas(dims) : o.lambdas;
+  cfg.mu0 = o.mu0;
+  cfg.mu_max = o.mu_max;
+  cfg.rho = o.mu_growth;
+  cfg.eps = o.eps;
+  cfg.maxiter = o.maxiter;
+  cfg.output_weights = o.alphas;
+  return cfg;  // SnnConfig::validate runs inside pasd_b200_snn_recover (baselines.cpp:12-29)
+}
+
 SolverOptions options_from_manifest(const Manifest& m) {  // cli.cpp:222-242
   SolverOptions o;
   o.solver = m.get("solver");
@@ -520,8 +532,8 @@ int do_recover(const std::vector<std::string>& argv) {
   }
   if (input.empty()) throw ArgumentError("recover needs --input (or --from-manifest)");
   if (!a.has("--out-prefix")) throw ArgumentError("recover needs --out-prefix");
-  if (so.solver != "pasd")
-    throw ArgumentError("solver '" + so.solver + "' is not part of this build (PASD hot path only)");
+  if (so.solver == "rpca")
+    throw ArgumentError("solver 'rpca' is not part of this build (PASD hot path and the SNN baseline only)");
   const std::string prefix = a.str("--out-prefix");
   const DenseTensor observed = read_tensor(input);
   const std::vector<Index>& dims = observed.dims();
@@ -533,12 +545,20 @@ int do_recover(const std::vector<std::string>& argv) {
   man.set("input_checksum", checksum_hex(tensor_checksum(observed)));
   man.set_indices("dims", dims);
   const auto start = std::chrono::steady_clock::now();
-  const PasdConfig cfg = build_pasd_config(so, dims);
-  const RecoveryResult res = pasd_recover(observed, cfg);
+  RecoveryResult res;
+  if (so.solver == "pasd") {  // cli.cpp:272-277
+    const PasdConfig cfg = build_pasd_config(so, dims);
+    res = pasd_recover(observed, cfg);
+    man.set_doubles("lambdas", cfg.lambdas);
+    man.set_indices("ranks", cfg.ranks);
+    man.set_doubles("alphas", cfg.alphas());
+  } else {  // snn (cli.cpp:278-282)
+    const SnnConfig cfg = build_snn_config(so, dims);
+    res = snn_recover(observed, cfg);
+    man.set_doubles("lambdas", cfg.lambdas);
+    man.set_doubles("alphas", cfg.alphas());
+  }
   const double elapsed = std::chrono::duration<double>(std::chrono::steady_clock::now() - start).count();
-  man.set_doubles("lambdas", cfg.lambdas);
-  man.set_indices("ranks", cfg.ranks);
-  man.set_doubles("alphas", cfg.alphas());
   man.set_double("mu0", so.mu0);
   man.set_double("mu_max", so.mu_max);
   man.set_double("mu_growth", so.mu_growth);
