@@ -87,7 +87,7 @@ class LoopbackGroup:
 
 def run_loopback(t, config, nranks: int, iters: int, *, fixed_iters: bool = True, slabs=None,
                  check_replicas: bool = True, device: int = 0, poll_every: int = 0, want_z: bool = False,
-                 want_y: bool = False):
+                 want_y: bool = False, fp32: bool = False):
     """Solve `t` (I_1 x I_2 x I_3) as `nranks` mode-3 slabs through the library's
     sharded path on one device (LoopbackGroup).  Returns (iters, converged,
     per-rank finalize() results, slabs)."""
@@ -112,7 +112,7 @@ def run_loopback(t, config, nranks: int, iters: int, *, fixed_iters: bool = True
         try:
             shard = Shard(r, nranks, slabs[r], None, loopback=group)
             sol = Solver(dims, config, device=device, fixed_iters=fixed_iters, poll_every=poll_every,
-                         shard=shard, flags=flags)
+                         shard=shard, flags=flags, fp32=fp32)
             sol.load(np.asfortranarray(t[:, :, slabs[r][0]:slabs[r][1]]))
             done, conv = sol.run(iters)
             results[r] = (done, conv, sol.finalize(want_x=True, want_e=True, want_z=want_z, want_y=want_y))

@@ -58,3 +58,22 @@ def test_fp32_rejects_other_orders(gpu):
     cfg = PasdConfig(lambdas=[1.0] * 4, ranks=[1] * 4, maxiter=2)
     with pytest.raises(ArgumentError, match="fp32 mode supports order-3"):
         gpu.pasd_recover(np.ones((3, 3, 3, 3)), cfg, fp32=True)
+
+
+def test_fp32_sharded_loopback_and_observer(gpu, oracle_mod):
+    """The fp32 mode through the sharded path (3 ragged slabs on one GPU, the loopback
+    group) equals the unsharded fp32 solve bit for bit in the V = 0 phase, and observer
+    views carry the float32 state widened to float64."""
+    from paper_1712_09999_b200.sharding import run_loopback
+
+    L0, T = instance(oracle_mod, (40, 36, 31), 3, 0.10, seed=3)
+    cfg = PasdConfig(lambdas=oracle_mod.default_lambdas(T.shape), ranks=[3, 3, 3], maxiter=20)
+    seen = []
+    r0 = gpu.pasd_recover(T, cfg, fixed_iters=True, fp32=True,
+                          observer=lambda v: seen.append((v.iter, v.e.astype(np.float32).astype(np.float64) == v.e)))
+    assert [s[0] for s in seen] == list(range(1, 21)) and all(s[1].all() for s in seen)
+    it, conv, parts, slabs = run_loopback(T, cfg, 3, 20, fp32=True)
+    e = np.empty(T.shape)
+    for p, (b, en) in zip(parts, slabs):
+        e[:, :, b:en] = p.e
+    np.testing.assert_array_equal(e, r0.e)
