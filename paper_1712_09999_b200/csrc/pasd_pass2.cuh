@@ -39,7 +39,8 @@ namespace pasd {
 #endif
 #ifndef PASD_P2_PROBE
 #define PASD_P2_PROBE 0  // timing probes only (wrong results): 1 = skip the Wt DMMAs, 2 = skip the Z DMMAs,
-                         // 3 = skip both, 4 = skip the elementwise arithmetic (loads and stores stay)
+                         // 3 = skip both, 4 = skip the elementwise arithmetic (loads and stores stay),
+                         // 5 = Z products with the pencil-constant operands loaded once (register reuse bound)
 #endif
 #ifndef PASD_P2_EPF
 #define PASD_P2_EPF 0  // T / Y_n element bricks staged into shared memory with cp.async a step ahead
@@ -562,16 +563,35 @@ __global__ void __launch_bounds__(P2_THREADS, 1) k_pass2_fused(const Pass2Args a
       double z1[4] = {0, 0, 0, 0}, z2[4] = {0, 0, 0, 0}, z3[4] = {0, 0, 0, 0};
       {
         double y1[4] = {0, 0, 0, 0}, y2[4] = {0, 0, 0, 0}, y3[4] = {0, 0, 0, 0};
-#pragma unroll
-        for (int ks = 0; ks < KS; ++ks) {
-          if (ks >= ksz || PASD_P2_PROBE == 2 || PASD_P2_PROBE == 3) break;  // k-steps past max R_n only multiply zero padding
+        // k-steps past max R_n only multiply zero padding: max R_n > RP - 8, so
+        // ksz is KS - 1 or KS.  The first KS - 1 run as straight-line code (no
+        // per-step branch, so the compiler can hoist the next step's operand
+        // loads above this step's DMMAs), the last one behind a single test.
+        auto zstep = [&](int ks) {
           const int k = 4 * ks + t;
           double(&c1)[4] = (ks & 1) ? y1 : z1;
           double(&c2)[4] = (ks & 1) ? y2 : z2;
           double(&c3)[4] = (ks & 1) ? y3 : z3;
-          dmma(c1, U1s[g * L::LDU + k], U1s[(g + 8) * L::LDU + k], A1c[(g + 8 * w) * L::LD1 + k]);
-          dmma(c2, A2s[k * L::LD2 + g + 16 * w], A2s[k * L::LD2 + g + 8 + 16 * w], U2s[g * L::LDU + k]);
-          dmma(c3, A3s[k * L::LD3 + g + 16 * w], A3s[k * L::LD3 + g + 8 + 16 * w], U3s[g * L::LDU + k]);
+          const int kc = PASD_P2_PROBE == 5 ? t : k;  // probe 5: pencil-constant operands loaded once
+          dmma(c1, U1s[g * L::LDU + kc], U1s[(g + 8) * L::LDU + kc], A1c[(g + 8 * w) * L::LD1 + k]);
+          dmma(c2, A2s[kc * L::LD2 + g + 16 * w], A2s[kc * L::LD2 + g + 8 + 16 * w], U2s[g * L::LDU + k]);
+          dmma(c3, A3s[k * L::LD3 + g + 16 * w], A3s[k * L::LD3 + g + 8 + 16 * w], U3s[g * L::LDU + kc]);
+        };
+        if (PASD_P2_PROBE != 2 && PASD_P2_PROBE != 3) {
+          if constexpr (RP >= 48) {
+            // at RP >= 48 the hoisted loads push the kernel to 254 registers and the
+            // Z phase measured slower (C5: 4.5 vs 4.25 k cycles per step): keep one
+            // test per k-step there, which pins each step's loads next to its DMMAs
+#pragma unroll
+            for (int ks = 0; ks < KS; ++ks) {
+              if (ks >= ksz) break;
+              zstep(ks);
+            }
+          } else {  // C3 / C4: 2.13 -> 2.10 / 2.08 -> 2.03 ms per launch
+#pragma unroll
+            for (int ks = 0; ks < KS - 1; ++ks) zstep(ks);
+            if (ksz == KS) zstep(KS - 1);
+          }
         }
 #pragma unroll
         for (int q = 0; q < 4; ++q) {

@@ -228,9 +228,9 @@ __global__ void __launch_bounds__(M8_THREADS, M8_CTAS) k_pass2_m8(const Pass2Arg
       double z1[2] = {0, 0}, z2[2] = {0, 0}, z3[2] = {0, 0};
       {
         double y1[2] = {0, 0}, y2[2] = {0, 0}, y3[2] = {0, 0};
-#pragma unroll
-        for (int ks = 0; ks < KS; ++ks) {
-          if (ks >= ksz) break;  // k-steps past max R_n only multiply zero padding
+        // k-steps past max R_n only multiply zero padding; ksz is KS - 1 or KS
+        // (RP = max R_n rounded up to 8), so the first KS - 1 run branch-free
+        auto zstep = [&](int ks) {
           const int k = 4 * ks + t;
           double(&c1)[2] = (ks & 1) ? y1 : z1;
           double(&c2)[2] = (ks & 1) ? y2 : z2;
@@ -238,7 +238,10 @@ __global__ void __launch_bounds__(M8_THREADS, M8_CTAS) k_pass2_m8(const Pass2Arg
           dmma8(c1, U1s[swu<RP>(g, k)], A1s[sw(k, g + 8 * w)]);  // rows i1, cols i2 at i3 = w
           dmma8(c2, A2s[sw(k, g + 8 * w)], U2s[swu<RP>(g, k)]);  // rows i1, cols i2 at i3 = w
           dmma8(c3, A3s[sw(k, g + 8 * w)], U3s[swu<RP>(g, k)]);  // rows i1, cols i3 at i2 = w
-        }
+        };
+#pragma unroll
+        for (int ks = 0; ks < KS - 1; ++ks) zstep(ks);
+        if (ksz == KS) zstep(KS - 1);
         z1[0] += y1[0]; z1[1] += y1[1];
         z2[0] += y2[0]; z2[1] += y2[1];
         z3[0] += y3[0]; z3[1] += y3[1];
