@@ -106,14 +106,20 @@ def run_loopback(t, config, nranks: int, iters: int, *, fixed_iters: bool = True
     flags = A.PASD_FLAG_CHECK_REPLICAS if check_replicas else 0
     results = [None] * nranks
     errors = [None] * nranks
+    ready = threading.Barrier(nranks)  # no rank enters a collective unless every rank was built
 
     def rank_main(r):
         sol = None
         try:
-            shard = Shard(r, nranks, slabs[r], None, loopback=group)
-            sol = Solver(dims, config, device=device, fixed_iters=fixed_iters, poll_every=poll_every,
-                         shard=shard, flags=flags, fp32=fp32)
-            sol.load(np.asfortranarray(t[:, :, slabs[r][0]:slabs[r][1]]))
+            try:
+                shard = Shard(r, nranks, slabs[r], None, loopback=group)
+                sol = Solver(dims, config, device=device, fixed_iters=fixed_iters, poll_every=poll_every,
+                             shard=shard, flags=flags, fp32=fp32)
+                sol.load(np.asfortranarray(t[:, :, slabs[r][0]:slabs[r][1]]))
+            except BaseException:
+                ready.abort()
+                raise
+            ready.wait()
             done, conv = sol.run(iters)
             results[r] = (done, conv, sol.finalize(want_x=True, want_e=True, want_z=want_z, want_y=want_y))
         except BaseException as exc:  # re-raised on the caller's thread
@@ -128,9 +134,9 @@ def run_loopback(t, config, nranks: int, iters: int, *, fixed_iters: bool = True
     for th in threads:
         th.join()
     group.close()
-    for exc in errors:
-        if exc is not None:
-            raise exc
+    real = [e for e in errors if e is not None and not isinstance(e, threading.BrokenBarrierError)]
+    if real or any(e is not None for e in errors):
+        raise (real or [e for e in errors if e is not None])[0]
     done = {r[0] for r in results}
     conv = {r[1] for r in results}
     if len(done) != 1 or len(conv) != 1:

@@ -118,3 +118,17 @@ def test_two_rank_reductions_match_unsharded():
     for _, errs, _ in res:
         for k, v in errs.items():
             assert v <= 1e-12, (k, v)
+
+
+def test_loopback_group_rejects_bad_sizes():
+    """pasd_b200_loopback_create validates its size before any device work."""
+    import paper_1712_09999_b200  # noqa: F401
+    from paper_1712_09999_b200.api import ArgumentError
+    from paper_1712_09999_b200.sharding import LoopbackGroup
+
+    for n in (0, 9):
+        with pytest.raises(ArgumentError, match="loopback groups hold 1..8 ranks"):
+            LoopbackGroup(n)
+    g = LoopbackGroup(3)
+    assert g.handle
+    g.close()
