@@ -105,6 +105,10 @@ __global__ void __launch_bounds__(M8_THREADS, M8_CTAS) k_pass2_m8(const Pass2Arg
   const int64_t S12 = I1 * I2;
   const int ksz = (max(R1, max(R2, R3)) + 3) / 4;  // Z k-steps that touch a nonzero rank row
   const bool al1 = (I1 % 2) == 0;
+#if PASD_P2_TIMING
+  unsigned long long ph_acc[12] = {};
+  long long ph_t = clock64();
+#endif
 
   // Work items: pencil x i2 segment (segments keep small tensors, where the
   // pencil count is near the CTA count, from ending on a partial wave).
@@ -222,8 +226,11 @@ __global__ void __launch_bounds__(M8_THREADS, M8_CTAS) k_pass2_m8(const Pass2Arg
     load_elems(i2b);
 
     for (int64_t i2o = i2b; i2o < i2e; i2o += M8_B) {
+      P2T(0);
       cp_async_wait_all();
+      P2T(1);
       __syncthreads();
+      P2T(2);
       // ---- Z products: three 8x8 tiles per warp, 2 chains each ----
       double z1[2] = {0, 0}, z2[2] = {0, 0}, z3[2] = {0, 0};
       {
@@ -248,7 +255,9 @@ __global__ void __launch_bounds__(M8_THREADS, M8_CTAS) k_pass2_m8(const Pass2Arg
       }
       Zx[z8x(g, w, 2 * t)] = z3[0];
       Zx[z8x(g, w, 2 * t + 1)] = z3[1];
+      P2T(3);
       __syncthreads();
+      P2T(4);
       // ---- elementwise (reference op order, no FMA contraction) ----
       double g1v[2];
 #pragma unroll
@@ -287,7 +296,9 @@ __global__ void __launch_bounds__(M8_THREADS, M8_CTAS) k_pass2_m8(const Pass2Arg
       }
       const bool more = i2o + M8_B < i2e;
       if (more) load_elems(i2o + M8_B);  // next step's T, Y in flight during the Wt products
+      P2T(5);
       __syncthreads();
+      P2T(6);
       // ---- Wt_1: A operand = own G_1 (cols permuted: lane t supplies i2 = 2t + p) ----
 #pragma unroll
       for (int p = 0; p < 2; ++p) {
@@ -335,8 +346,11 @@ __global__ void __launch_bounds__(M8_THREADS, M8_CTAS) k_pass2_m8(const Pass2Arg
           }
         }
       }
+      P2T(7);
       __syncthreads();  // A1s / A3s / U2s free: stage the next step under the Wt_2 flush
+      P2T(8);
       if (more) stage_step(i2o + M8_B);
+      P2T(9);
       if (w < 4) {
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
@@ -351,6 +365,7 @@ __global__ void __launch_bounds__(M8_THREADS, M8_CTAS) k_pass2_m8(const Pass2Arg
           }
         }
       }
+      P2T(10);
     }
     // ---- end of pencil: Wt_1 (sum of the 8 warps' column sets) and Wt_3 ----
     __syncthreads();
@@ -391,6 +406,11 @@ __global__ void __launch_bounds__(M8_THREADS, M8_CTAS) k_pass2_m8(const Pass2Arg
       if (r >= Rn) sm[idx] = 0.0;
     }
   }
+#if PASD_P2_TIMING
+  P2T(11);
+  if (tid == 0)
+    for (int k = 0; k < 12; ++k) atomicAdd(&g_p2_phase[k], ph_acc[k]);
+#endif
   for (int n = 0; n < 3; ++n) {
     const double wv = block_reduce(worst[n], MaxOp(), red);
     const double gv = block_reduce(gsq[n], AddOp(), red);

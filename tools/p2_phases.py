@@ -33,8 +33,9 @@ L.pasd_b200_debug_p2_phases(out)  # reset
 prof = sol.profile(2)
 L.pasd_b200_debug_p2_phases(out)
 cyc = np.array(out[:])
-steps = 2 * w.size / 1024.0
-print(f"{w.name}: pass 2 {prof['update']['ms'] / 2:.2f} ms/launch; warp-0 cycles per 16x8x8 step by phase:")
+brick = 512.0 if max(w.ranks) <= 24 else 1024.0  # k_pass2_m8: 8x8x8 bricks
+steps = 2 * w.size / brick
+print(f"{w.name}: pass 2 {prof['update']['ms'] / 2:.3f} ms/launch; warp-0 cycles per {int(brick)}-element step:")
 for n, c in zip(NAMES, cyc):
     print(f"  {n:28s} {c / cyc.sum() * 100:5.1f}%  {c / steps:8.0f} cyc/step")
 print(f"  {'total':28s}        {cyc.sum() / steps:8.0f} cyc/step (summed over CTAs / steps)")
