@@ -60,10 +60,11 @@ def load_peaks():
         peaks["source_hbm"] = "measured (MEASURED_PEAKS.json)"
     except Exception:
         pass
-    # FP64 pipe: measured on this pool with tools/fp64_peak.cu (profiles/r01_fp64_peak.txt):
-    # DMMA m16n8k4 37.0 TF/s, DFMA 34.1 TF/s (burst).
+    # FP64 tensor pipe: measured on this pool with tools/fp64_peak.sh (profiles/r02_fp64_peak.txt):
+    # DMMA m16n8k4 37.0 TF/s burst, 36.9 sustained over 5 s at 1965 MHz (no throttle reason);
+    # DFMA 34.1.  The burst figure is the (larger, so stricter) denominator.
     peaks["fp64_tflops"] = 37.0
-    peaks["source_fp64"] = "measured DMMA burst, profiles/r01_fp64_peak.txt"
+    peaks["source_fp64"] = "measured DMMA burst 37.0 (36.9 sustained), profiles/r02_fp64_peak.txt"
     return peaks
 
 
@@ -326,7 +327,9 @@ def roofline_from_profile(prof, peaks, iters, workload):
     total_ms = sum(v["ms"] for v in prof.values())
     shares = {k: round(v["ms"] / total_ms, 4) for k, v in prof.items()}
     if intensity > ridge:
-        r = {"bound": "fp64", "achieved": round(tfs, 3), "peak": peaks["fp64_tflops"], "unit": "TFLOP/s",
+        # FP64 tensor-core (DMMA) bound: "tensor" in the contract's vocabulary
+        r = {"bound": "tensor", "pipe": "fp64 DMMA", "achieved": round(tfs, 3), "peak": peaks["fp64_tflops"],
+             "unit": "TFLOP/s",
              "frac": round(fp_frac, 4), "peak_source": peaks["source_fp64"]}
     else:
         r = {"bound": "hbm", "achieved": round(gbs, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
@@ -346,7 +349,7 @@ def roofline_from_profile(prof, peaks, iters, workload):
         t = f_l / (ms_l * 1e-3) / 1e12
         fp = f_l / max(1.0, b_l) > ridge
         per[k] = {"ms_per_launch": round(ms_l, 4), "hbm_gbs": round(g, 1), "fp64_tflops": round(t, 3),
-                  "bound": "fp64" if fp else "hbm",
+                  "bound": "tensor" if fp else "hbm",
                   "frac": round(t / peaks["fp64_tflops"] if fp else g / peaks["hbm_gbs"], 4)}
     r["per_kernel"] = per
     return r
