@@ -48,9 +48,6 @@ namespace pasd {
 #ifndef PASD_P2_WS
 #define PASD_P2_WS 1  // warps 0-3 run the Wt_2 products over the full K while warps 4-7 issue the next staging
 #endif
-#ifndef PASD_P2_ZPIPE
-#define PASD_P2_ZPIPE 0  // RP >= 48: Z products with an explicit two-stage operand pipeline
-#endif
 #ifndef PASD_P2_TIMING
 #define PASD_P2_TIMING 0  // probe build: per-phase clock64() sums of warp 0 (pasd_b200_debug_p2_phases)
 #endif
@@ -581,38 +578,10 @@ __global__ void __launch_bounds__(P2_THREADS, 1) k_pass2_fused(const Pass2Args a
           dmma(c3, A3s[k * L::LD3 + g + 16 * w], A3s[k * L::LD3 + g + 8 + 16 * w], U3s[g * L::LDU + kc]);
         };
         if (PASD_P2_PROBE != 2 && PASD_P2_PROBE != 3) {
-          if constexpr (RP >= 48 && PASD_P2_ZPIPE) {
-            // explicit two-stage operand pipeline: the next k-step's 9 operands are
-            // loaded before this k-step's 3 DMMAs (a rolled loop: no register blow-up)
-            auto ld = [&](int ks, double (&o)[9]) {
-              const int k = 4 * ks + t;
-              o[0] = U1s[g * L::LDU + k];
-              o[1] = U1s[(g + 8) * L::LDU + k];
-              o[2] = A1c[(g + 8 * w) * L::LD1 + k];
-              o[3] = A2s[k * L::LD2 + g + 16 * w];
-              o[4] = A2s[k * L::LD2 + g + 8 + 16 * w];
-              o[5] = U2s[g * L::LDU + k];
-              o[6] = A3s[k * L::LD3 + g + 16 * w];
-              o[7] = A3s[k * L::LD3 + g + 8 + 16 * w];
-              o[8] = U3s[g * L::LDU + k];
-            };
-            double cur[9], nxt[9];
-            ld(0, cur);
-#pragma unroll 1
-            for (int ks = 0; ks < ksz; ks += 2) {
-              if (ks + 1 < ksz) ld(ks + 1, nxt);
-              dmma(z1, cur[0], cur[1], cur[2]);
-              dmma(z2, cur[3], cur[4], cur[5]);
-              dmma(z3, cur[6], cur[7], cur[8]);
-              if (ks + 1 >= ksz) break;
-              if (ks + 2 < ksz) ld(ks + 2, cur);
-              dmma(y1, nxt[0], nxt[1], nxt[2]);
-              dmma(y2, nxt[3], nxt[4], nxt[5]);
-              dmma(y3, nxt[6], nxt[7], nxt[8]);
-            }
-          } else if constexpr (RP >= 48) {
+          if constexpr (RP >= 48) {
             // at RP >= 48 the hoisted loads push the kernel to 254 registers and the
-            // Z phase measured slower (C5: 4.5 vs 4.25 k cycles per step): keep one
+            // Z phase measured slower (C5: 4.5 vs 4.25 k cycles per step), as did an
+            // explicit two-stage operand pipeline in a rolled loop (5.2 k): keep one
             // test per k-step there, which pins each step's loads next to its DMMAs
 #pragma unroll
             for (int ks = 0; ks < KS; ++ks) {
