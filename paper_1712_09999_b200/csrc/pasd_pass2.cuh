@@ -40,7 +40,8 @@ namespace pasd {
 #ifndef PASD_P2_PROBE
 #define PASD_P2_PROBE 0  // timing probes only (wrong results): 1 = skip the Wt DMMAs, 2 = skip the Z DMMAs,
                          // 3 = skip both, 4 = skip the elementwise arithmetic (loads and stores stay),
-                         // 5 = Z products with the pencil-constant operands loaded once (register reuse bound)
+                         // 5 = Z products with the pencil-constant operands loaded once (register reuse bound),
+                         // 6 = no element stores (E, D, Y_n), 7 = no element loads (T, Y_n)
 #endif
 #ifndef PASD_P2_EPF
 #define PASD_P2_EPF 0  // T / Y_n element bricks staged into shared memory with cp.async a step ahead
@@ -48,14 +49,22 @@ namespace pasd {
 #ifndef PASD_P2_WS
 #define PASD_P2_WS 1  // warps 0-3 run the Wt_2 products over the full K while warps 4-7 issue the next staging
 #endif
+#ifndef PASD_P2_TIL
+#define PASD_P2_TIL 1  // TMA variant (TIO) loads only: the T, Y_n bricks of the next step arrive by TMA (requested
+                       // right after the elementwise phase), E / D / Y_n leave by plain stores, G_2 / G_3 go
+                       // through the padded exchange buffers (0: loads and stores by TMA, six bricks)
+#endif
 #ifndef PASD_P2_TIMING
 #define PASD_P2_TIMING 0  // probe build: per-phase clock64() sums of warp 0 (pasd_b200_debug_p2_phases)
+#endif
+#ifndef PASD_P2_TWARP
+#define PASD_P2_TWARP 0  // the warp whose lane 0 records the phase clocks
 #endif
 #if PASD_P2_TIMING
 __device__ unsigned long long g_p2_phase[12];
 #define P2T(k)                                   \
   do {                                           \
-    if (tid == 0) {                              \
+    if (tid == 32 * PASD_P2_TWARP) {             \
       const long long now_ = clock64();          \
       ph_acc[k] += (unsigned long long)(now_ - ph_t); \
       ph_t = now_;                               \
@@ -100,6 +109,7 @@ struct Pass2Args {
 // shared memory as [l2][l3][l1] and the Wt_3 operand reads are conflict-free.
 struct P2Tmaps {
   CUtensorMap t, y1, y2, y3b;  // loads
+  CUtensorMap y3a;             // Y_3 in the A layout (PASD_P2_TIL)
   CUtensorMap e0, e1, d;       // stores (E double buffer: the kernel writes E[ecur ^ 1])
 };
 
@@ -222,13 +232,14 @@ struct P2Layout {
   // bricks (T->E, Y_1, Y_2, Y_3 [B layout], D, D [B layout]) read by the
   // Wt_2 / Wt_3 products directly (G = D + Y/mu formed in the fragment load).
   static constexpr int oG2 = oZ3 + 8 * 182;
-  static constexpr int oG3 = oG2 + (TIO ? 0 : 8 * 160);
-  static constexpr int oRed = oG3 + (TIO ? 0 : 8 * 180);
+  static constexpr bool TIL = TIO && PASD_P2_TIL;  // TMA loads only: four bricks (T, Y_1..3) + the exchange buffers
+  static constexpr int oG3 = oG2 + (TIO && !TIL ? 0 : 8 * 160);
+  static constexpr int oRed = oG3 + (TIO && !TIL ? 0 : 8 * 180);
   static constexpr int oBrick = oRed + 64;              // + runtime 1024-byte alignment
   // plain I/O with PASD_P2_EPF: the next step's T, Y_1..3 bricks (4 x 1024, swizzled rows)
   static constexpr bool EPF =
       !TIO && PASD_P2_EPF && sizeof(double) * (size_t)(oBrick + 4 * P2_BRICK) <= 227u * 1024u;
-  static constexpr int total = oBrick + (TIO ? 6 * P2_BRICK + 128 : (EPF ? 4 * P2_BRICK : 0));
+  static constexpr int total = oBrick + (TIO ? (TIL ? 4 : 6) * P2_BRICK + 128 : (EPF ? 4 * P2_BRICK : 0));
   static constexpr size_t bytes = sizeof(double) * (size_t)total;
   static_assert((RM - RP) * LD3 <= total - oU1, "M-tile overrun must stay inside shared memory");
   static_assert(128 * RP <= oA3 + RP * LD3, "end-of-pencil scratch must fit in A1s..A3s");
@@ -290,7 +301,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* mbar, unsigned parity) {
 // launch; at RP <= 40 (C3) the split Wt_2 partials it gives up were worth more.
 template <int RP, bool TIO>
 __host__ __device__ constexpr bool pass2_ws() {
-  return !TIO && PASD_P2_WS && RP >= 48;
+  return (!TIO || PASD_P2_TIL) && PASD_P2_WS && RP >= 48;
 }
 
 // RP = common padded rank (multiple of 8, >= every R_n); rows r >= R_n of each
@@ -308,6 +319,7 @@ __global__ void __launch_bounds__(P2_THREADS, 1) k_pass2_fused(const Pass2Args a
   constexpr int NT1 = RP / 8;  // n-tiles of the Wt_1 product
   constexpr int MT = L::RM / 16;
   constexpr bool WS = pass2_ws<RP, TIO>();  // warp-specialised Wt_2 / staging phase
+  constexpr bool TIL = L::TIL;              // TMA loads only (see PASD_P2_TIL)
   extern __shared__ double sm[];
   const ModeDev& m1 = a.m[0];
   const ModeDev& m2 = a.m[1];
@@ -353,11 +365,22 @@ __global__ void __launch_bounds__(P2_THREADS, 1) k_pass2_fused(const Pass2Args a
   for (int idx = tid; idx < (RP - R2) * 128; idx += P2_THREADS) A2s[(R2 + idx / 128) * L::LD2 + (idx & 127)] = 0.0;
   for (int idx = tid; idx < (RP - R3) * 128; idx += P2_THREADS) A3s[(R3 + idx / 128) * L::LD3 + (idx & 127)] = 0.0;
   for (int idx = tid; idx < L::oBrick - L::oU1; idx += P2_THREADS) U1s[idx] = 0.0;  // UM rows, exchange buffers
-  if (TIO && tid == 0) mbar_init(mbar);
+  if (TIO && tid == 0) {
+    mbar_init(mbar);
+  }
   __syncthreads();
   // TIO: the next brick's T, Y_1..3 (after the previous stores have read the bricks)
   auto load_bricks = [&](int64_t i1o_, int64_t i2o_, int64_t i3o_) {
-    if (TIO && tid == 0) {
+    if (TIL) {  // all four in the A layout; their slots are free once the elementwise phase has read them
+      if (tid == 0 && PASD_P2_PROBE != 7) {
+        mbar_expect(mbar, 4u * P2_BRICK * sizeof(double));
+        const int c0 = (int)i1o_, c1 = (int)i2o_, c2 = (int)i3o_;
+        tma_load3(brk, &tm.t, mbar, c0, c1, c2);
+        tma_load3(brk + P2_BRICK, &tm.y1, mbar, c0, c1, c2);
+        tma_load3(brk + 2 * P2_BRICK, &tm.y2, mbar, c0, c1, c2);
+        tma_load3(brk + 3 * P2_BRICK, &tm.y3a, mbar, c0, c1, c2);
+      }
+    } else if (TIO && tid == 0) {
       asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
       mbar_expect(mbar, 4u * P2_BRICK * sizeof(double));
       const int c0 = (int)i1o_, c1 = (int)i2o_, c2 = (int)i3o_;
@@ -514,9 +537,10 @@ __global__ void __launch_bounds__(P2_THREADS, 1) k_pass2_fused(const Pass2Args a
         const int64_t i1 = i1o + g + 8 * (q >> 1), i2 = i2o + 2 * t + (q & 1), i3 = i3o + w;
         inb[q] = i1 < I1 && i2 < I2 && i3 < I3;
         off[q] = i1 + I1 * i2 + S12 * i3;
-        tv[q] = inb[q] ? T[off[q]] : 0.0;
+        const bool ld = inb[q] && PASD_P2_PROBE != 7;
+        tv[q] = ld ? T[off[q]] : 0.0;
 #pragma unroll
-        for (int n = 0; n < 3; ++n) yv[n][q] = inb[q] ? (double)Yp[n][off[q]] : 0.0;
+        for (int n = 0; n < 3; ++n) yv[n][q] = ld ? (double)Yp[n][off[q]] : 0.0;
       }
     };
     // PASD_P2_EPF: this thread's 8 copies of a step's T, Y_1..3 brick (stream ts,
@@ -658,12 +682,12 @@ __global__ void __launch_bounds__(P2_THREADS, 1) k_pass2_fused(const Pass2Args a
               const double ar = fabs(r);
               if (ar > worst[n]) worst[n] = ar;
               bad |= !isfinite(r);
-              Yp[n][off[q]] = (EL)ynew;
+              if (PASD_P2_PROBE != 6) Yp[n][off[q]] = (EL)ynew;
             }
             gn[n] = inb[q] ? g_elem(tt, e, ynew, inv_mu_next) : 0.0;  // next G_n
             gsq[n] = fma(gn[n], gn[n], gsq[n]);
           }
-          if (inb[q]) {
+          if (inb[q] && PASD_P2_PROBE != 6) {
             Enew[off[q]] = (EL)e;
             Dp[off[q]] = (EL)__dsub_rn(tt, e);  // next pass 1 reads D = T - E
           }
@@ -679,12 +703,51 @@ __global__ void __launch_bounds__(P2_THREADS, 1) k_pass2_fused(const Pass2Args a
         // T, Y_n from the TMA bricks; E, D, Y_n written back in place.  Entries
         // outside the tensor arrive as zeros (TMA fill) with zero Z, so they
         // produce zeros everywhere and the stores clip them.
-        mbar_wait(mbar, mph);
+        if (!(TIL && PASD_P2_PROBE == 7)) mbar_wait(mbar, mph);
         mph ^= 1;
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
           const int l1 = g + 8 * (q >> 1), l2 = 2 * t + (q & 1);
           const int pa = swzA(l1, l2, w), pb = swzB(l1, l2, w);
+          if constexpr (TIL) {
+            // loads from the bricks, plain stores
+            const int64_t i1 = i1o + l1, i2 = i2o + l2, i3 = i3o + w;
+            const bool in = i1 < I1 && i2 < I2 && i3 < I3;
+            const int64_t o = i1 + I1 * i2 + S12 * i3;
+            const double zz[3] = {z1[q], z2[q], Z3s[zx(l1, l2, w)]};
+            const double tt = brk[pa];
+            const double yq[3] = {brk[P2_BRICK + pa], brk[2 * P2_BRICK + pa], brk[3 * P2_BRICK + pa]};
+            double zt[3], h = 0.0;
+#pragma unroll
+            for (int n = 0; n < 3; ++n) {
+              zt[n] = __dsub_rn(tt, zz[n]);
+              h = __dadd_rn(h, __dadd_rn(zt[n], __dmul_rn(yq[n], inv_mu)));  // pasd.cpp:202
+            }
+            const double e = soft(__dmul_rn(h, inv_n), tau);  // pasd.cpp:208
+            double gn[3];
+#pragma unroll
+            for (int n = 0; n < 3; ++n) {
+              const double r = __dsub_rn(zt[n], e);                    // pasd.cpp:220
+              const double ynew = __dadd_rn(yq[n], __dmul_rn(mu, r));  // pasd.cpp:221
+              if (in) {
+                const double ar = fabs(r);
+                if (ar > worst[n]) worst[n] = ar;
+                bad |= !isfinite(r);
+                if (PASD_P2_PROBE != 6) Yp[n][o] = (EL)ynew;
+              }
+              gn[n] = in ? g_elem(tt, e, ynew, inv_mu_next) : 0.0;  // next G_n
+              gsq[n] = fma(gn[n], gn[n], gsq[n]);
+            }
+            if (in && PASD_P2_PROBE != 6) {
+              Enew[o] = (EL)e;
+              Dp[o] = (EL)__dsub_rn(tt, e);  // next pass 1 reads D = T - E
+            }
+            g1v[q] = gn[0];
+            G2s[g2x(l1, l2, w)] = gn[1];
+            G3s[g3x(l1, l2, w)] = gn[2];
+            (void)pb;
+            continue;
+          }
           const double zz[3] = {z1[q], z2[q], Z3s[zx(l1, l2, w)]};
           const double tt = brk[pa];
           const double yq[3] = {brk[P2_BRICK + pa], brk[2 * P2_BRICK + pa], brk[3 * P2_BRICK + pb]};
@@ -719,7 +782,8 @@ __global__ void __launch_bounds__(P2_THREADS, 1) k_pass2_fused(const Pass2Args a
       __syncthreads();  // G exchange / bricks complete
       P2T(6);  // 6: barrier C
       if (L::EPF && !WS && more) stage_elems(i2o + P2_B2, tid, All{});  // the element bricks are consumed: next step's
-      if (TIO && tid == 0) {  // E, Y_1..3, D of this brick: TMA tensor stores
+      if (TIL && more) load_bricks(i1o, i2o + P2_B2, i3o);  // the bricks are consumed: next step's T, Y_n
+      if (TIO && !TIL && tid == 0) {  // E, Y_1..3, D of this brick: TMA tensor stores
         const int c0 = (int)i1o, c1 = (int)i2o, c2 = (int)i3o;
         tma_store3(ctl->ecur ? &tm.e0 : &tm.e1, brk, c0, c1, c2);
         tma_store3(&tm.y1, brk + P2_BRICK, c0, c1, c2);
@@ -749,7 +813,7 @@ __global__ void __launch_bounds__(P2_THREADS, 1) k_pass2_fused(const Pass2Args a
           const int k = 64 * kh + 4 * ks + t;
           double(&c)[4] = (ks & 3) == 0 ? w3acc : acc[(ks & 3) - 1];
           double b3;
-          if constexpr (TIO) {  // G_3 at (i1 = k & 15, i2 = k >> 4, i3 = g) from the B-layout bricks
+          if constexpr (TIO && !TIL) {  // G_3 at (i1 = k & 15, i2 = k >> 4, i3 = g) from the B-layout bricks
             const int pb = swzB(k & 15, k >> 4, g);
             b3 = __dadd_rn(brk[5 * P2_BRICK + pb], __dmul_rn(brk[3 * P2_BRICK + pb], inv_mu_next));
           } else {
@@ -820,7 +884,7 @@ __global__ void __launch_bounds__(P2_THREADS, 1) k_pass2_fused(const Pass2Args a
           const int k = 64 * kh + 4 * ks + t;
           double(&c)[4] = (ks & 3) == 0 ? acc2 : acc[(ks & 3) - 1];
           double b2;
-          if constexpr (TIO) {  // G_2 at (i1 = k & 15, i2 = g, i3 = k >> 4) from the A-layout bricks
+          if constexpr (TIO && !TIL) {  // G_2 at (i1 = k & 15, i2 = g, i3 = k >> 4) from the A-layout bricks
             const int pa = swzA(k & 15, g, k >> 4);
             b2 = __dadd_rn(brk[4 * P2_BRICK + pa], __dmul_rn(brk[2 * P2_BRICK + pa], inv_mu_next));
           } else {
@@ -835,12 +899,12 @@ __global__ void __launch_bounds__(P2_THREADS, 1) k_pass2_fused(const Pass2Args a
           for (int q = 0; q < 4; ++q) Z3s[(mt * 32 + lane) * 4 + q] = acc2[q];  // exchange (Z3s free now)
         }
       }
-      if (TIO || (!w2s && !PASD_P2_PAIRBAR)) {
+      if ((TIO && !TIL) || (!w2s && !PASD_P2_PAIRBAR)) {
         __syncthreads();
       } else if (!w2s && mt < MT) {  // only the two K-half warps of m-tile mt exchange
         asm volatile("bar.sync %0, 64;" ::"r"(1 + mt) : "memory");
       }
-      if (more) load_bricks(i1o, i2o + P2_B2, i3o);  // the bricks are free: next step's T, Y (TIO)
+      if (more && !TIL) load_bricks(i1o, i2o + P2_B2, i3o);  // the bricks are free: next step's T, Y (TIO)
       if (w2s && mt < MT) {
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
@@ -901,10 +965,10 @@ __global__ void __launch_bounds__(P2_THREADS, 1) k_pass2_fused(const Pass2Args a
   }
 #if PASD_P2_TIMING
   P2T(11);  // 11: pencil ends (reductions, restores)
-  if (tid == 0)
+  if (tid == 32 * PASD_P2_TWARP)
     for (int k = 0; k < 12; ++k) atomicAdd(&g_p2_phase[k], ph_acc[k]);
 #endif
-  if (TIO && tid == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // element stores done
+  if (TIO && !TIL && tid == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // element stores done
   // ---- per-CTA residual / NaN / ||G||^2 partials ----
   for (int n = 0; n < 3; ++n) {
     const double wv = block_reduce(worst[n], MaxOp(), red);

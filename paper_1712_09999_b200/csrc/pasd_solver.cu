@@ -951,6 +951,7 @@ pasd_solver* create_solver(const pasd_options* o, const pasd_shard* shard) {
       encode_brick_map(&s->p2_tmaps.y1, s->Y[0], da, sa);
       encode_brick_map(&s->p2_tmaps.y2, s->Y[1], da, sa);
       encode_brick_map(&s->p2_tmaps.y3b, s->Y[2], db, sb);
+      encode_brick_map(&s->p2_tmaps.y3a, s->Y[2], da, sa);
       encode_brick_map(&s->p2_tmaps.e0, s->E[0], da, sa);
       encode_brick_map(&s->p2_tmaps.e1, s->E[1], da, sa);
       encode_brick_map(&s->p2_tmaps.d, s->D, da, sa);
@@ -962,7 +963,7 @@ pasd_solver* create_solver(const pasd_options* o, const pasd_shard* shard) {
     // (C3 38 MB, C4 18 MB: one barrier per step fewer, -2..5% pass 2); at C5 the
     // 118 MB they would take thrash L2 (+1 ms), so one per CTA there.
     const double w2_split_bytes = 2.0 * s->p2_grid * (double)s->dims[1] * s->modes[1].R * sizeof(double);
-    const bool ws = !s->use_m8 && !s->p2_tio && PASD_P2_WS && s->p2_rp >= 48;  // pass2_ws<RP, false>()
+    const bool ws = !s->use_m8 && (!s->p2_tio || PASD_P2_TIL) && PASD_P2_WS && s->p2_rp >= 48;  // pass2_ws<RP, TIO>()
     a.nw2 = (!s->use_m8 && !s->p2_tio && !ws && w2_split_bytes <= 48e6) ? 2 * s->p2_grid : s->p2_grid;
     a.W2part = s->alloc<double>((size_t)a.nw2 * s->dims[1] * s->modes[1].R);
     a.gpart = s->alloc<double>((size_t)s->p2_grid * 3);

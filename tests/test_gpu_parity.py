@@ -261,16 +261,18 @@ def test_sharded_single_rank_matches_unsharded(gpu, oracle_mod):
     assert r0.certificate.epsilon_hat == r1.certificate.epsilon_hat
 
 
-def test_tma_element_streams_match_plain(monkeypatch):
-    """k_pass2_fused<RP, true> (T/Y loads and E/D/Y stores through TMA bricks)
-    gives bit-identical iterates to the LDG/STG variant."""
+@pytest.mark.parametrize("ranks", [[40, 36, 33], [50, 44, 41]], ids=["rp40", "rp56_warp_specialised"])
+def test_tma_element_streams_match_plain(monkeypatch, ranks):
+    """k_pass2_fused<RP, true> (T / Y_n bricks loaded by TMA) gives bit-identical
+    iterates to the LDG variant, at a padded rank below and above the
+    warp-specialised Wt_2 phase."""
     import paper_1712_09999_b200 as pb
     from paper_1712_09999_b200.api import PasdConfig
 
     rng = np.random.default_rng(7)
     dims = (50, 44, 41)  # I1 even (TMA strides), ragged bricks in every mode
     X = rng.standard_normal(dims)
-    cfg = PasdConfig(lambdas=[1.0, 1.0, 1.0], ranks=[40, 36, 33], maxiter=12)
+    cfg = PasdConfig(lambdas=[1.0, 1.0, 1.0], ranks=ranks, maxiter=12)
     monkeypatch.setenv("PASD_PASS2_M16", "1")
     monkeypatch.setenv("PASD_P2_TIO", "0")
     pb.release_cache()  # solvers read the variant switches when they are built
