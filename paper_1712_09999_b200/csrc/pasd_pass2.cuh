@@ -52,7 +52,19 @@ namespace pasd {
 #ifndef PASD_P2_TIL
 #define PASD_P2_TIL 1  // TMA variant (TIO) loads only: the T, Y_n bricks of the next step arrive by TMA (requested
                        // right after the elementwise phase), E / D / Y_n leave by plain stores, G_2 / G_3 go
-                       // through the padded exchange buffers (0: loads and stores by TMA, six bricks)
+                       // through the padded exchange buffers (0: loads and stores by TMA, six bricks;
+                       // 2: as 1, but E and Y_n also leave by TMA from the load bricks, in place; D by plain stores)
+#endif
+#ifndef PASD_P2_BULK
+#define PASD_P2_BULK 1  // A_1 / A_2 / A_3 slices and the UM_2 rows arrive as single cp.async.bulk copies from
+                        // pre-tiled, pre-padded copies of A_n (k_retile, one launch before pass 2) instead of
+                        // ~190 warp-LDGSTS per step; buffers are released per slice (shared-memory counters),
+                        // barrier D and the warp-specialised staging phase go away
+#endif
+#ifndef PASD_P2_ELD
+#define PASD_P2_ELD 0  // (bulk variant) where a step's T / Y_n element loads are issued: 0 = at the step's top (in
+                       // flight during the Z products), 1 = before the previous step's Wt_2 products,
+                       // 2 = right after the previous step's elementwise phase
 #endif
 #ifndef PASD_P2_TIMING
 #define PASD_P2_TIMING 0  // probe build: per-phase clock64() sums of warp 0 (pasd_b200_debug_p2_phases)
@@ -76,6 +88,20 @@ __device__ unsigned long long g_p2_phase[12];
 #ifndef PASD_P2_BW
 #define PASD_P2_BW 12  // i1-block band width of the pencil order
 #endif
+#ifndef PASD_P2_DW2
+#define PASD_P2_DW2 0  // (bulk variant) the Wt_2 products of a step are deferred into the next step's
+                       // elementwise phase (one instruction stream: the DMMAs fill the phase that had none);
+                       // G_2 exchange buffer doubled, K-half partials through their own exchange buffer
+#endif
+// Bulk-staged slices (PASD_P2_BULK): plain element I/O only.
+template <bool TIO>
+constexpr bool pass2_bulk() {
+  return !TIO && PASD_P2_BULK && !PASD_P2_EPF;
+}
+template <bool TIO>
+constexpr bool pass2_dw2() {
+  return pass2_bulk<TIO>() && PASD_P2_DW2;
+}
 constexpr int P2_B1 = 16, P2_B2 = 8, P2_B3 = 8;
 constexpr int P2_THREADS = 256;
 constexpr int P2_BRICK = P2_B1 * P2_B2 * P2_B3;  // 1024
@@ -101,6 +127,12 @@ struct Pass2Args {
   // history, stop rule) -- one launch fewer per iteration
   int* finish_ticket;  // nullptr: k_finish runs separately
   double* history;
+  // PASD_P2_BULK: tiled copies of A_n / UM_2 in the shared-memory slice layouts of k_pass2_fused (k_retile)
+  double* At1;  // [ib3][i2 block][64 columns (l2 + 8 l3)][RP + 4]
+  double* At2;  // [ib3][ib1][RP][132]  (column 16 l3 + l1)
+  double* At3;  // [ib1][i2 block][RP][132]  (column 16 l2 + l1)
+  double* U2t;  // [i2 block][8][RP + 4]
+  int n2b;      // i2 blocks of 8
 };
 
 // TMA descriptors of the element streams of k_pass2_fused<RP, true>: 3-D
@@ -233,8 +265,10 @@ struct P2Layout {
   // Wt_2 / Wt_3 products directly (G = D + Y/mu formed in the fragment load).
   static constexpr int oG2 = oZ3 + 8 * 182;
   static constexpr bool TIL = TIO && PASD_P2_TIL;  // TMA loads only: four bricks (T, Y_1..3) + the exchange buffers
-  static constexpr int oG3 = oG2 + (TIO && !TIL ? 0 : 8 * 160);
-  static constexpr int oRed = oG3 + (TIO && !TIL ? 0 : 8 * 180);
+  static constexpr bool DW2 = pass2_dw2<TIO>();  // two G_2 buffers (step parity) + the Wt_2 K-half exchange
+  static constexpr int oG3 = oG2 + (TIO && !TIL ? 0 : 8 * 160) * (DW2 ? 2 : 1);
+  static constexpr int oX2 = oG3 + (TIO && !TIL ? 0 : 8 * 180);
+  static constexpr int oRed = oX2 + (DW2 ? 512 : 0);
   static constexpr int oBrick = oRed + 64;              // + runtime 1024-byte alignment
   // plain I/O with PASD_P2_EPF: the next step's T, Y_1..3 bricks (4 x 1024, swizzled rows)
   static constexpr bool EPF =
@@ -297,11 +331,25 @@ __device__ __forceinline__ void mbar_wait(uint64_t* mbar, unsigned parity) {
       : "memory");
 }
 
+// 1-D bulk copy global -> shared (TMA engine, no tensor map): `bytes` a multiple of 16,
+// both addresses 16-byte aligned; completion is signalled on `mbar` (complete_tx).
+__device__ __forceinline__ void bulk_load(double* dst, const double* src, unsigned bytes, uint64_t* mbar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               :
+               : "r"(static_cast<unsigned>(__cvta_generic_to_shared(dst))), "l"(src), "r"(bytes),
+                 "r"(static_cast<unsigned>(__cvta_generic_to_shared(mbar)))
+               : "memory");
+}
+__device__ __forceinline__ void mbar_init_n(uint64_t* mbar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(static_cast<unsigned>(__cvta_generic_to_shared(mbar))),
+               "r"(count)
+               : "memory");
+}
 // Warp-specialised Wt_2 / staging phase: measured at C5 (RP 56) 41.1 -> 38.9 ms per
 // launch; at RP <= 40 (C3) the split Wt_2 partials it gives up were worth more.
 template <int RP, bool TIO>
 __host__ __device__ constexpr bool pass2_ws() {
-  return (!TIO || PASD_P2_TIL) && PASD_P2_WS && RP >= 48;
+  return (!TIO || PASD_P2_TIL) && PASD_P2_WS && RP >= 48 && !pass2_bulk<TIO>();
 }
 
 // RP = common padded rank (multiple of 8, >= every R_n); rows r >= R_n of each
@@ -320,6 +368,10 @@ __global__ void __launch_bounds__(P2_THREADS, 1) k_pass2_fused(const Pass2Args a
   constexpr int MT = L::RM / 16;
   constexpr bool WS = pass2_ws<RP, TIO>();  // warp-specialised Wt_2 / staging phase
   constexpr bool TIL = L::TIL;              // TMA loads only (see PASD_P2_TIL)
+  constexpr bool TILS = TIL && PASD_P2_TIL == 2;  // ... and TMA stores of E, Y_n from the same bricks
+  constexpr bool BS = pass2_bulk<TIO>();          // slices by cp.async.bulk from the tiled copies (PASD_P2_BULK)
+  constexpr unsigned kBytesA1 = 64u * L::LD1 * 8u, kBytesA2 = (unsigned)RP * L::LD2 * 8u,
+                     kBytesA3 = (unsigned)RP * L::LD3 * 8u, kBytesU2 = 8u * L::LDU * 8u;
   extern __shared__ double sm[];
   const ModeDev& m1 = a.m[0];
   const ModeDev& m2 = a.m[1];
@@ -335,11 +387,20 @@ __global__ void __launch_bounds__(P2_THREADS, 1) k_pass2_fused(const Pass2Args a
   double* Z3s = sm + L::oZ3;
   double* G2s = sm + L::oG2;
   double* G3s = sm + L::oG3;
+  double* X2s = sm + L::oX2;
+  constexpr bool DW2 = L::DW2;
   double* red = sm + L::oRed;
   // TIO bricks: [0] T -> E, [1] Y_1, [2] Y_2, [3] Y_3 (layout B), [4] D, [5] D (layout B)
   double* brk = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(sm + L::oBrick) + 1023) & ~uintptr_t(1023));
   uint64_t* mbar = reinterpret_cast<uint64_t*>(red + 56);
   unsigned mph = 0;  // mbarrier phase parity of the next element-brick load
+  // BS: "step slices landed" (3 arrivals: A_3, A_1, UM_2 copies), "pencil slice landed" (A_2), and the
+  // per-slice release counters (8 warps each; the last one to arrive issues the next step's copy)
+  uint64_t* full_s = reinterpret_cast<uint64_t*>(red + 57);
+  uint64_t* full_p = reinterpret_cast<uint64_t*>(red + 58);
+  int* rel3 = reinterpret_cast<int*>(red + 59);
+  int* rel1 = rel3 + 1;
+  unsigned phs = 0, php = 0;
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5, g = lane >> 2, t = lane & 3;
 
   const EL* __restrict__ T = reinterpret_cast<const EL*>(a.T);
@@ -361,18 +422,29 @@ __global__ void __launch_bounds__(P2_THREADS, 1) k_pass2_fused(const Pass2Args a
   const int NW2 = w2s ? 2 : 1;
   double* W2c = a.W2part + (int64_t)blockIdx.x * NW2 * I2 * R2;  // per-CTA Wt_2 partial(s)
   for (int64_t idx = tid; idx < NW2 * I2 * R2; idx += P2_THREADS) W2c[idx] = 0.0;
+  const int mt = w & 3, kh = w >> 2;  // m-tile and K-half of the Wt_2 / Wt_3 products
+  double* W2k = W2c + (w2s ? (int64_t)kh * I2 * R2 : 0);
   // zero padding rows once (never overwritten by the staging copies)
   for (int idx = tid; idx < (RP - R2) * 128; idx += P2_THREADS) A2s[(R2 + idx / 128) * L::LD2 + (idx & 127)] = 0.0;
   for (int idx = tid; idx < (RP - R3) * 128; idx += P2_THREADS) A3s[(R3 + idx / 128) * L::LD3 + (idx & 127)] = 0.0;
   for (int idx = tid; idx < L::oBrick - L::oU1; idx += P2_THREADS) U1s[idx] = 0.0;  // UM rows, exchange buffers
+  if (BS) __syncthreads();  // (the zero fill above covers `red`)
   if (TIO && tid == 0) {
     mbar_init(mbar);
+  }
+  if (BS && tid == 0) {
+    mbar_init_n(full_s, 3);
+    mbar_init_n(full_p, 1);
+    *rel3 = 0;
+    *rel1 = 0;
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
   // TIO: the next brick's T, Y_1..3 (after the previous stores have read the bricks)
   auto load_bricks = [&](int64_t i1o_, int64_t i2o_, int64_t i3o_) {
     if (TIL) {  // all four in the A layout; their slots are free once the elementwise phase has read them
       if (tid == 0 && PASD_P2_PROBE != 7) {
+        if (TILS) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // ... and the stores have left
         mbar_expect(mbar, 4u * P2_BRICK * sizeof(double));
         const int c0 = (int)i1o_, c1 = (int)i2o_, c2 = (int)i3o_;
         tma_load3(brk, &tm.t, mbar, c0, c1, c2);
@@ -424,10 +496,38 @@ __global__ void __launch_bounds__(P2_THREADS, 1) k_pass2_fused(const Pass2Args a
     const int nbc1 = (nv1 - 2 * (tid & 7)) >= 2 ? 16 : ((nv1 - 2 * (tid & 7)) == 1 ? 8 : 0);  // A_3 chunk bytes
     __syncthreads();  // previous pencil fully done with shared memory
     load_bricks(i1o, i2b, i3o);
+    // BS: one bulk copy per slice from the tiled copies (issued by a single thread; the proxy fence orders
+    // the generic-proxy accesses of the slice before the asynchronous write)
+    auto issue_a3 = [&](int64_t i2o_) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      mbar_expect(full_s, kBytesA3);
+      bulk_load(A3s, a.At3 + ((int64_t)ib1 * a.n2b + i2o_ / P2_B2) * (RP * L::LD3), kBytesA3, full_s);
+    };
+    auto issue_a1 = [&](int64_t i2o_) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      mbar_expect(full_s, kBytesA1);
+      bulk_load(A1s, a.At1 + ((int64_t)ib3 * a.n2b + i2o_ / P2_B2) * (64 * L::LD1), kBytesA1, full_s);
+    };
+    auto issue_u2 = [&](int64_t i2o_) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      mbar_expect(full_s, kBytesU2);
+      bulk_load(U2s, a.U2t + (i2o_ / P2_B2) * (8 * L::LDU), kBytesU2, full_s);
+    };
     // ---- pencil-resident: A_2 slice (I1, R2, I3 layout), UM_1 rows, UM_3 rows ----
-    for (int l3 = 0; l3 < 8; ++l3) {
-      const bool in3 = i3o + l3 < I3;
-      stage_rows16(A2s + 16 * l3, L::LD2, m2.A + i1o + I1 * (int64_t)R2 * (i3o + l3), I1, R2, in3 ? nv1 : 0, al1, m2.A);
+    if constexpr (BS) {
+      if (tid == 0) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_expect(full_p, kBytesA2);
+        bulk_load(A2s, a.At2 + ((int64_t)ib3 * a.n1b + ib1) * (RP * L::LD2), kBytesA2, full_p);
+        issue_a3(i2b);
+        issue_a1(i2b);
+        issue_u2(i2b);
+      }
+    } else {
+      for (int l3 = 0; l3 < 8; ++l3) {
+        const bool in3 = i3o + l3 < I3;
+        stage_rows16(A2s + 16 * l3, L::LD2, m2.A + i1o + I1 * (int64_t)R2 * (i3o + l3), I1, R2, in3 ? nv1 : 0, al1, m2.A);
+      }
     }
     for (int idx = tid; idx < 16 * R1; idx += P2_THREADS) {
       const int l1 = idx & 15, r = idx >> 4;
@@ -569,17 +669,62 @@ __global__ void __launch_bounds__(P2_THREADS, 1) k_pass2_fused(const Pass2Args a
         }
       }
     };
-    stage_a1(i2b, A1s, w, 8);
-    stage_a3u2(i2b, tid, All{});
+    if constexpr (!BS) {
+      stage_a1(i2b, A1s, w, 8);
+      stage_a3u2(i2b, tid, All{});
+    }
     if (L::EPF) stage_elems(i2b, tid, All{});
+
+    double d2old[4] = {0, 0, 0, 0};  // DW2: deferred Wt_2 product of the previous step
+    double d2acc[4][4] = {};
+    auto w2_quarter = [&](int qq, const double* G2b) {
+      if (mt < MT && PASD_P2_PROBE != 1 && PASD_P2_PROBE != 3) {
+        const double* rowa = A2s + (16 * mt + g) * L::LD2 + 64 * kh;
+        const double* rowb = rowa + 8 * L::LD2;
+#pragma unroll
+        for (int ks = 4 * qq; ks < 4 * qq + 4; ++ks) {
+          const int k = 64 * kh + 4 * ks + t;
+          dmma(d2acc[ks & 3], rowa[4 * ks + t], rowb[4 * ks + t], G2b[g2x(k & 15, g, k >> 4)]);
+        }
+      }
+    };
+    // K-half sum in the order of the undeferred product, then (after a barrier) the partial update
+    auto w2_sum = [&]() {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) d2acc[0][q] += (d2acc[1][q] + d2acc[2][q]) + d2acc[3][q];
+      if (!w2s && kh == 1 && mt < MT) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) X2s[(mt * 32 + lane) * 4 + q] = d2acc[0][q];
+      }
+    };
+    auto w2_store = [&](int64_t i2base) {
+      if (mt < MT && (w2s || kh == 0)) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int r = 16 * mt + g + 8 * (q >> 1);
+          const int64_t i2 = i2base + 2 * t + (q & 1);
+          const double v = w2s ? d2acc[0][q] : (d2acc[0][q] + X2s[(mt * 32 + lane) * 4 + q]);
+          if (r < R2 && i2 < I2) W2k[i2 * R2 + r] = d2old[q] + v;
+        }
+      }
+    };
 
     for (int64_t i2o = i2b; i2o < i2e; i2o += P2_B2) {
       const bool more = i2o + P2_B2 < i2e;
       const double* A1c = A1s;
       P2T(0);  // 0: pencil setup / loop top
-      if (!TIO && !L::EPF) load_elems(i2o);  // this step's T, Y: in flight while the staging lands and Z runs
+      constexpr int ELD = BS ? PASD_P2_ELD : 0;
+      if (!TIO && !L::EPF && (ELD == 0 || i2o == i2b)) load_elems(i2o);  // this step's T, Y: in flight while the staging lands and Z runs
                                              // (measured 2 ms faster at C5 than prefetching them a step ahead)
       cp_async_wait_all();
+      if constexpr (BS) {
+        mbar_wait(full_s, phs);  // this step's A_1, A_3, UM_2 slices
+        phs ^= 1;
+        if (i2o == i2b) {
+          mbar_wait(full_p, php);  // the pencil's A_2 slice
+          php ^= 1;
+        }
+      }
       P2T(1);  // 1: element-load issue + staging wait
       __syncthreads();  // step data staged; previous step's smem consumers done
       P2T(2);  // 2: barrier A
@@ -632,6 +777,24 @@ __global__ void __launch_bounds__(P2_THREADS, 1) k_pass2_fused(const Pass2Args a
       P2T(3);  // 3: Z products
       __syncthreads();
       P2T(4);  // 4: barrier B
+      if (BS && more && tid == 0) issue_u2(i2o + P2_B2);  // UM_2 rows are read by the Z products only
+      // DW2: the previous step's Wt_2 products (m-tile mt, K-half kh) run inside this step's elementwise
+      // phase, a quarter of the K range after each of the thread's four elements.  On a pencil's first
+      // step they multiply stale G_2 values and the result is dropped.
+      const int gpar = (int)((i2o - i2b) >> 3) & 1;  // this step's G_2 buffer; the previous step's is the other
+      double* G2w = G2s + (DW2 ? gpar * (8 * 160) : 0);
+      const double* G2r = G2s + (DW2 ? (gpar ^ 1) * (8 * 160) : 0);
+      const bool w2prev = DW2 && i2o > i2b && mt < MT;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) d2old[q] = d2acc[0][q] = d2acc[1][q] = d2acc[2][q] = d2acc[3][q] = 0.0;
+      if (w2prev && (w2s || kh == 0)) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int r = 16 * mt + g + 8 * (q >> 1);
+          const int64_t i2 = i2o - P2_B2 + 2 * t + (q & 1);
+          if (r < R2) d2old[q] = W2k[i2 * R2 + r];
+        }
+      }
       // ---- elementwise (reference op order, no FMA contraction) ----
       double g1v[4];
       if constexpr (!TIO) {
@@ -662,8 +825,9 @@ __global__ void __launch_bounds__(P2_THREADS, 1) k_pass2_fused(const Pass2Args a
               Dp[off[q]] = (EL)tt;
             }
             g1v[q] = tt;
-            G2s[g2x(l1, l2, w)] = yv[1][q];
+            G2w[g2x(l1, l2, w)] = yv[1][q];
             G3s[g3x(l1, l2, w)] = yv[2][q];
+            if constexpr (DW2) w2_quarter(q, G2r);
             continue;
           }
           double zt[3], h = 0.0;
@@ -692,11 +856,13 @@ __global__ void __launch_bounds__(P2_THREADS, 1) k_pass2_fused(const Pass2Args a
             Dp[off[q]] = (EL)__dsub_rn(tt, e);  // next pass 1 reads D = T - E
           }
           g1v[q] = gn[0];
-          G2s[g2x(l1, l2, w)] = gn[1];
+          G2w[g2x(l1, l2, w)] = gn[1];
           G3s[g3x(l1, l2, w)] = gn[2];
           offc[q] = off[q];
           inc[q] = inb[q];
+          if constexpr (DW2) w2_quarter(q, G2r);
         }
+        if constexpr (DW2) w2_sum();
         (void)offc;
         (void)inc;
       } else {
@@ -733,13 +899,15 @@ __global__ void __launch_bounds__(P2_THREADS, 1) k_pass2_fused(const Pass2Args a
                 const double ar = fabs(r);
                 if (ar > worst[n]) worst[n] = ar;
                 bad |= !isfinite(r);
-                if (PASD_P2_PROBE != 6) Yp[n][o] = (EL)ynew;
+                if (PASD_P2_PROBE != 6 && !TILS) Yp[n][o] = (EL)ynew;
               }
               gn[n] = in ? g_elem(tt, e, ynew, inv_mu_next) : 0.0;  // next G_n
               gsq[n] = fma(gn[n], gn[n], gsq[n]);
+              if (TILS) brk[(1 + n) * P2_BRICK + pa] = ynew;  // (entries outside the tensor are clipped by the store)
             }
+            if (TILS) brk[pa] = e;
             if (in && PASD_P2_PROBE != 6) {
-              Enew[o] = (EL)e;
+              if (!TILS) Enew[o] = (EL)e;
               Dp[o] = (EL)__dsub_rn(tt, e);  // next pass 1 reads D = T - E
             }
             g1v[q] = gn[0];
@@ -781,8 +949,17 @@ __global__ void __launch_bounds__(P2_THREADS, 1) k_pass2_fused(const Pass2Args a
       P2T(5);  // 5: elementwise (incl. waiting for this step's element loads)
       __syncthreads();  // G exchange / bricks complete
       P2T(6);  // 6: barrier C
+      if (w2prev) w2_store(i2o - P2_B2);
       if (L::EPF && !WS && more) stage_elems(i2o + P2_B2, tid, All{});  // the element bricks are consumed: next step's
-      if (TIL && more) load_bricks(i1o, i2o + P2_B2, i3o);  // the bricks are consumed: next step's T, Y_n
+      if (TIL && !TILS && more) load_bricks(i1o, i2o + P2_B2, i3o);  // the bricks are consumed: next step's T, Y_n
+      if (TILS && tid == 0) {  // E, Y_1..3 of this brick leave from the bricks they arrived in
+        const int c0 = (int)i1o, c1 = (int)i2o, c2 = (int)i3o;
+        tma_store3(ctl->ecur ? &tm.e0 : &tm.e1, brk, c0, c1, c2);
+        tma_store3(&tm.y1, brk + P2_BRICK, c0, c1, c2);
+        tma_store3(&tm.y2, brk + 2 * P2_BRICK, c0, c1, c2);
+        tma_store3(&tm.y3a, brk + 3 * P2_BRICK, c0, c1, c2);
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      }
       if (TIO && !TIL && tid == 0) {  // E, Y_1..3, D of this brick: TMA tensor stores
         const int c0 = (int)i1o, c1 = (int)i2o, c2 = (int)i3o;
         tma_store3(ctl->ecur ? &tm.e0 : &tm.e1, brk, c0, c1, c2);
@@ -800,8 +977,17 @@ __global__ void __launch_bounds__(P2_THREADS, 1) k_pass2_fused(const Pass2Args a
           for (int j = 0; j < NT1; ++j) dmma(w1acc[j], g1v[p], g1v[2 + p], A1c[(8 * w + 2 * t + p) * L::LD1 + 8 * j + g]);
         }
       };
-      const int mt = w & 3, kh = w >> 2;  // m-tile and K-half of the Wt_2 / Wt_3 products
-      if (PASD_P2_PROBE != 1 && PASD_P2_PROBE != 3) wt1();
+      // BS: a warp is done with a slice -> count it; the last of the 8 issues the next step's copy
+      auto release = [&](int* cnt, auto&& issue) {
+        __syncwarp();
+        if (lane == 0) {
+          __threadfence_block();
+          const int old = atomicAdd(cnt, 1);
+          if ((old & 7) == 7 && more) issue(i2o + P2_B2);
+        }
+      };
+      if (ELD == 2 && more) load_elems(i2o + P2_B2);
+      if (!BS && PASD_P2_PROBE != 1 && PASD_P2_PROBE != 3) wt1();
       // ---- Wt_3^T (m-tile mt, K-half kh), K = (i1, i2) ----
       if (mt < MT && PASD_P2_PROBE != 1 && PASD_P2_PROBE != 3) {
         double acc[3][4] = {};
@@ -824,10 +1010,15 @@ __global__ void __launch_bounds__(P2_THREADS, 1) k_pass2_fused(const Pass2Args a
 #pragma unroll
         for (int q = 0; q < 4; ++q) w3acc[q] += (acc[0][q] + acc[1][q]) + acc[2][q];
       }
+      if constexpr (BS) {
+        release(rel3, issue_a3);
+        if (PASD_P2_PROBE != 1 && PASD_P2_PROBE != 3) wt1();
+        release(rel1, issue_a1);
+        if (ELD == 1 && more) load_elems(i2o + P2_B2);
+      }
       // prefetch this step's Wt_2 partial rows (read-modify-write below)
       double w2old[4] = {0, 0, 0, 0};
-      double* W2k = W2c + (w2s ? (int64_t)kh * I2 * R2 : 0);
-      if (WS ? (w < MT) : ((w2s || kh == 0) && mt < MT)) {
+      if (!DW2 && (WS ? (w < MT) : ((w2s || kh == 0) && mt < MT))) {
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
           const int r = 16 * mt + g + 8 * (q >> 1);
@@ -836,8 +1027,13 @@ __global__ void __launch_bounds__(P2_THREADS, 1) k_pass2_fused(const Pass2Args a
         }
       }
       P2T(7);  // 7: Wt_1 + Wt_3 products, Wt_2 partial prefetch
-      __syncthreads();  // A1s / A3s / U2s no longer needed this step
+      if constexpr (!BS) __syncthreads();  // A1s / A3s / U2s no longer needed this step
       P2T(8);  // 8: barrier D
+      if (TILS && more) load_bricks(i1o, i2o + P2_B2, i3o);  // the stores have read the bricks by now
+      if constexpr (DW2) {  // this step's Wt_2 products run in the next step's elementwise phase (or the drain)
+        P2T(10);
+        continue;
+      }
       if constexpr (WS) {
         // Warp-specialised: warps 4-7 issue the next step's staging (LSU-bound,
         // ~1.8k cycles) while warps 0-3 run the Wt_2 products over the full K
@@ -868,7 +1064,7 @@ __global__ void __launch_bounds__(P2_THREADS, 1) k_pass2_fused(const Pass2Args a
         P2T(10);
         continue;
       }
-      if (more) {
+      if (more && !BS) {
         stage_a1(i2o + P2_B2, A1s, w, 8);
         stage_a3u2(i2o + P2_B2, tid, All{});
       }
@@ -922,6 +1118,26 @@ __global__ void __launch_bounds__(P2_THREADS, 1) k_pass2_fused(const Pass2Args a
       }
       P2T(10);  // 10: Wt_2 products + K-half exchange + partial update
     }
+    if constexpr (DW2) {  // drain: the last step's Wt_2 products
+      const int64_t i2l = i2b + ((i2e - i2b - 1) / P2_B2) * P2_B2;
+      const double* G2r = G2s + ((int)((i2l - i2b) >> 3) & 1) * (8 * 160);
+      __syncthreads();  // the last step's partial update has read X2s
+#pragma unroll
+      for (int q = 0; q < 4; ++q) d2old[q] = d2acc[0][q] = d2acc[1][q] = d2acc[2][q] = d2acc[3][q] = 0.0;
+      if (mt < MT && (w2s || kh == 0)) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int r = 16 * mt + g + 8 * (q >> 1);
+          const int64_t i2 = i2l + 2 * t + (q & 1);
+          if (r < R2 && i2 < I2) d2old[q] = W2k[i2 * R2 + r];
+        }
+      }
+#pragma unroll
+      for (int qq = 0; qq < 4; ++qq) w2_quarter(qq, G2r);
+      w2_sum();
+      __syncthreads();
+      w2_store(i2l);
+    }
     // combine the two K-halves of Wt_3 through shared memory
     __syncthreads();
     if (w >= 4 && mt_dummy_guard(w, MT)) {
@@ -968,7 +1184,7 @@ __global__ void __launch_bounds__(P2_THREADS, 1) k_pass2_fused(const Pass2Args a
   if (tid == 32 * PASD_P2_TWARP)
     for (int k = 0; k < 12; ++k) atomicAdd(&g_p2_phase[k], ph_acc[k]);
 #endif
-  if (TIO && !TIL && tid == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // element stores done
+  if (TIO && (!TIL || TILS) && tid == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // element stores done
   // ---- per-CTA residual / NaN / ||G||^2 partials ----
   for (int n = 0; n < 3; ++n) {
     const double wv = block_reduce(worst[n], MaxOp(), red);
@@ -984,6 +1200,91 @@ __global__ void __launch_bounds__(P2_THREADS, 1) k_pass2_fused(const Pass2Args a
   __syncthreads();  // the block reductions above are done with `red`
   if (a.finish_ticket && last_cta(a.finish_ticket, reinterpret_cast<int*>(red + 48)))
     finish_body(const_cast<Ctl*>(ctl), a.resid_part, a.bad_part, gridDim.x, a.history, nullptr, red);
+}
+
+// PASD_P2_BULK: copy A_1..3 and UM_2 into the tiled, padded slice layouts k_pass2_fused<RP> stages with
+// one cp.async.bulk each (entries outside the tensor / rank rows >= R_n / pad columns are zero, so every
+// copy is full-size and unpredicated).  One CTA per tile; ~2.3x the bytes of A_n (1.2 GB at C5) per iteration.
+template <int RP>
+__global__ void __launch_bounds__(256) k_retile(const Pass2Args a, const Ctl* ctl) {
+  if (ctl->done) return;
+  using L = P2Layout<RP, false>;
+  const ModeDev& m1 = a.m[0];
+  const ModeDev& m2 = a.m[1];
+  const ModeDev& m3 = a.m[2];
+  const int R1 = m1.R, R2 = m2.R, R3 = m3.R;
+  const int64_t I1 = m1.I, I2 = m2.I, I3 = m3.I, S12 = I1 * I2;
+  const int nt3 = a.n1b * a.n2b, nt2 = a.n1b * a.n3b, nt1 = a.n3b * a.n2b;
+  int b = blockIdx.x;
+  const int tid = threadIdx.x;
+  if (b < nt3) {  // A_3 (I1, I2, R3): tile (ib1, i2 block), [r][16 l2 + l1]
+    const int64_t i1o = (int64_t)(b / a.n2b) * P2_B1, i2o = (int64_t)(b % a.n2b) * P2_B2;
+    double* out = a.At3 + (int64_t)b * (RP * L::LD3);
+    for (int idx = tid; idx < RP * L::LD3; idx += 256) {
+      const int r = idx / L::LD3, c = idx - r * L::LD3;
+      const int64_t i1 = i1o + (c & 15), i2 = i2o + (c >> 4);
+      out[idx] = (c < 128 && r < R3 && i1 < I1 && i2 < I2) ? m3.A[i1 + I1 * i2 + S12 * r] : 0.0;
+    }
+    return;
+  }
+  b -= nt3;
+  if (b < nt2) {  // A_2 (I1, R2, I3): tile (ib3, ib1), [r][16 l3 + l1]
+    const int64_t i1o = (int64_t)(b % a.n1b) * P2_B1, i3o = (int64_t)(b / a.n1b) * P2_B3;
+    double* out = a.At2 + (int64_t)b * (RP * L::LD2);
+    for (int idx = tid; idx < RP * L::LD2; idx += 256) {
+      const int r = idx / L::LD2, c = idx - r * L::LD2;
+      const int64_t i1 = i1o + (c & 15), i3 = i3o + (c >> 4);
+      out[idx] = (c < 128 && r < R2 && i1 < I1 && i3 < I3) ? m2.A[i1 + I1 * (r + (int64_t)R2 * i3)] : 0.0;
+    }
+    return;
+  }
+  b -= nt2;
+  if (b < nt1) {  // A_1 (R1, I2, I3): tile (ib3, i2 block), [column l2 + 8 l3][r]
+    const int64_t i2o = (int64_t)(b % a.n2b) * P2_B2, i3o = (int64_t)(b / a.n2b) * P2_B3;
+    double* out = a.At1 + (int64_t)b * (64 * L::LD1);
+    for (int idx = tid; idx < 64 * L::LD1; idx += 256) {
+      const int c = idx / L::LD1, r = idx - c * L::LD1;
+      const int64_t i2 = i2o + (c & 7), i3 = i3o + (c >> 3);
+      out[idx] = (r < R1 && i2 < I2 && i3 < I3) ? m1.A[r + (int64_t)R1 * (i2 + I2 * i3)] : 0.0;
+    }
+    return;
+  }
+  b -= nt1;
+  {  // UM_2 rows: tile (i2 block), [l2][r]
+    const int64_t i2o = (int64_t)b * P2_B2;
+    double* out = a.U2t + (int64_t)b * (8 * L::LDU);
+    for (int idx = tid; idx < 8 * L::LDU; idx += 256) {
+      const int l2 = idx / L::LDU, r = idx - l2 * L::LDU;
+      out[idx] = (r < R2 && i2o + l2 < I2) ? m2.UM[m2.ioff + i2o + l2 + m2.Ifull * r] : 0.0;
+    }
+  }
+}
+// doubles of the tiled copies (At1, At2, At3, U2t) for padded rank rp
+struct RetileSizes {
+  size_t at1, at2, at3, u2t;
+  int blocks;
+};
+inline RetileSizes retile_sizes(int rp, int n1b, int n2b, int n3b) {
+  RetileSizes z;
+  z.at1 = (size_t)n3b * n2b * 64 * (rp + 4);
+  z.at2 = (size_t)n3b * n1b * rp * 132;
+  z.at3 = (size_t)n1b * n2b * rp * 132;
+  z.u2t = (size_t)n2b * 8 * (rp + 4);
+  z.blocks = n1b * n2b + n1b * n3b + n3b * n2b + n2b;
+  return z;
+}
+inline void retile_launch(int rp, const Pass2Args& a, const Ctl* ctl, cudaStream_t st) {
+  const int blocks = retile_sizes(rp, a.n1b, a.n2b, a.n3b).blocks;
+  switch (rp) {
+    case 8: k_retile<8><<<blocks, 256, 0, st>>>(a, ctl); break;
+    case 16: k_retile<16><<<blocks, 256, 0, st>>>(a, ctl); break;
+    case 24: k_retile<24><<<blocks, 256, 0, st>>>(a, ctl); break;
+    case 32: k_retile<32><<<blocks, 256, 0, st>>>(a, ctl); break;
+    case 40: k_retile<40><<<blocks, 256, 0, st>>>(a, ctl); break;
+    case 48: k_retile<48><<<blocks, 256, 0, st>>>(a, ctl); break;
+    case 56: k_retile<56><<<blocks, 256, 0, st>>>(a, ctl); break;
+    default: k_retile<64><<<blocks, 256, 0, st>>>(a, ctl); break;
+  }
 }
 
 template <int RP, bool TIO, class EL = double>

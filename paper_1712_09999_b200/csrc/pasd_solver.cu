@@ -342,6 +342,7 @@ struct pasd_solver {
   // fused order-3 pass 2 (pasd_pass2.cuh)
   bool fused = false;
   bool use_m8 = false;
+  bool p2_bulk = false;  // k_pass2_fused stages its slices from the tiled copies (PASD_P2_BULK)
   int p2_rp = 0;
   Pass2Args p2{};
   int p2_grid = 0;
@@ -540,8 +541,13 @@ void launch_iteration_marked(pasd_solver* s, cudaStream_t st, Mark&& mark, bool 
     mark(PASD_K_UPDATE, true);
     if (s->use_m8)
       m8_launch(s->p2_rp, s->p2, s->d_ctl, s->p2_grid, st, s->f32);
-    else
+    else {
+      if (s->p2_bulk) {
+        retile_launch(s->p2_rp, s->p2, s->d_ctl, st);
+        ++launches;
+      }
       pass2_launch(s->p2_rp, s->p2_tio, s->p2, s->d_ctl, s->p2_tmaps, s->p2_grid, st, s->f32);
+    }
     mark(PASD_K_UPDATE, false);
     ++launches;
     int64_t maxir = 1;
@@ -963,7 +969,17 @@ pasd_solver* create_solver(const pasd_options* o, const pasd_shard* shard) {
     // (C3 38 MB, C4 18 MB: one barrier per step fewer, -2..5% pass 2); at C5 the
     // 118 MB they would take thrash L2 (+1 ms), so one per CTA there.
     const double w2_split_bytes = 2.0 * s->p2_grid * (double)s->dims[1] * s->modes[1].R * sizeof(double);
-    const bool ws = !s->use_m8 && (!s->p2_tio || PASD_P2_TIL) && PASD_P2_WS && s->p2_rp >= 48;  // pass2_ws<RP, TIO>()
+    s->p2_bulk = !s->use_m8 && !s->p2_tio && pass2_bulk<false>();
+    a.n2b = (int)((s->dims[1] + P2_B2 - 1) / P2_B2);
+    if (s->p2_bulk) {  // tiled, padded copies of A_n / UM_2 (k_retile), ~1.17x the bytes of A_n each
+      const RetileSizes z = retile_sizes(s->p2_rp, a.n1b, a.n2b, a.n3b);
+      a.At1 = s->alloc<double>(z.at1);
+      a.At2 = s->alloc<double>(z.at2);
+      a.At3 = s->alloc<double>(z.at3);
+      a.U2t = s->alloc<double>(z.u2t);
+    }
+    const bool ws = !s->use_m8 && (!s->p2_tio || PASD_P2_TIL) && PASD_P2_WS && s->p2_rp >= 48 &&
+                    !s->p2_bulk;  // pass2_ws<RP, TIO>()
     a.nw2 = (!s->use_m8 && !s->p2_tio && !ws && w2_split_bytes <= 48e6) ? 2 * s->p2_grid : s->p2_grid;
     a.W2part = s->alloc<double>((size_t)a.nw2 * s->dims[1] * s->modes[1].R);
     a.gpart = s->alloc<double>((size_t)s->p2_grid * 3);
