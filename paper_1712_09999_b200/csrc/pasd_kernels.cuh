@@ -80,6 +80,15 @@ __device__ __forceinline__ double soft(double x, double tau) {
   return 0.0;
 }
 
+// Same values as soft(), written as selects: both candidates are formed and no branch splits the
+// caller's basic block (the fused pass 2 then interleaves the dependent FP64 chains of its four elements).
+__device__ __forceinline__ double soft_sel(double x, double tau) {
+  const double a = __dsub_rn(x, tau), b = __dadd_rn(x, tau);
+  double r = (x < -tau) ? b : 0.0;
+  r = (x > tau) ? a : r;
+  return r;
+}
+
 __device__ __forceinline__ int64_t elem_offset(const ModeDev& m, int64_t kap, int64_t i) {
   const int64_t q = kap / m.inner;
   const int64_t p = kap - q * m.inner;

@@ -8,7 +8,9 @@
 //   Y_n += mu ((T - Z_n) - E) ; resid_n = max |.| ; NaN flag
 //   Wt_n = G_n^{next} A_n^T with G_n^{next} = (T - E) + Y_n/mu_next, and ||G_n^{next}||^2
 // HBM traffic: T, Y_1..3 read once, E, Y_1..3 written once; A_n slices come
-// through L2.
+// through L2: by default (PASD_P2_BULK) as one
+// cp.async.bulk copy per slice from the tiled, padded copies k_retile writes
+// (released per slice by shared-memory counters, completed on mbarriers).
 //
 // Work decomposition.  A persistent CTA walks "pencils": a 16 (i1) x 8 (i3)
 // patch swept over all i2 in steps of 8.  Per step the brick is
@@ -65,6 +67,17 @@ namespace pasd {
 #define PASD_P2_ELD 0  // (bulk variant) where a step's T / Y_n element loads are issued: 0 = at the step's top (in
                        // flight during the Z products), 1 = before the previous step's Wt_2 products,
                        // 2 = right after the previous step's elementwise phase
+#endif
+#ifndef PASD_P2_ZPIPE
+#define PASD_P2_ZPIPE 0  // Z products software-pipelined by hand: the nine operand loads of k-step s + 1 are issued
+                         // (volatile ld.shared, so ptxas keeps the order) before the DMMAs of k-step s.  ncu's
+                         // per-instruction samples showed the unpipelined loop waiting ~120 cycles per k-step on
+                         // its own operand loads: all 8 warps issue their loads in the same burst
+#endif
+#ifndef PASD_P2_SOFTSEL
+#define PASD_P2_SOFTSEL 0  // elementwise phase without branches (soft threshold as selects, unguarded residual
+                           // reductions: 399 -> 264 instructions, the four elements' FP64 chains interleaved).
+                           // Parity-green; measured slower: C5 38.1 vs 37.4, C3 2.135 vs 2.109 ms per launch
 #endif
 #ifndef PASD_P2_TIMING
 #define PASD_P2_TIMING 0  // probe build: per-phase clock64() sums of warp 0 (pasd_b200_debug_p2_phases)
@@ -216,6 +229,12 @@ __device__ __forceinline__ void cp8z(unsigned s, const void* gmem, bool valid) {
       : "memory");
 }
 
+// Shared-memory load the compiler may not reorder against the DMMAs (both volatile asm).
+__device__ __forceinline__ double lds_f64(unsigned addr) {
+  double v;
+  asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(addr));
+  return v;
+}
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
 // Brick element index e = i1 + 16 * (i2 + 8 * i3) (local coordinates).
@@ -746,7 +765,44 @@ __global__ void __launch_bounds__(P2_THREADS, 1) k_pass2_fused(const Pass2Args a
           dmma(c2, A2s[kc * L::LD2 + g + 16 * w], A2s[kc * L::LD2 + g + 8 + 16 * w], U2s[g * L::LDU + k]);
           dmma(c3, A3s[k * L::LD3 + g + 16 * w], A3s[k * L::LD3 + g + 8 + 16 * w], U3s[g * L::LDU + kc]);
         };
-        if (PASD_P2_PROBE != 2 && PASD_P2_PROBE != 3) {
+        if (PASD_P2_ZPIPE && PASD_P2_PROBE != 2 && PASD_P2_PROBE != 3 && PASD_P2_PROBE != 5) {
+          // two operand sets; loads of k-step s + 1, then the DMMAs of k-step s
+          const unsigned pu1 = smem_u32(U1s + g * L::LDU + t), pa1 = smem_u32(A1c + (g + 8 * w) * L::LD1 + t);
+          const unsigned pa2 = smem_u32(A2s + t * L::LD2 + g + 16 * w), pu2 = smem_u32(U2s + g * L::LDU + t);
+          const unsigned pa3 = smem_u32(A3s + t * L::LD3 + g + 16 * w), pu3 = smem_u32(U3s + g * L::LDU + t);
+          double o[2][9];
+          auto zload = [&](int ks, double(&d)[9]) {
+            d[0] = lds_f64(pu1 + 32 * ks);
+            d[1] = lds_f64(pu1 + 32 * ks + 64 * L::LDU);
+            d[2] = lds_f64(pa1 + 32 * ks);
+            d[3] = lds_f64(pa2 + 32 * ks * L::LD2);
+            d[4] = lds_f64(pa2 + 32 * ks * L::LD2 + 64);
+            d[5] = lds_f64(pu2 + 32 * ks);
+            d[6] = lds_f64(pa3 + 32 * ks * L::LD3);
+            d[7] = lds_f64(pa3 + 32 * ks * L::LD3 + 64);
+            d[8] = lds_f64(pu3 + 32 * ks);
+          };
+          auto zmma = [&](int ks, const double(&d)[9]) {
+            dmma((ks & 1) ? y1 : z1, d[0], d[1], d[2]);
+            dmma((ks & 1) ? y2 : z2, d[3], d[4], d[5]);
+            dmma((ks & 1) ? y3 : z3, d[6], d[7], d[8]);
+          };
+          const bool lastk = ksz == KS;  // the last k-step touches a nonzero rank row
+          zload(0, o[0]);
+#pragma unroll
+          for (int ks = 0; ks < KS; ++ks) {
+            if (ks + 1 < KS - 1) {
+              zload(ks + 1, o[(ks + 1) & 1]);
+            } else if (ks + 1 == KS - 1) {
+              if (lastk) zload(ks + 1, o[(ks + 1) & 1]);
+            }
+            if (ks < KS - 1) {
+              zmma(ks, o[ks & 1]);
+            } else if (lastk) {
+              zmma(ks, o[ks & 1]);
+            }
+          }
+        } else if (PASD_P2_PROBE != 2 && PASD_P2_PROBE != 3) {
           if constexpr (RP >= 48) {
             // at RP >= 48 the hoisted loads push the kernel to 254 registers and the
             // Z phase measured slower (C5: 4.5 vs 4.25 k cycles per step), as did an
@@ -836,18 +892,28 @@ __global__ void __launch_bounds__(P2_THREADS, 1) k_pass2_fused(const Pass2Args a
             zt[n] = __dsub_rn(tt, zz[n]);
             h = __dadd_rn(h, __dadd_rn(zt[n], __dmul_rn(yv[n][q], inv_mu)));  // pasd.cpp:202
           }
-          const double e = soft(__dmul_rn(h, inv_n), tau);  // pasd.cpp:208
+          const double e = PASD_P2_SOFTSEL ? soft_sel(__dmul_rn(h, inv_n), tau) : soft(__dmul_rn(h, inv_n), tau);  // pasd.cpp:208
           double gn[3];
 #pragma unroll
           for (int n = 0; n < 3; ++n) {
             const double r = __dsub_rn(zt[n], e);                       // pasd.cpp:220
             const double ynew = __dadd_rn(yv[n][q], __dmul_rn(mu, r));  // pasd.cpp:221
+#if PASD_P2_SOFTSEL
+            // entries outside the tensor have T = Y_n = Z_n = 0 (zero-filled loads, zero slice entries), so
+            // r = 0 there: the residual / NaN reductions need no guard, and the only guarded statement
+            // left is the store (one predicated STG, no branch: the four elements' chains interleave)
+            const double ar = fabs(r);
+            worst[n] = ar > worst[n] ? ar : worst[n];
+            bad |= !isfinite(r);
+            if (inb[q] && PASD_P2_PROBE != 6) Yp[n][off[q]] = (EL)ynew;
+#else
             if (inb[q]) {
               const double ar = fabs(r);
               if (ar > worst[n]) worst[n] = ar;
               bad |= !isfinite(r);
               if (PASD_P2_PROBE != 6) Yp[n][off[q]] = (EL)ynew;
             }
+#endif
             gn[n] = inb[q] ? g_elem(tt, e, ynew, inv_mu_next) : 0.0;  // next G_n
             gsq[n] = fma(gn[n], gn[n], gsq[n]);
           }

@@ -271,18 +271,26 @@ __global__ void __launch_bounds__(M8_THREADS, M8_CTAS) k_pass2_m8(const Pass2Arg
           zt[n] = __dsub_rn(tt, zz[n]);
           h = __dadd_rn(h, __dadd_rn(zt[n], __dmul_rn(yv[n][p], inv_mu)));  // pasd.cpp:202
         }
-        const double e = soft(__dmul_rn(h, inv_n), tau);  // pasd.cpp:208
+        const double e = PASD_P2_SOFTSEL ? soft_sel(__dmul_rn(h, inv_n), tau) : soft(__dmul_rn(h, inv_n), tau);  // pasd.cpp:208
         double gn[3];
 #pragma unroll
         for (int n = 0; n < 3; ++n) {
           const double r = __dsub_rn(zt[n], e);                       // pasd.cpp:220
           const double ynew = __dadd_rn(yv[n][p], __dmul_rn(mu, r));  // pasd.cpp:221
+#if PASD_P2_SOFTSEL
+          // entries outside the tensor have T = Y_n = Z_n = 0, so r = 0 there: only the store is guarded
+          const double ar = fabs(r);
+          worst[n] = ar > worst[n] ? ar : worst[n];
+          bad |= !isfinite(r);
+          if (inb[p]) Yp[n][off[p]] = (EL)ynew;
+#else
           if (inb[p]) {
             const double ar = fabs(r);
             if (ar > worst[n]) worst[n] = ar;
             bad |= !isfinite(r);
             Yp[n][off[p]] = (EL)ynew;
           }
+#endif
           gn[n] = inb[p] ? g_elem(tt, e, ynew, inv_mu_next) : 0.0;
           gsq[n] = fma(gn[n], gn[n], gsq[n]);
         }

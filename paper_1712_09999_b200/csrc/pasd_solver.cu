@@ -38,6 +38,7 @@
 #include "pasd_pass1.cuh"
 #include "pasd_gram.cuh"
 #include "pasd_pass2m8.cuh"
+#include "pasd_pass2ts.cuh"
 #include "pasd_comm.cuh"
 
 using namespace pasd;
@@ -343,6 +344,7 @@ struct pasd_solver {
   bool fused = false;
   bool use_m8 = false;
   bool p2_bulk = false;  // k_pass2_fused stages its slices from the tiled copies (PASD_P2_BULK)
+  bool p2_ts = false;    // two-team kernel k_pass2_ts (pasd_pass2ts.cuh) instead of k_pass2_fused
   int p2_rp = 0;
   Pass2Args p2{};
   int p2_grid = 0;
@@ -546,7 +548,10 @@ void launch_iteration_marked(pasd_solver* s, cudaStream_t st, Mark&& mark, bool 
         retile_launch(s->p2_rp, s->p2, s->d_ctl, st);
         ++launches;
       }
-      pass2_launch(s->p2_rp, s->p2_tio, s->p2, s->d_ctl, s->p2_tmaps, s->p2_grid, st, s->f32);
+      if (s->p2_ts)
+        ts_launch(s->p2_rp, s->f32, s->p2, s->d_ctl, s->p2_grid, st);
+      else
+        pass2_launch(s->p2_rp, s->p2_tio, s->p2, s->d_ctl, s->p2_tmaps, s->p2_grid, st, s->f32);
     }
     mark(PASD_K_UPDATE, false);
     ++launches;
@@ -992,10 +997,16 @@ pasd_solver* create_solver(const pasd_options* o, const pasd_shard* shard) {
       a.finish_ticket = s->alloc<int>(1);
       CK(cudaMemset(a.finish_ticket, 0, sizeof(int)));
     }
+    {
+      const char* ts_env = std::getenv("PASD_P2_TS");
+      // opt-in (PASD_P2_TS=1): parity-green, measured slower (C5 47.2 vs 37.0 ms per launch)
+      s->p2_ts = s->p2_bulk && PASD_P2_TS && ts_supported(s->p2_rp) && ts_env && ts_env[0] == '1';
+    }
     if (s->use_m8)
       m8_setup(s->p2_rp);
     else
       pass2_setup(s->p2_rp);
+    if (s->p2_ts) ts_setup(s->p2_rp);
     CK(cudaGetLastError());
   }
   s->d_stats = s->alloc<double>(2 * 2048);

@@ -286,6 +286,33 @@ def test_tma_element_streams_match_plain(monkeypatch, ranks):
     np.testing.assert_array_equal(plain.e, tio.e)
 
 
+@pytest.mark.parametrize("ranks", [[40, 36, 33], [50, 44, 41]], ids=["rp40", "rp56"])
+def test_two_team_kernel_matches_fused(monkeypatch, ranks):
+    """k_pass2_ts (opt-in, PASD_P2_TS=1: Z_3 and the Wt products on a second warp
+    team) against k_pass2_fused on the same input.  Its Wt_1 partial sums are
+    taken in a different order, so agreement is to rounding, not bit-for-bit."""
+    import paper_1712_09999_b200 as pb
+    from paper_1712_09999_b200.api import PasdConfig
+
+    rng = np.random.default_rng(11)
+    dims = (50, 44, 41)  # ragged bricks in every mode
+    X = rng.standard_normal(dims)
+    cfg = PasdConfig(lambdas=[1.0, 1.0, 1.0], ranks=ranks, maxiter=12)
+    monkeypatch.setenv("PASD_PASS2_M16", "1")
+    monkeypatch.setenv("PASD_P2_TS", "0")
+    pb.release_cache()  # solvers read the variant switches when they are built
+    fused = pb.pasd_recover(X, cfg)
+    pb.release_cache()
+    monkeypatch.setenv("PASD_P2_TS", "1")
+    ts = pb.pasd_recover(X, cfg)
+    pb.release_cache()
+    assert fused.iters == ts.iters
+    nx = np.linalg.norm(fused.x)
+    assert np.linalg.norm(fused.x - ts.x) <= 1e-11 * nx
+    assert np.linalg.norm(fused.e - ts.e) <= 1e-11 * max(np.linalg.norm(fused.e), nx)
+    assert np.array_equal(fused.e != 0, ts.e != 0)
+
+
 def _oracle_pair(oracle_mod, dims, ranks, k, seed=3, rho=0.05):
     """Oracle iterates k and k+1 of a low-rank instance (full-rank phase)."""
     L0 = oracle_mod.gen_tucker(dims, list(ranks), seed=seed)

@@ -1,6 +1,6 @@
 """Per-kernel summary CSV (+ traffic.json entries) from an `ncu --set full` report.
 
-usage: python tools/ncu_summary.py report.ncu-rep out.csv [traffic.json]
+usage: python tools/ncu_summary.py report.ncu-rep out.csv [traffic.json [workload]]
 """
 import csv
 import io
@@ -44,11 +44,17 @@ def main():
             for cls, prefixes in CLASSES.items():
                 if name.startswith(prefixes):
                     traffic.setdefault(cls, []).append(b)
-    if len(sys.argv) > 3:
-        tj = {"_source": f"ncu --set full --clock-control none ({rep}): dram__bytes_read.sum + "
-                         "dram__bytes_write.sum per launch, mean over the captured launches of the class"}
-        for cls, v in traffic.items():
-            tj[cls] = sum(v) / len(v)
+    if len(sys.argv) > 3:  # merged into the file under the workload's name (bench.py keys it that way)
+        wl = sys.argv[4] if len(sys.argv) > 4 else "c5_1000cube_r50"
+        try:
+            tj = json.load(open(sys.argv[3]))
+        except (OSError, ValueError):
+            tj = {}
+        tj["_source"] = (f"ncu --set full --clock-control none ({rep}): dram__bytes_read.sum + "
+                         "dram__bytes_write.sum per launch, mean over the captured launches of the class")
+        tj["_keys"] = ("workload name -> kernel class -> DRAM bytes per launch; a workload or class not captured "
+                       "is absent and bench.py reports roofline.traffic = null")
+        tj[wl] = {cls: sum(v) / len(v) for cls, v in traffic.items()}
         with open(sys.argv[3], "w") as f:
             json.dump(tj, f, indent=1)
     print(open(out).read())

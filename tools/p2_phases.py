@@ -20,6 +20,8 @@ from paper_1712_09999_b200.workloads import WORKLOADS  # noqa: E402
 
 NAMES = ["loop top", "load issue + staging wait", "barrier A", "Z products", "barrier B", "elementwise",
          "barrier C", "Wt_1 + Wt_3", "barrier D", "staging issue", "Wt_2 + exchange", "pencil end"]
+if os.environ.get("P2_NAMES"):
+    NAMES = os.environ["P2_NAMES"].split(",")
 w = WORKLOADS[sys.argv[1] if len(sys.argv) > 1 else "c5"]
 T = bench.generate_input(w)
 cfg = PasdConfig(lambdas=w.lambdas(), ranks=list(w.ranks), maxiter=40)
