@@ -796,6 +796,7 @@ __global__ void __launch_bounds__(P2_THREADS, 1) k_pass2_fused(const Pass2Args a
             } else if (ks + 1 == KS - 1) {
               if (lastk) zload(ks + 1, o[(ks + 1) & 1]);
             }
+            if (PASD_P2_ZPIPE == 2) __syncwarp();  // keeps ptxas from hoisting the loads of later k-steps above this point
             if (ks < KS - 1) {
               zmma(ks, o[ks & 1]);
             } else if (lastk) {
