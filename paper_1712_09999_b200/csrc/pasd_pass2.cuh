@@ -79,6 +79,9 @@ namespace pasd {
                            // reductions: 399 -> 264 instructions, the four elements' FP64 chains interleaved).
                            // Parity-green; measured slower: C5 38.1 vs 37.4, C3 2.135 vs 2.109 ms per launch
 #endif
+#ifndef PASD_P2_L2HINT
+#define PASD_P2_L2HINT 1  // bulk copies of the tiled slices carry an L2 evict_last policy
+#endif
 #ifndef PASD_P2_TIMING
 #define PASD_P2_TIMING 0  // probe build: per-phase clock64() sums of warp 0 (pasd_b200_debug_p2_phases)
 #endif
@@ -359,6 +362,22 @@ __device__ __forceinline__ void bulk_load(double* dst, const double* src, unsign
                  "r"(static_cast<unsigned>(__cvta_generic_to_shared(mbar)))
                : "memory");
 }
+// ... with an L2 cache policy (createpolicy): the tiled A slices are re-read by every pencil of a band, the
+// element streams pass through L2 once
+__device__ __forceinline__ void bulk_load_hint(double* dst, const double* src, unsigned bytes, uint64_t* mbar,
+                                               uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;"
+      :
+      : "r"(static_cast<unsigned>(__cvta_generic_to_shared(dst))), "l"(src), "r"(bytes),
+        "r"(static_cast<unsigned>(__cvta_generic_to_shared(mbar))), "l"(policy)
+      : "memory");
+}
+__device__ __forceinline__ uint64_t l2_policy_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
 __device__ __forceinline__ void mbar_init_n(uint64_t* mbar, unsigned count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(static_cast<unsigned>(__cvta_generic_to_shared(mbar))),
                "r"(count)
@@ -420,6 +439,7 @@ __global__ void __launch_bounds__(P2_THREADS, 1) k_pass2_fused(const Pass2Args a
   int* rel3 = reinterpret_cast<int*>(red + 59);
   int* rel1 = rel3 + 1;
   unsigned phs = 0, php = 0;
+  const uint64_t l2pol = (BS && PASD_P2_L2HINT) ? l2_policy_evict_last() : 0;
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5, g = lane >> 2, t = lane & 3;
 
   const EL* __restrict__ T = reinterpret_cast<const EL*>(a.T);
@@ -517,27 +537,33 @@ __global__ void __launch_bounds__(P2_THREADS, 1) k_pass2_fused(const Pass2Args a
     load_bricks(i1o, i2b, i3o);
     // BS: one bulk copy per slice from the tiled copies (issued by a single thread; the proxy fence orders
     // the generic-proxy accesses of the slice before the asynchronous write)
+    auto bulk = [&](double* dst, const double* src, unsigned bytes, uint64_t* mb) {
+      if (PASD_P2_L2HINT)
+        bulk_load_hint(dst, src, bytes, mb, l2pol);
+      else
+        bulk_load(dst, src, bytes, mb);
+    };
     auto issue_a3 = [&](int64_t i2o_) {
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       mbar_expect(full_s, kBytesA3);
-      bulk_load(A3s, a.At3 + ((int64_t)ib1 * a.n2b + i2o_ / P2_B2) * (RP * L::LD3), kBytesA3, full_s);
+      bulk(A3s, a.At3 + ((int64_t)ib1 * a.n2b + i2o_ / P2_B2) * (RP * L::LD3), kBytesA3, full_s);
     };
     auto issue_a1 = [&](int64_t i2o_) {
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       mbar_expect(full_s, kBytesA1);
-      bulk_load(A1s, a.At1 + ((int64_t)ib3 * a.n2b + i2o_ / P2_B2) * (64 * L::LD1), kBytesA1, full_s);
+      bulk(A1s, a.At1 + ((int64_t)ib3 * a.n2b + i2o_ / P2_B2) * (64 * L::LD1), kBytesA1, full_s);
     };
     auto issue_u2 = [&](int64_t i2o_) {
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       mbar_expect(full_s, kBytesU2);
-      bulk_load(U2s, a.U2t + (i2o_ / P2_B2) * (8 * L::LDU), kBytesU2, full_s);
+      bulk(U2s, a.U2t + (i2o_ / P2_B2) * (8 * L::LDU), kBytesU2, full_s);
     };
     // ---- pencil-resident: A_2 slice (I1, R2, I3 layout), UM_1 rows, UM_3 rows ----
     if constexpr (BS) {
       if (tid == 0) {
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         mbar_expect(full_p, kBytesA2);
-        bulk_load(A2s, a.At2 + ((int64_t)ib3 * a.n1b + ib1) * (RP * L::LD2), kBytesA2, full_p);
+        bulk_load(A2s, a.At2 + ((int64_t)ib3 * a.n1b + ib1) * (RP * L::LD2), kBytesA2, full_p);  // read once
         issue_a3(i2b);
         issue_a1(i2b);
         issue_u2(i2b);
