@@ -1299,7 +1299,7 @@ __global__ void __launch_bounds__(P2_THREADS, 1) k_pass2_fused(const Pass2Args a
 // one cp.async.bulk each (entries outside the tensor / rank rows >= R_n / pad columns are zero, so every
 // copy is full-size and unpredicated).  One CTA per tile; ~2.3x the bytes of A_n (1.2 GB at C5) per iteration.
 template <int RP>
-__global__ void __launch_bounds__(256) k_retile(const Pass2Args a, const Ctl* ctl) {
+__global__ void __launch_bounds__(256) k_retile(const Pass2Args a, const Ctl* ctl, int boff) {
   if (ctl->done) return;
   using L = P2Layout<RP, false>;
   const ModeDev& m1 = a.m[0];
@@ -1308,7 +1308,7 @@ __global__ void __launch_bounds__(256) k_retile(const Pass2Args a, const Ctl* ct
   const int R1 = m1.R, R2 = m2.R, R3 = m3.R;
   const int64_t I1 = m1.I, I2 = m2.I, I3 = m3.I, S12 = I1 * I2;
   const int nt3 = a.n1b * a.n2b, nt2 = a.n1b * a.n3b, nt1 = a.n3b * a.n2b;
-  int b = blockIdx.x;
+  int b = blockIdx.x + boff;  // boff: first tile of this launch (the A tiles and the UM_2 tiles can go separately)
   const int tid = threadIdx.x;
   if (b < nt3) {  // A_3 (I1, I2, R3): tile (ib1, i2 block), [r][16 l2 + l1]
     const int64_t i1o = (int64_t)(b / a.n2b) * P2_B1, i2o = (int64_t)(b % a.n2b) * P2_B2;
@@ -1366,17 +1366,20 @@ inline RetileSizes retile_sizes(int rp, int n1b, int n2b, int n3b) {
   z.blocks = n1b * n2b + n1b * n3b + n3b * n2b + n2b;
   return z;
 }
-inline void retile_launch(int rp, const Pass2Args& a, const Ctl* ctl, cudaStream_t st) {
-  const int blocks = retile_sizes(rp, a.n1b, a.n2b, a.n3b).blocks;
+// part 0: all tiles; 1: the A_1..3 tiles (ready after pass 1); 2: the UM_2 tiles (ready after the SVT)
+inline void retile_launch(int rp, const Pass2Args& a, const Ctl* ctl, cudaStream_t st, int part = 0) {
+  const int all = retile_sizes(rp, a.n1b, a.n2b, a.n3b).blocks;
+  const int boff = part == 2 ? all - a.n2b : 0;
+  const int blocks = part == 0 ? all : (part == 1 ? all - a.n2b : a.n2b);
   switch (rp) {
-    case 8: k_retile<8><<<blocks, 256, 0, st>>>(a, ctl); break;
-    case 16: k_retile<16><<<blocks, 256, 0, st>>>(a, ctl); break;
-    case 24: k_retile<24><<<blocks, 256, 0, st>>>(a, ctl); break;
-    case 32: k_retile<32><<<blocks, 256, 0, st>>>(a, ctl); break;
-    case 40: k_retile<40><<<blocks, 256, 0, st>>>(a, ctl); break;
-    case 48: k_retile<48><<<blocks, 256, 0, st>>>(a, ctl); break;
-    case 56: k_retile<56><<<blocks, 256, 0, st>>>(a, ctl); break;
-    default: k_retile<64><<<blocks, 256, 0, st>>>(a, ctl); break;
+    case 8: k_retile<8><<<blocks, 256, 0, st>>>(a, ctl, boff); break;
+    case 16: k_retile<16><<<blocks, 256, 0, st>>>(a, ctl, boff); break;
+    case 24: k_retile<24><<<blocks, 256, 0, st>>>(a, ctl, boff); break;
+    case 32: k_retile<32><<<blocks, 256, 0, st>>>(a, ctl, boff); break;
+    case 40: k_retile<40><<<blocks, 256, 0, st>>>(a, ctl, boff); break;
+    case 48: k_retile<48><<<blocks, 256, 0, st>>>(a, ctl, boff); break;
+    case 56: k_retile<56><<<blocks, 256, 0, st>>>(a, ctl, boff); break;
+    default: k_retile<64><<<blocks, 256, 0, st>>>(a, ctl, boff); break;
   }
 }
 

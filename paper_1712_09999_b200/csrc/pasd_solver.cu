@@ -451,6 +451,7 @@ template <class Mark>
 void launch_iteration_marked(pasd_solver* s, cudaStream_t st, Mark&& mark, bool concurrent = false) {
   const int N = s->N;
   int launches = 0;
+  bool retiled_a = false;  // the A tiles of the bulk-staged pass 2 were written on a branch
   if (!s->sharded && concurrent) {
     // Graph capture, unsharded: the Procrustes step (U_n) and pass 1 (A_n from D,
     // Y_n, U_n) are per mode, so each mode is one branch and the branches share
@@ -466,12 +467,23 @@ void launch_iteration_marked(pasd_solver* s, cudaStream_t st, Mark&& mark, bool 
       launches += 2;
     }
     for (int n = 0; n < N; ++n) CK(cudaStreamWaitEvent(st, s->ev_p1join[n], 0));
+    if (s->fused && s->p2_bulk && !s->use_m8) {
+      // the A tiles of pass 2 only need pass 1: retiled on a branch next to the Gram products and the SVTs
+      // (HBM-bound copy next to tensor-bound / latency-bound kernels); the UM_2 tiles follow the SVT
+      CK(cudaEventRecord(s->ev_p1fork, st));
+      CK(cudaStreamWaitEvent(s->p1s[0], s->ev_p1fork, 0));
+      retile_launch(s->p2_rp, s->p2, s->d_ctl, s->p1s[0], 1);
+      CK(cudaEventRecord(s->ev_p1join[0], s->p1s[0]));
+      ++launches;
+      retiled_a = true;
+    }
     // all modes' Gram partials, reductions and SVTs in three launches (per-mode
     // Gram / SVT branches measured slower: more, smaller launches)
     launch_gram_all(s->gram_rp, s->d_pack, s->d_ctl, s->gram_grid, st);
     k_gram_reduce_all<<<s->gram_red_grid, 256, 0, st>>>(s->d_pack, s->d_ctl);
     k_svt<<<N * kSmallCluster, kSmallThreads, s->small_smem, st>>>(s->d_pack, s->d_ctl);
     launches += 3;
+    if (retiled_a) CK(cudaStreamWaitEvent(st, s->ev_p1join[0], 0));
   } else {
     mark(PASD_K_POLAR, true);
     k_polar<<<N * kSmallCluster, kSmallThreads, s->small_smem, st>>>(s->d_pack, s->d_ctl);
@@ -545,7 +557,7 @@ void launch_iteration_marked(pasd_solver* s, cudaStream_t st, Mark&& mark, bool 
       m8_launch(s->p2_rp, s->p2, s->d_ctl, s->p2_grid, st, s->f32);
     else {
       if (s->p2_bulk) {
-        retile_launch(s->p2_rp, s->p2, s->d_ctl, st);
+        retile_launch(s->p2_rp, s->p2, s->d_ctl, st, retiled_a ? 2 : 0);
         ++launches;
       }
       if (s->p2_ts)
