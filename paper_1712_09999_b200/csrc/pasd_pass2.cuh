@@ -532,6 +532,11 @@ __global__ void __launch_bounds__(P2_THREADS, 1) k_pass2_fused(const Pass2Args a
     const int pen = ib1 + a.n1b * ib3 + a.npencils * seg;  // index of the Wt_1 / Wt_3 partials
     const int64_t i1o = (int64_t)ib1 * P2_B1, i3o = (int64_t)ib3 * P2_B3;
     const int nv1 = (int)imin64(16, I1 - i1o);
+    if (i2b >= i2e) {  // empty i2 segment (the segment count does not divide the steps): zero partials, no staging
+      for (int idx = tid; idx < 16 * R1; idx += P2_THREADS) a.W1p[(int64_t)pen * 16 * R1 + idx] = 0.0;
+      for (int idx = tid; idx < 8 * R3; idx += P2_THREADS) a.W3p[(int64_t)pen * 8 * R3 + idx] = 0.0;
+      continue;
+    }
     const int nbc1 = (nv1 - 2 * (tid & 7)) >= 2 ? 16 : ((nv1 - 2 * (tid & 7)) == 1 ? 8 : 0);  // A_3 chunk bytes
     __syncthreads();  // previous pencil fully done with shared memory
     load_bricks(i1o, i2b, i3o);

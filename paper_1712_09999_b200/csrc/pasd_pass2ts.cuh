@@ -167,6 +167,11 @@ __global__ void __launch_bounds__(TS_THREADS, 1) k_pass2_ts(const Pass2Args a, c
     const int pen = ib1 + a.n1b * ib3 + a.npencils * seg;
     const int64_t i1o = (int64_t)ib1 * P2_B1, i3o = (int64_t)ib3 * P2_B3;
     const int nv1 = (int)imin64(16, I1 - i1o);
+    if (i2b >= i2e) {  // empty i2 segment (the segment count does not divide the steps): zero partials, no staging
+      for (int idx = tid; idx < 16 * R1; idx += TS_THREADS) a.W1p[(int64_t)pen * 16 * R1 + idx] = 0.0;
+      for (int idx = tid; idx < 8 * R3; idx += TS_THREADS) a.W3p[(int64_t)pen * 8 * R3 + idx] = 0.0;
+      continue;
+    }
     __syncthreads();  // previous pencil fully done with shared memory
     auto issue_a3 = [&](int64_t i2o_) {
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");

@@ -941,7 +941,10 @@ pasd_solver* create_solver(const pasd_options* o, const pasd_shard* shard) {
     // slots of k_pass2_m8, C2: 625; C3: 1250 on 148 of k_pass2_fused).
     // Segments keep >= 4 steps each so the pencil-resident A_2 slice is reused.
     a.nseg = 1;
-    {
+    const char* nseg_env = std::getenv("PASD_P2_NSEG");  // test hook: force the segment count (1..8)
+    if (nseg_env && std::atoi(nseg_env) >= 1 && std::atoi(nseg_env) <= 8) {
+      a.nseg = std::atoi(nseg_env);
+    } else {
       const int slots = (s->use_m8 ? M8_CTAS : 1) * sms;
       const int64_t steps = (s->dims[1] + (s->use_m8 ? M8_B : P2_B2) - 1) / (s->use_m8 ? M8_B : P2_B2);
       // modelled time ~ waves x (steps per item + per-item overhead), the
@@ -950,6 +953,7 @@ pasd_solver* create_solver(const pasd_options* o, const pasd_shard* shard) {
       const double c0 = s->use_m8 ? 1.0 : 2.0;
       double best = 1e300;
       for (int sg = 1; sg <= 8 && (steps + sg - 1) / sg >= 4; ++sg) {
+        if ((int64_t)(sg - 1) * ((steps + sg - 1) / sg) >= steps) continue;  // would leave the last segment empty
         const double waves = std::ceil((double)a.npencils * sg / slots);
         const double t = waves * ((double)((steps + sg - 1) / sg) + c0);
         if (t < best * 0.99) {  // fewer segments unless clearly better
@@ -1481,7 +1485,7 @@ int pasd_b200_nccl_unique_id(void* out128, char* errbuf, size_t errlen) {
 }
 
 const char* pasd_b200_build_info(void) {
-  return "pasd_b200 sm_100a fp64; kernels: polar,pass1,gram,svt,pass2,finish,pass2_reduce; comm: nccl,loopback";
+  return "pasd_b200 sm_100a fp64; kernels: polar,pass1,gram,svt,retile,pass2,finish,pass2_reduce; comm: nccl,loopback";
 }
 
 int pasd_b200_loopback_create(int32_t nranks, void** out, char* errbuf, size_t errlen) {

@@ -313,6 +313,34 @@ def test_two_team_kernel_matches_fused(monkeypatch, ranks):
     assert np.array_equal(fused.e != 0, ts.e != 0)
 
 
+@pytest.mark.parametrize("ts", ["0", "1"], ids=["fused", "two_team"])
+def test_empty_i2_segment(monkeypatch, ts):
+    """A forced segment count that leaves the last i2 segment of every pencil empty
+    (16 steps in 5 segments of 4): the bulk-staged kernels must skip it (no slice
+    copies, zero partials) and agree with the unsegmented sweep to rounding."""
+    import paper_1712_09999_b200 as pb
+    from paper_1712_09999_b200.api import PasdConfig
+
+    rng = np.random.default_rng(5)
+    dims = (34, 128, 20)
+    X = rng.standard_normal(dims)
+    cfg = PasdConfig(lambdas=[1.0, 1.0, 1.0], ranks=[33, 40, 20], maxiter=10)
+    monkeypatch.setenv("PASD_PASS2_M16", "1")
+    monkeypatch.setenv("PASD_P2_TS", ts)
+    monkeypatch.setenv("PASD_P2_NSEG", "1")
+    pb.release_cache()
+    one = pb.pasd_recover(X, cfg)
+    pb.release_cache()
+    monkeypatch.setenv("PASD_P2_NSEG", "5")
+    five = pb.pasd_recover(X, cfg)
+    pb.release_cache()
+    assert one.iters == five.iters
+    nx = np.linalg.norm(one.x)
+    assert np.isfinite(five.x).all() and np.isfinite(five.e).all()
+    assert np.linalg.norm(one.x - five.x) <= 1e-11 * nx
+    assert np.linalg.norm(one.e - five.e) <= 1e-11 * max(np.linalg.norm(one.e), nx)
+
+
 def _oracle_pair(oracle_mod, dims, ranks, k, seed=3, rho=0.05):
     """Oracle iterates k and k+1 of a low-rank instance (full-rank phase)."""
     L0 = oracle_mod.gen_tucker(dims, list(ranks), seed=seed)

@@ -4,7 +4,7 @@
 mkdir -p gpurun_out
 for v in $VARIANTS; do
   if [ "$v" = default ]; then unset PASD_B200_LIB; else export PASD_B200_LIB=$PWD/build/$v.so; fi
-  timeout 300 python -m pytest tests/test_gpu_parity.py -x -q -p no:cacheprovider -k "single_step or trivial_phase or steady_state" > gpurun_out/vq_$v.log 2>&1
+  [ "${SKIP_TESTS:-0}" = 1 ] || timeout 300 python -m pytest tests/test_gpu_parity.py -x -q -p no:cacheprovider -k "single_step or trivial_phase or steady_state" > gpurun_out/vq_$v.log 2>&1
   echo "$v tests rc=$? $(tail -1 gpurun_out/vq_$v.log)"
   for c in ${CONFIGS:-c5}; do
     timeout 300 python bench.py --config $c --steps 10 --warmup 3 --no-cpu-baseline --no-e2e --steady-after 0 > gpurun_out/vq_${v}_$c.json 2> gpurun_out/vq_${v}_$c.err
