@@ -82,6 +82,10 @@ namespace pasd {
 #ifndef PASD_P2_L2HINT
 #define PASD_P2_L2HINT 1  // bulk copies of the tiled slices carry an L2 evict_last policy
 #endif
+#ifndef PASD_P2_EHINT
+#define PASD_P2_EHINT 0  // (bulk variant, float64 storage) the element streams T, Y_n, E, D carry an L2 evict_first
+                         // policy.  Measured worse at C5: DRAM reads 46.6 -> 50.5 GB, 37.1 -> 37.9 ms per launch
+#endif
 #ifndef PASD_P2_TIMING
 #define PASD_P2_TIMING 0  // probe build: per-phase clock64() sums of warp 0 (pasd_b200_debug_p2_phases)
 #endif
@@ -378,6 +382,28 @@ __device__ __forceinline__ uint64_t l2_policy_evict_last() {
   asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
   return p;
 }
+__device__ __forceinline__ uint64_t l2_policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+// Predicated float64 load / store with an L2 cache policy (no branch: the predicate is part of the instruction).
+__device__ __forceinline__ double ldg_hint(const double* p, bool ok, uint64_t policy) {
+  double v = 0.0;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %2, 0;\n\t"
+      "@p ld.global.L2::cache_hint.f64 %0, [%1], %3;\n\t}"
+      : "+d"(v)
+      : "l"(p), "r"((unsigned)ok), "l"(policy));
+  return v;
+}
+__device__ __forceinline__ void stg_hint(double* p, double v, bool ok, uint64_t policy) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %2, 0;\n\t"
+      "@p st.global.L2::cache_hint.f64 [%0], %1, %3;\n\t}" ::"l"(p),
+      "d"(v), "r"((unsigned)ok), "l"(policy)
+      : "memory");
+}
 __device__ __forceinline__ void mbar_init_n(uint64_t* mbar, unsigned count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(static_cast<unsigned>(__cvta_generic_to_shared(mbar))),
                "r"(count)
@@ -440,6 +466,8 @@ __global__ void __launch_bounds__(P2_THREADS, 1) k_pass2_fused(const Pass2Args a
   int* rel1 = rel3 + 1;
   unsigned phs = 0, php = 0;
   const uint64_t l2pol = (BS && PASD_P2_L2HINT) ? l2_policy_evict_last() : 0;
+  constexpr bool EH = BS && PASD_P2_EHINT && sizeof(EL) == 8;  // element streams with an evict_first policy
+  const uint64_t l2ef = EH ? l2_policy_evict_first() : 0;
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5, g = lane >> 2, t = lane & 3;
 
   const EL* __restrict__ T = reinterpret_cast<const EL*>(a.T);
@@ -688,9 +716,15 @@ __global__ void __launch_bounds__(P2_THREADS, 1) k_pass2_fused(const Pass2Args a
         inb[q] = i1 < I1 && i2 < I2 && i3 < I3;
         off[q] = i1 + I1 * i2 + S12 * i3;
         const bool ld = inb[q] && PASD_P2_PROBE != 7;
-        tv[q] = ld ? T[off[q]] : 0.0;
+        if constexpr (EH) {
+          tv[q] = ldg_hint(reinterpret_cast<const double*>(T) + off[q], ld, l2ef);
 #pragma unroll
-        for (int n = 0; n < 3; ++n) yv[n][q] = ld ? (double)Yp[n][off[q]] : 0.0;
+          for (int n = 0; n < 3; ++n) yv[n][q] = ldg_hint(reinterpret_cast<const double*>(Yp[n]) + off[q], ld, l2ef);
+        } else {
+          tv[q] = ld ? T[off[q]] : 0.0;
+#pragma unroll
+          for (int n = 0; n < 3; ++n) yv[n][q] = ld ? (double)Yp[n][off[q]] : 0.0;
+        }
       }
     };
     // PASD_P2_EPF: this thread's 8 copies of a step's T, Y_1..3 brick (stream ts,
@@ -943,13 +977,17 @@ __global__ void __launch_bounds__(P2_THREADS, 1) k_pass2_fused(const Pass2Args a
               const double ar = fabs(r);
               if (ar > worst[n]) worst[n] = ar;
               bad |= !isfinite(r);
-              if (PASD_P2_PROBE != 6) Yp[n][off[q]] = (EL)ynew;
+              if (!EH && PASD_P2_PROBE != 6) Yp[n][off[q]] = (EL)ynew;
             }
+            if constexpr (EH) stg_hint(reinterpret_cast<double*>(Yp[n]) + off[q], ynew, inb[q] && PASD_P2_PROBE != 6, l2ef);
 #endif
             gn[n] = inb[q] ? g_elem(tt, e, ynew, inv_mu_next) : 0.0;  // next G_n
             gsq[n] = fma(gn[n], gn[n], gsq[n]);
           }
-          if (inb[q] && PASD_P2_PROBE != 6) {
+          if constexpr (EH) {
+            stg_hint(reinterpret_cast<double*>(Enew) + off[q], e, inb[q] && PASD_P2_PROBE != 6, l2ef);
+            stg_hint(reinterpret_cast<double*>(Dp) + off[q], __dsub_rn(tt, e), inb[q] && PASD_P2_PROBE != 6, l2ef);
+          } else if (inb[q] && PASD_P2_PROBE != 6) {
             Enew[off[q]] = (EL)e;
             Dp[off[q]] = (EL)__dsub_rn(tt, e);  // next pass 1 reads D = T - E
           }
