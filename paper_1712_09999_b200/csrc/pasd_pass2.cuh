@@ -86,6 +86,12 @@ namespace pasd {
 #define PASD_P2_EHINT 0  // (bulk variant, float64 storage) the element streams T, Y_n, E, D carry an L2 evict_first
                          // policy.  Measured worse at C5: DRAM reads 46.6 -> 50.5 GB, 37.1 -> 37.9 ms per launch
 #endif
+#ifndef PASD_P2_HALF
+#define PASD_P2_HALF 0  // padded ranks 8 mod 16 (RP 40, 56): the last m-tile of the Wt_2 / Wt_3 products has only
+                        // padding in its upper 8 rows -> one DMMA.8x8x4 per k-step instead of two; the m-tiles are
+                        // assigned so that each scheduler hosts exactly one of the four light (m-tile, K-half) items.
+                        // Parity-green; measured slower (C5 38.3 vs 37.1 ms per launch, 250 registers)
+#endif
 #ifndef PASD_P2_TIMING
 #define PASD_P2_TIMING 0  // probe build: per-phase clock64() sums of warp 0 (pasd_b200_debug_p2_phases)
 #endif
@@ -172,6 +178,14 @@ __device__ __forceinline__ void dmma(double (&c)[4], double a0, double a1, doubl
       "mma.sync.aligned.m16n8k4.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5}, {%6}, {%0,%1,%2,%3};"
       : "+d"(c[0]), "+d"(c[1]), "+d"(c[2]), "+d"(c[3])
       : "d"(a0), "d"(a1), "d"(b0));
+}
+
+// Upper half of an m16n8k4 product skipped: rows 0-7 only (mma.sync.m8n8k4.f64, one DMMA.8x8x4), accumulating
+// into c[0], c[1] (the same fragment positions as the m16n8k4 accumulator's rows g).
+__device__ __forceinline__ void dmma_lo(double (&c)[4], double a0, double b0) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(c[0]), "+d"(c[1])
+               : "d"(a0), "d"(b0));
 }
 
 // Asynchronous global->shared copy of one double (LDGSTS); src_bytes = 0
@@ -489,7 +503,13 @@ __global__ void __launch_bounds__(P2_THREADS, 1) k_pass2_fused(const Pass2Args a
   const int NW2 = w2s ? 2 : 1;
   double* W2c = a.W2part + (int64_t)blockIdx.x * NW2 * I2 * R2;  // per-CTA Wt_2 partial(s)
   for (int64_t idx = tid; idx < NW2 * I2 * R2; idx += P2_THREADS) W2c[idx] = 0.0;
-  const int mt = w & 3, kh = w >> 2;  // m-tile and K-half of the Wt_2 / Wt_3 products
+  // m-tile and K-half of the Wt_2 (mt) / Wt_3 (mt3) products.  The two warps of a K-half pair are any two
+  // warps; rotating the tiles puts the last m-tile of the four (product, K-half) items on four different
+  // schedulers (warp w issues on scheduler w & 3).
+  constexpr bool HALF = PASD_P2_HALF && (L::RM - RP == 8) && !(TIO && !TIL) && !WS;
+  const int kh = w >> 2;
+  const int mt = !HALF ? (w & 3) : ((w + kh + 2) & 3);
+  const int mt3 = !HALF ? (w & 3) : ((w + kh) & 3);
   double* W2k = W2c + (w2s ? (int64_t)kh * I2 * R2 : 0);
   // zero padding rows once (never overwritten by the staging copies)
   for (int idx = tid; idx < (RP - R2) * 128; idx += P2_THREADS) A2s[(R2 + idx / 128) * L::LD2 + (idx & 127)] = 0.0;
@@ -1125,9 +1145,21 @@ __global__ void __launch_bounds__(P2_THREADS, 1) k_pass2_fused(const Pass2Args a
       if (ELD == 2 && more) load_elems(i2o + P2_B2);
       if (!BS && PASD_P2_PROBE != 1 && PASD_P2_PROBE != 3) wt1();
       // ---- Wt_3^T (m-tile mt, K-half kh), K = (i1, i2) ----
-      if (mt < MT && PASD_P2_PROBE != 1 && PASD_P2_PROBE != 3) {
+      if (HALF && mt3 == MT - 1 && PASD_P2_PROBE != 1 && PASD_P2_PROBE != 3) {  // rows 8-15 of the tile are padding
         double acc[3][4] = {};
-        const double* rowa = A3s + (16 * mt + g) * L::LD3 + 64 * kh;
+        const double* rowa = A3s + (16 * mt3 + g) * L::LD3 + 64 * kh;
+        const double* gcol = G3s + 180 * g;
+#pragma unroll
+        for (int ks = 0; ks < 16; ++ks) {
+          const int k = 64 * kh + 4 * ks + t;
+          double(&c)[4] = (ks & 3) == 0 ? w3acc : acc[(ks & 3) - 1];
+          dmma_lo(c, rowa[4 * ks + t], gcol[(k & 15) + 22 * (k >> 4)]);
+        }
+#pragma unroll
+        for (int q = 0; q < 2; ++q) w3acc[q] += (acc[0][q] + acc[1][q]) + acc[2][q];
+      } else if (mt3 < MT && PASD_P2_PROBE != 1 && PASD_P2_PROBE != 3) {
+        double acc[3][4] = {};
+        const double* rowa = A3s + (16 * mt3 + g) * L::LD3 + 64 * kh;
         const double* rowb = rowa + 8 * L::LD3;
         const double* gcol = G3s + 180 * g;
 #pragma unroll
@@ -1207,7 +1239,22 @@ __global__ void __launch_bounds__(P2_THREADS, 1) k_pass2_fused(const Pass2Args a
       P2T(9);  // 9: staging issue
       // ---- W-b: Wt_2^T (m-tile mt, K-half kh), K = (i1, i3) ----
       double acc2[4] = {0, 0, 0, 0};
-      if (mt < MT && PASD_P2_PROBE != 1 && PASD_P2_PROBE != 3) {
+      if (HALF && mt == MT - 1 && PASD_P2_PROBE != 1 && PASD_P2_PROBE != 3) {  // rows 8-15 of the tile are padding
+        double acc[3][4] = {};
+        const double* rowa = A2s + (16 * mt + g) * L::LD2 + 64 * kh;
+#pragma unroll
+        for (int ks = 0; ks < 16; ++ks) {
+          const int k = 64 * kh + 4 * ks + t;
+          double(&c)[4] = (ks & 3) == 0 ? acc2 : acc[(ks & 3) - 1];
+          dmma_lo(c, rowa[4 * ks + t], G2s[g2x(k & 15, g, k >> 4)]);
+        }
+#pragma unroll
+        for (int q = 0; q < 2; ++q) acc2[q] += (acc[0][q] + acc[1][q]) + acc[2][q];
+        if (!w2s && kh == 1) {
+#pragma unroll
+          for (int q = 0; q < 4; ++q) Z3s[(mt * 32 + lane) * 4 + q] = acc2[q];  // exchange (Z3s free now)
+        }
+      } else if (mt < MT && PASD_P2_PROBE != 1 && PASD_P2_PROBE != 3) {
         double acc[3][4] = {};
         const double* rowa = A2s + (16 * mt + g) * L::LD2 + 64 * kh;
         const double* rowb = rowa + 8 * L::LD2;
@@ -1276,9 +1323,9 @@ __global__ void __launch_bounds__(P2_THREADS, 1) k_pass2_fused(const Pass2Args a
     }
     // combine the two K-halves of Wt_3 through shared memory
     __syncthreads();
-    if (w >= 4 && mt_dummy_guard(w, MT)) {
+    if (w >= 4 && mt3 < MT) {  // K-half 1 of m-tile mt3 (K-half 0 of m-tile w is warp w)
 #pragma unroll
-      for (int q = 0; q < 4; ++q) Z3s[((w & 3) * 32 + lane) * 4 + q] = w3acc[q];
+      for (int q = 0; q < 4; ++q) Z3s[(mt3 * 32 + lane) * 4 + q] = w3acc[q];
     }
     __syncthreads();
     if (w < 4 && w < MT) {
