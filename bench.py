@@ -488,8 +488,10 @@ def main():
         "data": "synthetic",
         "config": {"workload": w.name, "dims": list(w.dims), "ranks": list(w.ranks), "rho": w.rho,
                    "noise": list(w.noise), "iters_fixed": True,
-                   "input": "reference generator (synth.cpp:71-121, rng.hpp streams, seed 0) on the device", "l2": "inputs larger than L2 (T, E x2, D, Y x3: 7 x 8 GB resident)"
-                   if S * 8 > 126e6 else "inputs L2-resident"},
+                   "input": "reference generator (synth.cpp:71-121, rng.hpp streams, seed 0) on the device", "l2": (f"inputs larger than L2 (T, E x2, D, Y x3: 7 x {S * es / 1e9:.3g} GB resident, re-streamed "
+                          "every iteration)")
+                   if 7 * S * es > 126e6 else
+                   f"working set 7 x {S * es / 1e6:.3g} MB fits the 126 MB L2 (an iterative solve re-reads it every step)"},
         "elem_iters_per_s": value * S,
         "gpu_launches": int(launches),
         "clocks": clocks,
