@@ -90,7 +90,8 @@ namespace pasd {
 #define PASD_P2_HALF 0  // padded ranks 8 mod 16 (RP 40, 56): the last m-tile of the Wt_2 / Wt_3 products has only
                         // padding in its upper 8 rows -> one DMMA.8x8x4 per k-step instead of two; the m-tiles are
                         // assigned so that each scheduler hosts exactly one of the four light (m-tile, K-half) items.
-                        // Parity-green; measured slower (C5 38.3 vs 37.1 ms per launch, 250 registers)
+                        // Parity-green; no gain (predicated upper half: C5 36.7 vs 36.8, C3 2.12 vs 2.08 ms per
+                        // launch; as separate m8n8k4 loops: 38.3 ms, 250 registers)
 #endif
 #ifndef PASD_P2_TIMING
 #define PASD_P2_TIMING 0  // probe build: per-phase clock64() sums of warp 0 (pasd_b200_debug_p2_phases)
@@ -180,12 +181,14 @@ __device__ __forceinline__ void dmma(double (&c)[4], double a0, double a1, doubl
       : "d"(a0), "d"(a1), "d"(b0));
 }
 
-// Upper half of an m16n8k4 product skipped: rows 0-7 only (mma.sync.m8n8k4.f64, one DMMA.8x8x4), accumulating
-// into c[0], c[1] (the same fragment positions as the m16n8k4 accumulator's rows g).
-__device__ __forceinline__ void dmma_lo(double (&c)[4], double a0, double b0) {
-  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
-               : "+d"(c[0]), "+d"(c[1])
-               : "d"(a0), "d"(b0));
+// m16n8k4 as two m8n8k4 (the same two DMMA.8x8x4), the rows 8-15 half under a warp-uniform predicate.
+__device__ __forceinline__ void dmma_split(double (&c)[4], double a0, double a1, double b0, bool upper) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %7, 0;\n\t"
+      "mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%4}, {%6}, {%0,%1};\n\t"
+      "@p mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%2,%3}, {%5}, {%6}, {%2,%3};\n\t}"
+      : "+d"(c[0]), "+d"(c[1]), "+d"(c[2]), "+d"(c[3])
+      : "d"(a0), "d"(a1), "d"(b0), "r"((unsigned)upper));
 }
 
 // Asynchronous global->shared copy of one double (LDGSTS); src_bytes = 0
@@ -1145,19 +1148,7 @@ __global__ void __launch_bounds__(P2_THREADS, 1) k_pass2_fused(const Pass2Args a
       if (ELD == 2 && more) load_elems(i2o + P2_B2);
       if (!BS && PASD_P2_PROBE != 1 && PASD_P2_PROBE != 3) wt1();
       // ---- Wt_3^T (m-tile mt, K-half kh), K = (i1, i2) ----
-      if (HALF && mt3 == MT - 1 && PASD_P2_PROBE != 1 && PASD_P2_PROBE != 3) {  // rows 8-15 of the tile are padding
-        double acc[3][4] = {};
-        const double* rowa = A3s + (16 * mt3 + g) * L::LD3 + 64 * kh;
-        const double* gcol = G3s + 180 * g;
-#pragma unroll
-        for (int ks = 0; ks < 16; ++ks) {
-          const int k = 64 * kh + 4 * ks + t;
-          double(&c)[4] = (ks & 3) == 0 ? w3acc : acc[(ks & 3) - 1];
-          dmma_lo(c, rowa[4 * ks + t], gcol[(k & 15) + 22 * (k >> 4)]);
-        }
-#pragma unroll
-        for (int q = 0; q < 2; ++q) w3acc[q] += (acc[0][q] + acc[1][q]) + acc[2][q];
-      } else if (mt3 < MT && PASD_P2_PROBE != 1 && PASD_P2_PROBE != 3) {
+      if (mt3 < MT && PASD_P2_PROBE != 1 && PASD_P2_PROBE != 3) {
         double acc[3][4] = {};
         const double* rowa = A3s + (16 * mt3 + g) * L::LD3 + 64 * kh;
         const double* rowb = rowa + 8 * L::LD3;
@@ -1173,7 +1164,10 @@ __global__ void __launch_bounds__(P2_THREADS, 1) k_pass2_fused(const Pass2Args a
           } else {
             b3 = gcol[(k & 15) + 22 * (k >> 4)];
           }
-          dmma(c, rowa[4 * ks + t], rowb[4 * ks + t], b3);
+          if constexpr (HALF)
+            dmma_split(c, rowa[4 * ks + t], rowb[4 * ks + t], b3, mt3 != MT - 1);  // last m-tile: rows 8-15 are padding
+          else
+            dmma(c, rowa[4 * ks + t], rowb[4 * ks + t], b3);
         }
 #pragma unroll
         for (int q = 0; q < 4; ++q) w3acc[q] += (acc[0][q] + acc[1][q]) + acc[2][q];
@@ -1239,22 +1233,7 @@ __global__ void __launch_bounds__(P2_THREADS, 1) k_pass2_fused(const Pass2Args a
       P2T(9);  // 9: staging issue
       // ---- W-b: Wt_2^T (m-tile mt, K-half kh), K = (i1, i3) ----
       double acc2[4] = {0, 0, 0, 0};
-      if (HALF && mt == MT - 1 && PASD_P2_PROBE != 1 && PASD_P2_PROBE != 3) {  // rows 8-15 of the tile are padding
-        double acc[3][4] = {};
-        const double* rowa = A2s + (16 * mt + g) * L::LD2 + 64 * kh;
-#pragma unroll
-        for (int ks = 0; ks < 16; ++ks) {
-          const int k = 64 * kh + 4 * ks + t;
-          double(&c)[4] = (ks & 3) == 0 ? acc2 : acc[(ks & 3) - 1];
-          dmma_lo(c, rowa[4 * ks + t], G2s[g2x(k & 15, g, k >> 4)]);
-        }
-#pragma unroll
-        for (int q = 0; q < 2; ++q) acc2[q] += (acc[0][q] + acc[1][q]) + acc[2][q];
-        if (!w2s && kh == 1) {
-#pragma unroll
-          for (int q = 0; q < 4; ++q) Z3s[(mt * 32 + lane) * 4 + q] = acc2[q];  // exchange (Z3s free now)
-        }
-      } else if (mt < MT && PASD_P2_PROBE != 1 && PASD_P2_PROBE != 3) {
+      if (mt < MT && PASD_P2_PROBE != 1 && PASD_P2_PROBE != 3) {
         double acc[3][4] = {};
         const double* rowa = A2s + (16 * mt + g) * L::LD2 + 64 * kh;
         const double* rowb = rowa + 8 * L::LD2;
@@ -1269,7 +1248,10 @@ __global__ void __launch_bounds__(P2_THREADS, 1) k_pass2_fused(const Pass2Args a
           } else {
             b2 = G2s[g2x(k & 15, g, k >> 4)];
           }
-          dmma(c, rowa[4 * ks + t], rowb[4 * ks + t], b2);
+          if constexpr (HALF)
+            dmma_split(c, rowa[4 * ks + t], rowb[4 * ks + t], b2, mt != MT - 1);
+          else
+            dmma(c, rowa[4 * ks + t], rowb[4 * ks + t], b2);
         }
 #pragma unroll
         for (int q = 0; q < 4; ++q) acc2[q] += (acc[0][q] + acc[1][q]) + acc[2][q];
